@@ -1,0 +1,188 @@
+/*
+ * krt.h — C ABI of the KARMA out-of-core data-parallel runtime for B200.
+ *
+ * The reference (oocsched, /root/reference/pkg) has no executor: its drop-in
+ * boundary for this path is the ExecutionPlan / plan.json wire format
+ * (plan.py:75-106, :179-231) plus the op semantics of build_engine_ops /
+ * run_engine (simulator.py:67-135, :253-349) and simulate_distributed
+ * (distsim.py:140-266).  Every entry point below replaces one of those, or one
+ * executor step the paper describes and the reference only
+ * simulates; the comment on each names the reference interface it stands in
+ * for.  Plain pointers and sizes only; no C++ exceptions cross this boundary.
+ *
+ * Error protocol: every int-returning function returns KRT_OK (0) or one of
+ * the codes below (they mirror the reference CLI's exit codes, cli.py:23-26);
+ * krt_last_error() returns a thread-local message naming the failing op, in
+ * the style of DeadlockError (simulator.py:36-39).
+ */
+#ifndef KRT_H_
+#define KRT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum krt_status {
+  KRT_OK = 0,
+  KRT_INFEASIBLE = 1, /* plan violates residency/capacity, deadlock   (cli.py:24) */
+  KRT_USAGE = 2,      /* malformed input / bad argument               (cli.py:25) */
+  KRT_INTERNAL = 3    /* CUDA / NCCL / host failure                   (cli.py:26) */
+};
+
+/* plan actions (plan.py:24-29) followed by the DP pipeline ops (distsim.py:168-236) */
+enum krt_action {
+  KRT_FW = 0, KRT_BW = 1, KRT_SWAP_IN = 2, KRT_SWAP_OUT = 3, KRT_RECOMPUTE_FW = 4,
+  KRT_WEIGHT_IN = 5, KRT_GRAD_OUT = 6, KRT_EXCHANGE = 7, KRT_HOST_UPDATE = 8
+};
+
+enum krt_dtype { KRT_F32 = 0, KRT_BF16 = 1 };
+enum krt_optim { KRT_SGD = 0, KRT_ADAM = 1 };
+
+const char* krt_last_error(void);
+const char* krt_version(void);
+void krt_string_free(char* s);
+
+/* ------------------------------------------------------------------------
+ * Plan bundle: model graph + hardware spec + execution plan.  Host-only; no
+ * GPU needed.
+ * ---------------------------------------------------------------------- */
+typedef struct krt_plan krt_plan;
+
+/* Parses model text (model_ir.py:281-330), hardware key=value text
+ * (cost_model.py:308-339) and plan.json (plan.py:205-231). */
+int krt_plan_load(const char* model_text, const char* hw_text, const char* plan_json,
+                  krt_plan** out);
+void krt_plan_free(krt_plan* plan);
+/* Override hardware capacity (bytes) for validation / simulation. */
+int krt_plan_set_capacity(krt_plan* plan, double capacity_bytes);
+
+/* plan_string (plan.py:166-167), UTF-8 " → " separators; caller frees. */
+int krt_plan_string(const krt_plan* plan, char** out);
+/* plan_to_dict (plan.py:179-202) rendered as JSON; caller frees. */
+int krt_plan_json(const krt_plan* plan, char** out);
+/* validate_plan (planner.py:342-413): JSON array of violation strings; *n_violations
+ * receives the count (0 = plan accepted). */
+int krt_plan_validate(const krt_plan* plan, char** out_json, int* n_violations);
+/* simulate (simulator.py:364-399): JSON {makespan,total_stall,peak_mem,events,csv}
+ * or {deadlock:[...]}.  enforce_capacity as in the reference. */
+int krt_plan_simulate(const krt_plan* plan, int enforce_capacity, char** out_json);
+
+typedef struct krt_dist_config {
+  int workers;        /* DistConfig.workers            (distsim.py:48) */
+  int ring;           /* 1 = Collective.RING, 0 = FLAT (distsim.py:49) */
+  double net_bw;      /* bytes/s                       (distsim.py:50) */
+  double net_latency; /* seconds                       (distsim.py:51) */
+  int groups;         /* 0 = one group per block       (distsim.py:52) */
+} krt_dist_config;
+
+/* simulate_distributed (distsim.py:140-266): JSON {iteration_time, iteration_times,
+ * exposed_comm, peak_mem, makespan, events} or {error}. */
+int krt_plan_simulate_dist(const krt_plan* plan, const krt_dist_config* cfg, int iterations,
+                           char** out_json);
+
+/* ------------------------------------------------------------------------
+ * Executor context: one per rank / GPU.
+ * ---------------------------------------------------------------------- */
+typedef struct krt_ctx krt_ctx;
+
+typedef struct krt_config {
+  int device;               /* CUDA device ordinal */
+  int world_size;           /* data-parallel workers (DistConfig.workers) */
+  int rank;                 /* this worker */
+  const void* nccl_id;      /* 128-byte ncclUniqueId (rank 0's) when world_size > 1 */
+  int dist_groups;          /* gradient groups, 0 = one per block (distsim.py:52) */
+  int weight_dtype;         /* enum krt_dtype: device copy of the weights */
+  int optimizer;            /* enum krt_optim */
+  float lr, beta1, beta2, eps, weight_decay, momentum;
+  float grad_scale;         /* multiplies summed gradients (1/world_size = mean) */
+  int host_threads;         /* host update worker threads, 0 = auto */
+  size_t arena_slack_bytes; /* extra arena bytes beyond the static assignment */
+} krt_config;
+
+/* The executor's compute step for one plan op (KRT_FW, KRT_RECOMPUTE_FW,
+ * KRT_BW) of `block`.  `slot` is the block's device arena slot
+ * (slot_bytes long), `stream` the cudaStream_t all work must be issued on.
+ * Return 0 on success. */
+typedef int (*krt_compute_cb)(void* user, int action, int block, void* slot,
+                              size_t slot_bytes, void* stream);
+
+int krt_create(const krt_config* cfg, krt_ctx** out);
+int krt_destroy(krt_ctx* ctx);
+
+/* One block's physical footprint: saved-activation bytes (the arena slot)
+ * and the element counts of its parameter tensors in order.  Replaces the
+ * analytic BlockCost.bytes / weight_elems (cost_model.py:225-273) with what
+ * the block really stores.  Call for every block before krt_prepare. */
+int krt_register_block(krt_ctx* ctx, int block, size_t act_bytes, const int64_t* param_numel,
+                       int n_params);
+
+/* Bind a validated plan: builds the op DAG (build_engine_ops + the DP ops),
+ * the issue order (run_engine), the static arena assignment from the byte
+ * ledger, and allocates device/pinned-host memory.  Fails with
+ * KRT_INFEASIBLE if validate_plan rejects the plan or a block's physical
+ * bytes exceed the plan's swap_bytes. */
+int krt_prepare(krt_ctx* ctx, const krt_plan* plan);
+
+enum krt_region {
+  KRT_REGION_WEIGHTS = 0, /* device weights of a block (weight_dtype) */
+  KRT_REGION_GRADS = 1,   /* device fp32 gradients of a block */
+  KRT_REGION_ARENA = 2,   /* the whole device arena (block ignored) */
+  KRT_REGION_HOST_SWAP = 3/* pinned host swap area of a block */
+};
+int krt_region(krt_ctx* ctx, int which, int block, void** ptr, size_t* bytes);
+/* device stream handles: 0 compute, 1 H2D, 2 D2H, 3 network */
+int krt_stream(krt_ctx* ctx, int which, void** stream);
+
+/* Device address of `block`'s currently resident arena slot; valid inside a
+ * compute callback (e.g. a recompute that regenerates its input from the
+ * previous block, which the plan guarantees resident, plan.py:129-138). */
+int krt_block_slot(krt_ctx* ctx, int block, void** slot);
+
+/* Copy the device weights into the fp32 master copies (host shards for
+ * host-path blocks, device masters otherwise).  Call once after writing the
+ * initial weights into KRT_REGION_WEIGHTS. */
+int krt_init_master(krt_ctx* ctx);
+
+/* Run one training iteration: the plan's ops plus weight_in / grad_out /
+ * exchange / host_update, issued in the simulator's start order with every
+ * dependency, start gate and arena reuse expressed as CUDA events. */
+int krt_run_iteration(krt_ctx* ctx, krt_compute_cb cb, void* user);
+/* Wait for all device streams and host updates of the last iteration. */
+int krt_synchronize(krt_ctx* ctx);
+
+/* Measured trace of the last iteration in the SimTrace CSV schema
+ * (simulator.py:225-230) extended with the DP ops; caller frees. */
+int krt_trace_csv(krt_ctx* ctx, char** out);
+/* JSON counters: bytes per direction, arena size, launches, ... ; caller frees. */
+int krt_stats(krt_ctx* ctx, char** out_json);
+
+/* Fetch the fp32 master weights of a block into host memory `out`
+ * (numel floats); for world_size > 1 only this rank's shard is valid. */
+int krt_read_master(krt_ctx* ctx, int block, float* out, size_t numel);
+
+/* ------------------------------------------------------------------------
+ * Kernels exposed for tests and the driver (all asynchronous on `stream`).
+ * ---------------------------------------------------------------------- */
+/* out[i] = (bf16|f32)(scale * sum_r in_r[i]) for r < n_in (fused grad
+ * scale/cast/reduce; n_in = 1 is the plain pack). */
+int krt_reduce_cast(const float* const* in, int n_in, void* out, int out_dtype, size_t n,
+                    float scale, void* stream);
+/* Device Adam/SGD over `n` fp32 elements; updates master/m/v in place and
+ * writes the weight copy (weight_dtype).  Same arithmetic as the host path. */
+int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights,
+                      int weight_dtype, size_t n, int optimizer, float lr, float beta1,
+                      float beta2, float eps, float weight_decay, float momentum, int step,
+                      void* stream);
+/* Host Adam/SGD (the paper's CPU update kernel). */
+int krt_host_update(float* master, float* m, float* v, const float* grad, void* weights,
+                    int weight_dtype, size_t n, int optimizer, float lr, float beta1,
+                    float beta2, float eps, float weight_decay, float momentum, int step,
+                    int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRT_H_ */

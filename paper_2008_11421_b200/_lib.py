@@ -1,0 +1,122 @@
+"""ctypes binding of libkrt.so (include/krt.h).
+
+This is the reference-side FFI for the executor path: the reference package is
+Python, so its natural binding to a C ABI is ctypes.  The library is built
+in-tree by ``__graft_entry__.build()``; importing this module without it
+raises immediately — there is no Python fallback for any runtime op.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).with_name("libkrt.so")
+
+KRT_OK, KRT_INFEASIBLE, KRT_USAGE, KRT_INTERNAL = 0, 1, 2, 3
+FW, BW, SWAP_IN, SWAP_OUT, RECOMPUTE_FW, WEIGHT_IN, GRAD_OUT, EXCHANGE, HOST_UPDATE = range(9)
+ACTION_NAMES = ("fw", "bw", "swap_in", "swap_out", "recompute_fw",
+                "weight_in", "grad_out", "exchange", "host_update")
+F32, BF16 = 0, 1
+SGD, ADAM = 0, 1
+REGION_WEIGHTS, REGION_GRADS, REGION_ARENA, REGION_HOST_SWAP = 0, 1, 2, 3
+
+
+class KrtError(RuntimeError):
+    """A non-zero krt status; ``code`` mirrors the reference CLI exit codes."""
+
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        super().__init__(f"krt error {code}: {msg}")
+
+
+class InfeasiblePlanError(KrtError):
+    pass
+
+
+class DistConfig(C.Structure):
+    _fields_ = [("workers", C.c_int), ("ring", C.c_int), ("net_bw", C.c_double),
+                ("net_latency", C.c_double), ("groups", C.c_int)]
+
+
+class Config(C.Structure):
+    _fields_ = [("device", C.c_int), ("world_size", C.c_int), ("rank", C.c_int),
+                ("nccl_id", C.c_void_p), ("dist_groups", C.c_int), ("weight_dtype", C.c_int),
+                ("optimizer", C.c_int), ("lr", C.c_float), ("beta1", C.c_float),
+                ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
+                ("momentum", C.c_float), ("grad_scale", C.c_float), ("host_threads", C.c_int),
+                ("arena_slack_bytes", C.c_size_t)]
+
+
+COMPUTE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p)
+
+EXPORTS = {
+    "krt_last_error": (C.c_char_p, []),
+    "krt_version": (C.c_char_p, []),
+    "krt_string_free": (None, [C.c_void_p]),
+    "krt_plan_load": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "krt_plan_free": (None, [C.c_void_p]),
+    "krt_plan_set_capacity": (C.c_int, [C.c_void_p, C.c_double]),
+    "krt_plan_string": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "krt_plan_json": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "krt_plan_validate": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
+    "krt_plan_simulate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "krt_plan_simulate_dist": (C.c_int, [C.c_void_p, C.POINTER(DistConfig), C.c_int,
+                                         C.POINTER(C.c_void_p)]),
+    "krt_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
+    "krt_destroy": (C.c_int, [C.c_void_p]),
+    "krt_register_block": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.POINTER(C.c_int64), C.c_int]),
+    "krt_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "krt_region": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                             C.POINTER(C.c_size_t)]),
+    "krt_stream": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "krt_block_slot": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "krt_init_master": (C.c_int, [C.c_void_p]),
+    "krt_run_iteration": (C.c_int, [C.c_void_p, COMPUTE_CB, C.c_void_p]),
+    "krt_synchronize": (C.c_int, [C.c_void_p]),
+    "krt_trace_csv": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "krt_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "krt_read_master": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float), C.c_size_t]),
+    "krt_reduce_cast": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_int, C.c_size_t,
+                                  C.c_float, C.c_void_p]),
+    "krt_device_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_int, C.c_size_t, C.c_int, C.c_float, C.c_float, C.c_float,
+                                    C.c_float, C.c_float, C.c_float, C.c_int, C.c_void_p]),
+    "krt_host_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_int, C.c_size_t, C.c_int, C.c_float, C.c_float, C.c_float,
+                                  C.c_float, C.c_float, C.c_float, C.c_int, C.c_int]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libkrt.so once; raises if the in-tree build is missing."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the runtime has no Python fallback)")
+        handle = C.CDLL(os.fspath(LIB_PATH), mode=C.RTLD_GLOBAL)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(code: int):
+    if code != KRT_OK:
+        msg = lib().krt_last_error().decode("utf-8", "replace")
+        if code == KRT_INFEASIBLE:
+            raise InfeasiblePlanError(code, msg)
+        raise KrtError(code, msg)
+
+
+def take_string(ptr: C.c_void_p) -> str:
+    """Copy a malloc'ed C string returned through an out-pointer and free it."""
+    try:
+        return C.string_at(ptr.value).decode("utf-8")
+    finally:
+        lib().krt_string_free(ptr)

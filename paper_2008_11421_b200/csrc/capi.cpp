@@ -1,0 +1,300 @@
+// extern "C" boundary (include/krt.h).  Exceptions stop here: each entry
+// point maps them to a status code and a thread-local message.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "../../include/krt.h"
+#include "engine.hpp"
+#include "host_optim.hpp"
+#include "kernels.hpp"
+#include "runtime.hpp"
+
+using namespace krt;
+
+struct krt_plan {
+  Model model;
+  Hardware hw;
+  Plan plan;
+};
+
+struct krt_ctx {
+  std::unique_ptr<Runtime> rt;
+};
+
+namespace {
+thread_local std::string g_err;
+
+struct Infeasible : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.data(), s.size() + 1);
+  return p;
+}
+
+std::string jstr(const std::string& s) {
+  std::string o = "\"";
+  for (unsigned char c : s) {
+    switch (c) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\n': o += "\\n"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (c < 0x20) {
+          char b[8];
+          std::snprintf(b, sizeof b, "\\u%04x", c);
+          o += b;
+        } else {
+          o += (char)c;
+        }
+    }
+  }
+  return o + "\"";
+}
+
+std::string jnum(double v) { return py_float_repr(v); }
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return KRT_OK;
+  } catch (const Infeasible& e) {
+    g_err = e.what();
+    return KRT_INFEASIBLE;
+  } catch (const FormatError& e) {
+    g_err = e.what();
+    return KRT_USAGE;
+  } catch (const JsonError& e) {
+    g_err = e.what();
+    return KRT_USAGE;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return KRT_USAGE;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return KRT_USAGE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return KRT_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return KRT_INTERNAL;
+  }
+}
+
+std::string list_json(const std::vector<std::string>& v) {
+  std::string s = "[";
+  for (size_t i = 0; i < v.size(); ++i) s += (i ? ", " : "") + jstr(v[i]);
+  return s + "]";
+}
+}  // namespace
+
+extern "C" {
+
+const char* krt_last_error(void) { return g_err.c_str(); }
+const char* krt_version(void) { return "karma-b200 krt 0.1 (sm_100a)"; }
+void krt_string_free(char* s) { std::free(s); }
+
+int krt_plan_load(const char* model_text, const char* hw_text, const char* plan_json, krt_plan** out) {
+  return guard([&] {
+    if (!model_text || !hw_text || !plan_json || !out) throw std::invalid_argument("null argument");
+    auto p = std::make_unique<krt_plan>();
+    p->model = parse_model_text(model_text);
+    p->hw = parse_hardware_text(hw_text);
+    p->plan = plan_from_json_text(plan_json);
+    *out = p.release();
+  });
+}
+
+void krt_plan_free(krt_plan* p) { delete p; }
+
+int krt_plan_set_capacity(krt_plan* p, double cap) {
+  return guard([&] {
+    if (!p || !(cap > 0)) throw std::invalid_argument("capacity must be positive");
+    p->hw.capacity_bytes = cap;
+  });
+}
+
+int krt_plan_string(const krt_plan* p, char** out) {
+  return guard([&] { *out = dup(plan_string(p->plan)); });
+}
+
+int krt_plan_json(const krt_plan* p, char** out) {
+  return guard([&] { *out = dup(plan_to_json(p->plan)); });
+}
+
+int krt_plan_validate(const krt_plan* p, char** out, int* n) {
+  return guard([&] {
+    auto v = validate_plan(p->plan, p->model, p->hw);
+    if (n) *n = (int)v.size();
+    if (out) *out = dup(list_json(v));
+  });
+}
+
+int krt_plan_simulate(const krt_plan* p, int enforce, char** out) {
+  return guard([&] {
+    SimResult r = simulate(p->plan, p->model, p->hw, enforce != 0);
+    std::ostringstream os;
+    if (r.deadlock) {
+      os << "{\"deadlock\": " << list_json(r.blocked) << "}";
+    } else {
+      os << "{\"makespan\": " << jnum(r.makespan) << ", \"total_stall\": " << jnum(r.total_stall)
+         << ", \"peak_mem\": " << jnum(r.peak) << ", \"events\": [";
+      for (size_t i = 0; i < r.events.size(); ++i) {
+        auto& e = r.events[i];
+        auto& op = r.ops[e.op];
+        os << (i ? ", " : "") << "[" << jnum(e.t_start) << ", " << jnum(e.t_end) << ", \"" << res_name(e.res)
+           << "\", " << op.block << ", \"" << action_name(op.action) << "\", " << jnum(e.stall_before) << "]";
+      }
+      os << "], \"csv\": " << jstr(r.csv()) << "}";
+    }
+    *out = dup(os.str());
+  });
+}
+
+int krt_plan_simulate_dist(const krt_plan* p, const krt_dist_config* c, int iterations, char** out) {
+  return guard([&] {
+    if (!c) throw std::invalid_argument("null dist config");
+    DistConfig cfg;
+    cfg.workers = c->workers;
+    cfg.ring = c->ring != 0;
+    cfg.net_bw = c->net_bw;
+    cfg.net_latency = c->net_latency;
+    cfg.groups = c->groups;
+    if (cfg.workers < 1) throw std::invalid_argument("workers must be >= 1");
+    if (!(cfg.net_bw > 0)) throw std::invalid_argument("net_bw must be strictly positive");
+    if (cfg.net_latency < 0) throw std::invalid_argument("net_latency must be non-negative");
+    if (cfg.groups < 0) throw std::invalid_argument("groups must be >= 0 (0 = per block)");
+    DistResult r = simulate_distributed(p->plan, p->model, p->hw, cfg, iterations);
+    std::ostringstream os;
+    if (!r.error.empty() && r.events.empty()) {
+      os << "{\"error\": " << jstr(r.error) << "}";
+    } else {
+      os << "{";
+      if (!r.error.empty()) os << "\"error\": " << jstr(r.error) << ", ";
+      os << "\"iteration_time\": " << jnum(r.iteration_time) << ", \"iteration_times\": [";
+      for (size_t i = 0; i < r.iteration_times.size(); ++i) os << (i ? ", " : "") << jnum(r.iteration_times[i]);
+      os << "], \"exposed_comm\": " << jnum(r.exposed_comm) << ", \"peak_mem\": " << jnum(r.peak)
+         << ", \"makespan\": " << jnum(r.makespan) << ", \"events\": [";
+      for (size_t i = 0; i < r.events.size(); ++i) {
+        auto& e = r.events[i];
+        auto& op = r.ops[e.op];
+        int worker = e.res == R_NETWORK ? -1 : 0;
+        os << (i ? ", " : "") << "[" << worker << ", \"" << res_name(e.res) << "\", " << jnum(e.t_start) << ", "
+           << jnum(e.t_end) << ", \"" << action_name(op.action) << "\", " << op.block << ", " << op.group << ", "
+           << op.iteration << ", " << jnum(e.stall_before) << "]";
+      }
+      os << "]}";
+    }
+    *out = dup(os.str());
+  });
+}
+
+int krt_create(const krt_config* cfg, krt_ctx** out) {
+  return guard([&] {
+    if (!cfg || !out) throw std::invalid_argument("null argument");
+    auto c = std::make_unique<krt_ctx>();
+    c->rt = std::make_unique<Runtime>(*cfg);
+    *out = c.release();
+  });
+}
+
+int krt_destroy(krt_ctx* ctx) {
+  return guard([&] { delete ctx; });
+}
+
+int krt_register_block(krt_ctx* ctx, int block, size_t act_bytes, const int64_t* numel, int n) {
+  return guard([&] {
+    if (n > 0 && !numel) throw std::invalid_argument("null numel");
+    ctx->rt->register_block(block, act_bytes, numel, n);
+  });
+}
+
+int krt_prepare(krt_ctx* ctx, const krt_plan* plan) {
+  return guard([&] {
+    auto v = validate_plan(plan->plan, plan->model, plan->hw);
+    if (!v.empty()) throw Infeasible("plan rejected by validate_plan: " + v[0]);
+    ctx->rt->prepare(plan->plan, plan->model, plan->hw);
+  });
+}
+
+int krt_region(krt_ctx* ctx, int which, int block, void** ptr, size_t* bytes) {
+  return guard([&] { ctx->rt->region(which, block, ptr, bytes); });
+}
+
+int krt_stream(krt_ctx* ctx, int which, void** stream) {
+  return guard([&] { *stream = (void*)ctx->rt->stream(which); });
+}
+
+int krt_block_slot(krt_ctx* ctx, int block, void** slot) {
+  return guard([&] { *slot = ctx->rt->block_slot(block); });
+}
+
+int krt_init_master(krt_ctx* ctx) {
+  return guard([&] { ctx->rt->init_master(); });
+}
+
+int krt_run_iteration(krt_ctx* ctx, krt_compute_cb cb, void* user) {
+  return guard([&] {
+    if (!cb) throw std::invalid_argument("null compute callback");
+    ctx->rt->run_iteration(cb, user);
+  });
+}
+
+int krt_synchronize(krt_ctx* ctx) {
+  return guard([&] { ctx->rt->synchronize(); });
+}
+
+int krt_trace_csv(krt_ctx* ctx, char** out) {
+  return guard([&] { *out = dup(ctx->rt->trace_csv()); });
+}
+
+int krt_stats(krt_ctx* ctx, char** out) {
+  return guard([&] { *out = dup(ctx->rt->stats_json()); });
+}
+
+int krt_read_master(krt_ctx* ctx, int block, float* out, size_t numel) {
+  return guard([&] { ctx->rt->read_master(block, out, numel); });
+}
+
+int krt_reduce_cast(const float* const* in, int n_in, void* out, int out_dtype, size_t n, float scale,
+                    void* stream) {
+  return guard([&] {
+    cudaError_t e = launch_reduce_cast(in, n_in, out, out_dtype, n, scale, (cudaStream_t)stream);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("reduce_cast: ") + cudaGetErrorString(e));
+  });
+}
+
+int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,
+                      size_t n, int optimizer, float lr, float beta1, float beta2, float eps, float wd,
+                      float momentum, int step, void* stream) {
+  return guard([&] {
+    OptimScalars s = make_scalars(optimizer, lr, beta1, beta2, eps, wd, momentum, step, 1.0f);
+    cudaError_t e = launch_update(master, m, v, grad, weights, weight_dtype, n, s, (cudaStream_t)stream);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("device_update: ") + cudaGetErrorString(e));
+  });
+}
+
+int krt_host_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,
+                    size_t n, int optimizer, float lr, float beta1, float beta2, float eps, float wd,
+                    float momentum, int step, int threads) {
+  return guard([&] {
+    OptimScalars s = make_scalars(optimizer, lr, beta1, beta2, eps, wd, momentum, step, 1.0f);
+    std::unique_ptr<ThreadPool> pool;
+    if (threads > 1) pool = std::make_unique<ThreadPool>(threads);
+    host_update(pool.get(), master, m, v, grad, weights, weight_dtype, n, s);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// Op DAG + deterministic event engine: the execution semantics every plan
+// op obeys, shared by the schedule simulator, the DP pipeline model and the
+// executor's issue order / static arena assignment.
+//   simulator.py:67-135  run_engine      simulator.py:253-349 build_engine_ops
+//   simulator.py:364-399 simulate        planner.py:342-499  validate_plan
+//   distsim.py:140-266   simulate_distributed (5-stage DP pipeline)
+#pragma once
+#include <map>
+#include <string>
+#include <vector>
+
+#include "model.hpp"
+#include "plan.hpp"
+
+namespace krt {
+
+enum Res : int { R_COMPUTE = 0, R_XFER_IN, R_XFER_OUT, R_XFER, R_NETWORK, R_HOST, R_COUNT };
+const char* res_name(int r);
+
+struct EngineOp {
+  Action action = Action::FW;
+  int block = -1;       // -1 for group-level ops
+  int group = -1;       // DP group (1-based) or -1
+  int stage = -1;       // plan stage index (0-based) or -1
+  int iteration = 0;    // 0 = single-iteration simulate (no "iter" tag)
+  bool has_stage_tag = false;
+  int res = R_COMPUTE;
+  double duration = 0.0;
+  std::vector<int> deps;   // ops that must have completed
+  int gate = -1;           // op that must have started
+  double alloc = 0.0;      // bytes reserved at start
+  double free_end = 0.0;   // bytes released at end
+  std::string missing;     // unsatisfiable precondition
+  std::string tag() const; // simulator.py:159-167 _tag_str
+};
+
+struct EngineEvent {
+  int op = -1;
+  int res = 0;
+  double t_start = 0, t_end = 0, stall_before = 0;
+};
+
+struct EngineResult {
+  bool deadlock = false;
+  std::vector<std::string> blocked;   // DeadlockError.blocked
+  std::vector<EngineEvent> events;    // in op-index order (started ops only)
+  std::vector<int> start_order;       // op indices in the order they started
+  double peak = 0.0, makespan = 0.0;
+};
+
+EngineResult run_engine(const std::vector<EngineOp>& ops, const std::vector<int>& resources,
+                        double capacity, bool enforce);
+
+std::map<int, BlockCost> plan_costs(const Plan& p, const Model& g, const Hardware& hw);
+std::vector<EngineOp> build_engine_ops(const Plan& p, const Model& g, const Hardware& hw,
+                                       const std::map<int, BlockCost>& costs);
+std::vector<int> base_resources(const Hardware& hw);
+
+struct SimResult {
+  bool deadlock = false;
+  std::vector<std::string> blocked;
+  std::vector<EngineEvent> events;  // sorted by (t_start, resource name)
+  std::vector<EngineOp> ops;
+  double makespan = 0, total_stall = 0, peak = 0;
+  std::string csv() const;          // SimTrace.to_csv schema
+};
+SimResult simulate(const Plan& p, const Model& g, const Hardware& hw, bool enforce);
+
+std::vector<std::string> validate_plan(const Plan& p, const Model& g, const Hardware& hw);
+std::vector<std::string> residency_memory_walk(const Plan& p, const Model& g, const Hardware& hw,
+                                               double* peak_demand);
+
+// ---- data-parallel pipeline -------------------------------------------------
+struct DistConfig {
+  int workers = 1;
+  bool ring = true;
+  double net_bw = 12.5e9, net_latency = 0.0;
+  int groups = 0;  // 0 = one group per block
+};
+double allreduce_time(double bytes, const DistConfig& cfg);
+std::vector<std::vector<int>> assign_groups(int num_blocks, int groups);
+
+struct DistResult {
+  std::string error;                // deadlock / lower-bound failure text
+  std::vector<EngineEvent> events;  // sorted by (t_start, resource, block)
+  std::vector<EngineOp> ops;
+  std::vector<double> iteration_times;
+  double iteration_time = 0, exposed_comm = 0, peak = 0, makespan = 0;
+};
+// Builds the multi-iteration op list exactly as distsim.py:140-237.
+std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardware& hw,
+                                     const DistConfig& cfg, int iterations,
+                                     const std::map<int, BlockCost>& costs);
+DistResult simulate_distributed(const Plan& p, const Model& g, const Hardware& hw,
+                                const DistConfig& cfg, int iterations);
+
+}  // namespace krt

@@ -1,0 +1,914 @@
+#include "runtime.hpp"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace krt {
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+#define NK(call)                                                                                  \
+  do {                                                                                            \
+    ncclResult_t r_ = (call);                                                                     \
+    if (r_ != ncclSuccess) throw CudaError(std::string(#call) + ": " + ncclGetErrorString(r_));   \
+  } while (0)
+
+double host_now() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+size_t dtype_bytes(int dt) { return dt == KRT_BF16 ? 2 : 4; }
+
+}  // namespace
+
+Runtime::Runtime(const krt_config& cfg) : cfg_(cfg) {
+  world_ = std::max(1, cfg.world_size);
+  rank_ = cfg.rank;
+  if (rank_ < 0 || rank_ >= world_) throw std::invalid_argument("rank out of range");
+  if (cfg.weight_dtype != KRT_F32 && cfg.weight_dtype != KRT_BF16)
+    throw std::invalid_argument("weight_dtype must be KRT_F32 or KRT_BF16");
+  CK(cudaSetDevice(cfg.device));
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // compute at normal priority; copies and the collective at high priority so
+  // their short control work is never queued behind long kernels
+  CK(cudaStreamCreateWithPriority(&streams_[0], cudaStreamNonBlocking, lo));
+  for (int i = 1; i < 4; ++i) CK(cudaStreamCreateWithPriority(&streams_[i], cudaStreamNonBlocking, hi));
+  CK(cudaEventCreate(&ev_base_));
+  if (world_ > 1) {
+    if (!cfg.nccl_id) throw std::invalid_argument("world_size > 1 needs nccl_id");
+    ncclUniqueId id;
+    std::memcpy(&id, cfg.nccl_id, sizeof(id));
+    ncclComm_t comm;
+    NK(ncclCommInitRank(&comm, world_, id, rank_));
+    nccl_comm_ = comm;
+  }
+  int nt = cfg.host_threads;
+  if (nt <= 0) nt = std::max(1, (int)std::thread::hardware_concurrency() - 2);
+  pool_ = std::make_unique<ThreadPool>(nt);
+  host_thread_ = std::thread([this] { host_loop(); });
+}
+
+Runtime::~Runtime() {
+  {
+    std::lock_guard<std::mutex> lk(hmu_);
+    hstop_ = true;
+  }
+  hcv_.notify_all();
+  if (host_thread_.joinable()) host_thread_.join();
+  cudaSetDevice(cfg_.device);
+  for (auto s : streams_)
+    if (s) cudaStreamSynchronize(s);
+  if (nccl_comm_) ncclCommDestroy((ncclComm_t)nccl_comm_);
+  for (auto e : ev_start_) cudaEventDestroy(e);
+  for (auto e : ev_done_) cudaEventDestroy(e);
+  if (ev_base_) cudaEventDestroy(ev_base_);
+  cudaFree(d_arena_);
+  cudaFree(d_weights_);
+  cudaFree(d_grads_);
+  cudaFree(d_master_);
+  cudaFree(d_m_);
+  cudaFree(d_v_);
+  cudaFree(d_shard_);
+  cudaFreeHost(h_swap_);
+  cudaFreeHost(h_grad_);
+  cudaFreeHost(h_wstage_);
+  for (auto s : streams_)
+    if (s) cudaStreamDestroy(s);
+}
+
+void Runtime::register_block(int block, size_t act_bytes, const int64_t* numel, int n) {
+  if (prepared_) throw std::logic_error("register_block after prepare");
+  if (block < 1) throw std::invalid_argument("block ids start at 1");
+  BlockPhys b;
+  b.act_bytes = align_up(act_bytes);
+  for (int i = 0; i < n; ++i) {
+    if (numel[i] < 0) throw std::invalid_argument("negative numel");
+    b.numel.push_back(numel[i]);
+    b.n_params += numel[i];
+  }
+  blocks_[block] = b;
+}
+
+void* Runtime::d_weight(int64_t p_off) const {
+  return static_cast<uint8_t*>(d_weights_) + (size_t)p_off * dtype_bytes(cfg_.weight_dtype);
+}
+
+// ---------------------------------------------------------------------------
+// op DAG
+// ---------------------------------------------------------------------------
+void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw) {
+  auto costs = plan_costs(plan, model, hw);
+  std::vector<EngineOp> base = build_engine_ops(plan, model, hw, costs);
+  for (auto& e : base)
+    if (!e.missing.empty()) throw std::runtime_error(e.missing);
+
+  // --- static arena assignment from the base ledger (simulator.py:67-135) ---
+  EngineResult er = run_engine(base, base_resources(hw), hw.capacity_bytes, true);
+  if (er.deadlock) {
+    std::string s = "simulation deadlock; blocked ops: ";
+    for (size_t i = 0; i < er.blocked.size(); ++i) s += (i ? "; " : "") + er.blocked[i];
+    throw std::runtime_error(s);
+  }
+  ledger_peak_ = (size_t)er.peak;
+  std::map<int, int> cur;  // block -> live instance
+  std::vector<int> inst_of_alloc(base.size(), -1), inst_read(base.size(), -1);
+  for (size_t i = 0; i < base.size(); ++i) {
+    const EngineOp& e = base[i];
+    int b = e.block;
+    switch (e.action) {
+      case Action::FW:
+      case Action::RECOMPUTE_FW:
+      case Action::SWAP_IN: {
+        Instance in;
+        in.block = b;
+        in.bytes = blocks_.at(b).act_bytes;
+        in.alloc_op = (int)i;
+        inst_of_alloc[i] = (int)instances_.size();
+        cur[b] = (int)instances_.size();
+        instances_.push_back(in);
+        if (e.action == Action::FW && b >= 2 && plan.block(b - 1).recompute) {
+          auto it = cur.find(b - 1);
+          if (it != cur.end()) {  // recompute buffers discarded at the consumer's end
+            instances_[it->second].free_op = (int)i;
+            cur.erase(it);
+          }
+        }
+        break;
+      }
+      case Action::SWAP_OUT:
+      case Action::BW: {
+        auto it = cur.find(b);
+        if (it == cur.end()) throw std::runtime_error("block " + std::to_string(b) + " not resident");
+        inst_read[i] = it->second;
+        instances_[it->second].free_op = (int)i;
+        cur.erase(it);
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  // event times of the base simulation
+  std::vector<double> t_start(base.size(), 0), t_end(base.size(), 0);
+  for (auto& ev : er.events) {
+    t_start[ev.op] = ev.t_start;
+    t_end[ev.op] = ev.t_end;
+  }
+  // sweep: frees at t_end, allocs at t_start; at equal time frees first
+  struct Ev { double t; int kind; int order; int inst; };  // kind 0 free, 1 alloc
+  std::vector<Ev> evs;
+  std::vector<int> rank_of(base.size(), 0);
+  for (size_t k = 0; k < er.start_order.size(); ++k) rank_of[er.start_order[k]] = (int)k;
+  for (size_t k = 0; k < instances_.size(); ++k) {
+    auto& in = instances_[k];
+    evs.push_back({t_start[in.alloc_op], 1, rank_of[in.alloc_op], (int)k});
+    if (in.free_op >= 0) evs.push_back({t_end[in.free_op], 0, rank_of[in.free_op], (int)k});
+  }
+  std::sort(evs.begin(), evs.end(), [](const Ev& a, const Ev& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.kind != b.kind) return a.kind < b.kind;
+    return a.order < b.order;
+  });
+  std::map<size_t, size_t> free_list;  // off -> bytes (coalesced)
+  size_t top = 0;
+  std::vector<int> live(instances_.size(), 0);
+  std::vector<std::vector<int>> arena_deps(base.size());
+  // history of freed regions: (off, bytes, free_op)
+  struct Freed { size_t off, bytes; int free_op; };
+  std::vector<Freed> freed;
+  std::vector<int> pending_free(instances_.size(), 0);
+  for (size_t ei = 0; ei < evs.size(); ++ei) {
+    Ev ev = evs[ei];
+    auto& in = instances_[ev.inst];
+    if (ev.kind == 0 && !live[ev.inst]) {
+      pending_free[ev.inst] = 1;  // zero-length op: free right after its alloc
+      continue;
+    }
+    if (ev.kind == 0) {
+      live[ev.inst] = 0;
+      freed.push_back({in.off, in.bytes, in.free_op});
+      size_t off = in.off, len = in.bytes;
+      auto nx = free_list.lower_bound(off);
+      if (nx != free_list.end() && off + len == nx->first) {
+        len += nx->second;
+        nx = free_list.erase(nx);
+      }
+      if (nx != free_list.begin()) {
+        auto pv = std::prev(nx);
+        if (pv->first + pv->second == off) {
+          off = pv->first;
+          len += pv->second;
+          free_list.erase(pv);
+        }
+      }
+      if (off + len == top) top = off;
+      else free_list[off] = len;
+    } else {
+      // best fit among free holes, else bump the top
+      size_t need = in.bytes;
+      auto best = free_list.end();
+      for (auto it = free_list.begin(); it != free_list.end(); ++it)
+        if (it->second >= need && (best == free_list.end() || it->second < best->second)) best = it;
+      if (best != free_list.end()) {
+        in.off = best->first;
+        size_t rest = best->second - need;
+        free_list.erase(best);
+        if (rest) free_list[in.off + need] = rest;
+      } else {
+        in.off = top;
+        top += need;
+      }
+      arena_bytes_ = std::max(arena_bytes_, top);
+      live[ev.inst] = 1;
+      // every earlier user of these bytes must have completed its freeing op
+      std::set<int> deps;
+      for (auto& f : freed)
+        if (f.off < in.off + in.bytes && in.off < f.off + f.bytes && f.free_op >= 0) deps.insert(f.free_op);
+      for (int d : deps) arena_deps[in.alloc_op].push_back(d);
+      if (pending_free[ev.inst]) {
+        pending_free[ev.inst] = 0;
+        evs.insert(evs.begin() + ei + 1, Ev{ev.t, 0, ev.order, ev.inst});
+      }
+    }
+  }
+  if (arena_bytes_ == 0) arena_bytes_ = kAlign;
+
+  // --- executor op lists: DP pipeline around the base ops -------------------
+  auto groups = assign_groups(nb_, cfg_.dist_groups);
+  groups_.clear();
+  std::set<int> host_blocks;
+  if (world_ >= 2)
+    for (auto& b : plan.blocks) host_blocks.insert(b.id);
+  else
+    for (int b : plan.swapped_blocks()) host_blocks.insert(b);
+  for (auto& [id, bp] : blocks_) {
+    bp.host_path = host_blocks.count(id) > 0;
+    bp.swapped = false;
+  }
+  for (int b : plan.swapped_blocks()) blocks_.at(b).swapped = true;
+  int64_t off = 0;
+  int64_t pad = (int64_t)world_ * 64;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    GroupPhys g;
+    g.members = groups[gi];
+    g.p_lo = off;
+    int64_t n = 0;
+    for (int b : g.members) {
+      blocks_.at(b).p_off = off + n;
+      blocks_.at(b).group = (int)gi + 1;
+      n += blocks_.at(b).n_params;
+      g.host |= blocks_.at(b).host_path;
+    }
+    g.p_n = (n + pad - 1) / pad * pad;
+    g.shard_n = g.p_n / world_;
+    off += g.p_n;
+    groups_.push_back(g);
+  }
+  total_params_ = off;
+  // host state layout
+  host_elems_ = 0;
+  for (auto& g : groups_) {
+    g.host_off = host_elems_;
+    if (world_ >= 2) g.host_n = g.shard_n;
+    else {
+      g.host_n = 0;
+      for (int b : g.members)
+        if (blocks_.at(b).host_path) g.host_n += (blocks_.at(b).n_params + 63) / 64 * 64;
+    }
+    host_elems_ += g.host_n;
+  }
+
+  double swap_rate = hw.swap_throughput();
+  double net_rate = 700e9, host_rate = hw.host_update_rate;
+  auto make_list = [&](bool steady, std::vector<XOp>& out) {
+    out.clear();
+    std::map<int, int> weight_in_of;  // block -> op
+    if (steady) {
+      if (world_ >= 2) {
+        for (size_t gi = 0; gi < groups_.size(); ++gi) {
+          XOp x;
+          x.e.action = Action::WEIGHT_IN;
+          x.e.group = (int)gi + 1;
+          x.e.block = -1;
+          x.e.res = hw.duplex ? R_XFER_IN : R_XFER;
+          x.e.duration = groups_[gi].shard_n * dtype_bytes(cfg_.weight_dtype) / swap_rate;
+          x.prev_host_group = (int)gi + 1;
+          for (int b : groups_[gi].members) weight_in_of[b] = (int)out.size();
+          out.push_back(x);
+        }
+      } else {
+        for (int b : host_blocks) {
+          XOp x;
+          x.e.action = Action::WEIGHT_IN;
+          x.e.block = b;
+          x.e.group = blocks_.at(b).group;
+          x.e.res = hw.duplex ? R_XFER_IN : R_XFER;
+          x.e.duration = blocks_.at(b).n_params * dtype_bytes(cfg_.weight_dtype) / swap_rate;
+          x.prev_host_group = blocks_.at(b).group;
+          weight_in_of[b] = (int)out.size();
+          out.push_back(x);
+        }
+      }
+    }
+    int offset = (int)out.size();
+    std::map<int, int> bw_done;
+    for (size_t i = 0; i < base.size(); ++i) {
+      XOp x;
+      x.e = base[i];
+      for (auto& d : x.e.deps) d += offset;
+      if (x.e.gate >= 0) x.e.gate += offset;
+      for (int d : arena_deps[i]) x.e.deps.push_back(d + offset);
+      x.instance = inst_of_alloc[i];
+      x.reads_instance = inst_read[i];
+      if (x.e.action == Action::FW && weight_in_of.count(x.e.block)) x.e.deps.push_back(weight_in_of[x.e.block]);
+      if (x.e.action == Action::BW) bw_done[x.e.block] = (int)out.size();
+      out.push_back(x);
+    }
+    int out_res = hw.duplex ? R_XFER_OUT : R_XFER;
+    if (world_ >= 2) {
+      for (int gi = (int)groups_.size(); gi >= 1; --gi) {
+        auto& g = groups_[gi - 1];
+        XOp ex;
+        ex.e.action = Action::EXCHANGE;
+        ex.e.group = gi;
+        ex.e.block = -1;
+        ex.e.res = R_NETWORK;
+        ex.e.duration = g.p_n * 4.0 / net_rate;
+        for (int b : g.members) ex.e.deps.push_back(bw_done.at(b));
+        int ex_idx = (int)out.size();
+        out.push_back(ex);
+        XOp go;
+        go.e.action = Action::GRAD_OUT;
+        go.e.group = gi;
+        go.e.block = -1;
+        go.e.res = out_res;
+        go.e.duration = g.shard_n * 4.0 / swap_rate;
+        go.e.deps = {ex_idx};
+        int go_idx = (int)out.size();
+        out.push_back(go);
+        XOp hu;
+        hu.e.action = Action::HOST_UPDATE;
+        hu.e.group = gi;
+        hu.e.block = -1;
+        hu.e.res = R_HOST;
+        hu.e.duration = g.host_n / host_rate;
+        hu.e.deps = {go_idx};
+        out.push_back(hu);
+      }
+    } else {
+      std::map<int, int> go_of;
+      for (auto it = host_blocks.rbegin(); it != host_blocks.rend(); ++it) {
+        int b = *it;
+        XOp go;
+        go.e.action = Action::GRAD_OUT;
+        go.e.block = b;
+        go.e.group = blocks_.at(b).group;
+        go.e.res = out_res;
+        go.e.duration = blocks_.at(b).n_params * 4.0 / swap_rate;
+        go.e.deps = {bw_done.at(b)};
+        go_of[b] = (int)out.size();
+        out.push_back(go);
+      }
+      for (int gi = (int)groups_.size(); gi >= 1; --gi) {
+        auto& g = groups_[gi - 1];
+        if (!g.host) continue;
+        XOp hu;
+        hu.e.action = Action::HOST_UPDATE;
+        hu.e.group = gi;
+        hu.e.block = -1;
+        hu.e.res = R_HOST;
+        hu.e.duration = g.host_n / host_rate;
+        for (int b : g.members)
+          if (go_of.count(b)) hu.e.deps.push_back(go_of[b]);
+        out.push_back(hu);
+      }
+    }
+  };
+  make_list(false, ops_first_);
+  make_list(true, ops_steady_);
+  auto order_of = [&](std::vector<XOp>& ops, std::vector<int>& order) {
+    std::vector<EngineOp> eo;
+    for (auto& x : ops) eo.push_back(x.e);
+    auto res = base_resources(hw);
+    res.push_back(R_NETWORK);
+    res.push_back(R_HOST);
+    EngineResult r = run_engine(eo, res, hw.capacity_bytes, false);
+    if (r.deadlock) throw std::runtime_error("executor op DAG deadlocks: " + (r.blocked.empty() ? std::string() : r.blocked[0]));
+    order = r.start_order;
+  };
+  order_of(ops_first_, order_first_);
+  order_of(ops_steady_, order_steady_);
+}
+
+void Runtime::prepare(const Plan& plan, const Model& model, const Hardware& hw) {
+  if (prepared_) throw std::logic_error("prepare called twice");
+  nb_ = (int)plan.blocks.size();
+  for (auto& b : plan.blocks) {
+    auto it = blocks_.find(b.id);
+    if (it == blocks_.end()) throw std::invalid_argument("block " + std::to_string(b.id) + " not registered");
+    if ((double)it->second.act_bytes > b.swap_bytes + 0.5)
+      throw std::invalid_argument("block " + std::to_string(b.id) + " stores " + std::to_string(it->second.act_bytes) +
+                                  " B but the plan budgets " + py_g(b.swap_bytes) + " B");
+  }
+  if ((int)blocks_.size() != nb_) throw std::invalid_argument("registered blocks do not match the plan");
+  build_ops(plan, model, hw);
+  allocate();
+  prepared_ = true;
+}
+
+void Runtime::allocate() {
+  CK(cudaSetDevice(cfg_.device));
+  arena_bytes_ = align_up(arena_bytes_ + cfg_.arena_slack_bytes, (size_t)2 << 20);
+  CK(cudaMalloc(&d_arena_, arena_bytes_));
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  size_t np = (size_t)std::max<int64_t>(total_params_, 64);
+  CK(cudaMalloc(&d_weights_, np * wb));
+  CK(cudaMemset(d_weights_, 0, np * wb));
+  CK(cudaMalloc((void**)&d_grads_, np * 4));
+  CK(cudaMemset(d_grads_, 0, np * 4));
+  // device optimizer state for blocks that never take the host path (P = 1)
+  bool any_dev = false;
+  for (auto& [id, b] : blocks_) any_dev |= !b.host_path;
+  if (any_dev) {
+    if (cfg_.weight_dtype == KRT_BF16) {
+      CK(cudaMalloc((void**)&d_master_, np * 4));
+      CK(cudaMemset(d_master_, 0, np * 4));
+    }
+    CK(cudaMalloc((void**)&d_m_, np * 4));
+    CK(cudaMemset(d_m_, 0, np * 4));
+    CK(cudaMalloc((void**)&d_v_, np * 4));
+    CK(cudaMemset(d_v_, 0, np * 4));
+  }
+  if (world_ > 1) {
+    size_t ns = 0;
+    for (auto& g : groups_) ns += (size_t)g.shard_n;
+    CK(cudaMalloc((void**)&d_shard_, std::max<size_t>(ns, 64) * 4));
+  }
+  // pinned host: swap area + gradient landing + weight staging
+  h_swap_bytes_ = 0;
+  for (auto& [id, b] : blocks_)
+    if (b.swapped) {
+      b.host_swap_off = h_swap_bytes_;
+      h_swap_bytes_ += b.act_bytes;
+    }
+  if (h_swap_bytes_) CK(cudaHostAlloc((void**)&h_swap_, h_swap_bytes_, cudaHostAllocDefault));
+  size_t he = std::max<size_t>(host_elems_, 64);
+  CK(cudaHostAlloc((void**)&h_grad_, he * 4, cudaHostAllocDefault));
+  CK(cudaHostAlloc(&h_wstage_, he * wb, cudaHostAllocDefault));
+  h_master_.assign(he, 0.f);
+  h_m_.assign(he, 0.f);
+  h_v_.assign(he, 0.f);
+  size_t nev = std::max(ops_first_.size(), ops_steady_.size());
+  ev_start_.resize(nev);
+  ev_done_.resize(nev);
+  for (size_t i = 0; i < nev; ++i) {
+    CK(cudaEventCreate(&ev_start_[i]));
+    CK(cudaEventCreate(&ev_done_[i]));
+  }
+}
+
+void Runtime::region(int which, int block, void** ptr, size_t* bytes) {
+  if (!prepared_) throw std::logic_error("region before prepare");
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  switch (which) {
+    case KRT_REGION_WEIGHTS: {
+      auto& b = blocks_.at(block);
+      *ptr = d_weight(b.p_off);
+      *bytes = (size_t)b.n_params * wb;
+      return;
+    }
+    case KRT_REGION_GRADS: {
+      auto& b = blocks_.at(block);
+      *ptr = d_grad(b.p_off);
+      *bytes = (size_t)b.n_params * 4;
+      return;
+    }
+    case KRT_REGION_ARENA:
+      *ptr = d_arena_;
+      *bytes = arena_bytes_;
+      return;
+    case KRT_REGION_HOST_SWAP: {
+      auto& b = blocks_.at(block);
+      *ptr = b.swapped ? h_swap_ + b.host_swap_off : nullptr;
+      *bytes = b.swapped ? b.act_bytes : 0;
+      return;
+    }
+  }
+  throw std::invalid_argument("unknown region");
+}
+
+cudaStream_t Runtime::stream(int which) const {
+  if (which < 0 || which > 3) throw std::invalid_argument("stream index 0..3");
+  return streams_[which];
+}
+
+// host element offset of a block's state (P = 1 host path)
+static int64_t host_block_off(const std::map<int, BlockPhys>& blocks, const GroupPhys& g, int block) {
+  int64_t o = (int64_t)g.host_off;
+  for (int b : g.members) {
+    if (b == block) return o;
+    if (blocks.at(b).host_path) o += (blocks.at(b).n_params + 63) / 64 * 64;
+  }
+  return -1;
+}
+
+void Runtime::init_master() {
+  if (!prepared_) throw std::logic_error("init_master before prepare");
+  CK(cudaSetDevice(cfg_.device));
+  CK(cudaDeviceSynchronize());
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  std::vector<uint8_t> tmp;
+  auto fetch_f32 = [&](int64_t p_off, int64_t n, float* dst) {
+    tmp.resize((size_t)n * wb);
+    CK(cudaMemcpy(tmp.data(), d_weight(p_off), (size_t)n * wb, cudaMemcpyDeviceToHost));
+    if (cfg_.weight_dtype == KRT_BF16) {
+      const uint16_t* s = reinterpret_cast<const uint16_t*>(tmp.data());
+      for (int64_t i = 0; i < n; ++i) {
+        uint32_t u = (uint32_t)s[i] << 16;
+        std::memcpy(&dst[i], &u, 4);
+      }
+    } else {
+      std::memcpy(dst, tmp.data(), (size_t)n * 4);
+    }
+  };
+  std::fill(h_m_.begin(), h_m_.end(), 0.f);
+  std::fill(h_v_.begin(), h_v_.end(), 0.f);
+  for (auto& g : groups_) {
+    if (world_ >= 2) {
+      fetch_f32(g.p_lo + (int64_t)rank_ * g.shard_n, g.shard_n, h_master_.data() + g.host_off);
+    } else {
+      for (int b : g.members) {
+        auto& bp = blocks_.at(b);
+        if (!bp.host_path) continue;
+        int64_t ho = host_block_off(blocks_, g, b);
+        fetch_f32(bp.p_off, bp.n_params, h_master_.data() + ho);
+      }
+    }
+  }
+  if (d_m_) {
+    size_t np = (size_t)std::max<int64_t>(total_params_, 64);
+    CK(cudaMemset(d_m_, 0, np * 4));
+    CK(cudaMemset(d_v_, 0, np * 4));
+    if (d_master_) {
+      std::vector<float> f((size_t)total_params_);
+      fetch_f32(0, total_params_, f.data());
+      CK(cudaMemcpy(d_master_, f.data(), (size_t)total_params_ * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  step_ = 0;
+  last_first_ = true;
+}
+
+// ---------------------------------------------------------------------------
+// host update thread (the HOST resource, FIFO like run_engine's queue)
+// ---------------------------------------------------------------------------
+void Runtime::host_loop() {
+  for (;;) {
+    HostTask t;
+    {
+      std::unique_lock<std::mutex> lk(hmu_);
+      hcv_.wait(lk, [&] { return hstop_ || !hq_.empty(); });
+      if (hstop_ && hq_.empty()) return;
+      t = hq_.front();
+      hq_.pop_front();
+    }
+    double t0 = host_now();
+    std::string err;
+    try {
+      for (auto e : t.waits) CK(cudaEventSynchronize(e));
+      t0 = host_now();
+      run_host_task(t);
+    } catch (const std::exception& ex) {
+      err = ex.what();
+    }
+    double t1 = host_now();
+    {
+      std::lock_guard<std::mutex> lk(hmu_);
+      if (!err.empty() && host_error_.empty()) host_error_ = err;
+      host_done_step_[t.group] = t.step;
+      host_times_[{t.group, t.step}] = {t0, t1};
+    }
+    hcv_.notify_all();
+  }
+}
+
+void Runtime::run_host_task(const HostTask& t) {
+  auto& g = groups_.at((size_t)t.group - 1);
+  OptimScalars s = make_scalars(cfg_.optimizer, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps, cfg_.weight_decay,
+                                cfg_.momentum, t.step, world_ >= 2 ? cfg_.grad_scale : 1.0f);
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  auto stage_ptr = [&](size_t host_off) { return static_cast<uint8_t*>(h_wstage_) + host_off * wb; };
+  if (world_ >= 2) {
+    size_t o = g.host_off;
+    host_update(pool_.get(), h_master_.data() + o, h_m_.data() + o, h_v_.data() + o, h_grad_ + o, stage_ptr(o),
+                cfg_.weight_dtype, (size_t)g.host_n, s);
+  } else {
+    for (int b : g.members) {
+      auto& bp = blocks_.at(b);
+      if (!bp.host_path) continue;
+      size_t o = (size_t)host_block_off(blocks_, g, b);
+      host_update(pool_.get(), h_master_.data() + o, h_m_.data() + o, h_v_.data() + o, h_grad_ + o, stage_ptr(o),
+                  cfg_.weight_dtype, (size_t)bp.n_params, s);
+    }
+  }
+}
+
+void Runtime::wait_host_done(int group, int step) {
+  std::unique_lock<std::mutex> lk(hmu_);
+  hcv_.wait(lk, [&] {
+    auto it = host_done_step_.find(group);
+    return !host_error_.empty() || (it != host_done_step_.end() && it->second >= step);
+  });
+  if (!host_error_.empty()) throw std::runtime_error("host update failed: " + host_error_);
+}
+
+// ---------------------------------------------------------------------------
+// issue
+// ---------------------------------------------------------------------------
+void Runtime::wait_deps(cudaStream_t s, const XOp& x, const std::vector<XOp>& ops) {
+  (void)ops;
+  for (int d : x.e.deps) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
+  if (x.e.gate >= 0) CK(cudaStreamWaitEvent(s, ev_start_[x.e.gate], 0));
+}
+
+void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* user, int step) {
+  XOp& x = ops[idx];
+  const EngineOp& e = x.e;
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  switch (e.action) {
+    case Action::FW:
+    case Action::RECOMPUTE_FW:
+    case Action::BW: {
+      cudaStream_t s = streams_[0];
+      wait_deps(s, x, ops);
+      int inst = e.action == Action::BW ? x.reads_instance : x.instance;
+      auto& in = instances_.at(inst);
+      CK(cudaEventRecord(ev_start_[idx], s));
+      cur_slot_[e.block] = d_arena_ + in.off;
+      int rc = cb(user, (int)e.action, e.block, d_arena_ + in.off, in.bytes, (void*)s);
+      if (rc != 0)
+        throw std::runtime_error(std::string("compute callback failed for ") + action_name(e.action) + " block " +
+                                 std::to_string(e.block));
+      if (e.action == Action::BW) {
+        auto& bp = blocks_.at(e.block);
+        if (!bp.host_path && bp.n_params > 0) {
+          OptimScalars sc = make_scalars(cfg_.optimizer, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps,
+                                         cfg_.weight_decay, cfg_.momentum, step, 1.0f);
+          float* master = d_master_ ? d_master_ + bp.p_off : reinterpret_cast<float*>(d_weight(bp.p_off));
+          CK(launch_update(master, d_m_ + bp.p_off, d_v_ + bp.p_off, d_grad(bp.p_off), d_weight(bp.p_off),
+                           cfg_.weight_dtype, (size_t)bp.n_params, sc, s));
+          ++kernel_launches_;
+          ++iter_launches_;
+        }
+      }
+      CK(cudaEventRecord(ev_done_[idx], s));
+      return;
+    }
+    case Action::SWAP_OUT: {
+      cudaStream_t s = streams_[2];
+      wait_deps(s, x, ops);
+      auto& in = instances_.at(x.reads_instance);
+      auto& bp = blocks_.at(e.block);
+      CK(cudaEventRecord(ev_start_[idx], s));
+      CK(cudaMemcpyAsync(h_swap_ + bp.host_swap_off, d_arena_ + in.off, in.bytes, cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(ev_done_[idx], s));
+      iter_bytes_d2h_ += in.bytes;
+      return;
+    }
+    case Action::SWAP_IN: {
+      cudaStream_t s = streams_[1];
+      wait_deps(s, x, ops);
+      auto& in = instances_.at(x.instance);
+      auto& bp = blocks_.at(e.block);
+      CK(cudaEventRecord(ev_start_[idx], s));
+      CK(cudaMemcpyAsync(d_arena_ + in.off, h_swap_ + bp.host_swap_off, in.bytes, cudaMemcpyHostToDevice, s));
+      cur_slot_[e.block] = d_arena_ + in.off;
+      CK(cudaEventRecord(ev_done_[idx], s));
+      iter_bytes_h2d_ += in.bytes;
+      return;
+    }
+    case Action::GRAD_OUT: {
+      cudaStream_t s = streams_[2];
+      wait_deps(s, x, ops);
+      CK(cudaEventRecord(ev_start_[idx], s));
+      if (world_ >= 2) {
+        auto& g = groups_.at((size_t)e.group - 1);
+        size_t shard_pos = 0;
+        for (int gi = 0; gi < e.group - 1; ++gi) shard_pos += (size_t)groups_[gi].shard_n;
+        CK(cudaMemcpyAsync(h_grad_ + g.host_off, d_shard_ + shard_pos, (size_t)g.shard_n * 4,
+                           cudaMemcpyDeviceToHost, s));
+        iter_bytes_d2h_ += (size_t)g.shard_n * 4;
+      } else {
+        auto& bp = blocks_.at(e.block);
+        auto& g = groups_.at((size_t)bp.group - 1);
+        int64_t ho = host_block_off(blocks_, g, e.block);
+        CK(cudaMemcpyAsync(h_grad_ + ho, d_grad(bp.p_off), (size_t)bp.n_params * 4, cudaMemcpyDeviceToHost, s));
+        iter_bytes_d2h_ += (size_t)bp.n_params * 4;
+      }
+      CK(cudaEventRecord(ev_done_[idx], s));
+      return;
+    }
+    case Action::EXCHANGE: {
+      cudaStream_t s = streams_[3];
+      wait_deps(s, x, ops);
+      auto& g = groups_.at((size_t)e.group - 1);
+      size_t shard_pos = 0;
+      for (int gi = 0; gi < e.group - 1; ++gi) shard_pos += (size_t)groups_[gi].shard_n;
+      CK(cudaEventRecord(ev_start_[idx], s));
+      NK(ncclReduceScatter(d_grad(g.p_lo), d_shard_ + shard_pos, (size_t)g.shard_n, ncclFloat, ncclSum,
+                           (ncclComm_t)nccl_comm_, s));
+      CK(cudaEventRecord(ev_done_[idx], s));
+      bytes_net_ += (size_t)g.p_n * 4 * (world_ - 1) / world_;
+      return;
+    }
+    case Action::HOST_UPDATE: {
+      HostTask t;
+      t.op = idx;
+      t.group = e.group;
+      t.step = step;
+      for (int d : e.deps) t.waits.push_back(ev_done_[d]);
+      {
+        std::lock_guard<std::mutex> lk(hmu_);
+        hq_.push_back(t);
+      }
+      hcv_.notify_all();
+      return;
+    }
+    case Action::WEIGHT_IN: {
+      // the previous iteration's host update of this group must be complete
+      wait_host_done(x.prev_host_group, step - 1);
+      cudaStream_t s = streams_[1];
+      wait_deps(s, x, ops);
+      CK(cudaEventRecord(ev_start_[idx], s));
+      if (world_ >= 2) {
+        auto& g = groups_.at((size_t)e.group - 1);
+        void* dst = d_weight(g.p_lo + (int64_t)rank_ * g.shard_n);
+        CK(cudaMemcpyAsync(dst, static_cast<uint8_t*>(h_wstage_) + g.host_off * wb, (size_t)g.shard_n * wb,
+                           cudaMemcpyHostToDevice, s));
+        iter_bytes_h2d_ += (size_t)g.shard_n * wb;
+        // the all-gather rides the network stream behind the H2D
+        cudaStream_t ns = streams_[3];
+        CK(cudaEventRecord(ev_done_[idx], s));
+        CK(cudaStreamWaitEvent(ns, ev_done_[idx], 0));
+        NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
+                         cfg_.weight_dtype == KRT_BF16 ? ncclBfloat16 : ncclFloat, (ncclComm_t)nccl_comm_, ns));
+        CK(cudaEventRecord(ev_done_[idx], ns));
+        bytes_net_ += (size_t)g.p_n * wb * (world_ - 1) / world_;
+      } else {
+        auto& bp = blocks_.at(e.block);
+        auto& g = groups_.at((size_t)bp.group - 1);
+        int64_t ho = host_block_off(blocks_, g, e.block);
+        CK(cudaMemcpyAsync(d_weight(bp.p_off), static_cast<uint8_t*>(h_wstage_) + (size_t)ho * wb,
+                           (size_t)bp.n_params * wb, cudaMemcpyHostToDevice, s));
+        iter_bytes_h2d_ += (size_t)bp.n_params * wb;
+        CK(cudaEventRecord(ev_done_[idx], s));
+      }
+      return;
+    }
+  }
+}
+
+void Runtime::run_iteration(krt_compute_cb cb, void* user) {
+  if (!prepared_) throw std::logic_error("run_iteration before prepare");
+  CK(cudaSetDevice(cfg_.device));
+  {
+    std::lock_guard<std::mutex> lk(hmu_);
+    if (!host_error_.empty()) throw std::runtime_error("host update failed: " + host_error_);
+  }
+  int step = ++step_;
+  bool first = step == 1;
+  auto& ops = first ? ops_first_ : ops_steady_;
+  auto& order = first ? order_first_ : order_steady_;
+  iter_bytes_h2d_ = iter_bytes_d2h_ = iter_launches_ = 0;
+  cur_slot_.clear();
+  iter_host_t0_ = host_now();
+  CK(cudaEventRecord(ev_base_, streams_[0]));
+  for (int idx : order) issue(idx, ops, cb, user, step);
+  bytes_h2d_ += iter_bytes_h2d_;
+  bytes_d2h_ += iter_bytes_d2h_;
+  last_first_ = first;
+}
+
+void Runtime::synchronize() {
+  CK(cudaSetDevice(cfg_.device));
+  for (auto s : streams_) CK(cudaStreamSynchronize(s));
+  int step = step_;
+  for (size_t gi = 0; gi < groups_.size(); ++gi) {
+    bool has_host = false;
+    auto& ops = last_first_ ? ops_first_ : ops_steady_;
+    for (auto& x : ops)
+      if (x.e.action == Action::HOST_UPDATE && x.e.group == (int)gi + 1) has_host = true;
+    if (has_host && step > 0) wait_host_done((int)gi + 1, step);
+  }
+}
+
+std::string Runtime::trace_csv() {
+  synchronize();
+  auto& ops = last_first_ ? ops_first_ : ops_steady_;
+  std::ostringstream os;
+  os << "t_start,t_end,resource,block,action,group,stall_before\n";
+  struct Row { double t0, t1; int res; int op; };
+  std::vector<Row> rows;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    const EngineOp& e = ops[i].e;
+    double t0 = 0, t1 = 0;
+    if (e.action == Action::HOST_UPDATE) {
+      std::lock_guard<std::mutex> lk(hmu_);
+      auto it = host_times_.find({e.group, step_});
+      if (it == host_times_.end()) continue;
+      t0 = it->second.first - iter_host_t0_;
+      t1 = it->second.second - iter_host_t0_;
+    } else {
+      float ms0 = 0, ms1 = 0;
+      if (cudaEventElapsedTime(&ms0, ev_base_, ev_start_[i]) != cudaSuccess) continue;
+      if (cudaEventElapsedTime(&ms1, ev_base_, ev_done_[i]) != cudaSuccess) continue;
+      t0 = ms0 * 1e-3;
+      t1 = ms1 * 1e-3;
+    }
+    rows.push_back({t0, t1, e.res, (int)i});
+  }
+  std::stable_sort(rows.begin(), rows.end(), [](const Row& a, const Row& b) {
+    if (a.t0 != b.t0) return a.t0 < b.t0;
+    return std::string(res_name(a.res)) < std::string(res_name(b.res));
+  });
+  std::map<int, double> last_end;
+  for (auto& r : rows) {
+    const EngineOp& e = ops[r.op].e;
+    double stall = 0;
+    auto it = last_end.find(r.res);
+    if (it != last_end.end()) stall = std::max(0.0, r.t0 - it->second);
+    last_end[r.res] = std::max(r.t1, it != last_end.end() ? it->second : r.t1);
+    os << py_9g(r.t0) << "," << py_9g(r.t1) << "," << res_name(r.res) << "," << e.block << ","
+       << action_name(e.action) << "," << e.group << "," << py_9g(stall) << "\n";
+  }
+  return os.str();
+}
+
+std::string Runtime::stats_json() {
+  std::ostringstream os;
+  size_t nswapped = 0;
+  for (auto& [id, b] : blocks_) nswapped += b.swapped;
+  os << "{\"arena_bytes\": " << arena_bytes_ << ", \"ledger_peak_bytes\": " << ledger_peak_
+     << ", \"instances\": " << instances_.size() << ", \"host_swap_bytes\": " << h_swap_bytes_
+     << ", \"swapped_blocks\": " << nswapped << ", \"params\": " << total_params_
+     << ", \"host_elems\": " << host_elems_ << ", \"bytes_h2d_total\": " << bytes_h2d_
+     << ", \"bytes_d2h_total\": " << bytes_d2h_ << ", \"bytes_net_total\": " << bytes_net_
+     << ", \"iter_bytes_h2d\": " << iter_bytes_h2d_ << ", \"iter_bytes_d2h\": " << iter_bytes_d2h_
+     << ", \"kernel_launches_total\": " << kernel_launches_ << ", \"iter_kernel_launches\": " << iter_launches_
+     << ", \"ops_per_iteration\": " << ops_steady_.size() << ", \"step\": " << step_ << ", \"world\": " << world_
+     << ", \"groups\": " << groups_.size() << "}";
+  return os.str();
+}
+
+void* Runtime::block_slot(int block) const {
+  auto it = cur_slot_.find(block);
+  if (it == cur_slot_.end()) throw std::invalid_argument("block " + std::to_string(block) + " has no resident slot");
+  return it->second;
+}
+
+void Runtime::read_master(int block, float* out, size_t numel) {
+  synchronize();
+  auto& bp = blocks_.at(block);
+  if (numel < (size_t)bp.n_params) throw std::invalid_argument("output too small");
+  auto& g = groups_.at((size_t)bp.group - 1);
+  if (bp.host_path) {
+    if (world_ >= 2) {
+      int64_t lo = g.p_lo + (int64_t)rank_ * g.shard_n, hi = lo + g.shard_n;
+      for (int64_t i = 0; i < bp.n_params; ++i) {
+        int64_t p = bp.p_off + i;
+        out[i] = (p >= lo && p < hi) ? h_master_[g.host_off + (size_t)(p - lo)] : 0.f;
+      }
+    } else {
+      int64_t ho = host_block_off(blocks_, g, block);
+      std::memcpy(out, h_master_.data() + ho, (size_t)bp.n_params * 4);
+    }
+  } else {
+    const void* src = d_master_ ? (const void*)(d_master_ + bp.p_off) : d_weight(bp.p_off);
+    CK(cudaMemcpy(out, src, (size_t)bp.n_params * 4, cudaMemcpyDeviceToHost));
+  }
+}
+
+}  // namespace krt

@@ -1,0 +1,155 @@
+// Per-rank executor of a KARMA execution plan on one B200.
+//
+// The plan's ops (plan.py:24-29) and the DP pipeline ops (distsim.py:168-236)
+// become CUDA work on four streams — compute (fw / recompute_fw / bw),
+// H2D (swap_in, weight_in), D2H (swap_out, grad_out), network (exchange) —
+// plus a host-update thread.  Every dependency of build_engine_ops /
+// simulate_distributed is a cudaStreamWaitEvent; the start gate
+// (simulator.py:324-329) waits on an event recorded just before the gating
+// compute op; the capacity ledger (simulator.py:90) is realised by a static
+// arena assignment whose address reuse adds free->alloc event edges.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/krt.h"
+#include "engine.hpp"
+#include "host_optim.hpp"
+
+namespace krt {
+
+struct BlockPhys {
+  size_t act_bytes = 0;          // arena slot bytes
+  std::vector<int64_t> numel;    // parameter tensors
+  int64_t n_params = 0;
+  int64_t p_off = 0;             // element offset in the flat parameter space
+  bool host_path = false;
+  int group = 0;                 // 1-based
+  size_t host_swap_off = 0;
+  bool swapped = false;
+};
+
+struct GroupPhys {
+  std::vector<int> members;
+  int64_t p_lo = 0, p_n = 0;     // flat element range, padded to world*64
+  int64_t shard_n = 0;           // p_n / world
+  bool host = false;             // any member on the host path
+  size_t host_off = 0;           // offset (elements) of this group's host state
+  int64_t host_n = 0;            // host elements (shard for P>1, host members for P=1)
+};
+
+// executor op: an engine op plus the physical bindings
+struct XOp {
+  EngineOp e;
+  int instance = -1;             // arena instance allocated (fw/recompute/swap_in)
+  int reads_instance = -1;       // instance read by bw / swap_out
+  std::vector<int> arena_deps;   // ops whose completion frees our region
+  int prev_host_group = -1;      // weight_in: host_update of the previous iteration
+};
+
+struct Instance {
+  int block = 0;
+  size_t off = 0, bytes = 0;
+  int alloc_op = -1, free_op = -1;
+};
+
+struct HostTask {
+  int op = -1;
+  int group = 0;
+  std::vector<cudaEvent_t> waits;
+  int step = 0;
+};
+
+class Runtime {
+ public:
+  explicit Runtime(const krt_config& cfg);
+  ~Runtime();
+
+  void register_block(int block, size_t act_bytes, const int64_t* numel, int n);
+  void prepare(const Plan& plan, const Model& model, const Hardware& hw);
+  void region(int which, int block, void** ptr, size_t* bytes);
+  cudaStream_t stream(int which) const;
+  void init_master();
+  void run_iteration(krt_compute_cb cb, void* user);
+  void synchronize();
+  std::string trace_csv();
+  std::string stats_json();
+  void read_master(int block, float* out, size_t numel);
+  void* block_slot(int block) const;
+
+ private:
+  void build_ops(const Plan& plan, const Model& model, const Hardware& hw);
+  void assign_arena(const Plan& plan, const Model& model, const Hardware& hw);
+  void allocate();
+  void issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* user, int step);
+  void wait_deps(cudaStream_t s, const XOp& x, const std::vector<XOp>& ops);
+  void host_loop();
+  void run_host_task(const HostTask& t);
+  void wait_host_done(int group, int step);
+  float* d_grad(int64_t p_off) const { return d_grads_ + p_off; }
+  void* d_weight(int64_t p_off) const;
+
+  krt_config cfg_;
+  int world_ = 1, rank_ = 0;
+  std::map<int, BlockPhys> blocks_;
+  std::vector<GroupPhys> groups_;     // index = group-1
+  int nb_ = 0;
+  int64_t total_params_ = 0;
+
+  std::vector<XOp> ops_first_, ops_steady_;
+  std::vector<int> order_first_, order_steady_;
+  std::vector<Instance> instances_;
+  size_t arena_bytes_ = 0, ledger_peak_ = 0;
+  std::vector<size_t> instance_off_;
+
+  // memory
+  uint8_t* d_arena_ = nullptr;
+  void* d_weights_ = nullptr;
+  float* d_grads_ = nullptr;
+  float* d_master_ = nullptr;   // device-path masters (bf16 weights only)
+  float* d_m_ = nullptr;
+  float* d_v_ = nullptr;
+  float* d_shard_ = nullptr;    // reduce-scatter landing (P>1)
+  uint8_t* h_swap_ = nullptr;
+  size_t h_swap_bytes_ = 0;
+  float* h_grad_ = nullptr;     // pinned, host_n per group
+  void* h_wstage_ = nullptr;    // pinned weight copies for weight_in
+  std::vector<float> h_master_, h_m_, h_v_;
+  size_t host_elems_ = 0;
+
+  cudaStream_t streams_[4] = {};
+  std::vector<cudaEvent_t> ev_start_, ev_done_;
+  cudaEvent_t ev_base_ = nullptr;
+  void* nccl_comm_ = nullptr;
+
+  // host-update thread
+  std::unique_ptr<ThreadPool> pool_;
+  std::thread host_thread_;
+  std::mutex hmu_;
+  std::condition_variable hcv_;
+  std::deque<HostTask> hq_;
+  std::map<int, int> host_done_step_;   // group -> last completed iteration
+  std::map<std::pair<int, int>, std::pair<double, double>> host_times_;  // (group,step) -> t0,t1
+  std::string host_error_;
+  bool hstop_ = false;
+  double iter_host_t0_ = 0.0;
+
+  std::map<int, uint8_t*> cur_slot_;   // block -> resident slot during issue
+  int step_ = 0;
+  bool prepared_ = false;
+  bool last_first_ = true;
+  // stats
+  uint64_t bytes_h2d_ = 0, bytes_d2h_ = 0, bytes_net_ = 0, kernel_launches_ = 0;
+  uint64_t iter_bytes_h2d_ = 0, iter_bytes_d2h_ = 0, iter_launches_ = 0;
+};
+
+}  // namespace krt
