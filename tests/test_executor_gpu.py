@@ -1,0 +1,156 @@
+"""GPU parity of the executor (libkrt) against the CPU oracle and against
+itself in-core.  Every call goes through the C ABI (include/krt.h)."""
+import ctypes as C
+import json
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fc_chain_oracle as orc
+from paper_2008_11421_b200 import _lib
+from paper_2008_11421_b200.executor import ExecConfig, Executor
+from paper_2008_11421_b200.plan import PlanBundle, simulate
+from paper_2008_11421_b200.units import FCUnit, mse_zero_loss
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-5, 1e-6   # fp32 tolerance vs the numpy oracle (stated in DESIGN.md)
+
+
+def cfg0_case(sched_cases):
+    return next(c for c in sched_cases if c["name"] == "cfg0_fc_chain")
+
+
+def incore_plan(nb: int) -> dict:
+    """Everything resident: F1..Fn then Bn..B1 (the in-core schedule)."""
+    stages = [{"id": i + 1, "duration": 0.0, "ops": [["fw", i + 1]]} for i in range(nb)]
+    stages += [{"id": nb + i + 1, "duration": 0.0, "ops": [["bw", nb - i]]} for i in range(nb)]
+    return {"strategy": "capacity", "predicted_makespan": 0.0, "theta": None,
+            "blocks": [{"id": i + 1, "layers": [i + 1, i + 1], "swap_bytes": 16896.0,
+                        "recompute": False, "checkpoint": True} for i in range(nb)],
+            "stages": stages}
+
+
+def run_fc(bundle, optimizer, lr, iterations=3, batch=2, w0=None, rank=0):
+    units = [FCUnit(64, 64) for _ in range(6)]
+    ex = Executor(units, bundle, batch=batch, loss_fn=mse_zero_loss,
+                  cfg=ExecConfig(optimizer=optimizer, lr=lr))
+    w0 = w0 if w0 is not None else orc.init_weights()
+    ex.load_weights({i + 1: [torch.from_numpy(w)] for i, w in enumerate(w0)})
+    losses = []
+    for it in range(1, iterations + 1):
+        x = torch.from_numpy(orc.inputs(rank, it, batch)).cuda()
+        losses.append(float(ex.step(x)))
+    ex.synchronize()
+    w = ex.unit_weights()
+    trace = ex.trace_csv()
+    stats = ex.stats()
+    ex.close()
+    return losses, [w[i + 1][0].cpu().numpy() for i in range(6)], trace, stats
+
+
+@pytest.mark.parametrize("optimizer,lr", [("sgd", 1e-2), ("adam", 1e-3)])
+def test_cfg0_golden_plan_matches_oracle(sched_cases, optimizer, lr):
+    c = cfg0_case(sched_cases)
+    b = PlanBundle(c["model"], c["hardware"], c["plan"])
+    losses, ws, trace, stats = run_fc(b, optimizer, lr)
+    ref_losses, ref_w = orc.train(workers=1, iterations=3, optimizer=optimizer, lr=lr)
+    np.testing.assert_allclose(losses, [l[0] for l in ref_losses], rtol=RTOL)
+    for g, r in zip(ws, ref_w):
+        np.testing.assert_allclose(g, r, rtol=RTOL, atol=ATOL)
+    # blocks 1 and 3 are swapped: their activations crossed PCIe both ways,
+    # and (P = 1) their gradients/weights took the host path
+    assert stats["swapped_blocks"] == 2
+    assert stats["iter_bytes_d2h"] == 2 * 512 + 2 * 64 * 64 * 4
+    assert stats["iter_bytes_h2d"] == 2 * 512 + 2 * 64 * 64 * 4
+
+
+@pytest.mark.parametrize("optimizer,lr", [("sgd", 1e-2), ("adam", 1e-3)])
+def test_out_of_core_equals_in_core_bitwise(sched_cases, optimizer, lr):
+    c = cfg0_case(sched_cases)
+    ooc = run_fc(PlanBundle(c["model"], c["hardware"], c["plan"]), optimizer, lr, iterations=4)
+    inc_bundle = PlanBundle(c["model"], c["hardware"], incore_plan(6)).set_capacity(1e9)
+    inc = run_fc(inc_bundle, optimizer, lr, iterations=4)
+    assert ooc[0] == inc[0]
+    for a, b in zip(ooc[1], inc[1]):
+        assert np.array_equal(a, b)
+    assert inc[3]["iter_bytes_h2d"] == 0 and inc[3]["iter_bytes_d2h"] == 0
+
+
+def test_trace_follows_simulated_queue_order(sched_cases):
+    """Per resource, the executor runs the plan's ops in run_engine's FIFO order
+    (simulator.py:67-135) and never starts a swap before its gating compute."""
+    c = cfg0_case(sched_cases)
+    b = PlanBundle(c["model"], c["hardware"], c["plan"])
+    _, _, trace, _ = run_fc(b, "sgd", 1e-2, iterations=2)
+    sim = b.simulate()
+    rows = [r.split(",") for r in trace.strip().splitlines()[1:]]
+    for res in ("compute", "xfer_in", "xfer_out"):
+        want = [(e[4], e[3]) for e in sim["events"] if e[2] == res]
+        got = [(r[4], int(r[3])) for r in rows if r[2] == res and r[4] in
+               ("fw", "bw", "recompute_fw", "swap_in", "swap_out")]
+        assert got == want, res
+    # start gate: S1out may not start before F2 started, S3in not before B6
+    t = {(r[4], int(r[3])): (float(r[0]), float(r[1])) for r in rows}
+    assert t[("swap_out", 1)][0] >= t[("fw", 2)][0] - 1e-6
+    assert t[("swap_in", 3)][0] >= t[("bw", 6)][0] - 1e-6
+    assert t[("bw", 3)][0] >= t[("swap_in", 3)][1] - 1e-6
+
+
+def test_host_and_device_update_bitwise():
+    n = 1 << 16
+    g = torch.Generator().manual_seed(3)
+    p0 = torch.randn(n, generator=g)
+    grad = torch.randn(n, generator=g)
+    L = _lib.lib()
+    for opt, (lr, mom, wd) in ((_lib.ADAM, (1e-3, 0.0, 0.01)), (_lib.SGD, (1e-2, 0.9, 0.0))):
+        hp, hm, hv = p0.clone(), torch.zeros(n), torch.zeros(n)
+        hw = torch.empty(n, dtype=torch.bfloat16)
+        dp, dm, dv = p0.cuda(), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+        dw = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        dg = grad.cuda()
+        for step in (1, 2, 3):
+            _lib.check(L.krt_host_update(hp.data_ptr(), hm.data_ptr(), hv.data_ptr(), grad.data_ptr(),
+                                         hw.data_ptr(), _lib.BF16, n, opt, lr, 0.9, 0.999, 1e-8, wd, mom,
+                                         step, 4))
+            _lib.check(L.krt_device_update(dp.data_ptr(), dm.data_ptr(), dv.data_ptr(), dg.data_ptr(),
+                                           dw.data_ptr(), _lib.BF16, n, opt, lr, 0.9, 0.999, 1e-8, wd,
+                                           mom, step, None))
+        torch.cuda.synchronize()
+        assert torch.equal(hp, dp.cpu())
+        assert torch.equal(hw, dw.cpu())
+        if opt == _lib.ADAM:
+            ref = p0.clone().requires_grad_(True)
+            o = torch.optim.Adam([ref], lr=lr, weight_decay=wd, foreach=False)
+            for _ in range(3):
+                ref.grad = grad.clone()
+                o.step()
+            torch.testing.assert_close(hp, ref.detach(), rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("n_in,dtype", [(1, _lib.F32), (4, _lib.F32), (3, _lib.BF16)])
+def test_reduce_cast_kernel(n_in, dtype):
+    n = (1 << 20) + 7
+    ins = [torch.randn(n, device="cuda") for _ in range(n_in)]
+    out = torch.empty(n, device="cuda", dtype=torch.float32 if dtype == _lib.F32 else torch.bfloat16)
+    ptrs = (C.c_void_p * n_in)(*[t.data_ptr() for t in ins])
+    _lib.check(_lib.lib().krt_reduce_cast(ptrs, n_in, out.data_ptr(), dtype, n, 0.5, None))
+    torch.cuda.synchronize()
+    ref = ins[0].clone()
+    for t in ins[1:]:
+        ref = ref + t
+    ref = ref * 0.5
+    if dtype == _lib.F32:
+        assert torch.equal(out, ref)
+    else:
+        assert torch.equal(out, ref.to(torch.bfloat16))
+
+
+def test_rejects_invalid_plan(sched_cases):
+    c = cfg0_case(sched_cases)
+    bad = next(p for p in c["perturbed"] if p["violations"])
+    b = PlanBundle(c["model"], c["hardware"], bad["plan"])
+    with pytest.raises(_lib.InfeasiblePlanError):
+        Executor([FCUnit(64, 64) for _ in range(6)], b, batch=2, loss_fn=mse_zero_loss)
