@@ -153,6 +153,11 @@ int krt_run_iteration(krt_ctx* ctx, krt_compute_cb cb, void* user);
 /* Wait for all device streams and host updates of the last iteration. */
 int krt_synchronize(krt_ctx* ctx);
 
+/* Wait for the last iteration, then return every host-updated weight to the
+ * device copy now (the weight_in the next iteration would do), so the device
+ * weights equal the masters — for evaluation and checkpoints. */
+int krt_flush_weights(krt_ctx* ctx);
+
 /* Measured trace of the last iteration in the SimTrace CSV schema
  * (simulator.py:225-230) extended with the DP ops; caller frees. */
 int krt_trace_csv(krt_ctx* ctx, char** out);

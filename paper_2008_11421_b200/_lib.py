@@ -74,6 +74,7 @@ EXPORTS = {
     "krt_init_master": (C.c_int, [C.c_void_p]),
     "krt_run_iteration": (C.c_int, [C.c_void_p, COMPUTE_CB, C.c_void_p]),
     "krt_synchronize": (C.c_int, [C.c_void_p]),
+    "krt_flush_weights": (C.c_int, [C.c_void_p]),
     "krt_trace_csv": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_read_master": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float), C.c_size_t]),
@@ -97,7 +98,10 @@ def lib():
         if not LIB_PATH.exists():
             raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                               "(the runtime has no Python fallback)")
-        handle = C.CDLL(os.fspath(LIB_PATH), mode=C.RTLD_GLOBAL)
+        # torch first: its bundled libnccl.so.2 (newer than the system one) must
+        # be the copy the process resolves; libkrt links NCCL by soname.
+        import torch  # noqa: F401
+        handle = C.CDLL(os.fspath(LIB_PATH))
         for name, (res, args) in EXPORTS.items():
             fn = getattr(handle, name)
             fn.restype = res

@@ -256,6 +256,10 @@ int krt_synchronize(krt_ctx* ctx) {
   return guard([&] { ctx->rt->synchronize(); });
 }
 
+int krt_flush_weights(krt_ctx* ctx) {
+  return guard([&] { ctx->rt->flush_weights(); });
+}
+
 int krt_trace_csv(krt_ctx* ctx, char** out) {
   return guard([&] { *out = dup(ctx->rt->trace_csv()); });
 }

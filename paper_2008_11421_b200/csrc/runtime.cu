@@ -883,6 +883,31 @@ std::string Runtime::stats_json() {
   return os.str();
 }
 
+void Runtime::flush_weights() {
+  synchronize();
+  if (step_ == 0) return;
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  cudaStream_t s = streams_[1];
+  for (auto& g : groups_) {
+    if (world_ >= 2) {
+      void* dst = d_weight(g.p_lo + (int64_t)rank_ * g.shard_n);
+      CK(cudaMemcpyAsync(dst, static_cast<uint8_t*>(h_wstage_) + g.host_off * wb, (size_t)g.shard_n * wb,
+                         cudaMemcpyHostToDevice, s));
+      NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
+                       cfg_.weight_dtype == KRT_BF16 ? ncclBfloat16 : ncclFloat, (ncclComm_t)nccl_comm_, s));
+    } else {
+      for (int b : g.members) {
+        auto& bp = blocks_.at(b);
+        if (!bp.host_path) continue;
+        int64_t ho = host_block_off(blocks_, g, b);
+        CK(cudaMemcpyAsync(d_weight(bp.p_off), static_cast<uint8_t*>(h_wstage_) + (size_t)ho * wb,
+                           (size_t)bp.n_params * wb, cudaMemcpyHostToDevice, s));
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
 void* Runtime::block_slot(int block) const {
   auto it = cur_slot_.find(block);
   if (it == cur_slot_.end()) throw std::invalid_argument("block " + std::to_string(block) + " has no resident slot");

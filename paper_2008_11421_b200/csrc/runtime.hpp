@@ -85,6 +85,7 @@ class Runtime {
   std::string stats_json();
   void read_master(int block, float* out, size_t numel);
   void* block_slot(int block) const;
+  void flush_weights();
 
  private:
   void build_ops(const Plan& plan, const Model& model, const Hardware& hw);

@@ -231,9 +231,13 @@ class Executor:
                                               C.cast(out.data_ptr(), C.POINTER(C.c_float)), n))
         return out[:n]
 
+    def flush_weights(self):
+        """Return host-updated weights to the device now (krt_flush_weights)."""
+        _lib.check(_lib.lib().krt_flush_weights(self._ctx))
+
     def unit_weights(self) -> dict:
-        """Current device weights per unit (after synchronize)."""
-        self.synchronize()
+        """Current weights per unit, host-path updates included."""
+        self.flush_weights()
         return {ui: [p.detach().clone() for p in ps] for ui, ps in self.params.items()}
 
     # ------------------------------------------------------------------ compute

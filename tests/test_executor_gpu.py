@@ -44,8 +44,8 @@ def run_fc(bundle, optimizer, lr, iterations=3, batch=2, w0=None, rank=0):
         x = torch.from_numpy(orc.inputs(rank, it, batch)).cuda()
         losses.append(float(ex.step(x)))
     ex.synchronize()
-    w = ex.unit_weights()
     trace = ex.trace_csv()
+    w = ex.unit_weights()
     stats = ex.stats()
     ex.close()
     return losses, [w[i + 1][0].cpu().numpy() for i in range(6)], trace, stats
@@ -92,10 +92,13 @@ def test_trace_follows_simulated_queue_order(sched_cases):
         got = [(r[4], int(r[3])) for r in rows if r[2] == res and r[4] in
                ("fw", "bw", "recompute_fw", "swap_in", "swap_out")]
         assert got == want, res
-    # start gate: S1out may not start before F2 started, S3in not before B6
+    # start gate (simulator.py:324-329): a transfer waits until every compute op
+    # of an earlier stage has started — S1out (stage F2||S1out) after F1, S3in
+    # (stage B6||S3in) after F6, S1in (stage B4||S1in) after recompute F4
     t = {(r[4], int(r[3])): (float(r[0]), float(r[1])) for r in rows}
-    assert t[("swap_out", 1)][0] >= t[("fw", 2)][0] - 1e-6
-    assert t[("swap_in", 3)][0] >= t[("bw", 6)][0] - 1e-6
+    assert t[("swap_out", 1)][0] >= t[("fw", 1)][1] - 1e-6      # dep: F1 done
+    assert t[("swap_in", 3)][0] >= t[("fw", 6)][0] - 1e-6
+    assert t[("swap_in", 1)][0] >= t[("recompute_fw", 4)][0] - 1e-6
     assert t[("bw", 3)][0] >= t[("swap_in", 3)][1] - 1e-6
 
 
