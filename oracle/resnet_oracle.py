@@ -1,0 +1,62 @@
+"""TEST INFRASTRUCTURE ONLY — torch CPU fp32 in-core reference for the
+bottleneck-ResNet units (cfg1/cfg2 model family).
+
+A plain autograd model (conv / batch-stat BatchNorm / ReLU / residual add,
+stride on the 3x3 conv) rebuilt from the same parameter tensors the executor
+holds (its conv weights are stored O-H-W-I; converted here to O-I-H-W).  The
+reference has no tensor code (numerics parity unpinned); this is
+the in-core result the out-of-core executor must reproduce.
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+EPS = 1e-5
+
+
+def _w(t):
+    return t.permute(0, 3, 1, 2).contiguous() if t.dim() == 4 else t
+
+
+def _bn(x, g, b):
+    return F.batch_norm(x, None, None, g, b, training=True, momentum=0.0, eps=EPS)
+
+
+def forward(units, params, x):
+    """params: unit index (1-based) -> list of fp32 CPU tensors requiring grad."""
+    from paper_2008_11421_b200.units import BottleneckUnit, HeadUnit, StemUnit
+    h = x
+    for k, u in enumerate(units, start=1):
+        p = params[k]
+        if isinstance(u, StemUnit):
+            h = F.conv2d(h, _w(p[0]), stride=2, padding=3)
+            h = F.relu(_bn(h, p[1], p[2]))
+            h = F.max_pool2d(h, 3, 2, 1)
+        elif isinstance(u, BottleneckUnit):
+            o = F.relu(_bn(F.conv2d(h, _w(p[0])), p[1], p[2]))
+            o = F.relu(_bn(F.conv2d(o, _w(p[3]), stride=u.s, padding=1), p[4], p[5]))
+            o = _bn(F.conv2d(o, _w(p[6])), p[7], p[8])
+            idn = _bn(F.conv2d(h, _w(p[9]), stride=u.s), p[10], p[11]) if u.down else h
+            h = F.relu(o + idn)
+        elif isinstance(u, HeadUnit):
+            h = h.mean(dim=(2, 3)) @ p[0].t() + p[1]
+        else:
+            raise TypeError(type(u))
+    return h
+
+
+def train(units, init, inputs, targets, lr=0.1, optimizer="sgd"):
+    """In-core fp32 training: returns (losses, final params)."""
+    params = {k: [t.detach().clone().float().requires_grad_(True) for t in ts] for k, ts in init.items()}
+    flat = [t for k in sorted(params) for t in params[k]]
+    opt = (torch.optim.SGD(flat, lr=lr, foreach=False) if optimizer == "sgd"
+           else torch.optim.Adam(flat, lr=lr, foreach=False))
+    losses = []
+    for x, y in zip(inputs, targets):
+        opt.zero_grad(set_to_none=True)
+        loss = F.cross_entropy(forward(units, params, x.float()), y)
+        loss.backward()
+        opt.step()
+        losses.append(float(loss))
+    return losses, {k: [t.detach() for t in ts] for k, ts in params.items()}

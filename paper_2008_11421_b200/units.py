@@ -78,3 +78,329 @@ def model_text(units, batch, analytic=False) -> str:
     for i, u in enumerate(units, start=1):
         lines.append(u.ir_line(i, batch, analytic) if analytic else u.ir_line(i, batch))
     return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------------------
+# ResNet (bottleneck, [3, 24, 36, 3] = ResNet-200; stride on the 3x3 conv)
+# Activations bf16 NHWC (channels_last); BN statistics fp32.  Each conv's
+# output is saved once; BN-apply/ReLU are recomputed inside backward from the
+# saved conv output and the BN statistics (elementwise, HBM-bound).
+# ---------------------------------------------------------------------------
+_aten = torch.ops.aten
+BN_EPS = 1e-5
+
+
+def _cl(t):
+    """NHWC storage -> NCHW logical tensor with channels_last strides."""
+    return t.permute(0, 3, 1, 2)
+
+
+def _conv(x, w, stride, pad):
+    return _aten.convolution(x, w, None, [stride, stride], [pad, pad], [1, 1], False, [0, 0], 1)
+
+
+def _conv_bw(dy, x, w, stride, pad, need_dx=True):
+    return _aten.convolution_backward(dy, x, w, None, [stride, stride], [pad, pad], [1, 1], False,
+                                      [0, 0], 1, [need_dx, True, False])
+
+
+def _bn_fw(c, g, b):
+    return _aten.native_batch_norm(c, g, b, None, None, True, 0.0, BN_EPS)
+
+
+def _bn_apply(c, g, b, m, i):
+    return _aten.batch_norm_elemt(c, g, b, m, i, BN_EPS)
+
+
+def _bn_bw(dy, c, g, m, i):
+    return _aten.native_batch_norm_backward(dy, c, g, None, None, m, i, True, BN_EPS,
+                                            [True, True, True])
+
+
+def _kaiming(shape_ohwi, gen):
+    fan_in = shape_ohwi[1] * shape_ohwi[2] * shape_ohwi[3]
+    return torch.randn(shape_ohwi, generator=gen) * math.sqrt(2.0 / fan_in)
+
+
+class _ConvNetUnit(Unit):
+    act = torch.bfloat16
+
+    def _ir(self, lid, batch, kind_fields):
+        grad_bytes = 4 * sum(math.prod(p) for p in self.param_specs())
+        return (f"{lid} {kind_fields} elem=2 mem_fwd={self.saved_bytes(batch)} mem_wt=0 "
+                f"mem_grad={grad_bytes}")
+
+
+class StemUnit(_ConvNetUnit):
+    """conv7x7/2 (3->64) + BN + ReLU + maxpool3x3/2."""
+
+    name = "stem"
+
+    def __init__(self, res=224, cout=64):
+        self.res, self.cout = res, cout
+        self.co = res // 2          # conv output side
+        self.po = self.co // 2      # pool output side
+
+    def param_specs(self):
+        return [(self.cout, 7, 7, 3), (self.cout,), (self.cout,)]
+
+    def saved_specs(self, n):
+        return [SavedSpec((n, self.res, self.res, 3), self.act),
+                SavedSpec((n, self.co, self.co, self.cout), self.act),
+                SavedSpec((2 * self.cout,), torch.float32)]
+
+    def init_params(self, gen):
+        return [_kaiming((self.cout, 7, 7, 3), gen), torch.ones(self.cout), torch.zeros(self.cout)]
+
+    def forward(self, x, params, saved):
+        w, g, b = params
+        wv = _cl(w)
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+        c = _conv(x, wv, 2, 3)
+        o, m, i = _bn_fw(c, g, b)
+        if saved is not None:
+            _cl(saved[1]).copy_(c)
+            saved[2][:self.cout].copy_(m)
+            saved[2][self.cout:].copy_(i)
+        a = o.relu_()
+        y, _ = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
+        return y
+
+    def backward(self, dy, params, saved, grads):
+        w, g, b = params
+        x, c = _cl(saved[0]), _cl(saved[1])
+        m, i = saved[2][:self.cout], saved[2][self.cout:]
+        a = _bn_apply(c, g, b, m, i).relu_()
+        _, idx = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
+        da = _aten.max_pool2d_with_indices_backward(dy, a, [3, 3], [2, 2], [1, 1], [1, 1], False, idx)
+        da = _aten.threshold_backward(da, a, 0)
+        dc, dg, db = _bn_bw(da, c, g, m, i)
+        _, dw, _ = _conv_bw(dc, x, _cl(w), 2, 3, need_dx=False)
+        _cl(grads[0]).copy_(dw)
+        grads[1].copy_(dg)
+        grads[2].copy_(db)
+        return None
+
+    def fwd_flops(self, n):
+        return 2.0 * n * self.co * self.co * self.cout * 49 * 3
+
+    def ir_line(self, lid, batch, analytic=False):
+        return self._ir(lid, batch, f"Conv Wout={self.co} Hout={self.co} Cin=3 Cout={self.cout} K=7")
+
+
+class BottleneckUnit(_ConvNetUnit):
+    """1x1 (cin->w) / 3x3 stride s (w->w) / 1x1 (w->4w), BN after each conv,
+    identity or 1x1/s projection shortcut, ReLU after the add."""
+
+    name = "bottleneck"
+
+    def __init__(self, cin, width, stride, side_in):
+        self.cin, self.w, self.s = cin, width, stride
+        self.cout = 4 * width
+        self.hi = side_in
+        self.ho = side_in // stride
+        self.down = stride != 1 or cin != self.cout
+
+    def param_specs(self):
+        p = [(self.w, 1, 1, self.cin), (self.w,), (self.w,),
+             (self.w, 3, 3, self.w), (self.w,), (self.w,),
+             (self.cout, 1, 1, self.w), (self.cout,), (self.cout,)]
+        if self.down:
+            p += [(self.cout, 1, 1, self.cin), (self.cout,), (self.cout,)]
+        return p
+
+    def _nstats(self):
+        return 2 * (2 * self.w + self.cout + (self.cout if self.down else 0))
+
+    def saved_specs(self, n):
+        s = [SavedSpec((n, self.hi, self.hi, self.cin), self.act),
+             SavedSpec((n, self.hi, self.hi, self.w), self.act),
+             SavedSpec((n, self.ho, self.ho, self.w), self.act),
+             SavedSpec((n, self.ho, self.ho, self.cout), self.act)]
+        if self.down:
+            s.append(SavedSpec((n, self.ho, self.ho, self.cout), self.act))
+        s.append(SavedSpec((self._nstats(),), torch.float32))
+        return s
+
+    def init_params(self, gen):
+        out = []
+        for shp in self.param_specs():
+            if len(shp) == 4:
+                out.append(_kaiming(shp, gen))
+            else:
+                out.append(torch.ones(shp) if len(out) % 3 == 1 else torch.zeros(shp))
+        # zero-init the last BN gamma of the residual branch (standard practice)
+        out[7] = torch.zeros(self.cout)
+        return out
+
+    def _stats_views(self, st):
+        sizes = [self.w, self.w, self.w, self.w, self.cout, self.cout]
+        if self.down:
+            sizes += [self.cout, self.cout]
+        views, o = [], 0
+        for k in sizes:
+            views.append(st[o:o + k])
+            o += k
+        return views
+
+    def forward(self, x, params, saved):
+        w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+        c1 = _conv(x, _cl(w1), 1, 0)
+        o1, m1, i1 = _bn_fw(c1, g1, b1)
+        a1 = o1.relu_()
+        c2 = _conv(a1, _cl(w2), self.s, 1)
+        o2, m2, i2 = _bn_fw(c2, g2, b2)
+        a2 = o2.relu_()
+        c3 = _conv(a2, _cl(w3), 1, 0)
+        o3, m3, i3 = _bn_fw(c3, g3, b3)
+        stats = [m1, i1, m2, i2, m3, i3]
+        if self.down:
+            wd, gd, bd = params[9:12]
+            cd = _conv(x, _cl(wd), self.s, 0)
+            od, md, idd = _bn_fw(cd, gd, bd)
+            stats += [md, idd]
+            o3.add_(od)
+        else:
+            o3.add_(x)
+        if saved is not None:
+            _cl(saved[1]).copy_(c1)
+            _cl(saved[2]).copy_(c2)
+            _cl(saved[3]).copy_(c3)
+            if self.down:
+                _cl(saved[4]).copy_(cd)
+            for v, t in zip(self._stats_views(saved[-1]), stats):
+                v.copy_(t)
+        return o3.relu_()
+
+    def backward(self, dy, params, saved, grads):
+        w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
+        x, c1, c2, c3 = (_cl(t) for t in saved[:4])
+        st = self._stats_views(saved[-1])
+        m1, i1, m2, i2, m3, i3 = st[:6]
+        a1 = _bn_apply(c1, g1, b1, m1, i1).relu_()
+        a2 = _bn_apply(c2, g2, b2, m2, i2).relu_()
+        y = _bn_apply(c3, g3, b3, m3, i3)
+        if self.down:
+            wd, gd, bd = params[9:12]
+            cd = _cl(saved[4])
+            md, idd = st[6], st[7]
+            y.add_(_bn_apply(cd, gd, bd, md, idd))
+        else:
+            y.add_(x)
+        y.relu_()
+        dz = _aten.threshold_backward(dy, y, 0)
+        del y
+        dc3, dg3, db3 = _bn_bw(dz, c3, g3, m3, i3)
+        da2, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0)
+        del dc3
+        da2 = _aten.threshold_backward(da2, a2, 0)
+        dc2, dg2, db2 = _bn_bw(da2, c2, g2, m2, i2)
+        del da2
+        da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
+        del dc2
+        da1 = _aten.threshold_backward(da1, a1, 0)
+        dc1, dg1, db1 = _bn_bw(da1, c1, g1, m1, i1)
+        del da1
+        dx, dw1, _ = _conv_bw(dc1, x, _cl(w1), 1, 0)
+        del dc1
+        gs = [dw1, dg1, db1, dw2, dg2, db2, dw3, dg3, db3]
+        if self.down:
+            dcd, dgd, dbd = _bn_bw(dz, cd, gd, md, idd)
+            dxd, dwd, _ = _conv_bw(dcd, x, _cl(wd), self.s, 0)
+            dx.add_(dxd)
+            gs += [dwd, dgd, dbd]
+        else:
+            dx.add_(dz)
+        for gv, t in zip(grads, gs):
+            (_cl(gv) if gv.dim() == 4 else gv).copy_(t)
+        return dx
+
+    def fwd_flops(self, n):
+        macs = (self.hi * self.hi * self.cin * self.w + self.ho * self.ho * 9 * self.w * self.w
+                + self.ho * self.ho * self.w * self.cout)
+        if self.down:
+            macs += self.ho * self.ho * self.cin * self.cout
+        return 2.0 * n * macs
+
+    def ir_line(self, lid, batch, analytic=False):
+        params = sum(math.prod(p) for p in self.param_specs() if len(p) == 4)
+        return self._ir(lid, batch, f"Conv Wout={self.ho} Hout={self.ho} Cin=1 Cout={params} K=1")
+
+
+class HeadUnit(_ConvNetUnit):
+    """global average pool + FullyConnected (with bias) -> logits."""
+
+    name = "head"
+
+    def __init__(self, cin=2048, classes=1000, side=7):
+        self.cin, self.k, self.side = cin, classes, side
+
+    def param_specs(self):
+        return [(self.k, self.cin), (self.k,)]
+
+    def saved_specs(self, n):
+        return [SavedSpec((n, self.side, self.side, self.cin), self.act)]
+
+    def init_params(self, gen):
+        bound = 1.0 / math.sqrt(self.cin)
+        return [torch.empty(self.k, self.cin).uniform_(-bound, bound, generator=gen),
+                torch.empty(self.k).uniform_(-bound, bound, generator=gen)]
+
+    def forward(self, x, params, saved):
+        w, b = params
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+        p = x.mean(dim=(2, 3))
+        return torch.addmm(b, p, w.t())
+
+    def backward(self, dy, params, saved, grads):
+        w, b = params
+        x = _cl(saved[0])
+        p = x.mean(dim=(2, 3))
+        grads[0].copy_(torch.mm(dy.t(), p, out_dtype=torch.float32))
+        grads[1].copy_(dy.float().sum(0))
+        dp = torch.mm(dy, w) * (1.0 / (self.side * self.side))
+        n = dp.shape[0]
+        return dp[:, :, None, None].expand(n, self.cin, self.side, self.side).contiguous(
+            memory_format=torch.channels_last)
+
+    def fwd_flops(self, n):
+        return 2.0 * n * self.cin * self.k
+
+    def ir_line(self, lid, batch, analytic=False):
+        return self._ir(lid, batch, f"FullyConnected X={self.cin} Y={self.k}")
+
+
+def cross_entropy_loss(logits, target):
+    """Softmax cross-entropy, mean over the batch; dlogits in the logits dtype."""
+    lf = logits.float()
+    loss = F.cross_entropy(lf, target)
+    p = torch.softmax(lf, dim=1)
+    p[torch.arange(p.shape[0], device=p.device), target] -= 1.0
+    return loss, (p * (1.0 / p.shape[0])).to(logits.dtype)
+
+
+RESNET_DEPTHS = {50: (3, 4, 6, 3), 101: (3, 4, 23, 3), 152: (3, 8, 36, 3), 200: (3, 24, 36, 3)}
+
+
+def resnet_units(depth: int = 200, res: int = 224, classes: int = 1000, stages=None,
+                 act_dtype=torch.bfloat16):
+    """ImageNet bottleneck ResNet as executor units: stem, sum(stages) bottlenecks, head."""
+    stages = stages or RESNET_DEPTHS[depth]
+    units = [StemUnit(res)]
+    side = res // 4
+    cin = 64
+    for si, count in enumerate(stages):
+        width = 64 * 2 ** si
+        for k in range(count):
+            stride = 2 if (k == 0 and si > 0) else 1
+            units.append(BottleneckUnit(cin, width, stride, side))
+            side //= stride
+            cin = 4 * width
+    units.append(HeadUnit(cin, classes, side))
+    for u in units:
+        u.act = act_dtype
+    return units

@@ -1,0 +1,102 @@
+"""Plan the executor's workloads with the UNMODIFIED reference planner.
+
+Run HERE (the reference is importable only in the build container):
+
+    PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src python scripts/make_plans.py
+
+For each workload: the units' model IR (one IR layer per executor unit, with
+measured memory overrides, model_ir.py:355-364) + a B200 hardware spec
+(cost_model.py:308-339) -> oocsched.plan_model (planner.py:890-912) ->
+plan_to_dict (plan.py:179-202).  Output: paper_2008_11421_b200/plans/<name>.json
+holding the three texts the executor loads through krt_plan_load.
+"""
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oocsched.cost_model import parse_hardware_text  # noqa: E402
+from oocsched.model_ir import parse_model_text  # noqa: E402
+from oocsched.plan import plan_string, plan_to_dict  # noqa: E402
+from oocsched.planner import plan_model  # noqa: E402
+from oocsched.simulator import simulate  # noqa: E402
+
+from paper_2008_11421_b200.units import model_text, resnet_units  # noqa: E402
+
+OUT = ROOT / "paper_2008_11421_b200" / "plans"
+
+# B200 calibration (MEASURED_PEAKS.json, scripts/probe_box.py, bench runs):
+# PCIe Gen5 x16 duplex 49.8 GB/s per direction (55.6 H2D / 57.3 D2H alone);
+# compute_rate in MAC/s (cost_model.py:3-4 counts a multiply-add as one op)
+B200 = dict(far_mem_bw=200e9, near_mem_bw=6.5e12, interconnect_bw=49.8e9,
+            compute_rate=2.0e14, host_update_rate=2.0e9, backward_multiplier=2.0)
+
+
+def hw_text(capacity, **over):
+    v = dict(B200, **over)
+    lines = [f"capacity_bytes = {capacity!r}"] + [f"{k} = {v[k]!r}" for k in
+                                                   ("far_mem_bw", "near_mem_bw", "interconnect_bw",
+                                                    "compute_rate", "host_update_rate",
+                                                    "backward_multiplier")]
+    lines.append("duplex = true")
+    return "\n".join(lines) + "\n"
+
+
+def make(name, units, batch, capacity, meta, **hw_over):
+    mt = model_text(units, batch)
+    ht = hw_text(float(capacity), **hw_over)
+    g, hw = parse_model_text(mt), parse_hardware_text(ht)
+    t0 = time.time()
+    plan = plan_model(g, hw)
+    dt = time.time() - t0
+    tr = simulate(plan, g, hw)
+    swapped = set(plan.swapped_blocks())
+    rec = {
+        "name": name, "model": mt, "hardware": ht, "plan": plan_to_dict(plan),
+        "plan_string": plan_string(plan), "meta": dict(meta, batch=batch),
+        "planner_seconds": dt, "predicted_makespan": tr.makespan,
+        "total_bytes": sum(b.swap_bytes for b in plan.blocks),
+        "swapped_bytes": sum(b.swap_bytes for b in plan.blocks if b.id in swapped),
+        "recompute_bytes": sum(b.swap_bytes for b in plan.blocks if b.recompute),
+        "generator": "scripts/make_plans.py (oocsched 0.1.0 reference planner)",
+    }
+    (OUT / f"{name}.json").write_text(json.dumps(rec, indent=1) + "\n")
+    print(f"{name}: {len(plan.blocks)} blocks, total {rec['total_bytes']/1e9:.2f} GB, swapped "
+          f"{rec['swapped_bytes']/1e9:.2f} GB, recompute {rec['recompute_bytes']/1e9:.2f} GB, "
+          f"planned in {dt:.2f}s", file=sys.stderr)
+    return rec
+
+
+def total_saved(units, batch):
+    return sum(u.saved_bytes(batch) for u in units)
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    # small ResNets for the parity tests (capacity as a fraction of the
+    # activations, slow link) so the plans swap, recompute runs from the model
+    # input, and recompute with input regeneration from a swapped-in block
+    for act, tag, frac in ((torch.float32, "f32_a", 0.62), (torch.float32, "f32_b", 0.70),
+                           (torch.bfloat16, "bf16", 0.62)):
+        units = resnet_units(stages=(1, 2, 2, 1), res=64, classes=10, act_dtype=act)
+        batch = 8
+        tot = total_saved(units, batch)
+        make(f"resnet_small_{tag}", units, batch, frac * tot,
+             {"family": "resnet", "stages": [1, 2, 2, 1], "res": 64, "classes": 10,
+              "act": tag.split("_")[0]}, interconnect_bw=1e9, compute_rate=1e11)
+    # cfg1: ResNet-200 224x224, per-GPU batch sized so activations exceed HBM
+    units = resnet_units(200)
+    for batch, cap in ((2560, 150e9), (512, 30e9)):
+        make(f"resnet200_b{batch}", units, batch, cap,
+             {"family": "resnet", "depth": 200, "res": 224, "classes": 1000, "act": "bf16"})
+
+
+if __name__ == "__main__":
+    main()
