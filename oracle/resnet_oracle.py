@@ -58,5 +58,5 @@ def train(units, init, inputs, targets, lr=0.1, optimizer="sgd"):
         loss = F.cross_entropy(forward(units, params, x.float()), y)
         loss.backward()
         opt.step()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     return losses, {k: [t.detach() for t in ts] for k, ts in params.items()}

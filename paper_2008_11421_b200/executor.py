@@ -88,6 +88,10 @@ class Unit:
     def init_params(self, gen: torch.Generator) -> list[torch.Tensor]:
         return []
 
+    def saved_input(self, saved: list) -> torch.Tensor:
+        """The unit's input as forward() takes it, rebuilt from its saved tensors."""
+        return saved[0]
+
     def fwd_flops(self, batch: int) -> float:
         return 0.0
 
@@ -259,7 +263,7 @@ class Executor:
         prev_views = self._slot_views(b - 1, p.value)
         _, lo, hi = self.blocks[b - 2]
         u = self.units[hi - 1]
-        return u.forward(prev_views[-1][0], self.params[hi], None)
+        return u.forward(u.saved_input(prev_views[-1]), self.params[hi], None)
 
     def _callback(self, user, action, block, slot, slot_bytes, stream):
         try:

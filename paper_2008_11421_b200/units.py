@@ -125,6 +125,9 @@ def _kaiming(shape_ohwi, gen):
 class _ConvNetUnit(Unit):
     act = torch.bfloat16
 
+    def saved_input(self, saved):
+        return _cl(saved[0])
+
     def _ir(self, lid, batch, kind_fields):
         grad_bytes = 4 * sum(math.prod(p) for p in self.param_specs())
         return (f"{lid} {kind_fields} elem=2 mem_fwd={self.saved_bytes(batch)} mem_wt=0 "
