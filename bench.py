@@ -1,0 +1,351 @@
+"""Benchmark: KARMA out-of-core data-parallel training on B200.
+
+Metric (BASELINE.json): samples/sec of a model whose activations exceed HBM,
+with the per-iteration roofline (compute / PCIe / NVLink).  Workload (N=1):
+cfg1 — ResNet-200, 224x224x3 synthetic N(0,1) images, 1000 classes, bf16,
+per-GPU batch 2560 (267 GB of saved activations per iteration vs 180 GB HBM),
+planned by the UNMODIFIED reference planner into a swap + recompute schedule
+(paper_2008_11421_b200/plans/resnet200_b2560.json, scripts/make_plans.py).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--plan NAME] [--impl reference]
+
+N > 1 is launched by torchrun (one rank per GPU, NCCL); weak scaling: every
+rank trains its own per-GPU batch and the exchange reduce-scatters gradients.
+`--impl reference` times the CPU reference arm (the in-core fp32 torch CPU
+oracle of the same model, oracle/resnet_oracle.py) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+PCIE_H2D, PCIE_D2H, PCIE_DUPLEX = 55.6e9, 57.3e9, 49.8e9   # scripts/probe_box.py on this pool
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAK_FALLBACK, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline: in-core fp32 torch CPU training step
+# ---------------------------------------------------------------------------
+def cpu_reference(rec, steps, warmup, sample_batch=4):
+    import torch
+
+    from oracle import resnet_oracle
+    from paper_2008_11421_b200 import workloads as W
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    units = W.units_for(rec)
+    m = rec["meta"]
+    gen = torch.Generator().manual_seed(0)
+    init = {i + 1: [t.float() for t in u.init_params(gen)] for i, u in enumerate(units)}
+    params = {k: [t.requires_grad_(True) for t in ts] for k, ts in init.items()}
+    flat = [t for k in sorted(params) for t in params[k]]
+    opt = torch.optim.SGD(flat, lr=0.1, foreach=False)
+    x = torch.randn(sample_batch, 3, m["res"], m["res"], generator=gen)
+    y = torch.randint(0, m["classes"], (sample_batch,), generator=gen)
+
+    def step():
+        opt.zero_grad(set_to_none=True)
+        loss = torch.nn.functional.cross_entropy(resnet_oracle.forward(units, params, x), y)
+        loss.backward()
+        opt.step()
+
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    return sample_batch * steps / dt, torch.get_num_threads(), dt
+
+
+def run_reference(args, rec):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    steps, warmup = max(1, min(args.steps, 3)), 1
+    value, cores, dt = cpu_reference(rec, steps, warmup)
+    m = rec["meta"]
+    line = {
+        "metric": "samples/sec (ResNet-200 224x224 training step, per-GPU batch beyond HBM)",
+        "impl": "reference", "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warmup, "ms_per_step": dt / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": rec["name"], "model": "resnet200",
+                                         "per_gpu_batch": m["batch"], "image": m["res"]},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": "in-core fp32 torch-CPU ResNet-200 step (oracle/resnet_oracle.py) "
+                                   "on 4 images per step"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args, rec):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_11421_b200 import workloads as W
+    from paper_2008_11421_b200.executor import ExecConfig, Executor
+    from paper_2008_11421_b200.units import cross_entropy_loss
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    torch.backends.cudnn.benchmark = True
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2008_11421_b200 import _lib
+        idbuf = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            idbuf = torch.tensor(list(_lib.nccl_unique_id()), dtype=torch.uint8)
+        idbuf = idbuf.cuda()
+        dist.broadcast(idbuf, 0)
+        nccl_id = bytes(idbuf.cpu().tolist())
+    m = rec["meta"]
+    batch, res, classes = m["batch"], m["res"], m["classes"]
+    units = W.units_for(rec)
+    bundle = W.bundle_for(rec)
+    t_setup = time.perf_counter()
+    ex = Executor(units, bundle, batch=batch, loss_fn=cross_entropy_loss,
+                  cfg=ExecConfig(device=local, world_size=world, rank=rank, nccl_id=nccl_id,
+                                 optimizer="sgd", lr=0.1, weight_dtype=torch.bfloat16,
+                                 momentum=0.9))
+    ex.init_weights(seed=0)
+    setup_s = time.perf_counter() - t_setup
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(batch, 3, res, res, device=dev, generator=gen, dtype=torch.float32).to(
+        torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    y = torch.randint(0, classes, (batch,), device=dev, generator=gen)
+    cs = ex.compute_stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up --------------------------------------------------------------
+    for _ in range(args.warmup):
+        ex.step(x, y)
+    ex.synchronize()
+    barrier()
+    # ---- timed region: inputs resident in HBM ----------------------------------
+    clk = Clocks(local)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ex.stats()["kernel_launches_total"]
+    h2d0, d2h0 = ex.stats()["bytes_h2d_total"], ex.stats()["bytes_d2h_total"]
+    e0.record(cs)
+    for _ in range(args.steps):
+        ex.step(x, y)
+    ex.synchronize()
+    e1.record(cs)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.stop()
+    st = ex.stats()
+    trace = ex.trace_csv()
+    launches = st["kernel_launches_total"] - launches0
+    h2d_iter = (st["bytes_h2d_total"] - h2d0) / args.steps
+    d2h_iter = (st["bytes_d2h_total"] - d2h0) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * batch * args.steps / (ms / 1e3)
+    # ---- e2e: host (pinned) inputs copied in, loss read back, every step --------
+    xh = x.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        xd = xh.to(dev, non_blocking=True)
+        yd = yh.to(dev, non_blocking=True)
+        loss = ex.step(xd, yd)
+        float(loss)    # D2H of the step's loss
+    ex.synchronize()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    tt = torch.tensor([e2e_s], device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_value = world * batch * e2e_steps / float(tt.item())
+    h2d_in = xh.numel() * xh.element_size() + yh.numel() * yh.element_size()
+
+    # ---- roofline ---------------------------------------------------------------
+    pk, pk_kind = peaks()
+    iter_s = ms / 1e3 / args.steps
+    fwd = sum(u.fwd_flops(batch) for u in units)
+    plan = rec["plan"]
+    rec_fwd = 0.0
+    for s in plan["stages"]:
+        for a, b in s["ops"]:
+            if a == "recompute_fw":
+                lo, hi = plan["blocks"][b - 1]["layers"]
+                rec_fwd += sum(units[i - 1].fwd_flops(batch) for i in range(lo, hi + 1))
+    alg_flops = 3.0 * fwd                     # fwd + bwd (2x) per training step
+    exec_flops = alg_flops + rec_fwd          # + recomputed forwards
+    sustained = pk["bf16_tflops_sustained"] * 1e12
+    terms = {"compute_s": exec_flops / sustained,
+             "pcie_h2d_s": h2d_iter / PCIE_H2D,
+             "pcie_d2h_s": d2h_iter / PCIE_D2H,
+             "nvlink_s": 0.0}
+    if world > 1:
+        terms["nvlink_s"] = st["params"] * 4 * (world - 1) / world * 2 / 770e9
+    bind = max(terms, key=terms.get)
+    rows = [r.split(",") for r in trace.strip().splitlines()[1:]]
+    comp = [(float(r[0]), float(r[1])) for r in rows if r[2] == "compute"]
+    busy = sum(b - a for a, b in comp)
+    span = (max(b for _, b in comp) - min(a for a, _ in comp)) if comp else 0.0
+    xin = [(float(r[0]), float(r[1])) for r in rows if r[4] in ("swap_in", "weight_in")]
+    xout = [(float(r[0]), float(r[1])) for r in rows if r[4] in ("swap_out", "grad_out")]
+    swap_in_bytes = st["iter_bytes_h2d"]
+    swap_out_bytes = st["iter_bytes_d2h"]
+    line = {
+        "metric": "samples/sec (ResNet-200 224x224 training step, per-GPU batch beyond HBM)",
+        "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": rec["name"], "model": "resnet200", "per_gpu_batch": batch,
+                   "global_batch": batch * world, "image": res, "parallelism": f"dp{world}",
+                   "plan": rec["plan_string"][:160] + " ...",
+                   "activations_bytes": rec["total_bytes"], "hbm_bytes": 183359 * 2 ** 20,
+                   "swapped_bytes": rec["swapped_bytes"], "recompute_bytes": rec["recompute_bytes"],
+                   "l2": "inputs > L2 (batch tensor 771 MB; 267 GB of activations per step)"},
+        "roofline": {"bound": "tensor", "achieved": alg_flops / iter_s / 1e12,
+                     "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": alg_flops / iter_s / sustained, "traffic": None,
+                     "peak_kind": f"{pk_kind} sustained bf16 (cuBLAS)",
+                     "note": "whole training step: algorithmic 3x forward FLOPs / step time"},
+        "iteration_roofline": dict(terms, binding=bind, bound_s=terms[bind],
+                                   frac=terms[bind] / iter_s,
+                                   pcie_h2d_GBps=swap_in_bytes / iter_s / 1e9,
+                                   pcie_d2h_GBps=swap_out_bytes / iter_s / 1e9),
+        "overlap": {"compute_busy_frac": busy / span if span else None,
+                    "exposed_stall_frac": 1 - busy / span if span else None,
+                    "swap_in_busy_s": sum(b - a for a, b in xin),
+                    "swap_out_busy_s": sum(b - a for a, b in xout)},
+        "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_in,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": launches,
+        "runtime": {k: st[k] for k in ("arena_bytes", "ledger_peak_bytes", "host_swap_bytes",
+                                       "swapped_blocks", "ops_per_iteration", "params")},
+        "setup_s": setup_s,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, dt = cpu_reference(rec, steps=2, warmup=1)
+        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
+                                "sample": "in-core fp32 torch-CPU ResNet-200 step "
+                                          "(oracle/resnet_oracle.py), 4 images x 2 steps"}
+    if args.trace_out and rank == 0:
+        Path(args.trace_out).write_text(trace)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ex.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--plan", default="resnet200_b2560")
+    ap.add_argument("--impl", default="krt", choices=["krt", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace-out", default=None)
+    args = ap.parse_args()
+    from paper_2008_11421_b200 import workloads as W
+    rec = W.load(args.plan)
+    if args.impl == "reference":
+        run_reference(args, rec)
+    else:
+        run_gpu(args, rec)
+
+
+if __name__ == "__main__":
+    main()

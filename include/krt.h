@@ -109,6 +109,9 @@ typedef struct krt_config {
 typedef int (*krt_compute_cb)(void* user, int action, int block, void* slot,
                               size_t slot_bytes, void* stream);
 
+/* ncclGetUniqueId for rank 0 to broadcast (128 bytes into out). */
+int krt_nccl_unique_id(void* out128);
+
 int krt_create(const krt_config* cfg, krt_ctx** out);
 int krt_destroy(krt_ctx* ctx);
 

@@ -63,6 +63,7 @@ EXPORTS = {
     "krt_plan_simulate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "krt_plan_simulate_dist": (C.c_int, [C.c_void_p, C.POINTER(DistConfig), C.c_int,
                                          C.POINTER(C.c_void_p)]),
+    "krt_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "krt_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "krt_destroy": (C.c_int, [C.c_void_p]),
     "krt_register_block": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.POINTER(C.c_int64), C.c_int]),
@@ -124,3 +125,9 @@ def take_string(ptr: C.c_void_p) -> str:
         return C.string_at(ptr.value).decode("utf-8")
     finally:
         lib().krt_string_free(ptr)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().krt_nccl_unique_id(buf))
+    return buf.raw

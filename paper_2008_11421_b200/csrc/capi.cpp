@@ -201,6 +201,16 @@ int krt_plan_simulate_dist(const krt_plan* p, const krt_dist_config* c, int iter
   });
 }
 
+int krt_nccl_unique_id(void* out) {
+  return guard([&] {
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
 int krt_create(const krt_config* cfg, krt_ctx** out) {
   return guard([&] {
     if (!cfg || !out) throw std::invalid_argument("null argument");
