@@ -185,7 +185,12 @@ def run_gpu(args, rec):
     m = rec["meta"]
     batch, res, classes = m["batch"], m["res"], m["classes"]
     units = W.units_for(rec)
-    bundle = W.bundle_for(rec)
+    if args.incore:
+        bundle = W.bundle_for(rec, W.incore_plan(rec["plan"])).set_capacity(1e12)
+        rec = dict(rec, plan=W.incore_plan(rec["plan"]), name=rec["name"] + "_incore",
+                   swapped_bytes=0.0, recompute_bytes=0.0, plan_string="in-core")
+    else:
+        bundle = W.bundle_for(rec)
     t_setup = time.perf_counter()
     ex = Executor(units, bundle, batch=batch, loss_fn=cross_entropy_loss,
                   cfg=ExecConfig(device=local, world_size=world, rank=rank, nccl_id=nccl_id,
@@ -338,6 +343,8 @@ def main():
     ap.add_argument("--impl", default="krt", choices=["krt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-out", default=None)
+    ap.add_argument("--incore", action="store_true",
+                    help="same blocks, everything resident (no swap/recompute): the in-core baseline")
     args = ap.parse_args()
     from paper_2008_11421_b200 import workloads as W
     rec = W.load(args.plan)
