@@ -3,9 +3,10 @@
 Metric (BASELINE.json): samples/sec of a model whose activations exceed HBM,
 with the per-iteration roofline (compute / PCIe / NVLink).  Workload (N=1):
 cfg1 — ResNet-200, 224x224x3 synthetic N(0,1) images, 1000 classes, bf16,
-per-GPU batch 2560 (267 GB of saved activations per iteration vs 180 GB HBM),
-planned by the UNMODIFIED reference planner into a swap + recompute schedule
-(paper_2008_11421_b200/plans/resnet200_b2560.json, scripts/make_plans.py).
+per-GPU batch 3072 (320 GB of saved activations per iteration = 1.67x the
+192 GB of HBM), planned by the UNMODIFIED reference planner into a swap +
+recompute schedule (paper_2008_11421_b200/plans/resnet200_b3072.json,
+scripts/make_plans.py).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--plan NAME] [--impl reference]
 
@@ -298,7 +299,8 @@ def run_gpu(args, rec):
                    "plan": rec["plan_string"][:160] + " ...",
                    "activations_bytes": rec["total_bytes"], "hbm_bytes": 183359 * 2 ** 20,
                    "swapped_bytes": rec["swapped_bytes"], "recompute_bytes": rec["recompute_bytes"],
-                   "l2": "inputs > L2 (batch tensor 771 MB; 267 GB of activations per step)"},
+                   "l2": f"inputs > L2 (batch tensor {x.numel() * 2 / 1e6:.0f} MB; "
+                         f"{rec['total_bytes'] / 1e9:.0f} GB of activations per step)"},
         "roofline": {"bound": "tensor", "achieved": alg_flops / iter_s / 1e12,
                      "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                      "frac": alg_flops / iter_s / sustained, "traffic": None,
@@ -318,6 +320,8 @@ def run_gpu(args, rec):
         "runtime": {k: st[k] for k in ("arena_bytes", "ledger_peak_bytes", "host_swap_bytes",
                                        "swapped_blocks", "ops_per_iteration", "params")},
         "setup_s": setup_s,
+        "device_memory": {"torch_max_allocated": torch.cuda.max_memory_allocated(dev),
+                          "free_total": list(torch.cuda.mem_get_info(dev))},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -339,7 +343,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--plan", default="resnet200_b2560")
+    ap.add_argument("--plan", default="resnet200_b3072")
     ap.add_argument("--impl", default="krt", choices=["krt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-out", default=None)
