@@ -100,7 +100,16 @@ typedef struct krt_config {
   float grad_scale;         /* multiplies summed gradients (1/world_size = mean) */
   int host_threads;         /* host update worker threads, 0 = auto */
   size_t arena_slack_bytes; /* extra arena bytes beyond the static assignment */
+  void* peer_group;         /* krt_peer_group* for in-process ranks (else NULL: NCCL) */
 } krt_config;
+
+/* In-process exchange group: world_size ranks living in one process (threads),
+ * e.g. logical ranks on one GPU or one process driving several GPUs.  The
+ * reduce-scatter is the fused scale/cast/reduce kernel over the peers'
+ * gradient buffers, the all-gather device-to-device copies. */
+typedef struct krt_peer_group krt_peer_group;
+int krt_peer_group_create(int world_size, krt_peer_group** out);
+int krt_peer_group_destroy(krt_peer_group* group);
 
 /* The executor's compute step for one plan op (KRT_FW, KRT_RECOMPUTE_FW,
  * KRT_BW) of `block`.  `slot` is the block's device arena slot
@@ -108,6 +117,16 @@ typedef struct krt_config {
  * Return 0 on success. */
 typedef int (*krt_compute_cb)(void* user, int action, int block, void* slot,
                               size_t slot_bytes, void* stream);
+
+/* Flat parameter layout of the DP pipeline (host-only): blocks in order,
+ * contiguous per gradient group (assign_groups, distsim.py:120-131), each
+ * group padded to world*64 elements; rank r owns elements
+ * [group_lo + r*shard_n, group_lo + (r+1)*shard_n) of every group.  Output
+ * arrays: block_off[n_blocks]; group_lo/group_n/shard_n[n_blocks] (at most
+ * n_blocks groups), *n_groups receives the group count. */
+int krt_dp_layout(const int64_t* block_params, int n_blocks, int groups, int world,
+                  int64_t* block_off, int* n_groups, int64_t* group_lo, int64_t* group_n,
+                  int64_t* shard_n);
 
 /* ncclGetUniqueId for rank 0 to broadcast (128 bytes into out). */
 int krt_nccl_unique_id(void* out128);

@@ -45,7 +45,7 @@ class Config(C.Structure):
                 ("optimizer", C.c_int), ("lr", C.c_float), ("beta1", C.c_float),
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
                 ("momentum", C.c_float), ("grad_scale", C.c_float), ("host_threads", C.c_int),
-                ("arena_slack_bytes", C.c_size_t)]
+                ("arena_slack_bytes", C.c_size_t), ("peer_group", C.c_void_p)]
 
 
 COMPUTE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -64,6 +64,11 @@ EXPORTS = {
     "krt_plan_simulate_dist": (C.c_int, [C.c_void_p, C.POINTER(DistConfig), C.c_int,
                                          C.POINTER(C.c_void_p)]),
     "krt_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "krt_dp_layout": (C.c_int, [C.POINTER(C.c_int64), C.c_int, C.c_int, C.c_int,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "krt_peer_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "krt_peer_group_destroy": (C.c_int, [C.c_void_p]),
     "krt_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "krt_destroy": (C.c_int, [C.c_void_p]),
     "krt_register_block": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.POINTER(C.c_int64), C.c_int]),
@@ -131,3 +136,31 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().krt_nccl_unique_id(buf))
     return buf.raw
+
+
+class PeerGroup:
+    """In-process exchange group (krt_peer_group) for ranks driven by threads."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib().krt_peer_group_create(world, C.byref(h)))
+        self.handle = h
+        self.world = world
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            lib().krt_peer_group_destroy(self.handle)
+            self.handle = None
+
+
+def dp_layout(block_params, groups: int, world: int) -> dict:
+    """krt_dp_layout: the runtime's flat parameter / shard layout."""
+    nb = len(block_params)
+    bp = (C.c_int64 * nb)(*block_params)
+    off = (C.c_int64 * nb)()
+    lo, n, sh = (C.c_int64 * nb)(), (C.c_int64 * nb)(), (C.c_int64 * nb)()
+    ng = C.c_int()
+    check(lib().krt_dp_layout(bp, nb, groups, world, off, C.byref(ng), lo, n, sh))
+    k = ng.value
+    return {"block_off": list(off), "group_lo": list(lo)[:k], "group_n": list(n)[:k],
+            "shard_n": list(sh)[:k]}

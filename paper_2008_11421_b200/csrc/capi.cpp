@@ -201,6 +201,33 @@ int krt_plan_simulate_dist(const krt_plan* p, const krt_dist_config* c, int iter
   });
 }
 
+int krt_dp_layout(const int64_t* block_params, int n_blocks, int groups, int world, int64_t* block_off,
+                  int* n_groups, int64_t* group_lo, int64_t* group_n, int64_t* shard_n) {
+  return guard([&] {
+    if (n_blocks < 1 || !block_params || groups < 0) throw std::invalid_argument("bad layout arguments");
+    std::vector<int64_t> bp(block_params, block_params + n_blocks);
+    DpLayout L = dp_layout(bp, groups, world);
+    for (int b = 0; b < n_blocks; ++b) block_off[b] = L.block_off[b];
+    *n_groups = (int)L.group_lo.size();
+    for (size_t g = 0; g < L.group_lo.size(); ++g) {
+      group_lo[g] = L.group_lo[g];
+      group_n[g] = L.group_n[g];
+      shard_n[g] = L.shard_n[g];
+    }
+  });
+}
+
+int krt_peer_group_create(int world, krt_peer_group** out) {
+  return guard([&] {
+    if (world < 1 || !out) throw std::invalid_argument("bad peer group size");
+    *out = reinterpret_cast<krt_peer_group*>(new PeerGroup(world));
+  });
+}
+
+int krt_peer_group_destroy(krt_peer_group* g) {
+  return guard([&] { delete reinterpret_cast<PeerGroup*>(g); });
+}
+
 int krt_nccl_unique_id(void* out) {
   return guard([&] {
     ncclUniqueId id;

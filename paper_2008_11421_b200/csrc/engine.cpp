@@ -637,6 +637,31 @@ std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardwa
   return all;
 }
 
+DpLayout dp_layout(const std::vector<int64_t>& block_params, int groups, int world) {
+  if (world < 1) throw std::invalid_argument("world must be >= 1");
+  DpLayout L;
+  int nb = (int)block_params.size();
+  auto gs = assign_groups(nb, groups);
+  L.block_off.assign(nb, 0);
+  L.group_of.assign(nb, 0);
+  int64_t off = 0, pad = (int64_t)world * 64;
+  for (size_t gi = 0; gi < gs.size(); ++gi) {
+    int64_t n = 0;
+    for (int b : gs[gi]) {
+      L.block_off[b - 1] = off + n;
+      L.group_of[b - 1] = (int)gi + 1;
+      n += block_params[b - 1];
+    }
+    int64_t pn = (n + pad - 1) / pad * pad;
+    L.group_lo.push_back(off);
+    L.group_n.push_back(pn);
+    L.shard_n.push_back(pn / world);
+    off += pn;
+  }
+  L.total = off;
+  return L;
+}
+
 DistResult simulate_distributed(const Plan& p, const Model& g, const Hardware& hw,
                                 const DistConfig& cfg, int iterations) {
   if (iterations < 2) throw std::runtime_error("need at least 2 iterations to observe the steady state");

@@ -91,6 +91,17 @@ struct DistResult {
 std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardware& hw,
                                      const DistConfig& cfg, int iterations,
                                      const std::map<int, BlockCost>& costs);
+// Flat parameter layout of the DP pipeline: blocks in order, contiguous per
+// group (assign_groups), each group padded to world*64 elements so every
+// rank's 1/world shard is 256-byte aligned.
+struct DpLayout {
+  std::vector<int64_t> block_off;              // per block (index = id-1)
+  std::vector<int64_t> group_lo, group_n, shard_n;
+  std::vector<int> group_of;                   // per block, 1-based
+  int64_t total = 0;
+};
+DpLayout dp_layout(const std::vector<int64_t>& block_params, int groups, int world);
+
 DistResult simulate_distributed(const Plan& p, const Model& g, const Hardware& hw,
                                 const DistConfig& cfg, int iterations);
 

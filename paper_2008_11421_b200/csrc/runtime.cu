@@ -43,6 +43,40 @@ size_t dtype_bytes(int dt) { return dt == KRT_BF16 ? 2 : 4; }
 
 }  // namespace
 
+void PeerGroup::mark(int rank, int kind, int group, int step) {
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    marks[{rank, kind, group}] = step;
+  }
+  cv.notify_all();
+}
+
+void PeerGroup::wait_all(int kind, int group, int step) {
+  std::unique_lock<std::mutex> lk(mu);
+  cv.wait(lk, [&] {
+    for (int r = 0; r < world; ++r) {
+      auto it = marks.find({r, kind, group});
+      if (it == marks.end() || it->second < step) return false;
+    }
+    return true;
+  });
+}
+
+cudaEvent_t PeerGroup::event(int rank, int kind, int group) {
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(rank, kind, group);
+  auto it = events.find(key);
+  if (it != events.end()) return it->second;
+  cudaEvent_t e;
+  CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  events[key] = e;
+  return e;
+}
+
+PeerGroup::~PeerGroup() {
+  for (auto& kv : events) cudaEventDestroy(kv.second);
+}
+
 Runtime::Runtime(const krt_config& cfg) : cfg_(cfg) {
   world_ = std::max(1, cfg.world_size);
   rank_ = cfg.rank;
@@ -57,8 +91,14 @@ Runtime::Runtime(const krt_config& cfg) : cfg_(cfg) {
   CK(cudaStreamCreateWithPriority(&streams_[0], cudaStreamNonBlocking, lo));
   for (int i = 1; i < 4; ++i) CK(cudaStreamCreateWithPriority(&streams_[i], cudaStreamNonBlocking, hi));
   CK(cudaEventCreate(&ev_base_));
-  if (world_ > 1) {
-    if (!cfg.nccl_id) throw std::invalid_argument("world_size > 1 needs nccl_id");
+  if (world_ > 1 && cfg.peer_group) {
+    peers_ = static_cast<PeerGroup*>(cfg.peer_group);
+    if (peers_->world != world_) throw std::invalid_argument("peer group size != world_size");
+    std::lock_guard<std::mutex> lk(peers_->mu);
+    if (peers_->ranks[rank_]) throw std::invalid_argument("rank already joined the peer group");
+    peers_->ranks[rank_] = this;
+  } else if (world_ > 1) {
+    if (!cfg.nccl_id) throw std::invalid_argument("world_size > 1 needs nccl_id or a peer group");
     ncclUniqueId id;
     std::memcpy(&id, cfg.nccl_id, sizeof(id));
     ncclComm_t comm;
@@ -82,6 +122,10 @@ Runtime::~Runtime() {
   for (auto s : streams_)
     if (s) cudaStreamSynchronize(s);
   if (nccl_comm_) ncclCommDestroy((ncclComm_t)nccl_comm_);
+  if (peers_) {
+    std::lock_guard<std::mutex> lk(peers_->mu);
+    peers_->ranks[rank_] = nullptr;
+  }
   for (auto e : ev_start_) cudaEventDestroy(e);
   for (auto e : ev_done_) cudaEventDestroy(e);
   if (ev_base_) cudaEventDestroy(ev_base_);
@@ -269,25 +313,26 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
     bp.swapped = false;
   }
   for (int b : plan.swapped_blocks()) blocks_.at(b).swapped = true;
-  int64_t off = 0;
-  int64_t pad = (int64_t)world_ * 64;
+  std::vector<int64_t> bparams;
+  for (int b = 1; b <= nb_; ++b) bparams.push_back(blocks_.at(b).n_params);
+  DpLayout lay = dp_layout(bparams, cfg_.dist_groups, world_);
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     GroupPhys g;
     g.members = groups[gi];
-    g.p_lo = off;
-    int64_t n = 0;
+    g.p_lo = lay.group_lo[gi];
+    g.p_n = lay.group_n[gi];
+    g.shard_n = lay.shard_n[gi];
     for (int b : g.members) {
-      blocks_.at(b).p_off = off + n;
+      blocks_.at(b).p_off = lay.block_off[b - 1];
       blocks_.at(b).group = (int)gi + 1;
-      n += blocks_.at(b).n_params;
       g.host |= blocks_.at(b).host_path;
     }
-    g.p_n = (n + pad - 1) / pad * pad;
-    g.shard_n = g.p_n / world_;
-    off += g.p_n;
     groups_.push_back(g);
   }
+  int64_t off = lay.total;
   total_params_ = off;
+  for (size_t gi = 0; gi < groups_.size(); ++gi)
+    group_first_block_[(int)gi + 1] = *std::min_element(groups_[gi].members.begin(), groups_[gi].members.end());
   // host state layout
   host_elems_ = 0;
   for (auto& g : groups_) {
@@ -685,6 +730,13 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         }
       }
       CK(cudaEventRecord(ev_done_[idx], s));
+      if (peers_ && e.action == Action::BW) {
+        int gi = blocks_.at(e.block).group;
+        if (group_first_block_.at(gi) == e.block) {  // last backward of the group
+          CK(cudaEventRecord(peers_->event(rank_, PK_BW, gi), s));
+          peers_->mark(rank_, PK_BW, gi, step);
+        }
+      }
       return;
     }
     case Action::SWAP_OUT: {
@@ -737,9 +789,24 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
       auto& g = groups_.at((size_t)e.group - 1);
       size_t shard_pos = 0;
       for (int gi = 0; gi < e.group - 1; ++gi) shard_pos += (size_t)groups_[gi].shard_n;
-      CK(cudaEventRecord(ev_start_[idx], s));
-      NK(ncclReduceScatter(d_grad(g.p_lo), d_shard_ + shard_pos, (size_t)g.shard_n, ncclFloat, ncclSum,
-                           (ncclComm_t)nccl_comm_, s));
+      if (peers_) {
+        peers_->wait_all(PK_BW, e.group, step);
+        std::vector<const float*> in((size_t)world_);
+        for (int p = 0; p < world_; ++p) {
+          Runtime* peer = peers_->ranks[p];
+          if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
+          CK(cudaStreamWaitEvent(s, peers_->event(p, PK_BW, e.group), 0));
+          in[p] = peer->grads_base() + g.p_lo + (int64_t)rank_ * g.shard_n;
+        }
+        CK(cudaEventRecord(ev_start_[idx], s));
+        CK(launch_reduce_cast(in.data(), world_, d_shard_ + shard_pos, KRT_F32, (size_t)g.shard_n, 1.0f, s));
+        ++kernel_launches_;
+        ++iter_launches_;
+      } else {
+        CK(cudaEventRecord(ev_start_[idx], s));
+        NK(ncclReduceScatter(d_grad(g.p_lo), d_shard_ + shard_pos, (size_t)g.shard_n, ncclFloat, ncclSum,
+                             (ncclComm_t)nccl_comm_, s));
+      }
       CK(cudaEventRecord(ev_done_[idx], s));
       bytes_net_ += (size_t)g.p_n * 4 * (world_ - 1) / world_;
       return;
@@ -773,8 +840,15 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         cudaStream_t ns = streams_[3];
         CK(cudaEventRecord(ev_done_[idx], s));
         CK(cudaStreamWaitEvent(ns, ev_done_[idx], 0));
-        NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
-                         cfg_.weight_dtype == KRT_BF16 ? ncclBfloat16 : ncclFloat, (ncclComm_t)nccl_comm_, ns));
+        if (peers_) {
+          CK(cudaEventRecord(peers_->event(rank_, PK_WSHARD, e.group), s));
+          peers_->mark(rank_, PK_WSHARD, e.group, step);
+          peers_->wait_all(PK_WSHARD, e.group, step);
+          gather_peer_shards(g, e.group, ns, PK_WSHARD);
+        } else {
+          NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
+                           cfg_.weight_dtype == KRT_BF16 ? ncclBfloat16 : ncclFloat, (ncclComm_t)nccl_comm_, ns));
+        }
         CK(cudaEventRecord(ev_done_[idx], ns));
         bytes_net_ += (size_t)g.p_n * wb * (world_ - 1) / world_;
       } else {
@@ -893,8 +967,16 @@ void Runtime::flush_weights() {
       void* dst = d_weight(g.p_lo + (int64_t)rank_ * g.shard_n);
       CK(cudaMemcpyAsync(dst, static_cast<uint8_t*>(h_wstage_) + g.host_off * wb, (size_t)g.shard_n * wb,
                          cudaMemcpyHostToDevice, s));
-      NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
-                       cfg_.weight_dtype == KRT_BF16 ? ncclBfloat16 : ncclFloat, (ncclComm_t)nccl_comm_, s));
+      if (peers_) {
+        int gi = (int)(&g - groups_.data()) + 1;
+        CK(cudaEventRecord(peers_->event(rank_, PK_FLUSH, gi), s));
+        peers_->mark(rank_, PK_FLUSH, gi, flush_count_ + 1);
+        peers_->wait_all(PK_FLUSH, gi, flush_count_ + 1);
+        gather_peer_shards(g, gi, s, PK_FLUSH);
+      } else {
+        NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
+                         cfg_.weight_dtype == KRT_BF16 ? ncclBfloat16 : ncclFloat, (ncclComm_t)nccl_comm_, s));
+      }
     } else {
       for (int b : g.members) {
         auto& bp = blocks_.at(b);
@@ -906,6 +988,21 @@ void Runtime::flush_weights() {
     }
   }
   CK(cudaStreamSynchronize(s));
+  ++flush_count_;
+}
+
+void Runtime::gather_peer_shards(const GroupPhys& g, int group, cudaStream_t s, int kind) {
+  size_t wb = dtype_bytes(cfg_.weight_dtype);
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) continue;
+    Runtime* peer = peers_->ranks[p];
+    if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
+    CK(cudaStreamWaitEvent(s, peers_->event(p, kind, group), 0));
+    size_t off = (size_t)(g.p_lo + (int64_t)p * g.shard_n) * wb;
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(d_weights_) + off, static_cast<uint8_t*>(peer->weights_base()) + off,
+                       (size_t)g.shard_n * wb, cudaMemcpyDeviceToDevice, s));
+  }
+  bytes_net_ += (size_t)g.shard_n * wb * (world_ - 1);
 }
 
 void* Runtime::block_slot(int block) const {

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/krt.h"
@@ -69,6 +70,29 @@ struct HostTask {
   int step = 0;
 };
 
+class Runtime;
+
+// In-process exchange between ranks that share one process (logical ranks on
+// one GPU, or one process driving several GPUs): the reduce-scatter is
+// krt_reduce_cast over the peers' gradient buffers and the all-gather a set
+// of device-to-device copies, ordered by per-(rank, kind, group) events.
+// Host-side "issued" marks make sure an event is recorded for the current
+// step before any peer waits on it.
+struct PeerGroup {
+  explicit PeerGroup(int w) : world(w), ranks(w, nullptr) {}
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<Runtime*> ranks;
+  std::map<std::tuple<int, int, int>, int> marks;         // (rank, kind, group) -> step
+  std::map<std::tuple<int, int, int>, cudaEvent_t> events;
+  void mark(int rank, int kind, int group, int step);
+  void wait_all(int kind, int group, int step);
+  cudaEvent_t event(int rank, int kind, int group);
+  ~PeerGroup();
+};
+enum PeerKind { PK_BW = 0, PK_WSHARD = 1, PK_FLUSH = 2 };
+
 class Runtime {
  public:
   explicit Runtime(const krt_config& cfg);
@@ -86,6 +110,8 @@ class Runtime {
   void read_master(int block, float* out, size_t numel);
   void* block_slot(int block) const;
   void flush_weights();
+  void* weights_base() const { return d_weights_; }
+  float* grads_base() const { return d_grads_; }
 
  private:
   void build_ops(const Plan& plan, const Model& model, const Hardware& hw);
@@ -96,6 +122,7 @@ class Runtime {
   void host_loop();
   void run_host_task(const HostTask& t);
   void wait_host_done(int group, int step);
+  void gather_peer_shards(const GroupPhys& g, int group, cudaStream_t s, int kind);
   float* d_grad(int64_t p_off) const { return d_grads_ + p_off; }
   void* d_weight(int64_t p_off) const;
 
@@ -131,6 +158,9 @@ class Runtime {
   std::vector<cudaEvent_t> ev_start_, ev_done_;
   cudaEvent_t ev_base_ = nullptr;
   void* nccl_comm_ = nullptr;
+  PeerGroup* peers_ = nullptr;     // in-process exchange instead of NCCL
+  int flush_count_ = 0;
+  std::map<int, int> group_first_block_;  // group -> lowest member (last bw of the group)
 
   // host-update thread
   std::unique_ptr<ThreadPool> pool_;

@@ -120,6 +120,7 @@ class ExecConfig:
     momentum: float = 0.0
     host_threads: int = 0
     arena_slack_bytes: int = 0
+    peer_group: Optional[object] = None   # _lib.PeerGroup for in-process ranks
 
 
 class Executor:
@@ -147,7 +148,8 @@ class Executor:
                          C.cast(self._nccl_id_buf, C.c_void_p) if self._nccl_id_buf else None,
                          cfg.dist_groups, wdt, _lib.ADAM if cfg.optimizer == "adam" else _lib.SGD,
                          cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.momentum,
-                         1.0 / cfg.world_size, cfg.host_threads, cfg.arena_slack_bytes)
+                         1.0 / cfg.world_size, cfg.host_threads, cfg.arena_slack_bytes,
+                         cfg.peer_group.handle if cfg.peer_group is not None else None)
         h = C.c_void_p()
         _lib.check(L.krt_create(C.byref(kc), C.byref(h)))
         self._ctx = h

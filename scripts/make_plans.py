@@ -93,7 +93,7 @@ def main():
               "act": tag.split("_")[0]}, interconnect_bw=1e9, compute_rate=1e11)
     # cfg1: ResNet-200 224x224, per-GPU batch sized so activations exceed HBM
     units = resnet_units(200)
-    for batch, cap in ((3072, 155e9), (2560, 150e9), (512, 30e9)):
+    for batch, cap in ((3072, 140e9), (2560, 150e9), (512, 30e9)):
         make(f"resnet200_b{batch}", units, batch, cap,
              {"family": "resnet", "depth": 200, "res": 224, "classes": 1000, "act": "bf16"})
 

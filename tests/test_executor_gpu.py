@@ -157,3 +157,53 @@ def test_rejects_invalid_plan(sched_cases):
     b = PlanBundle(c["model"], c["hardware"], bad["plan"])
     with pytest.raises(_lib.InfeasiblePlanError):
         Executor([FCUnit(64, 64) for _ in range(6)], b, batch=2, loss_fn=mse_zero_loss)
+
+
+@pytest.mark.parametrize("optimizer,lr", [("sgd", 1e-2), ("adam", 1e-3)])
+def test_cfg0_two_dp_workers_match_oracle(sched_cases, optimizer, lr):
+    """cfg0 proper (BASELINE configs[0]): 2 data-parallel workers.  Two
+    logical ranks on one GPU exchange through the in-process peer group
+    (reduce-scatter kernel over both gradient buffers, host update of each
+    rank's shard, all-gather by D2D copies) — the same DP op DAG as NCCL."""
+    import threading
+    c = cfg0_case(sched_cases)
+    pg = _lib.PeerGroup(2)
+    w0 = orc.init_weights()
+    exs = []
+    for r in range(2):
+        b = PlanBundle(c["model"], c["hardware"], c["plan"])
+        ex = Executor([FCUnit(64, 64) for _ in range(6)], b, batch=2, loss_fn=mse_zero_loss,
+                      cfg=ExecConfig(world_size=2, rank=r, peer_group=pg, optimizer=optimizer, lr=lr))
+        ex.load_weights({i + 1: [torch.from_numpy(w)] for i, w in enumerate(w0)})
+        exs.append(ex)
+    losses = [[None, None] for _ in range(3)]
+    finals = [None, None]
+    errors = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            for it in range(1, 4):
+                x = torch.from_numpy(orc.inputs(r, it)).cuda()
+                losses[it - 1][r] = float(exs[r].step(x))
+            w = exs[r].unit_weights()
+            finals[r] = [w[i + 1][0].cpu().numpy() for i in range(6)]
+        except BaseException as e:  # surface in the main thread
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    [t.start() for t in ts]
+    [t.join(timeout=120) for t in ts]
+    assert not any(t.is_alive() for t in ts), "logical ranks hung"
+    if errors:
+        raise errors[0]
+    ref_losses, ref_w = orc.train(workers=2, iterations=3, optimizer=optimizer, lr=lr, weights=w0)
+    np.testing.assert_allclose(np.array(losses), np.array(ref_losses), rtol=RTOL)
+    for a, b, r in zip(finals[0], finals[1], ref_w):
+        assert np.array_equal(a, b)               # replicas stay identical
+        np.testing.assert_allclose(a, r, rtol=RTOL, atol=ATOL)
+    st = exs[0].stats()
+    assert st["world"] == 2 and st["bytes_net_total"] > 0
+    for ex in exs:
+        ex.close()
+    pg.close()
