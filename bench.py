@@ -29,6 +29,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# unit temporaries come and go in multi-GB sizes next to a 140 GB arena
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 PCIE_H2D, PCIE_D2H, PCIE_DUPLEX = 55.6e9, 57.3e9, 49.8e9   # scripts/probe_box.py on this pool

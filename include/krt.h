@@ -209,6 +209,29 @@ int krt_host_update(float* master, float* m, float* v, const float* grad, void* 
                     float beta2, float eps, float weight_decay, float momentum, int step,
                     int threads);
 
+/* Fused NHWC batch-norm kernels for the convolutional units (bf16
+ * activations [rows, C], C % 8 == 0, C <= 2048; gamma/beta bf16; stats fp32).
+ * ws: krt_bn_workspace_bytes(C) bytes of device scratch. */
+size_t krt_bn_workspace_bytes(int C);
+/* batch statistics: mean[c], invstd[c] = 1/sqrt(var_biased + eps) */
+int krt_bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws,
+                 void* stream);
+/* y = relu?( bn(x) [+ res | + bn'(res)] ); res NULL: no residual, rmean NULL: identity residual */
+int krt_bn_apply(const void* x, const float* mean, const float* invstd, const void* gamma,
+                 const void* beta, const void* res, const float* rmean, const float* rinvstd,
+                 const void* rgamma, const void* rbeta, int relu, void* y, int64_t rows, int C,
+                 void* stream);
+/* dz = dy * ( bn(x) + (res | bn'(res)) > 0 ): backward of the residual add + ReLU */
+int krt_bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd,
+                        const void* gamma, const void* beta, const void* res, const float* rmean,
+                        const float* rinvstd, const void* rgamma, const void* rbeta, void* dz,
+                        int64_t rows, int C, void* stream);
+/* BN backward with the optional ReLU mask recomputed from x: dgamma/dbeta (fp32,
+ * may be NULL) and dx (bf16, may be NULL) */
+int krt_bn_backward(const void* dy, const void* x, const float* mean, const float* invstd,
+                    const void* gamma, const void* beta, int relu, void* dx, float* dgamma,
+                    float* dbeta, int64_t rows, int C, void* ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

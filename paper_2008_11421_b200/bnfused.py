@@ -1,0 +1,83 @@
+"""Thin torch-facing wrappers of libkrt's fused NHWC batch-norm kernels
+(csrc/bn_kernels.cu).  Tensors are NCHW-logical with channels_last strides
+(the NHWC storage the kernels read); everything is issued on torch's current
+stream, which inside the executor is libkrt's compute stream."""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+EPS = 1e-5
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _nhwc(t):
+    if not t.is_contiguous(memory_format=torch.channels_last):
+        t = t.contiguous(memory_format=torch.channels_last)
+    return t
+
+
+def _rows_c(t):
+    n, c, h, w = t.shape
+    return n * h * w, c
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ws(c, device):
+    return torch.empty(_lib.lib().krt_bn_workspace_bytes(c), dtype=torch.uint8, device=device)
+
+
+def supported(c: int) -> bool:
+    return c % 8 == 0 and c <= 2048 and 256 % (c // 8) == 0
+
+
+def stats(c, mean, invstd):
+    """Batch statistics of c (N,C,H,W channels_last bf16) into fp32 mean/invstd."""
+    rows, C = _rows_c(c)
+    ws = _ws(C, c.device)
+    _lib.check(_lib.lib().krt_bn_stats(_nhwc(c).data_ptr(), rows, C, EPS, mean.data_ptr(),
+                                       invstd.data_ptr(), ws.data_ptr(), _stream()))
+
+
+def apply(c, mean, invstd, g, b, relu, res=None, rstats=None, rg=None, rb=None, out=None):
+    """relu?(bn(c) [+ res | + bn'(res)]) -> new bf16 channels_last tensor (or out)."""
+    c = _nhwc(c)
+    rows, C = _rows_c(c)
+    y = out if out is not None else torch.empty_like(c, memory_format=torch.channels_last)
+    rm, ri = (rstats if rstats is not None else (None, None))
+    _lib.check(_lib.lib().krt_bn_apply(c.data_ptr(), mean.data_ptr(), invstd.data_ptr(), g.data_ptr(),
+                                       b.data_ptr(), _ptr(None if res is None else _nhwc(res)), _ptr(rm),
+                                       _ptr(ri), _ptr(rg), _ptr(rb), int(relu), y.data_ptr(), rows, C,
+                                       _stream()))
+    return y
+
+
+def add_relu_bwd(dy, c, mean, invstd, g, b, res, rstats=None, rg=None, rb=None):
+    c, dy, res = _nhwc(c), _nhwc(dy), _nhwc(res)
+    rows, C = _rows_c(c)
+    dz = torch.empty_like(c, memory_format=torch.channels_last)
+    rm, ri = (rstats if rstats is not None else (None, None))
+    _lib.check(_lib.lib().krt_bn_add_relu_bwd(dy.data_ptr(), c.data_ptr(), mean.data_ptr(),
+                                              invstd.data_ptr(), g.data_ptr(), b.data_ptr(),
+                                              res.data_ptr(), _ptr(rm), _ptr(ri), _ptr(rg), _ptr(rb),
+                                              dz.data_ptr(), rows, C, _stream()))
+    return dz
+
+
+def backward(dy, c, mean, invstd, g, b, relu, dgamma=None, dbeta=None, need_dx=True):
+    """BN backward (ReLU mask recomputed from c when relu); dgamma/dbeta fp32 outputs."""
+    c, dy = _nhwc(c), _nhwc(dy)
+    rows, C = _rows_c(c)
+    dx = torch.empty_like(c, memory_format=torch.channels_last) if need_dx else None
+    ws = _ws(C, c.device)
+    _lib.check(_lib.lib().krt_bn_backward(dy.data_ptr(), c.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                                          g.data_ptr(), b.data_ptr(), int(relu), _ptr(dx), _ptr(dgamma),
+                                          _ptr(dbeta), rows, C, ws.data_ptr(), _stream()))
+    return dx

@@ -1,0 +1,391 @@
+// Fused batch-norm kernels for NHWC bf16 activations (sm_100a).
+//
+// The ResNet units' hot elementwise work ("warp-level fused
+// elementwise/norm kernels elsewhere").  All are HBM-bound streaming kernels
+// over a [rows, C] matrix (rows = N*H*W, C contiguous, C % 8 == 0):
+//
+//   stats     : per-channel mean / invstd (batch statistics)       1R
+//   apply     : y = relu?(bn(x) [+ res | + bn'(res)])               1-2R + 1W
+//   add_relu_bwd_mask : dz = dy * (bn(x) + (res | bn'(res)) > 0)    2-3R + 1W
+//   bwd       : dgamma, dbeta (reduce) and dx (elementwise), with the
+//               ReLU mask recomputed from x when the BN feeds a ReLU   2R + 2R+1W
+//
+// Thread mapping: a thread owns 8 consecutive channels (one 16-byte vector)
+// for its whole life, so per-channel scale/shift stay in registers; the rows
+// are grid-strided.  Reductions: per-thread fp32 partials -> shared-memory
+// tree over the rows of a CTA -> one fp32 partial per CTA and channel ->
+// a finalize kernel sums the CTA partials in double (fixed order:
+// deterministic, so in-core and out-of-core runs stay bitwise equal).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bn_kernels.hpp"
+
+namespace krt {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxGrid = 148 * 4;
+
+struct Vec8 {
+  float v[8];
+};
+
+__device__ __forceinline__ Vec8 load8(const __nv_bfloat16* p) {
+  uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  Vec8 r;
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float2 f = __bfloat1622float2(h[k]);
+    r.v[2 * k] = f.x;
+    r.v[2 * k + 1] = f.y;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const Vec8& x) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(x.v[2 * k], x.v[2 * k + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ float bf(const __nv_bfloat16* p, int i) { return __bfloat162float(p[i]); }
+
+// threads of a CTA: tx = channel group (C/8 of them), ty = row lane
+struct Map {
+  int tc, rb, tx, ty;
+  __device__ Map(int C) {
+    tc = C / 8;
+    rb = kThreads / tc;  // rows per CTA sweep (>= 1 since C <= 2048)
+    tx = threadIdx.x % tc;
+    ty = threadIdx.x / tc;
+  }
+};
+
+// per-channel (scale, shift) of y = x*scale + shift
+__device__ __forceinline__ void bn_coeffs(const float* mean, const float* invstd, const __nv_bfloat16* g,
+                                          const __nv_bfloat16* b, int c0, float* sc, float* sh) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float s = invstd[c0 + k] * bf(g, c0 + k);
+    sc[k] = s;
+    sh[k] = bf(b, c0 + k) - mean[c0 + k] * s;
+  }
+}
+
+// reduce two 8-vectors over the ty dimension of the CTA; result in ty == 0
+__device__ __forceinline__ void cta_reduce2(float* a, float* b, float* smem, const Map& m) {
+  // smem: [rb][tc][16]
+  float* mine = smem + ((size_t)m.ty * m.tc + m.tx) * 16;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    mine[k] = a[k];
+    mine[8 + k] = b[k];
+  }
+  __syncthreads();
+  for (int s = 1; s < m.rb; s <<= 1) {
+    if ((m.ty % (2 * s)) == 0 && m.ty + s < m.rb) {
+      float* other = smem + ((size_t)(m.ty + s) * m.tc + m.tx) * 16;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) mine[k] += other[k];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = mine[k];
+    b[k] = mine[8 + k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
+                                                         float* __restrict__ part) {
+  extern __shared__ float smem[];
+  Map m(C);
+  int c0 = m.tx * 8;
+  float s[8] = {0}, q[8] = {0};
+  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
+    Vec8 v = load8(x + r * C + c0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      s[k] += v.v[k];
+      q[k] += v.v[k] * v.v[k];
+    }
+  }
+  cta_reduce2(s, q, smem, m);
+  if (m.ty == 0) {
+    float* out = part + (size_t)blockIdx.x * 2 * C;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      out[c0 + k] = s[k];
+      out[C + c0 + k] = q[k];
+    }
+  }
+}
+
+__global__ void stats_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C, float eps,
+                               float* __restrict__ mean, float* __restrict__ invstd) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int b = 0; b < nblk; ++b) {
+    s += part[(size_t)b * 2 * C + c];
+    q += part[(size_t)b * 2 * C + C + c];
+  }
+  double mu = s / (double)rows;
+  double var = q / (double)rows - mu * mu;
+  if (var < 0) var = 0;
+  mean[c] = (float)mu;
+  invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
+}
+
+// ---------------------------------------------------------------------------
+// mode: 0 none, 1 identity residual, 2 bn(residual)
+__global__ void __launch_bounds__(kThreads) apply_kernel(
+    const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ invstd,
+    const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b, const __nv_bfloat16* __restrict__ res,
+    const float* __restrict__ rmean, const float* __restrict__ rinvstd, const __nv_bfloat16* __restrict__ rg,
+    const __nv_bfloat16* __restrict__ rb_, int mode, int relu, __nv_bfloat16* __restrict__ y, int64_t rows, int C) {
+  Map m(C);
+  int c0 = m.tx * 8;
+  float sc[8], sh[8], rsc[8], rsh[8];
+  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+  if (mode == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
+  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
+    Vec8 v = load8(x + r * C + c0);
+    Vec8 o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o.v[k] = __fmaf_rn(v.v[k], sc[k], sh[k]);
+    if (mode != 0) {
+      Vec8 rv = load8(res + r * C + c0);
+      if (mode == 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o.v[k] = __fadd_rn(o.v[k], __fmaf_rn(rv.v[k], rsc[k], rsh[k]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o.v[k] = __fadd_rn(o.v[k], rv.v[k]);
+      }
+    }
+    if (relu) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o.v[k] = fmaxf(o.v[k], 0.0f);
+    }
+    store8(y + r * C + c0, o);
+  }
+}
+
+// dz = dy * ( bn(x) [+ res | + bn'(res)] > 0 )   (backward of the add + ReLU)
+__global__ void __launch_bounds__(kThreads) add_relu_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
+    const __nv_bfloat16* __restrict__ res, const float* __restrict__ rmean, const float* __restrict__ rinvstd,
+    const __nv_bfloat16* __restrict__ rg, const __nv_bfloat16* __restrict__ rb_, int mode,
+    __nv_bfloat16* __restrict__ dz, int64_t rows, int C) {
+  Map m(C);
+  int c0 = m.tx * 8;
+  float sc[8], sh[8], rsc[8], rsh[8];
+  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+  if (mode == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
+  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
+    Vec8 v = load8(x + r * C + c0);
+    Vec8 rv = load8(res + r * C + c0);
+    Vec8 d = load8(dy + r * C + c0);
+    Vec8 o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      // round the forward sum to bf16 exactly like the forward did
+      float pre = __fadd_rn(__fmaf_rn(v.v[k], sc[k], sh[k]), mode == 2 ? __fmaf_rn(rv.v[k], rsc[k], rsh[k]) : rv.v[k]);
+      float yk = __bfloat162float(__float2bfloat16_rn(pre));
+      o.v[k] = yk > 0.0f ? d.v[k] : 0.0f;
+    }
+    store8(dz + r * C + c0, o);
+  }
+}
+
+// backward reduce: sum(gm) and sum(gm * xhat) with gm = dy * mask
+__global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
+    int relu, int64_t rows, int C, float* __restrict__ part) {
+  extern __shared__ float smem[];
+  Map m(C);
+  int c0 = m.tx * 8;
+  float sc[8], sh[8], mu[8], is[8];
+  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    mu[k] = mean[c0 + k];
+    is[k] = invstd[c0 + k];
+  }
+  float s1[8] = {0}, s2[8] = {0};
+  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
+    Vec8 v = load8(x + r * C + c0);
+    Vec8 d = load8(dy + r * C + c0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float gm = d.v[k];
+      if (relu) {
+        float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
+        gm = yk > 0.0f ? gm : 0.0f;
+      }
+      float xh = (v.v[k] - mu[k]) * is[k];
+      s1[k] += gm;
+      s2[k] += gm * xh;
+    }
+  }
+  cta_reduce2(s1, s2, smem, m);
+  if (m.ty == 0) {
+    float* out = part + (size_t)blockIdx.x * 2 * C;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      out[c0 + k] = s1[k];
+      out[C + c0 + k] = s2[k];
+    }
+  }
+}
+
+// dbeta = sum(gm), dgamma = sum(gm*xhat)  (fp32, written straight into the
+// gradient region); coef = (dbeta/N, dgamma/N) for the elementwise pass
+__global__ void bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
+                             float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ coef) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s1 = 0, s2 = 0;
+  for (int b = 0; b < nblk; ++b) {
+    s1 += part[(size_t)b * 2 * C + c];
+    s2 += part[(size_t)b * 2 * C + C + c];
+  }
+  if (dbeta) dbeta[c] = (float)s1;
+  if (dgamma) dgamma[c] = (float)s2;
+  coef[c] = (float)(s1 / (double)rows);
+  coef[C + c] = (float)(s2 / (double)rows);
+}
+
+// dx = gamma*invstd * (gm - mean(gm) - xhat * mean(gm*xhat))
+__global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
+    int relu, const float* __restrict__ coef, __nv_bfloat16* __restrict__ dx, int64_t rows, int C) {
+  Map m(C);
+  int c0 = m.tx * 8;
+  float sc[8], sh[8], mu[8], is[8], k1[8], k2[8], gs[8];
+  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    mu[k] = mean[c0 + k];
+    is[k] = invstd[c0 + k];
+    k1[k] = coef[c0 + k];
+    k2[k] = coef[C + c0 + k];
+    gs[k] = bf(g, c0 + k) * is[k];
+  }
+  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
+    Vec8 v = load8(x + r * C + c0);
+    Vec8 d = load8(dy + r * C + c0);
+    Vec8 o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float gm = d.v[k];
+      if (relu) {
+        float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
+        gm = yk > 0.0f ? gm : 0.0f;
+      }
+      float xh = (v.v[k] - mu[k]) * is[k];
+      o.v[k] = gs[k] * (gm - k1[k] - xh * k2[k]);
+    }
+    store8(dx + r * C + c0, o);
+  }
+}
+
+size_t reduce_smem(int C);
+
+// persistent grid: one full wave of resident CTAs (148 SMs x occupancy),
+// capped at kMaxGrid so the reduction partials fit the workspace
+template <class K>
+int grid_rows(K kernel, size_t smem, int64_t rows, int C) {
+  static int resident = 0;  // per kernel instantiation
+  if (resident == 0) {
+    int per_sm = 0, sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    resident = sms * (per_sm < 1 ? 1 : per_sm);
+  }
+  int rb = kThreads / (C / 8);
+  int64_t want = (rows + rb - 1) / rb;
+  int cap = resident < kMaxGrid ? resident : kMaxGrid;
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+size_t reduce_smem(int C) {
+  int tc = C / 8, rb = kThreads / tc;
+  return (size_t)rb * tc * 16 * sizeof(float);
+}
+
+bool shape_ok(int64_t rows, int C) { return rows > 0 && C >= 8 && C % 8 == 0 && C <= 8 * kThreads && (kThreads % (C / 8)) == 0; }
+
+}  // namespace
+
+size_t bn_workspace_bytes(int C) { return (size_t)kMaxGrid * 2 * C * sizeof(float) + 2 * C * sizeof(float); }
+
+cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws,
+                     cudaStream_t s) {
+  if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
+  int grid = grid_rows(stats_kernel, reduce_smem(C), rows, C);
+  float* part = static_cast<float*>(ws);
+  stats_kernel<<<grid, kThreads, reduce_smem(C), s>>>(static_cast<const __nv_bfloat16*>(x), rows, C, part);
+  stats_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, grid, rows, C, eps, mean, invstd);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, const void* g, const void* b,
+                     const void* res, const float* rmean, const float* rinvstd, const void* rg, const void* rb,
+                     int relu, void* y, int64_t rows, int C, cudaStream_t s) {
+  if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
+  int mode = res == nullptr ? 0 : (rmean == nullptr ? 1 : 2);
+  apply_kernel<<<grid_rows(apply_kernel, 0, rows, C), kThreads, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(x), mean, invstd, static_cast<const __nv_bfloat16*>(g),
+      static_cast<const __nv_bfloat16*>(b), static_cast<const __nv_bfloat16*>(res), rmean, rinvstd,
+      static_cast<const __nv_bfloat16*>(rg), static_cast<const __nv_bfloat16*>(rb), mode, relu,
+      static_cast<__nv_bfloat16*>(y), rows, C);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                            const void* b, const void* res, const float* rmean, const float* rinvstd,
+                            const void* rg, const void* rb, void* dz, int64_t rows, int C, cudaStream_t s) {
+  if (!shape_ok(rows, C) || res == nullptr) return cudaErrorInvalidValue;
+  int mode = rmean == nullptr ? 1 : 2;
+  add_relu_bwd_kernel<<<grid_rows(add_relu_bwd_kernel, 0, rows, C), kThreads, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
+      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b),
+      static_cast<const __nv_bfloat16*>(res), rmean, rinvstd, static_cast<const __nv_bfloat16*>(rg),
+      static_cast<const __nv_bfloat16*>(rb), mode, static_cast<__nv_bfloat16*>(dz), rows, C);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                        const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
+                        void* ws, cudaStream_t s) {
+  if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
+  int grid = grid_rows(bwd_reduce_kernel, reduce_smem(C), rows, C);
+  float* part = static_cast<float*>(ws);
+  float* coef = part + (size_t)kMaxGrid * 2 * C;
+  bwd_reduce_kernel<<<grid, kThreads, reduce_smem(C), s>>>(
+      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
+      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), relu, rows, C, part);
+  bwd_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
+  if (dx)
+    bwd_elemt_kernel<<<grid_rows(bwd_elemt_kernel, 0, rows, C), kThreads, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
+        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), relu, coef,
+        static_cast<__nv_bfloat16*>(dx), rows, C);
+  return cudaGetLastError();
+}
+
+}  // namespace krt

@@ -12,6 +12,7 @@
 #include "../../include/krt.h"
 #include "engine.hpp"
 #include "host_optim.hpp"
+#include "bn_kernels.hpp"
 #include "kernels.hpp"
 #include "runtime.hpp"
 
@@ -315,6 +316,40 @@ int krt_reduce_cast(const float* const* in, int n_in, void* out, int out_dtype, 
     cudaError_t e = launch_reduce_cast(in, n_in, out, out_dtype, n, scale, (cudaStream_t)stream);
     if (e != cudaSuccess) throw std::runtime_error(std::string("reduce_cast: ") + cudaGetErrorString(e));
   });
+}
+
+size_t krt_bn_workspace_bytes(int C) { return bn_workspace_bytes(C); }
+
+#define KRT_CUDA_GUARD(expr, what)                                                     \
+  return guard([&] {                                                                   \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e_)); \
+  })
+
+int krt_bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws, void* stream) {
+  KRT_CUDA_GUARD(bn_stats(x, rows, C, eps, mean, invstd, ws, (cudaStream_t)stream), "bn_stats");
+}
+
+int krt_bn_apply(const void* x, const float* mean, const float* invstd, const void* g, const void* b,
+                 const void* res, const float* rmean, const float* rinvstd, const void* rg, const void* rb, int relu,
+                 void* y, int64_t rows, int C, void* stream) {
+  KRT_CUDA_GUARD(bn_apply(x, mean, invstd, g, b, res, rmean, rinvstd, rg, rb, relu, y, rows, C, (cudaStream_t)stream),
+                 "bn_apply");
+}
+
+int krt_bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                        const void* b, const void* res, const float* rmean, const float* rinvstd, const void* rg,
+                        const void* rb, void* dz, int64_t rows, int C, void* stream) {
+  KRT_CUDA_GUARD(bn_add_relu_bwd(dy, x, mean, invstd, g, b, res, rmean, rinvstd, rg, rb, dz, rows, C,
+                                 (cudaStream_t)stream),
+                 "bn_add_relu_bwd");
+}
+
+int krt_bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                    const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
+                    void* stream) {
+  KRT_CUDA_GUARD(bn_backward(dy, x, mean, invstd, g, b, relu, dx, dgamma, dbeta, rows, C, ws, (cudaStream_t)stream),
+                 "bn_backward");
 }
 
 int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,

@@ -18,6 +18,7 @@ from typing import Optional
 import torch
 import torch.nn.functional as F
 
+from . import bnfused
 from .executor import SavedSpec, Unit, _align
 
 
@@ -99,6 +100,16 @@ def _conv(x, w, stride, pad):
     return _aten.convolution(x, w, None, [stride, stride], [pad, pad], [1, 1], False, [0, 0], 1)
 
 
+def _conv_into(x, w, stride, pad, out=None):
+    """conv written straight into `out` (an arena-slot view) when given."""
+    if out is None:
+        return _conv(x, w, stride, pad)
+    cb = torch.backends.cudnn
+    _aten.cudnn_convolution.out(x, w, [pad, pad], [stride, stride], [1, 1], 1, cb.benchmark,
+                                cb.deterministic, cb.allow_tf32, out=out)
+    return out
+
+
 def _conv_bw(dy, x, w, stride, pad, need_dx=True):
     return _aten.convolution_backward(dy, x, w, None, [stride, stride], [pad, pad], [1, 1], False,
                                       [0, 0], 1, [need_dx, True, False])
@@ -155,11 +166,22 @@ class StemUnit(_ConvNetUnit):
     def init_params(self, gen):
         return [_kaiming((self.cout, 7, 7, 3), gen), torch.ones(self.cout), torch.zeros(self.cout)]
 
+    def _fused(self):
+        return self.act == torch.bfloat16 and bnfused.supported(self.cout)
+
     def forward(self, x, params, saved):
         w, g, b = params
         wv = _cl(w)
         if saved is not None:
             _cl(saved[0]).copy_(x)
+        if self._fused():
+            c = _conv_into(x, wv, 2, 3, None if saved is None else _cl(saved[1]))
+            st = saved[2] if saved is not None else torch.empty(2 * self.cout, device=x.device)
+            m, i = st[:self.cout], st[self.cout:]
+            bnfused.stats(c, m, i)
+            a = bnfused.apply(c, m, i, g, b, relu=True)
+            y, _ = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
+            return y
         c = _conv(x, wv, 2, 3)
         o, m, i = _bn_fw(c, g, b)
         if saved is not None:
@@ -174,6 +196,15 @@ class StemUnit(_ConvNetUnit):
         w, g, b = params
         x, c = _cl(saved[0]), _cl(saved[1])
         m, i = saved[2][:self.cout], saved[2][self.cout:]
+        if self._fused():
+            a = bnfused.apply(c, m, i, g, b, relu=True)
+            _, idx = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
+            da = _aten.max_pool2d_with_indices_backward(dy, a, [3, 3], [2, 2], [1, 1], [1, 1], False, idx)
+            del a, idx
+            dc = bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=grads[1], dbeta=grads[2])
+            _, dw, _ = _conv_bw(dc, x, _cl(w), 2, 3, need_dx=False)
+            _cl(grads[0]).copy_(dw)
+            return None
         a = _bn_apply(c, g, b, m, i).relu_()
         _, idx = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
         da = _aten.max_pool2d_with_indices_backward(dy, a, [3, 3], [2, 2], [1, 1], [1, 1], False, idx)
@@ -247,7 +278,74 @@ class BottleneckUnit(_ConvNetUnit):
             o += k
         return views
 
+    def _fused(self):
+        return self.act == torch.bfloat16 and all(bnfused.supported(c) for c in (self.w, self.cout))
+
+    def _forward_fused(self, x, params, saved):
+        w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+            st = self._stats_views(saved[-1])
+        else:
+            st = self._stats_views(torch.empty(self._nstats(), device=x.device))
+        sv = (lambda k: None) if saved is None else (lambda k: _cl(saved[k]))
+        c1 = _conv_into(x, _cl(w1), 1, 0, sv(1))
+        bnfused.stats(c1, st[0], st[1])
+        a1 = bnfused.apply(c1, st[0], st[1], g1, b1, relu=True)
+        c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
+        del a1
+        bnfused.stats(c2, st[2], st[3])
+        a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
+        c3 = _conv_into(a2, _cl(w3), 1, 0, sv(3))
+        del a2
+        bnfused.stats(c3, st[4], st[5])
+        if self.down:
+            wd, gd, bd = params[9:12]
+            cd = _conv_into(x, _cl(wd), self.s, 0, sv(4))
+            bnfused.stats(cd, st[6], st[7])
+            return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=cd, rstats=(st[6], st[7]),
+                                 rg=gd, rb=bd)
+        return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=x)
+
+    def _backward_fused(self, dy, params, saved, grads):
+        w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
+        x, c1, c2, c3 = (_cl(t) for t in saved[:4])
+        st = self._stats_views(saved[-1])
+        if self.down:
+            wd, gd, bd = params[9:12]
+            cd = _cl(saved[4])
+            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, cd, rstats=(st[6], st[7]), rg=gd, rb=bd)
+        else:
+            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, x)
+        dc3 = bnfused.backward(dz, c3, st[4], st[5], g3, b3, relu=False, dgamma=grads[7], dbeta=grads[8])
+        a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
+        da2, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0)
+        del dc3, a2
+        _cl(grads[6]).copy_(dw3)
+        dc2 = bnfused.backward(da2, c2, st[2], st[3], g2, b2, relu=True, dgamma=grads[4], dbeta=grads[5])
+        del da2
+        a1 = bnfused.apply(c1, st[0], st[1], g1, b1, relu=True)
+        da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
+        del dc2, a1
+        _cl(grads[3]).copy_(dw2)
+        dc1 = bnfused.backward(da1, c1, st[0], st[1], g1, b1, relu=True, dgamma=grads[1], dbeta=grads[2])
+        del da1
+        dx, dw1, _ = _conv_bw(dc1, x, _cl(w1), 1, 0)
+        del dc1
+        _cl(grads[0]).copy_(dw1)
+        if self.down:
+            dcd = bnfused.backward(dz, cd, st[6], st[7], gd, bd, relu=False, dgamma=grads[10],
+                                   dbeta=grads[11])
+            dxd, dwd, _ = _conv_bw(dcd, x, _cl(wd), self.s, 0)
+            _cl(grads[9]).copy_(dwd)
+            dx.add_(dxd)
+        else:
+            dx.add_(dz)
+        return dx
+
     def forward(self, x, params, saved):
+        if self._fused():
+            return self._forward_fused(x, params, saved)
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         if saved is not None:
             _cl(saved[0]).copy_(x)
@@ -279,6 +377,8 @@ class BottleneckUnit(_ConvNetUnit):
         return o3.relu_()
 
     def backward(self, dy, params, saved, grads):
+        if self._fused():
+            return self._backward_fused(dy, params, saved, grads)
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         x, c1, c2, c3 = (_cl(t) for t in saved[:4])
         st = self._stats_views(saved[-1])

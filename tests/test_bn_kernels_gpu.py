@@ -1,0 +1,101 @@
+"""Fused NHWC batch-norm kernels (csrc/bn_kernels.cu) vs a torch fp32
+reference on the same bf16 inputs.  Tolerances: statistics and parameter
+gradients are fp32 reductions (rtol 1e-4 / 1e-3); bf16 outputs are compared
+at bf16 resolution (one ulp = 2^-8 relative)."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2008_11421_b200 import bnfused
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = dict(rtol=1.6e-2, atol=1.6e-2)
+
+
+def rand(n, c, h, w, scale=1.0, shift=0.0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    t = torch.randn(n, c, h, w, device="cuda", generator=g) * scale + shift
+    return t.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+
+
+def params(c, seed=1):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    gamma = (1 + 0.2 * torch.randn(c, device="cuda", generator=g)).to(torch.bfloat16)
+    beta = (0.1 * torch.randn(c, device="cuda", generator=g)).to(torch.bfloat16)
+    return gamma, beta
+
+
+def ref_stats(x):
+    xf = x.float()
+    mean = xf.mean(dim=(0, 2, 3))
+    var = xf.var(dim=(0, 2, 3), unbiased=False)
+    return mean, torch.rsqrt(var + bnfused.EPS)
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 28, 28), (16, 256, 14, 14), (8, 2048, 7, 7), (3, 128, 5, 7)])
+def test_stats_and_apply(shape):
+    n, c, h, w = shape
+    x = rand(*shape, scale=2.0, shift=0.5)
+    g, b = params(c)
+    m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    bnfused.stats(x, m, i)
+    rm, ri = ref_stats(x)
+    torch.testing.assert_close(m, rm, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(i, ri, rtol=1e-4, atol=1e-5)
+    pre = ((x.float() - rm[None, :, None, None]) * ri[None, :, None, None] * g.float()[None, :, None, None]
+           + b.float()[None, :, None, None])
+    y = bnfused.apply(x, m, i, g, b, relu=True)
+    torch.testing.assert_close(y.float(), F.relu(pre), **BF16_TOL)
+    # residual forms: identity and bn'(res)
+    r = rand(*shape, seed=5)
+    y1 = bnfused.apply(x, m, i, g, b, relu=True, res=r)
+    torch.testing.assert_close(y1.float(), F.relu(pre + r.float()), **BF16_TOL)
+    y2 = bnfused.apply(x, m, i, g, b, relu=False, res=x, rstats=(m, i), rg=g, rb=b)
+    torch.testing.assert_close(y2.float(), 2 * pre, **BF16_TOL)
+
+
+def bn_ref_fwd(x, g, b):
+    return F.batch_norm(x, None, None, g, b, training=True, momentum=0.0, eps=bnfused.EPS)
+
+
+@pytest.mark.parametrize("relu", [False, True])
+@pytest.mark.parametrize("shape", [(32, 64, 28, 28), (16, 512, 7, 7), (4, 2048, 7, 7)])
+def test_backward_matches_autograd(shape, relu):
+    n, c, h, w = shape
+    x = rand(*shape, scale=1.5, shift=0.2, seed=2)
+    dy = rand(*shape, seed=3)
+    g, b = params(c, seed=4)
+    m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    bnfused.stats(x, m, i)
+    dg, db = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    dx = bnfused.backward(dy, x, m, i, g, b, relu=relu, dgamma=dg, dbeta=db)
+    xr = x.float().requires_grad_(True)
+    gr = g.float().requires_grad_(True)
+    br = b.float().requires_grad_(True)
+    out = bn_ref_fwd(xr, gr, br)
+    if relu:
+        out = F.relu(out)
+    out.backward(dy.float())
+    torch.testing.assert_close(db, br.grad, rtol=1e-3, atol=1e-2)
+    torch.testing.assert_close(dg, gr.grad, rtol=1e-3, atol=1e-2)
+    err = (dx.float() - xr.grad).abs().max() / xr.grad.abs().max()
+    assert err < 2e-2, float(err)
+
+
+def test_add_relu_backward_mask():
+    shape = (8, 256, 14, 14)
+    x = rand(*shape, seed=7)
+    r = rand(*shape, seed=8)
+    dy = rand(*shape, seed=9)
+    g, b = params(256)
+    gd, bd = params(256, seed=11)
+    m, i = torch.empty(256, device="cuda"), torch.empty(256, device="cuda")
+    md, idd = torch.empty(256, device="cuda"), torch.empty(256, device="cuda")
+    bnfused.stats(x, m, i)
+    bnfused.stats(r, md, idd)
+    y = bnfused.apply(x, m, i, g, b, relu=True, res=r, rstats=(md, idd), rg=gd, rb=bd)
+    dz = bnfused.add_relu_bwd(dy, x, m, i, g, b, r, rstats=(md, idd), rg=gd, rb=bd)
+    assert torch.equal(dz, torch.where(y > 0, dy, torch.zeros_like(dy)))
+    y1 = bnfused.apply(x, m, i, g, b, relu=True, res=r)
+    dz1 = bnfused.add_relu_bwd(dy, x, m, i, g, b, r)
+    assert torch.equal(dz1, torch.where(y1 > 0, dy, torch.zeros_like(dy)))

@@ -83,3 +83,14 @@ def test_resnet_out_of_core_equals_in_core_bitwise(name):
     for k in w_inc:
         for a, b in zip(w_ooc[k], w_inc[k]):
             assert torch.equal(a, b), k
+
+
+def test_resnet_bf16_fused_tracks_fp32_oracle():
+    """bf16 activations/weights through the fused NHWC BN kernels: losses
+    follow the fp32 CPU oracle at bf16 tolerance (3%)."""
+    rec = W.load("resnet_small_bf16")
+    units, init, losses, w, stats = run(rec, iters=3, lr=0.05)
+    assert all(u._fused() for u in units[:-1])
+    xs, ys = batches(rec, 3)
+    ref_losses, ref_w = resnet_oracle.train(units, init, xs, ys, lr=0.05)
+    torch.testing.assert_close(torch.tensor(losses), torch.tensor(ref_losses), rtol=3e-2, atol=3e-2)
