@@ -36,7 +36,7 @@ OUT = ROOT / "paper_2008_11421_b200" / "plans"
 # PCIe Gen5 x16 duplex 49.8 GB/s per direction (55.6 H2D / 57.3 D2H alone);
 # compute_rate in MAC/s (cost_model.py:3-4 counts a multiply-add as one op)
 B200 = dict(far_mem_bw=200e9, near_mem_bw=6.5e12, interconnect_bw=49.8e9,
-            compute_rate=5.0e13, host_update_rate=2.0e9, backward_multiplier=2.0)
+            compute_rate=1.25e14, host_update_rate=2.0e9, backward_multiplier=2.0)
 
 
 def hw_text(capacity, **over):
@@ -93,7 +93,7 @@ def main():
               "act": tag.split("_")[0]}, interconnect_bw=1e9, compute_rate=1e11)
     # cfg1: ResNet-200 224x224, per-GPU batch sized so activations exceed HBM
     units = resnet_units(200)
-    for batch, cap in ((3072, 140e9), (2560, 150e9), (512, 30e9)):
+    for batch, cap in ((3072, 150e9), (2560, 150e9), (512, 30e9)):
         make(f"resnet200_b{batch}", units, batch, cap,
              {"family": "resnet", "depth": 200, "res": 224, "classes": 1000, "act": "bf16"})
 
