@@ -83,6 +83,12 @@ typedef struct krt_dist_config {
 int krt_plan_simulate_dist(const krt_plan* plan, const krt_dist_config* cfg, int iterations,
                            char** out_json);
 
+/* Static arena assignment for physical block sizes (block_bytes[i] = slot
+ * bytes of block i+1): JSON {arena_bytes, ledger_peak, instances[{block, off,
+ * bytes, alloc_op, free_op}], deps[[op, free_op]...]}.  Host-only; this is
+ * what krt_prepare uses to realise the capacity ledger (simulator.py:90). */
+int krt_plan_arena(const krt_plan* plan, const size_t* block_bytes, int n_blocks, char** out_json);
+
 /* ------------------------------------------------------------------------
  * Executor context: one per rank / GPU.
  * ---------------------------------------------------------------------- */

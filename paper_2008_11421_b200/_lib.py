@@ -69,6 +69,7 @@ EXPORTS = {
                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "krt_peer_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "krt_peer_group_destroy": (C.c_int, [C.c_void_p]),
+    "krt_plan_arena": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.c_int, C.POINTER(C.c_void_p)]),
     "krt_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "krt_destroy": (C.c_int, [C.c_void_p]),
     "krt_register_block": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.POINTER(C.c_int64), C.c_int]),

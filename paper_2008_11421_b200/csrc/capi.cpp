@@ -239,6 +239,37 @@ int krt_nccl_unique_id(void* out) {
   });
 }
 
+int krt_plan_arena(const krt_plan* p, const size_t* block_bytes, int n_blocks, char** out_json) {
+  return guard([&] {
+    if ((int)p->plan.blocks.size() != n_blocks) throw std::invalid_argument("block count mismatch");
+    std::map<int, size_t> bb;
+    for (int i = 0; i < n_blocks; ++i) bb[i + 1] = (block_bytes[i] + 255) / 256 * 256;
+    auto costs = plan_costs(p->plan, p->model, p->hw);
+    auto base = build_engine_ops(p->plan, p->model, p->hw, costs);
+    for (auto& e : base)
+      if (!e.missing.empty()) throw Infeasible(e.missing);
+    ArenaPlan ap = plan_arena(p->plan, p->model, p->hw, base, bb);
+    std::ostringstream os;
+    os << "{\"arena_bytes\": " << ap.arena_bytes << ", \"ledger_peak\": " << jnum(ap.ledger_peak)
+       << ", \"instances\": [";
+    for (size_t i = 0; i < ap.inst.size(); ++i) {
+      auto& in = ap.inst[i];
+      os << (i ? ", " : "") << "{\"block\": " << in.block << ", \"off\": " << in.off << ", \"bytes\": " << in.bytes
+         << ", \"alloc_op\": " << in.alloc_op << ", \"free_op\": " << in.free_op << ", \"alloc_action\": \""
+         << action_name(base[in.alloc_op].action) << "\"}";
+    }
+    os << "], \"deps\": [";
+    bool first = true;
+    for (size_t i = 0; i < ap.deps.size(); ++i)
+      for (int d : ap.deps[i]) {
+        os << (first ? "" : ", ") << "[" << i << ", " << d << "]";
+        first = false;
+      }
+    os << "]}";
+    *out_json = dup(os.str());
+  });
+}
+
 int krt_create(const krt_config* cfg, krt_ctx** out) {
   return guard([&] {
     if (!cfg || !out) throw std::invalid_argument("null argument");

@@ -637,6 +637,142 @@ std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardwa
   return all;
 }
 
+ArenaPlan plan_arena(const Plan& p, const Model& g, const Hardware& hw, const std::vector<EngineOp>& base,
+                     const std::map<int, size_t>& block_bytes) {
+  (void)g;
+  ArenaPlan ap;
+  EngineResult er = run_engine(base, base_resources(hw), hw.capacity_bytes, true);
+  if (er.deadlock) {
+    std::string s = "simulation deadlock; blocked ops: ";
+    for (size_t i = 0; i < er.blocked.size(); ++i) s += (i ? "; " : "") + er.blocked[i];
+    throw std::runtime_error(s);
+  }
+  ap.ledger_peak = er.peak;
+  ap.start_order = er.start_order;
+  size_t n = base.size();
+  ap.inst_of_alloc.assign(n, -1);
+  ap.inst_read.assign(n, -1);
+  ap.deps.assign(n, {});
+  std::map<int, int> cur;
+  std::map<int, bool> rflag;
+  for (auto& b : p.blocks) rflag[b.id] = b.recompute;
+  for (size_t i = 0; i < n; ++i) {
+    const EngineOp& e = base[i];
+    int b = e.block;
+    if (e.action == Action::FW || e.action == Action::RECOMPUTE_FW || e.action == Action::SWAP_IN) {
+      ArenaInstance in;
+      in.block = b;
+      auto bb = block_bytes.find(b);
+      if (bb == block_bytes.end()) throw std::invalid_argument("no physical size for block " + std::to_string(b));
+      in.bytes = bb->second;
+      in.alloc_op = (int)i;
+      ap.inst_of_alloc[i] = (int)ap.inst.size();
+      cur[b] = (int)ap.inst.size();
+      ap.inst.push_back(in);
+      if (e.action == Action::FW && b >= 2 && rflag[b - 1]) {
+        auto it = cur.find(b - 1);
+        if (it != cur.end()) {  // recompute buffers discarded at the consumer's end
+          ap.inst[it->second].free_op = (int)i;
+          cur.erase(it);
+        }
+      }
+    } else if (e.action == Action::SWAP_OUT || e.action == Action::BW) {
+      auto it = cur.find(b);
+      if (it == cur.end()) throw std::runtime_error("block " + std::to_string(b) + " not resident");
+      ap.inst_read[i] = it->second;
+      ap.inst[it->second].free_op = (int)i;
+      cur.erase(it);
+    }
+  }
+  // lifetimes as ranks in the (time, frees-first, start order) event sweep
+  std::vector<double> ts(n, 0), te(n, 0);
+  for (auto& ev : er.events) {
+    ts[ev.op] = ev.t_start;
+    te[ev.op] = ev.t_end;
+  }
+  std::vector<int> rank_of(n, 0);
+  for (size_t k = 0; k < er.start_order.size(); ++k) rank_of[er.start_order[k]] = (int)k;
+  struct Ev { double t; int kind; int order; int inst; };
+  std::vector<Ev> evs;
+  for (size_t k = 0; k < ap.inst.size(); ++k) {
+    auto& in = ap.inst[k];
+    evs.push_back({ts[in.alloc_op], 1, rank_of[in.alloc_op], (int)k});
+    if (in.free_op >= 0) evs.push_back({te[in.free_op], 0, rank_of[in.free_op], (int)k});
+  }
+  std::sort(evs.begin(), evs.end(), [](const Ev& a, const Ev& b) {
+    if (a.t != b.t) return a.t < b.t;
+    if (a.kind != b.kind) return a.kind < b.kind;
+    return a.order < b.order;
+  });
+  std::vector<double> lo(ap.inst.size(), 0), hi(ap.inst.size(), 1e300);
+  for (size_t r = 0; r < evs.size(); ++r) {
+    if (evs[r].kind == 1) lo[evs[r].inst] = (double)r;
+    else hi[evs[r].inst] = (double)r;
+  }
+  for (size_t k = 0; k < ap.inst.size(); ++k)
+    if (hi[k] <= lo[k]) hi[k] = lo[k] + 0.5;  // zero-length op: freed right after its alloc
+  // first-fit over lifetimes; several orderings, keep the tightest arena
+  size_t ni = ap.inst.size();
+  auto place = [&](std::vector<int> order, std::vector<size_t>& offs) {
+    offs.assign(ni, 0);
+    size_t top = 0;
+    std::vector<int> placed;
+    for (int k : order) {
+      std::vector<std::pair<size_t, size_t>> busy;
+      for (int j : placed)
+        if (lo[j] < hi[k] && lo[k] < hi[j]) busy.emplace_back(offs[j], offs[j] + ap.inst[j].bytes);
+      std::sort(busy.begin(), busy.end());
+      size_t off = 0;
+      for (auto& bz : busy) {
+        if (bz.first >= off + ap.inst[k].bytes) break;
+        off = std::max(off, bz.second);
+      }
+      offs[k] = off;
+      top = std::max(top, off + ap.inst[k].bytes);
+      placed.push_back(k);
+    }
+    return top;
+  };
+  std::vector<int> base_order(ni);
+  for (size_t k = 0; k < ni; ++k) base_order[k] = (int)k;
+  auto by = [&](auto key) {
+    std::vector<int> o = base_order;
+    std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return key(a) > key(b); });
+    return o;
+  };
+  std::vector<std::vector<int>> orders = {
+      by([&](int k) { return (double)ap.inst[k].bytes; }),
+      by([&](int k) { return -lo[k]; }),
+      by([&](int k) { return std::min(hi[k], 1e12) - lo[k]; }),
+      by([&](int k) { return (double)ap.inst[k].bytes * (std::min(hi[k], 1e12) - lo[k]); }),
+  };
+  size_t best = (size_t)-1;
+  std::vector<size_t> offs, best_offs;
+  for (auto& o : orders) {
+    size_t top = place(o, offs);
+    if (top < best) {
+      best = top;
+      best_offs = offs;
+    }
+  }
+  for (size_t k = 0; k < ni; ++k) ap.inst[k].off = best_offs[k];
+  ap.arena_bytes = ni ? best : 0;
+  // address reuse -> dependency on the earlier instance's freeing op
+  for (size_t k = 0; k < ap.inst.size(); ++k)
+    for (size_t j = 0; j < ap.inst.size(); ++j) {
+      if (j == k) continue;
+      auto& a = ap.inst[k];
+      auto& b = ap.inst[j];
+      bool addr = b.off < a.off + a.bytes && a.off < b.off + b.bytes;
+      if (addr && hi[j] <= lo[k] && b.free_op >= 0) ap.deps[a.alloc_op].push_back(b.free_op);
+    }
+  for (auto& d : ap.deps) {
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+  }
+  return ap;
+}
+
 DpLayout dp_layout(const std::vector<int64_t>& block_params, int groups, int world) {
   if (world < 1) throw std::invalid_argument("world must be >= 1");
   DpLayout L;

@@ -91,6 +91,28 @@ struct DistResult {
 std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardware& hw,
                                      const DistConfig& cfg, int iterations,
                                      const std::map<int, BlockCost>& costs);
+// Static arena assignment realising the simulator's byte ledger
+// (simulator.py:67-135, alloc at fw/recompute/swap_in start, free at
+// swap_out/bw end and at the consumer fw of a recompute block).  Instances
+// are placed first-fit-decreasing by size over their simulated lifetimes;
+// every instance that reuses bytes of an earlier one depends on that
+// instance's freeing op, so the physical ledger holds for any real timing.
+struct ArenaInstance {
+  int block = 0;
+  size_t off = 0, bytes = 0;
+  int alloc_op = -1, free_op = -1;
+};
+struct ArenaPlan {
+  std::vector<ArenaInstance> inst;
+  std::vector<int> inst_of_alloc, inst_read;   // per base op
+  std::vector<std::vector<int>> deps;          // per base op: extra deps (free ops)
+  size_t arena_bytes = 0;
+  double ledger_peak = 0;
+  std::vector<int> start_order;                // base simulation start order
+};
+ArenaPlan plan_arena(const Plan& p, const Model& g, const Hardware& hw, const std::vector<EngineOp>& base,
+                     const std::map<int, size_t>& block_bytes);
+
 // Flat parameter layout of the DP pipeline: blocks in order, contiguous per
 // group (assign_groups), each group padded to world*64 elements so every
 // rank's 1/world shard is 256-byte aligned.

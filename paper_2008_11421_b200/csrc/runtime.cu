@@ -170,134 +170,24 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
     if (!e.missing.empty()) throw std::runtime_error(e.missing);
 
   // --- static arena assignment from the base ledger (simulator.py:67-135) ---
-  EngineResult er = run_engine(base, base_resources(hw), hw.capacity_bytes, true);
-  if (er.deadlock) {
-    std::string s = "simulation deadlock; blocked ops: ";
-    for (size_t i = 0; i < er.blocked.size(); ++i) s += (i ? "; " : "") + er.blocked[i];
-    throw std::runtime_error(s);
+  std::map<int, size_t> bb;
+  for (auto& [id, bp] : blocks_) bb[id] = bp.act_bytes;
+  ArenaPlan ap = plan_arena(plan, model, hw, base, bb);
+  ledger_peak_ = (size_t)ap.ledger_peak;
+  arena_bytes_ = ap.arena_bytes;
+  instances_.clear();
+  for (auto& a : ap.inst) {
+    Instance in;
+    in.block = a.block;
+    in.off = a.off;
+    in.bytes = a.bytes;
+    in.alloc_op = a.alloc_op;
+    in.free_op = a.free_op;
+    instances_.push_back(in);
   }
-  ledger_peak_ = (size_t)er.peak;
-  std::map<int, int> cur;  // block -> live instance
-  std::vector<int> inst_of_alloc(base.size(), -1), inst_read(base.size(), -1);
-  for (size_t i = 0; i < base.size(); ++i) {
-    const EngineOp& e = base[i];
-    int b = e.block;
-    switch (e.action) {
-      case Action::FW:
-      case Action::RECOMPUTE_FW:
-      case Action::SWAP_IN: {
-        Instance in;
-        in.block = b;
-        in.bytes = blocks_.at(b).act_bytes;
-        in.alloc_op = (int)i;
-        inst_of_alloc[i] = (int)instances_.size();
-        cur[b] = (int)instances_.size();
-        instances_.push_back(in);
-        if (e.action == Action::FW && b >= 2 && plan.block(b - 1).recompute) {
-          auto it = cur.find(b - 1);
-          if (it != cur.end()) {  // recompute buffers discarded at the consumer's end
-            instances_[it->second].free_op = (int)i;
-            cur.erase(it);
-          }
-        }
-        break;
-      }
-      case Action::SWAP_OUT:
-      case Action::BW: {
-        auto it = cur.find(b);
-        if (it == cur.end()) throw std::runtime_error("block " + std::to_string(b) + " not resident");
-        inst_read[i] = it->second;
-        instances_[it->second].free_op = (int)i;
-        cur.erase(it);
-        break;
-      }
-      default:
-        break;
-    }
-  }
-  // event times of the base simulation
-  std::vector<double> t_start(base.size(), 0), t_end(base.size(), 0);
-  for (auto& ev : er.events) {
-    t_start[ev.op] = ev.t_start;
-    t_end[ev.op] = ev.t_end;
-  }
-  // sweep: frees at t_end, allocs at t_start; at equal time frees first
-  struct Ev { double t; int kind; int order; int inst; };  // kind 0 free, 1 alloc
-  std::vector<Ev> evs;
-  std::vector<int> rank_of(base.size(), 0);
-  for (size_t k = 0; k < er.start_order.size(); ++k) rank_of[er.start_order[k]] = (int)k;
-  for (size_t k = 0; k < instances_.size(); ++k) {
-    auto& in = instances_[k];
-    evs.push_back({t_start[in.alloc_op], 1, rank_of[in.alloc_op], (int)k});
-    if (in.free_op >= 0) evs.push_back({t_end[in.free_op], 0, rank_of[in.free_op], (int)k});
-  }
-  std::sort(evs.begin(), evs.end(), [](const Ev& a, const Ev& b) {
-    if (a.t != b.t) return a.t < b.t;
-    if (a.kind != b.kind) return a.kind < b.kind;
-    return a.order < b.order;
-  });
-  std::map<size_t, size_t> free_list;  // off -> bytes (coalesced)
-  size_t top = 0;
-  std::vector<int> live(instances_.size(), 0);
-  std::vector<std::vector<int>> arena_deps(base.size());
-  // history of freed regions: (off, bytes, free_op)
-  struct Freed { size_t off, bytes; int free_op; };
-  std::vector<Freed> freed;
-  std::vector<int> pending_free(instances_.size(), 0);
-  for (size_t ei = 0; ei < evs.size(); ++ei) {
-    Ev ev = evs[ei];
-    auto& in = instances_[ev.inst];
-    if (ev.kind == 0 && !live[ev.inst]) {
-      pending_free[ev.inst] = 1;  // zero-length op: free right after its alloc
-      continue;
-    }
-    if (ev.kind == 0) {
-      live[ev.inst] = 0;
-      freed.push_back({in.off, in.bytes, in.free_op});
-      size_t off = in.off, len = in.bytes;
-      auto nx = free_list.lower_bound(off);
-      if (nx != free_list.end() && off + len == nx->first) {
-        len += nx->second;
-        nx = free_list.erase(nx);
-      }
-      if (nx != free_list.begin()) {
-        auto pv = std::prev(nx);
-        if (pv->first + pv->second == off) {
-          off = pv->first;
-          len += pv->second;
-          free_list.erase(pv);
-        }
-      }
-      if (off + len == top) top = off;
-      else free_list[off] = len;
-    } else {
-      // best fit among free holes, else bump the top
-      size_t need = in.bytes;
-      auto best = free_list.end();
-      for (auto it = free_list.begin(); it != free_list.end(); ++it)
-        if (it->second >= need && (best == free_list.end() || it->second < best->second)) best = it;
-      if (best != free_list.end()) {
-        in.off = best->first;
-        size_t rest = best->second - need;
-        free_list.erase(best);
-        if (rest) free_list[in.off + need] = rest;
-      } else {
-        in.off = top;
-        top += need;
-      }
-      arena_bytes_ = std::max(arena_bytes_, top);
-      live[ev.inst] = 1;
-      // every earlier user of these bytes must have completed its freeing op
-      std::set<int> deps;
-      for (auto& f : freed)
-        if (f.off < in.off + in.bytes && in.off < f.off + f.bytes && f.free_op >= 0) deps.insert(f.free_op);
-      for (int d : deps) arena_deps[in.alloc_op].push_back(d);
-      if (pending_free[ev.inst]) {
-        pending_free[ev.inst] = 0;
-        evs.insert(evs.begin() + ei + 1, Ev{ev.t, 0, ev.order, ev.inst});
-      }
-    }
-  }
+  const std::vector<int>& inst_of_alloc = ap.inst_of_alloc;
+  const std::vector<int>& inst_read = ap.inst_read;
+  const std::vector<std::vector<int>>& arena_deps = ap.deps;
   if (arena_bytes_ == 0) arena_bytes_ = kAlign;
 
   // --- executor op lists: DP pipeline around the base ops -------------------

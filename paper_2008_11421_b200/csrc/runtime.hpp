@@ -115,7 +115,6 @@ class Runtime {
 
  private:
   void build_ops(const Plan& plan, const Model& model, const Hardware& hw);
-  void assign_arena(const Plan& plan, const Model& model, const Hardware& hw);
   void allocate();
   void issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* user, int step);
   void wait_deps(cudaStream_t s, const XOp& x, const std::vector<XOp>& ops);
@@ -137,7 +136,6 @@ class Runtime {
   std::vector<int> order_first_, order_steady_;
   std::vector<Instance> instances_;
   size_t arena_bytes_ = 0, ledger_peak_ = 0;
-  std::vector<size_t> instance_off_;
 
   // memory
   uint8_t* d_arena_ = nullptr;

@@ -65,9 +65,12 @@ class PlanBundle:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _lib.lib().krt_plan_free(h)
-            self._h = None
+        try:
+            if h is not None and h.value:
+                _lib.lib().krt_plan_free(h)
+        except Exception:   # interpreter shutdown
+            pass
+        self._h = None
 
     def set_capacity(self, capacity_bytes: float) -> "PlanBundle":
         _lib.check(_lib.lib().krt_plan_set_capacity(self._h, float(capacity_bytes)))
@@ -96,6 +99,13 @@ class PlanBundle:
         if "deadlock" in res:
             raise DeadlockError(res["deadlock"])
         return res
+
+    def arena(self, block_bytes) -> dict:
+        """Static arena assignment for physical slot sizes (krt_plan_arena)."""
+        arr = (C.c_size_t * len(block_bytes))(*block_bytes)
+        out = C.c_void_p()
+        _lib.check(_lib.lib().krt_plan_arena(self._h, arr, len(block_bytes), C.byref(out)))
+        return json.loads(_lib.take_string(out))
 
     def simulate_distributed(self, cfg: DistConfig, iterations: int = 3) -> dict:
         if iterations < 2:
