@@ -176,6 +176,7 @@ class Executor:
         _lib.check(L.krt_stream(self._ctx, 0, C.byref(s)))
         self.compute_stream = torch.cuda.ExternalStream(s.value, device=self.dev)
         self._cb = _lib.COMPUTE_CB(self._callback)
+        self._loss_ready = torch.cuda.Event()
         self.handoff = None       # (block, activation) between consecutive forwards
         self.grad_handoff = None  # (block, gradient) between backwards
         self.input = None
@@ -287,6 +288,7 @@ class Executor:
             if action == _lib.FW and b == self.nb:
                 self.loss, dy = self.loss_fn(x, self.target)
                 self.grad_handoff = (b, dy)
+                self._loss_ready.record(self.compute_stream)
         elif action == _lib.BW:
             if self.grad_handoff is None or self.grad_handoff[0] != b:
                 raise RuntimeError(f"backward of block {b} without its output gradient")
@@ -306,7 +308,12 @@ class Executor:
         # inputs were produced on the caller's stream
         self.compute_stream.wait_stream(torch.cuda.current_stream(self.dev))
         rc = _lib.lib().krt_run_iteration(self._ctx, self._cb, None)
-        torch.cuda.current_stream(self.dev).wait_stream(self.compute_stream)
+        # the caller's stream waits for the loss only, not for the backward
+        # still queued behind it, so the host can issue the next iteration
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_event(self._loss_ready)
+        if self.loss is not None:
+            self.loss.record_stream(cur)
         if self._error is not None:
             err, self._error = self._error, None
             raise err
