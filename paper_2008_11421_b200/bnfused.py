@@ -10,6 +10,28 @@ from . import _lib
 
 EPS = 1e-5
 
+# When a list, every launch appends (kind, algorithmic_bytes, start_event,
+# end_event) recorded on the launching stream — bench.py's live roofline.
+PROFILE = None
+
+
+class _timed:
+    def __init__(self, kind, nbytes):
+        self.kind, self.nbytes = kind, nbytes
+
+    def __enter__(self):
+        if PROFILE is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e1 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+        return self
+
+    def __exit__(self, *exc):
+        if PROFILE is not None:
+            self.e1.record()
+            PROFILE.append((self.kind, self.nbytes, self.e0, self.e1))
+        return False
+
 
 def _ptr(t):
     return None if t is None else t.data_ptr()
@@ -42,8 +64,9 @@ def stats(c, mean, invstd):
     """Batch statistics of c (N,C,H,W channels_last bf16) into fp32 mean/invstd."""
     rows, C = _rows_c(c)
     ws = _ws(C, c.device)
-    _lib.check(_lib.lib().krt_bn_stats(_nhwc(c).data_ptr(), rows, C, EPS, mean.data_ptr(),
-                                       invstd.data_ptr(), ws.data_ptr(), _stream()))
+    with _timed("bn_stats", rows * C * 2):
+        _lib.check(_lib.lib().krt_bn_stats(_nhwc(c).data_ptr(), rows, C, EPS, mean.data_ptr(),
+                                           invstd.data_ptr(), ws.data_ptr(), _stream()))
 
 
 def apply(c, mean, invstd, g, b, relu, res=None, rstats=None, rg=None, rb=None, out=None):
@@ -52,10 +75,11 @@ def apply(c, mean, invstd, g, b, relu, res=None, rstats=None, rg=None, rb=None, 
     rows, C = _rows_c(c)
     y = out if out is not None else torch.empty_like(c, memory_format=torch.channels_last)
     rm, ri = (rstats if rstats is not None else (None, None))
-    _lib.check(_lib.lib().krt_bn_apply(c.data_ptr(), mean.data_ptr(), invstd.data_ptr(), g.data_ptr(),
+    with _timed("bn_apply", rows * C * 2 * (2 if res is None else 3)):
+        _lib.check(_lib.lib().krt_bn_apply(c.data_ptr(), mean.data_ptr(), invstd.data_ptr(), g.data_ptr(),
                                        b.data_ptr(), _ptr(None if res is None else _nhwc(res)), _ptr(rm),
-                                       _ptr(ri), _ptr(rg), _ptr(rb), int(relu), y.data_ptr(), rows, C,
-                                       _stream()))
+                                           _ptr(ri), _ptr(rg), _ptr(rb), int(relu), y.data_ptr(), rows, C,
+                                           _stream()))
     return y
 
 
@@ -64,7 +88,8 @@ def add_relu_bwd(dy, c, mean, invstd, g, b, res, rstats=None, rg=None, rb=None):
     rows, C = _rows_c(c)
     dz = torch.empty_like(c, memory_format=torch.channels_last)
     rm, ri = (rstats if rstats is not None else (None, None))
-    _lib.check(_lib.lib().krt_bn_add_relu_bwd(dy.data_ptr(), c.data_ptr(), mean.data_ptr(),
+    with _timed("bn_add_relu_bwd", rows * C * 2 * 4):
+        _lib.check(_lib.lib().krt_bn_add_relu_bwd(dy.data_ptr(), c.data_ptr(), mean.data_ptr(),
                                               invstd.data_ptr(), g.data_ptr(), b.data_ptr(),
                                               res.data_ptr(), _ptr(rm), _ptr(ri), _ptr(rg), _ptr(rb),
                                               dz.data_ptr(), rows, C, _stream()))
@@ -77,7 +102,8 @@ def backward(dy, c, mean, invstd, g, b, relu, dgamma=None, dbeta=None, need_dx=T
     rows, C = _rows_c(c)
     dx = torch.empty_like(c, memory_format=torch.channels_last) if need_dx else None
     ws = _ws(C, c.device)
-    _lib.check(_lib.lib().krt_bn_backward(dy.data_ptr(), c.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+    with _timed("bn_backward", rows * C * 2 * (5 if need_dx else 2)):
+        _lib.check(_lib.lib().krt_bn_backward(dy.data_ptr(), c.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
                                           g.data_ptr(), b.data_ptr(), int(relu), _ptr(dx), _ptr(dgamma),
                                           _ptr(dbeta), rows, C, ws.data_ptr(), _stream()))
     return dx

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __
   Map m(C);
   int c0 = m.tx * 8;
   float s[8] = {0}, q[8] = {0};
+#pragma unroll 2
   for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
     Vec8 v = load8(x + r * C + c0);
 #pragma unroll
@@ -129,15 +130,38 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __
   }
 }
 
-__global__ void stats_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C, float eps,
-                               float* __restrict__ mean, float* __restrict__ invstd) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0, q = 0;
-  for (int b = 0; b < nblk; ++b) {
-    s += part[(size_t)b * 2 * C + c];
-    q += part[(size_t)b * 2 * C + C + c];
+// Sum CTA partials for 32 channels per block: lane = channel, the 8 warps
+// stride over the partial rows, then a fixed-order tree over the warps
+// (deterministic).  Returns the two double sums in lane c of warp 0.
+__device__ __forceinline__ bool sum_partials(const float* __restrict__ part, int nblk, int C, double& s1,
+                                             double& s2) {
+  __shared__ double sh[2][8][32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int c = blockIdx.x * 32 + lane;
+  double a = 0, q = 0;
+  if (c < C)
+    for (int b = w; b < nblk; b += 8) {
+      a += part[(size_t)b * 2 * C + c];
+      q += part[(size_t)b * 2 * C + C + c];
+    }
+  sh[0][w][lane] = a;
+  sh[1][w][lane] = q;
+  __syncthreads();
+  if (w != 0 || c >= C) return false;
+  s1 = 0;
+  s2 = 0;
+  for (int k = 0; k < 8; ++k) {
+    s1 += sh[0][k][lane];
+    s2 += sh[1][k][lane];
   }
+  return true;
+}
+
+__global__ void __launch_bounds__(256) stats_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
+                                                      float eps, float* __restrict__ mean, float* __restrict__ invstd) {
+  double s, q;
+  if (!sum_partials(part, nblk, C, s, q)) return;
+  int c = blockIdx.x * 32 + (threadIdx.x & 31);
   double mu = s / (double)rows;
   double var = q / (double)rows - mu * mu;
   if (var < 0) var = 0;
@@ -146,65 +170,96 @@ __global__ void stats_finalize(const float* __restrict__ part, int nblk, int64_t
 }
 
 // ---------------------------------------------------------------------------
-// mode: 0 none, 1 identity residual, 2 bn(residual)
+// mode: 0 none, 1 identity residual, 2 bn(residual).  Two rows in flight
+// per thread (all loads issued before the math) for memory-level parallelism.
+template <int MODE, bool RELU>
+__device__ __forceinline__ Vec8 apply_row(const Vec8& v, const Vec8& rv, const float* sc, const float* sh,
+                                          const float* rsc, const float* rsh) {
+  Vec8 o;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    o.v[k] = __fmaf_rn(v.v[k], sc[k], sh[k]);
+    if (MODE == 2) o.v[k] = __fadd_rn(o.v[k], __fmaf_rn(rv.v[k], rsc[k], rsh[k]));
+    if (MODE == 1) o.v[k] = __fadd_rn(o.v[k], rv.v[k]);
+    if (RELU) o.v[k] = fmaxf(o.v[k], 0.0f);
+  }
+  return o;
+}
+
+template <int MODE, bool RELU>
 __global__ void __launch_bounds__(kThreads) apply_kernel(
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ invstd,
     const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b, const __nv_bfloat16* __restrict__ res,
     const float* __restrict__ rmean, const float* __restrict__ rinvstd, const __nv_bfloat16* __restrict__ rg,
-    const __nv_bfloat16* __restrict__ rb_, int mode, int relu, __nv_bfloat16* __restrict__ y, int64_t rows, int C) {
+    const __nv_bfloat16* __restrict__ rb_, __nv_bfloat16* __restrict__ y, int64_t rows, int C) {
   Map m(C);
   int c0 = m.tx * 8;
   float sc[8], sh[8], rsc[8], rsh[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
-  if (mode == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
-  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
-    Vec8 v = load8(x + r * C + c0);
-    Vec8 o;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) o.v[k] = __fmaf_rn(v.v[k], sc[k], sh[k]);
-    if (mode != 0) {
-      Vec8 rv = load8(res + r * C + c0);
-      if (mode == 2) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) o.v[k] = __fadd_rn(o.v[k], __fmaf_rn(rv.v[k], rsc[k], rsh[k]));
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) o.v[k] = __fadd_rn(o.v[k], rv.v[k]);
-      }
+  if (MODE == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
+  const int64_t step = (int64_t)gridDim.x * m.rb;
+  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
+  Vec8 z{};
+  for (; r + step < rows; r += 2 * step) {
+    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
+    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
+    Vec8 q0 = z, q1 = z;
+    if (MODE != 0) {
+      q0 = load8(res + o0);
+      q1 = load8(res + o1);
     }
-    if (relu) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) o.v[k] = fmaxf(o.v[k], 0.0f);
-    }
-    store8(y + r * C + c0, o);
+    store8(y + o0, apply_row<MODE, RELU>(v0, q0, sc, sh, rsc, rsh));
+    store8(y + o1, apply_row<MODE, RELU>(v1, q1, sc, sh, rsc, rsh));
+  }
+  if (r < rows) {
+    const int64_t o0 = r * C + c0;
+    Vec8 v0 = load8(x + o0), q0 = z;
+    if (MODE != 0) q0 = load8(res + o0);
+    store8(y + o0, apply_row<MODE, RELU>(v0, q0, sc, sh, rsc, rsh));
   }
 }
 
-// dz = dy * ( bn(x) [+ res | + bn'(res)] > 0 )   (backward of the add + ReLU)
+// dz = dy * ( bn(x) [+ res | + bn'(res)] > 0 )   (backward of the add + ReLU);
+// the forward sum is re-rounded to bf16 exactly as apply_kernel stored it
+template <int MODE>
+__device__ __forceinline__ Vec8 add_relu_row(const Vec8& v, const Vec8& rv, const Vec8& d, const float* sc,
+                                             const float* sh, const float* rsc, const float* rsh) {
+  Vec8 o;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float pre = __fadd_rn(__fmaf_rn(v.v[k], sc[k], sh[k]), MODE == 2 ? __fmaf_rn(rv.v[k], rsc[k], rsh[k]) : rv.v[k]);
+    float yk = __bfloat162float(__float2bfloat16_rn(pre));
+    o.v[k] = yk > 0.0f ? d.v[k] : 0.0f;
+  }
+  return o;
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kThreads) add_relu_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
     const __nv_bfloat16* __restrict__ res, const float* __restrict__ rmean, const float* __restrict__ rinvstd,
-    const __nv_bfloat16* __restrict__ rg, const __nv_bfloat16* __restrict__ rb_, int mode,
-    __nv_bfloat16* __restrict__ dz, int64_t rows, int C) {
+    const __nv_bfloat16* __restrict__ rg, const __nv_bfloat16* __restrict__ rb_, __nv_bfloat16* __restrict__ dz,
+    int64_t rows, int C) {
   Map m(C);
   int c0 = m.tx * 8;
   float sc[8], sh[8], rsc[8], rsh[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
-  if (mode == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
-  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
-    Vec8 v = load8(x + r * C + c0);
-    Vec8 rv = load8(res + r * C + c0);
-    Vec8 d = load8(dy + r * C + c0);
-    Vec8 o;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      // round the forward sum to bf16 exactly like the forward did
-      float pre = __fadd_rn(__fmaf_rn(v.v[k], sc[k], sh[k]), mode == 2 ? __fmaf_rn(rv.v[k], rsc[k], rsh[k]) : rv.v[k]);
-      float yk = __bfloat162float(__float2bfloat16_rn(pre));
-      o.v[k] = yk > 0.0f ? d.v[k] : 0.0f;
-    }
-    store8(dz + r * C + c0, o);
+  if (MODE == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
+  const int64_t step = (int64_t)gridDim.x * m.rb;
+  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
+  for (; r + step < rows; r += 2 * step) {
+    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
+    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
+    Vec8 q0 = load8(res + o0), q1 = load8(res + o1);
+    Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
+    store8(dz + o0, add_relu_row<MODE>(v0, q0, d0, sc, sh, rsc, rsh));
+    store8(dz + o1, add_relu_row<MODE>(v1, q1, d1, sc, sh, rsc, rsh));
+  }
+  if (r < rows) {
+    const int64_t o0 = r * C + c0;
+    Vec8 v0 = load8(x + o0), q0 = load8(res + o0), d0 = load8(dy + o0);
+    store8(dz + o0, add_relu_row<MODE>(v0, q0, d0, sc, sh, rsc, rsh));
   }
 }
 
@@ -224,6 +279,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
     is[k] = invstd[c0 + k];
   }
   float s1[8] = {0}, s2[8] = {0};
+#pragma unroll 2
   for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
     Vec8 v = load8(x + r * C + c0);
     Vec8 d = load8(dy + r * C + c0);
@@ -252,15 +308,12 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
 
 // dbeta = sum(gm), dgamma = sum(gm*xhat)  (fp32, written straight into the
 // gradient region); coef = (dbeta/N, dgamma/N) for the elementwise pass
-__global__ void bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
-                             float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ coef) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s1 = 0, s2 = 0;
-  for (int b = 0; b < nblk; ++b) {
-    s1 += part[(size_t)b * 2 * C + c];
-    s2 += part[(size_t)b * 2 * C + C + c];
-  }
+__global__ void __launch_bounds__(256) bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
+                                                    float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                    float* __restrict__ coef) {
+  double s1, s2;
+  if (!sum_partials(part, nblk, C, s1, s2)) return;
+  int c = blockIdx.x * 32 + (threadIdx.x & 31);
   if (dbeta) dbeta[c] = (float)s1;
   if (dgamma) dgamma[c] = (float)s2;
   coef[c] = (float)(s1 / (double)rows);
@@ -268,10 +321,29 @@ __global__ void bwd_finalize(const float* __restrict__ part, int nblk, int64_t r
 }
 
 // dx = gamma*invstd * (gm - mean(gm) - xhat * mean(gm*xhat))
+template <bool RELU>
+__device__ __forceinline__ Vec8 bwd_row(const Vec8& v, const Vec8& d, const float* sc, const float* sh,
+                                        const float* mu, const float* is, const float* k1, const float* k2,
+                                        const float* gs) {
+  Vec8 o;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float gm = d.v[k];
+    if (RELU) {
+      float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
+      gm = yk > 0.0f ? gm : 0.0f;
+    }
+    float xh = (v.v[k] - mu[k]) * is[k];
+    o.v[k] = gs[k] * (gm - k1[k] - xh * k2[k]);
+  }
+  return o;
+}
+
+template <bool RELU>
 __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
-    int relu, const float* __restrict__ coef, __nv_bfloat16* __restrict__ dx, int64_t rows, int C) {
+    const float* __restrict__ coef, __nv_bfloat16* __restrict__ dx, int64_t rows, int C) {
   Map m(C);
   int c0 = m.tx * 8;
   float sc[8], sh[8], mu[8], is[8], k1[8], k2[8], gs[8];
@@ -284,21 +356,19 @@ __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     k2[k] = coef[C + c0 + k];
     gs[k] = bf(g, c0 + k) * is[k];
   }
-  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
-    Vec8 v = load8(x + r * C + c0);
-    Vec8 d = load8(dy + r * C + c0);
-    Vec8 o;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float gm = d.v[k];
-      if (relu) {
-        float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
-        gm = yk > 0.0f ? gm : 0.0f;
-      }
-      float xh = (v.v[k] - mu[k]) * is[k];
-      o.v[k] = gs[k] * (gm - k1[k] - xh * k2[k]);
-    }
-    store8(dx + r * C + c0, o);
+  const int64_t step = (int64_t)gridDim.x * m.rb;
+  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
+  for (; r + step < rows; r += 2 * step) {
+    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
+    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
+    Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
+    store8(dx + o0, bwd_row<RELU>(v0, d0, sc, sh, mu, is, k1, k2, gs));
+    store8(dx + o1, bwd_row<RELU>(v1, d1, sc, sh, mu, is, k1, k2, gs));
+  }
+  if (r < rows) {
+    const int64_t o0 = r * C + c0;
+    Vec8 v0 = load8(x + o0), d0 = load8(dy + o0);
+    store8(dx + o0, bwd_row<RELU>(v0, d0, sc, sh, mu, is, k1, k2, gs));
   }
 }
 
@@ -339,7 +409,7 @@ cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean,
   int grid = grid_rows(stats_kernel, reduce_smem(C), rows, C);
   float* part = static_cast<float*>(ws);
   stats_kernel<<<grid, kThreads, reduce_smem(C), s>>>(static_cast<const __nv_bfloat16*>(x), rows, C, part);
-  stats_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, grid, rows, C, eps, mean, invstd);
+  stats_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, grid, rows, C, eps, mean, invstd);
   return cudaGetLastError();
 }
 
@@ -348,11 +418,20 @@ cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, cons
                      int relu, void* y, int64_t rows, int C, cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
   int mode = res == nullptr ? 0 : (rmean == nullptr ? 1 : 2);
-  apply_kernel<<<grid_rows(apply_kernel, 0, rows, C), kThreads, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(x), mean, invstd, static_cast<const __nv_bfloat16*>(g),
-      static_cast<const __nv_bfloat16*>(b), static_cast<const __nv_bfloat16*>(res), rmean, rinvstd,
-      static_cast<const __nv_bfloat16*>(rg), static_cast<const __nv_bfloat16*>(rb), mode, relu,
-      static_cast<__nv_bfloat16*>(y), rows, C);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto G = static_cast<const __nv_bfloat16*>(g);
+  auto B = static_cast<const __nv_bfloat16*>(b);
+  auto R = static_cast<const __nv_bfloat16*>(res);
+  auto RG = static_cast<const __nv_bfloat16*>(rg);
+  auto RB = static_cast<const __nv_bfloat16*>(rb);
+  auto Y = static_cast<__nv_bfloat16*>(y);
+#define KRT_APPLY(M, RL)                                                                              \
+  apply_kernel<M, RL><<<grid_rows(apply_kernel<M, RL>, 0, rows, C), kThreads, 0, s>>>(X, mean, invstd, G, B, R, \
+                                                                                      rmean, rinvstd, RG, RB, Y, rows, C)
+  if (mode == 0) { if (relu) KRT_APPLY(0, true); else KRT_APPLY(0, false); }
+  else if (mode == 1) { if (relu) KRT_APPLY(1, true); else KRT_APPLY(1, false); }
+  else { if (relu) KRT_APPLY(2, true); else KRT_APPLY(2, false); }
+#undef KRT_APPLY
   return cudaGetLastError();
 }
 
@@ -360,12 +439,15 @@ cudaError_t bn_add_relu_bwd(const void* dy, const void* x, const float* mean, co
                             const void* b, const void* res, const float* rmean, const float* rinvstd,
                             const void* rg, const void* rb, void* dz, int64_t rows, int C, cudaStream_t s) {
   if (!shape_ok(rows, C) || res == nullptr) return cudaErrorInvalidValue;
-  int mode = rmean == nullptr ? 1 : 2;
-  add_relu_bwd_kernel<<<grid_rows(add_relu_bwd_kernel, 0, rows, C), kThreads, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
-      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b),
-      static_cast<const __nv_bfloat16*>(res), rmean, rinvstd, static_cast<const __nv_bfloat16*>(rg),
-      static_cast<const __nv_bfloat16*>(rb), mode, static_cast<__nv_bfloat16*>(dz), rows, C);
+  auto args = [&](auto kernel) {
+    kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
+        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b),
+        static_cast<const __nv_bfloat16*>(res), rmean, rinvstd, static_cast<const __nv_bfloat16*>(rg),
+        static_cast<const __nv_bfloat16*>(rb), static_cast<__nv_bfloat16*>(dz), rows, C);
+  };
+  if (rmean == nullptr) args(add_relu_bwd_kernel<1>);
+  else args(add_relu_bwd_kernel<2>);
   return cudaGetLastError();
 }
 
@@ -379,12 +461,17 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
   bwd_reduce_kernel<<<grid, kThreads, reduce_smem(C), s>>>(
       static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
       static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), relu, rows, C, part);
-  bwd_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
-  if (dx)
-    bwd_elemt_kernel<<<grid_rows(bwd_elemt_kernel, 0, rows, C), kThreads, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
-        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), relu, coef,
-        static_cast<__nv_bfloat16*>(dx), rows, C);
+  bwd_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
+  if (dx) {
+    auto launch = [&](auto kernel) {
+      kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(
+          static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
+          static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), coef,
+          static_cast<__nv_bfloat16*>(dx), rows, C);
+    };
+    if (relu) launch(bwd_elemt_kernel<true>);
+    else launch(bwd_elemt_kernel<false>);
+  }
   return cudaGetLastError();
 }
 
