@@ -106,14 +106,34 @@ def dist_env():
 # ---------------------------------------------------------------------------
 # CPU reference arm / cpu_baseline: in-core fp32 torch CPU training step
 # ---------------------------------------------------------------------------
-def cpu_reference(rec, steps, warmup, sample_batch=4):
+def cpu_sample_batch(rec):
+    # bounded CPU sample: ~10-30 s of host work
+    return 4 if rec["meta"]["res"] <= 256 else 1
+
+
+def cpu_sample_note(rec):
+    return "" if rec["meta"]["res"] <= 256 else " at 512x512, scaled by the pixel ratio 1/16"
+
+
+def cpu_reference(rec, steps, warmup, sample_batch=None):
     import torch
 
     from oracle import resnet_oracle
     from paper_2008_11421_b200 import workloads as W
 
     torch.set_num_threads(os.cpu_count() or 1)
+    sample_batch = sample_batch or cpu_sample_batch(rec)
     units = W.units_for(rec)
+    scale = 1.0
+    if rec["meta"]["res"] > 256:
+        # in-core fp32 at 2048^2 needs ~314 GB of host RAM per image: time the
+        # same network on 512^2 images and scale by the pixel ratio (FLOPs and
+        # bytes of these convnets are linear in the pixel count)
+        from paper_2008_11421_b200 import units as U
+        m = dict(rec["meta"], res=512)
+        scale = (512 / rec["meta"]["res"]) ** 2
+        units = U.resnet1001_units(512, m["classes"], m["depth"], act_dtype=torch.float32)
+        rec = dict(rec, meta=m)
     m = rec["meta"]
     gen = torch.Generator().manual_seed(0)
     init = {i + 1: [t.float() for t in u.init_params(gen)] for i, u in enumerate(units)}
@@ -135,7 +155,18 @@ def cpu_reference(rec, steps, warmup, sample_batch=4):
     for _ in range(steps):
         step()
     dt = time.perf_counter() - t0
-    return sample_batch * steps / dt, torch.get_num_threads(), dt
+    return sample_batch * steps / dt * scale, torch.get_num_threads(), dt
+
+
+def model_name(rec):
+    m = rec["meta"]
+    return f"resnet{m['depth']}" if "depth" in m else rec["name"]
+
+
+def metric_name(rec):
+    m = rec["meta"]
+    return (f"samples/sec ({model_name(rec)} {m['res']}x{m['res']} training step, per-GPU batch "
+            f"beyond HBM)")
 
 
 def run_reference(args, rec):
@@ -146,15 +177,15 @@ def run_reference(args, rec):
     value, cores, dt = cpu_reference(rec, steps, warmup)
     m = rec["meta"]
     line = {
-        "metric": "samples/sec (ResNet-200 224x224 training step, per-GPU batch beyond HBM)",
+        "metric": metric_name(rec),
         "impl": "reference", "value": value, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warmup, "ms_per_step": dt / steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": rec["name"], "model": "resnet200",
+        "data": "synthetic", "config": {"workload": rec["name"], "model": model_name(rec),
                                          "per_gpu_batch": m["batch"], "image": m["res"]},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": "in-core fp32 torch-CPU ResNet-200 step (oracle/resnet_oracle.py) "
-                                   "on 4 images per step"},
+                         "sample": f"in-core fp32 torch-CPU {model_name(rec)} step (oracle/resnet_oracle.py) "
+                                   f"on {cpu_sample_batch(rec)} images per step{cpu_sample_note(rec)}"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -307,11 +338,11 @@ def run_gpu(args, rec):
                    "frac_of_hbm": v[0] / v[1] / 1e9 / pk["hbm_gbs"]} for k, v in fam.items() if v[1] > 0}
     dom = max(fam, key=lambda k: fam[k][1]) if fam else None
     line = {
-        "metric": "samples/sec (ResNet-200 224x224 training step, per-GPU batch beyond HBM)",
+        "metric": metric_name(rec),
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": rec["name"], "model": "resnet200", "per_gpu_batch": batch,
+        "config": {"workload": rec["name"], "model": model_name(rec), "per_gpu_batch": batch,
                    "global_batch": batch * world, "image": res, "parallelism": f"dp{world}",
                    "plan": rec["plan_string"][:160] + " ...",
                    "activations_bytes": rec["total_bytes"], "hbm_bytes": 183359 * 2 ** 20,
@@ -353,8 +384,9 @@ def run_gpu(args, rec):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, dt = cpu_reference(rec, steps=2, warmup=1)
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
-                                "sample": "in-core fp32 torch-CPU ResNet-200 step "
-                                          "(oracle/resnet_oracle.py), 4 images x 2 steps"}
+                                "sample": f"in-core fp32 torch-CPU {model_name(rec)} step "
+                                          f"(oracle/resnet_oracle.py), {cpu_sample_batch(rec)} images x 2 steps"
+                                          f"{cpu_sample_note(rec)}"}
     if args.trace_out and rank == 0:
         Path(args.trace_out).write_text(trace)
     if rank == 0:

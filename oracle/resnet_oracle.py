@@ -2,7 +2,8 @@
 bottleneck-ResNet units (cfg1/cfg2 model family).
 
 A plain autograd model (conv / batch-stat BatchNorm / ReLU / residual add,
-stride on the 3x3 conv) rebuilt from the same parameter tensors the executor
+stride on the 3x3 conv) (post-activation ImageNet bottleneck and the pre-activation CIFAR bottleneck of
+ResNet-1001) rebuilt from the same parameter tensors the executor
 holds (its conv weights are stored O-H-W-I; converted here to O-I-H-W).  The
 reference has no tensor code (numerics parity unpinned); this is
 the in-core result the out-of-core executor must reproduce.
@@ -25,7 +26,8 @@ def _bn(x, g, b):
 
 def forward(units, params, x):
     """params: unit index (1-based) -> list of fp32 CPU tensors requiring grad."""
-    from paper_2008_11421_b200.units import BottleneckUnit, HeadUnit, StemUnit
+    from paper_2008_11421_b200.units import (BottleneckUnit, CifarStemUnit, HeadUnit,
+                                             PreActBottleneckUnit, PreActHeadUnit, StemUnit)
     h = x
     for k, u in enumerate(units, start=1):
         p = params[k]
@@ -41,6 +43,16 @@ def forward(units, params, x):
             h = F.relu(o + idn)
         elif isinstance(u, HeadUnit):
             h = h.mean(dim=(2, 3)) @ p[0].t() + p[1]
+        elif isinstance(u, CifarStemUnit):
+            h = F.conv2d(h, _w(p[0]), padding=1)
+        elif isinstance(u, PreActBottleneckUnit):
+            a0 = F.relu(_bn(h, p[0], p[1]))
+            o = F.conv2d(a0, _w(p[2]))
+            o = F.conv2d(F.relu(_bn(o, p[3], p[4])), _w(p[5]), stride=u.s, padding=1)
+            o = F.conv2d(F.relu(_bn(o, p[6], p[7])), _w(p[8]))
+            h = o + (F.conv2d(a0, _w(p[9]), stride=u.s) if u.down else h)
+        elif isinstance(u, PreActHeadUnit):
+            h = F.relu(_bn(h, p[0], p[1])).mean(dim=(2, 3)) @ p[2].t() + p[3]
         else:
             raise TypeError(type(u))
     return h

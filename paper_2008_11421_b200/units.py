@@ -507,3 +507,251 @@ def resnet_units(depth: int = 200, res: int = 224, classes: int = 1000, stages=N
     for u in units:
         u.act = act_dtype
     return units
+
+
+# ---------------------------------------------------------------------------
+# Pre-activation bottleneck ResNet (He et al. 2016, "Identity Mappings"):
+# ResNet-1001 for CIFAR-style inputs, cfg2 = 2048x2048 images.
+# unit: a0 = relu(bn0(x)); c1 = conv1x1(a0); c2 = conv3x3/s(relu(bn1(c1)));
+#       y = conv1x1(relu(bn2(c2))) + (x | conv1x1/s(a0)).
+# Saved: x, c1, c2 and the three BN statistics; a0/a1/a2 are recomputed in
+# backward and c3 is never needed (no BN after the last conv).
+# ---------------------------------------------------------------------------
+def _stats_fw(c, st_m, st_i):
+    """Batch statistics into (mean, invstd) views; fused kernel for bf16."""
+    if c.dtype == torch.bfloat16 and bnfused.supported(c.shape[1]):
+        bnfused.stats(c, st_m, st_i)
+    else:
+        m = c.float().mean(dim=(0, 2, 3))
+        v = c.float().var(dim=(0, 2, 3), unbiased=False)
+        st_m.copy_(m)
+        st_i.copy_(torch.rsqrt(v + BN_EPS))
+
+
+def _bn_relu(c, m, i, g, b):
+    if c.dtype == torch.bfloat16 and bnfused.supported(c.shape[1]):
+        return bnfused.apply(c, m, i, g, b, relu=True)
+    return _bn_apply(c, g, b, m, i).relu_()
+
+
+def _bn_relu_bw(da, c, m, i, g, b, dg, db):
+    """Backward through relu(bn(c)) given d(relu output); writes dgamma/dbeta."""
+    if c.dtype == torch.bfloat16 and bnfused.supported(c.shape[1]):
+        return bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=dg, dbeta=db)
+    a = _bn_apply(c, g, b, m, i).relu_()
+    dpre = _aten.threshold_backward(da, a, 0)
+    dc, dgg, dbb = _bn_bw(dpre, c, g, m, i)
+    dg.copy_(dgg)
+    db.copy_(dbb)
+    return dc
+
+
+class PreActBottleneckUnit(_ConvNetUnit):
+    name = "preact_bottleneck"
+
+    def __init__(self, cin, width, stride, side_in):
+        self.cin, self.w, self.s = cin, width, stride
+        self.cout = 4 * width
+        self.hi, self.ho = side_in, side_in // stride
+        self.down = stride != 1 or cin != self.cout
+
+    def param_specs(self):
+        p = [(self.cin,), (self.cin,), (self.w, 1, 1, self.cin),
+             (self.w,), (self.w,), (self.w, 3, 3, self.w),
+             (self.w,), (self.w,), (self.cout, 1, 1, self.w)]
+        if self.down:
+            p.append((self.cout, 1, 1, self.cin))
+        return p
+
+    def _nstats(self):
+        return 2 * (self.cin + 2 * self.w)
+
+    def saved_specs(self, n):
+        return [SavedSpec((n, self.hi, self.hi, self.cin), self.act),
+                SavedSpec((n, self.hi, self.hi, self.w), self.act),
+                SavedSpec((n, self.ho, self.ho, self.w), self.act),
+                SavedSpec((self._nstats(),), torch.float32)]
+
+    def init_params(self, gen):
+        out = []
+        for shp in self.param_specs():
+            if len(shp) == 4:
+                out.append(_kaiming(shp, gen))
+            else:
+                out.append(torch.ones(shp) if len(out) % 3 == 0 else torch.zeros(shp))
+        return out
+
+    def _st(self, st):
+        k = [self.cin, self.cin, self.w, self.w, self.w, self.w]
+        v, o = [], 0
+        for n in k:
+            v.append(st[o:o + n])
+            o += n
+        return v
+
+    def forward(self, x, params, saved):
+        g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+            st = self._st(saved[3])
+        else:
+            st = self._st(torch.empty(self._nstats(), device=x.device))
+        sv = (lambda k: None) if saved is None else (lambda k: _cl(saved[k]))
+        _stats_fw(x, st[0], st[1])
+        a0 = _bn_relu(x, st[0], st[1], g0, b0)
+        c1 = _conv_into(a0, _cl(w1), 1, 0, sv(1))
+        sc = _conv(a0, _cl(params[9]), self.s, 0) if self.down else x
+        del a0
+        _stats_fw(c1, st[2], st[3])
+        a1 = _bn_relu(c1, st[2], st[3], g1, b1)
+        c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
+        del a1
+        _stats_fw(c2, st[4], st[5])
+        a2 = _bn_relu(c2, st[4], st[5], g2, b2)
+        y = _conv(a2, _cl(w3), 1, 0)
+        return y.add_(sc)
+
+    def backward(self, dy, params, saved, grads):
+        g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
+        x, c1, c2 = (_cl(t) for t in saved[:3])
+        st = self._st(saved[3])
+        a2 = _bn_relu(c2, st[4], st[5], g2, b2)
+        da2, dw3, _ = _conv_bw(dy, a2, _cl(w3), 1, 0)
+        del a2
+        _cl(grads[8]).copy_(dw3)
+        dc2 = _bn_relu_bw(da2, c2, st[4], st[5], g2, b2, grads[6], grads[7])
+        del da2
+        a1 = _bn_relu(c1, st[2], st[3], g1, b1)
+        da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
+        del dc2, a1
+        _cl(grads[5]).copy_(dw2)
+        dc1 = _bn_relu_bw(da1, c1, st[2], st[3], g1, b1, grads[3], grads[4])
+        del da1
+        a0 = _bn_relu(x, st[0], st[1], g0, b0)
+        da0, dw1, _ = _conv_bw(dc1, a0, _cl(w1), 1, 0)
+        del dc1
+        _cl(grads[2]).copy_(dw1)
+        if self.down:
+            das, dws, _ = _conv_bw(dy, a0, _cl(params[9]), self.s, 0)
+            _cl(grads[9]).copy_(dws)
+            da0.add_(das)
+            dx = _bn_relu_bw(da0, x, st[0], st[1], g0, b0, grads[0], grads[1])
+        else:
+            dx = _bn_relu_bw(da0, x, st[0], st[1], g0, b0, grads[0], grads[1])
+            dx.add_(dy)
+        return dx
+
+    def fwd_flops(self, n):
+        macs = (self.hi ** 2 * self.cin * self.w + self.ho ** 2 * 9 * self.w * self.w
+                + self.ho ** 2 * self.w * self.cout)
+        if self.down:
+            macs += self.ho ** 2 * self.cin * self.cout
+        return 2.0 * n * macs
+
+    def ir_line(self, lid, batch, analytic=False):
+        params = sum(math.prod(p) for p in self.param_specs() if len(p) == 4)
+        return self._ir(lid, batch, f"Conv Wout={self.ho} Hout={self.ho} Cin=1 Cout={params} K=1")
+
+
+class CifarStemUnit(_ConvNetUnit):
+    """conv3x3 (3 -> 16), no BN/ReLU (the pre-activation units normalise)."""
+
+    name = "cifar_stem"
+
+    def __init__(self, res, cout=16):
+        self.res, self.cout = res, cout
+
+    def param_specs(self):
+        return [(self.cout, 3, 3, 3)]
+
+    def saved_specs(self, n):
+        return [SavedSpec((n, self.res, self.res, 3), self.act)]
+
+    def init_params(self, gen):
+        return [_kaiming((self.cout, 3, 3, 3), gen)]
+
+    def forward(self, x, params, saved):
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+        return _conv(x, _cl(params[0]), 1, 1)
+
+    def backward(self, dy, params, saved, grads):
+        _, dw, _ = _conv_bw(dy, _cl(saved[0]), _cl(params[0]), 1, 1, need_dx=False)
+        _cl(grads[0]).copy_(dw)
+        return None
+
+    def fwd_flops(self, n):
+        return 2.0 * n * self.res * self.res * self.cout * 27
+
+    def ir_line(self, lid, batch, analytic=False):
+        return self._ir(lid, batch, f"Conv Wout={self.res} Hout={self.res} Cin=3 Cout={self.cout} K=3")
+
+
+class PreActHeadUnit(_ConvNetUnit):
+    """relu(bn(x)) -> global average pool -> FullyConnected (bias)."""
+
+    name = "preact_head"
+
+    def __init__(self, cin, classes, side):
+        self.cin, self.k, self.side = cin, classes, side
+
+    def param_specs(self):
+        return [(self.cin,), (self.cin,), (self.k, self.cin), (self.k,)]
+
+    def saved_specs(self, n):
+        return [SavedSpec((n, self.side, self.side, self.cin), self.act),
+                SavedSpec((2 * self.cin,), torch.float32)]
+
+    def init_params(self, gen):
+        bound = 1.0 / math.sqrt(self.cin)
+        return [torch.ones(self.cin), torch.zeros(self.cin),
+                torch.empty(self.k, self.cin).uniform_(-bound, bound, generator=gen),
+                torch.empty(self.k).uniform_(-bound, bound, generator=gen)]
+
+    def forward(self, x, params, saved):
+        g, b, w, bias = params
+        st = saved[1] if saved is not None else torch.empty(2 * self.cin, device=x.device)
+        if saved is not None:
+            _cl(saved[0]).copy_(x)
+        _stats_fw(x, st[:self.cin], st[self.cin:])
+        a = _bn_relu(x, st[:self.cin], st[self.cin:], g, b)
+        p = a.float().mean(dim=(2, 3)).to(a.dtype)
+        return torch.addmm(bias, p, w.t())
+
+    def backward(self, dy, params, saved, grads):
+        g, b, w, bias = params
+        x, st = _cl(saved[0]), saved[1]
+        a = _bn_relu(x, st[:self.cin], st[self.cin:], g, b)
+        p = a.float().mean(dim=(2, 3)).to(a.dtype)
+        grads[2].copy_(torch.mm(dy.t(), p, out_dtype=torch.float32) if dy.dtype != torch.float32
+                       else torch.mm(dy.t(), p))
+        grads[3].copy_(dy.float().sum(0))
+        dp = torch.mm(dy, w) * (1.0 / (self.side * self.side))
+        n = dp.shape[0]
+        da = dp[:, :, None, None].expand(n, self.cin, self.side, self.side).contiguous(
+            memory_format=torch.channels_last)
+        return _bn_relu_bw(da, x, st[:self.cin], st[self.cin:], g, b, grads[0], grads[1])
+
+    def fwd_flops(self, n):
+        return 2.0 * n * self.cin * self.k
+
+    def ir_line(self, lid, batch, analytic=False):
+        return self._ir(lid, batch, f"FullyConnected X={self.cin} Y={self.k}")
+
+
+def resnet1001_units(res: int = 2048, classes: int = 10, depth: int = 1001, act_dtype=torch.bfloat16):
+    """CIFAR-style pre-activation bottleneck ResNet: (depth-2)/9 units per stage, widths 16/32/64."""
+    per = (depth - 2) // 9
+    units = [CifarStemUnit(res, 16)]
+    side, cin = res, 16
+    for si in range(3):
+        width = 16 * 2 ** si
+        for k in range(per):
+            stride = 2 if (k == 0 and si > 0) else 1
+            units.append(PreActBottleneckUnit(cin, width, stride, side))
+            side //= stride
+            cin = 4 * width
+    units.append(PreActHeadUnit(cin, classes, side))
+    for u in units:
+        u.act = act_dtype
+    return units

@@ -28,7 +28,7 @@ from oocsched.plan import plan_string, plan_to_dict  # noqa: E402
 from oocsched.planner import plan_model  # noqa: E402
 from oocsched.simulator import simulate  # noqa: E402
 
-from paper_2008_11421_b200.units import model_text, resnet_units  # noqa: E402
+from paper_2008_11421_b200.units import model_text, resnet1001_units, resnet_units  # noqa: E402
 
 OUT = ROOT / "paper_2008_11421_b200" / "plans"
 
@@ -91,6 +91,17 @@ def main():
         make(f"resnet_small_{tag}", units, batch, frac * tot,
              {"family": "resnet", "stages": [1, 2, 2, 1], "res": 64, "classes": 10,
               "act": tag.split("_")[0]}, interconnect_bw=1e9, compute_rate=1e11)
+    # pre-activation CIFAR ResNet (ResNet-1001 family), small parity instances
+    for act, tag in ((torch.float32, "f32"), (torch.bfloat16, "bf16")):
+        units = resnet1001_units(res=32, classes=10, depth=29, act_dtype=act)
+        tot = total_saved(units, 4)
+        make(f"preact29_small_{tag}", units, 4, 0.62 * tot,
+             {"family": "preact", "depth": 29, "res": 32, "classes": 10, "act": tag},
+             interconnect_bw=1e9, compute_rate=1e11)
+    # cfg2: ResNet-1001 on 2048x2048 images, batch 2 = 314 GB of activations
+    units = resnet1001_units(res=2048, classes=10, depth=1001)
+    make("resnet1001_2048_b2", units, 2, 150e9,
+         {"family": "preact", "depth": 1001, "res": 2048, "classes": 10, "act": "bf16"}, max_blocks=64)
     # cfg1: ResNet-200 224x224, per-GPU batch sized so activations exceed HBM
     units = resnet_units(200)
     # max_blocks (plan_model's own bound, cli --max-blocks) steers the reference

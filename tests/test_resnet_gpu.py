@@ -94,3 +94,28 @@ def test_resnet_bf16_fused_tracks_fp32_oracle():
     xs, ys = batches(rec, 3)
     ref_losses, ref_w = resnet_oracle.train(units, init, xs, ys, lr=0.05)
     torch.testing.assert_close(torch.tensor(losses), torch.tensor(ref_losses), rtol=3e-2, atol=3e-2)
+
+
+def test_preact_plan_matches_cpu_oracle():
+    rec = W.load("preact29_small_f32")
+    assert any(b["recompute"] for b in rec["plan"]["blocks"])
+    units, init, losses, w, stats = run(rec)
+    xs, ys = batches(rec, 3)
+    ref_losses, ref_w = resnet_oracle.train(units, init, xs, ys, lr=0.1)
+    torch.testing.assert_close(torch.tensor(losses), torch.tensor(ref_losses), rtol=2e-4, atol=2e-5)
+    for k in ref_w:
+        for got, ref in zip(w[k], ref_w[k]):
+            torch.testing.assert_close(got.cpu().float(), ref, rtol=2e-3, atol=2e-4)
+
+
+def test_preact_bf16_out_of_core_equals_in_core_and_tracks_oracle():
+    rec = W.load("preact29_small_bf16")
+    units, init, l_ooc, w_ooc, s_ooc = run(rec, iters=3, lr=0.05)
+    _, _, l_inc, w_inc, _ = run(rec, plan=W.incore_plan(rec["plan"]), iters=3, lr=0.05, capacity=1e12)
+    assert s_ooc["iter_bytes_h2d"] > 0 and l_ooc == l_inc
+    for k in w_inc:
+        for a, b in zip(w_ooc[k], w_inc[k]):
+            assert torch.equal(a, b), k
+    xs, ys = batches(rec, 3)
+    ref_losses, _ = resnet_oracle.train(units, init, xs, ys, lr=0.05)
+    torch.testing.assert_close(torch.tensor(l_ooc), torch.tensor(ref_losses), rtol=3e-2, atol=3e-2)
