@@ -755,3 +755,289 @@ def resnet1001_units(res: int = 2048, classes: int = 10, depth: int = 1001, act_
     for u in units:
         u.act = act_dtype
     return units
+
+
+# ---------------------------------------------------------------------------
+# GPT-style transformer (cfg3 Megatron-8.3B shape, cfg4 Turing-NLG-17B shape):
+# token+position embedding, pre-LN decoder layers, final LN + LM head.
+# Tokens are flattened to rows T = batch*seq.  Each decoder layer saves x,
+# qkv, the attention output, x2 = x + attn, the fc1 pre-activation and the
+# LN statistics (+ softmax logsumexp for flash attention); LN outputs, GELU
+# and the attention probabilities are recomputed in backward.
+# IR mapping: a layer is `Conv Wout=seq Hout=1 K=1 Cin=H Cout=12H` so the
+# reference cost model counts seq*12H^2 MACs per sample and 12H^2 weights.
+# ---------------------------------------------------------------------------
+LN_EPS = 1e-5
+
+
+def _ln_fw(x, g, b, mean, rstd):
+    y, m, r = _aten.native_layer_norm(x, [x.shape[-1]], g, b, LN_EPS)
+    if mean is not None:
+        mean.copy_(m.view(-1))
+        rstd.copy_(r.view(-1))
+    return y, m, r
+
+
+def _ln_apply(x, g, b, mean, rstd):
+    return ((x.float() - mean.view(-1, 1)) * rstd.view(-1, 1) * g.float() + b.float()).to(x.dtype)
+
+
+def _ln_bw(dy, x, g, b, mean, rstd, dg, db):
+    dx, dgg, dbb = _aten.native_layer_norm_backward(dy, x, [x.shape[-1]], mean.view(-1, 1), rstd.view(-1, 1),
+                                                    g, b, [True, True, True])
+    dg.copy_(dgg)
+    db.copy_(dbb)
+    return dx
+
+
+def _linear(x, w, b):
+    return torch.addmm(b, x, w.t())
+
+
+def _linear_bw(dy, x, w, gw, gb, need_dx=True):
+    """y = x W^T + b: writes fp32 dW, db; returns dx."""
+    if dy.dtype == torch.float32:
+        torch.mm(dy.t(), x, out=gw)
+    else:
+        gw.copy_(torch.mm(dy.t(), x, out_dtype=torch.float32))
+    gb.copy_(dy.float().sum(0))
+    return torch.mm(dy, w) if need_dx else None
+
+
+class EmbeddingUnit(Unit):
+    name = "embedding"
+
+    def __init__(self, vocab, hidden, seq, act_dtype=torch.bfloat16):
+        self.v, self.h, self.s, self.act = vocab, hidden, seq, act_dtype
+
+    def param_specs(self):
+        return [(self.v, self.h), (self.s, self.h)]
+
+    def saved_specs(self, n):
+        return [SavedSpec((n * self.s,), torch.int32)]
+
+    def init_params(self, gen):
+        return [torch.randn(self.v, self.h, generator=gen) * 0.02, torch.randn(self.s, self.h, generator=gen) * 0.01]
+
+    def forward(self, tok, params, saved):
+        we, wp = params
+        t = tok.reshape(-1)
+        if saved is not None:
+            saved[0].copy_(t)
+        n = t.numel() // self.s
+        x = we.index_select(0, t.long()).view(n, self.s, self.h) + wp.unsqueeze(0)
+        return x.view(-1, self.h)
+
+    def backward(self, dy, params, saved, grads):
+        t = saved[0].long()
+        grads[0].zero_().index_add_(0, t, dy.float())
+        grads[1].copy_(dy.float().view(-1, self.s, self.h).sum(0))
+        return None
+
+    def fwd_flops(self, n):
+        return 0.0
+
+    def ir_line(self, lid, batch, analytic=False):
+        return (f"{lid} ElementWise X={self.s * self.h} elem=2 mem_fwd={self.saved_bytes(batch)} mem_wt=0 "
+                f"mem_grad={4 * (self.v + self.s) * self.h}")
+
+
+class TransformerLayerUnit(Unit):
+    name = "decoder_layer"
+
+    def __init__(self, hidden, heads, seq, act_dtype=torch.bfloat16):
+        self.h, self.nh, self.s, self.act = hidden, heads, seq, act_dtype
+        self.hd = hidden // heads
+
+    def param_specs(self):
+        h = self.h
+        return [(h,), (h,), (3 * h, h), (3 * h,), (h, h), (h,),
+                (h,), (h,), (4 * h, h), (4 * h,), (h, 4 * h), (h,)]
+
+    def _flash(self):
+        return self.act in (torch.bfloat16, torch.float16)
+
+    def saved_specs(self, n):
+        t, h = n * self.s, self.h
+        s = [SavedSpec((t, h), self.act), SavedSpec((t, 3 * h), self.act), SavedSpec((t, h), self.act),
+             SavedSpec((t, h), self.act), SavedSpec((t, 4 * h), self.act),
+             SavedSpec((4 * t,), torch.float32)]                      # ln1/ln2 mean, rstd
+        if self._flash():
+            s.append(SavedSpec((n, self.nh, self.s), torch.float32))  # logsumexp
+        return s
+
+    def init_params(self, gen):
+        h = self.h
+        std = 0.02
+        return [torch.ones(h), torch.zeros(h), torch.randn(3 * h, h, generator=gen) * std, torch.zeros(3 * h),
+                torch.randn(h, h, generator=gen) * std, torch.zeros(h), torch.ones(h), torch.zeros(h),
+                torch.randn(4 * h, h, generator=gen) * std, torch.zeros(4 * h),
+                torch.randn(h, 4 * h, generator=gen) * std, torch.zeros(h)]
+
+    def _heads(self, qkv):
+        n = qkv.shape[0] // self.s
+        q, k, v = qkv.view(n, self.s, 3, self.nh, self.hd).unbind(2)
+        return [z.transpose(1, 2) for z in (q, k, v)]   # [n, nh, s, hd]
+
+    def _merge(self, o):
+        return o.transpose(1, 2).reshape(-1, self.h)
+
+    def _attn_fw(self, qkv, lse_out):
+        q, k, v = self._heads(qkv)
+        if self._flash():
+            r = _aten._scaled_dot_product_flash_attention(q, k, v, 0.0, True, False)
+            if lse_out is not None:
+                lse_out.copy_(r[1])
+            return self._merge(r[0])
+        p = self._probs(q, k)
+        return self._merge(p @ v)
+
+    def _probs(self, q, k):
+        sc = (q @ k.transpose(-1, -2)) * (1.0 / math.sqrt(self.hd))
+        mask = torch.ones(self.s, self.s, dtype=torch.bool, device=q.device).triu(1)
+        return torch.softmax(sc.masked_fill(mask, float("-inf")), dim=-1)
+
+    def _attn_bw(self, do, qkv, o, lse):
+        q, k, v = self._heads(qkv)
+        n = do.shape[0] // self.s
+        dO = do.view(n, self.s, self.nh, self.hd).transpose(1, 2)
+        if self._flash():
+            O = o.view(n, self.s, self.nh, self.hd).transpose(1, 2)
+            z = torch.zeros((), dtype=torch.int64, device=q.device)
+            dq, dk, dv = _aten._scaled_dot_product_flash_attention_backward(
+                dO, q, k, v, O, lse, None, None, self.s, self.s, 0.0, True, z, z)
+        else:
+            p = self._probs(q, k)
+            dv = p.transpose(-1, -2) @ dO
+            dp = dO @ v.transpose(-1, -2)
+            ds = p * (dp - (dp * p).sum(-1, keepdim=True)) * (1.0 / math.sqrt(self.hd))
+            dq = ds @ k
+            dk = ds.transpose(-1, -2) @ q
+        d = torch.stack([z.transpose(1, 2) for z in (dq, dk, dv)], dim=2)   # [n, s, 3, nh, hd]
+        return d.reshape(-1, 3 * self.h)
+
+    def forward(self, x, params, saved):
+        g1, b1, wqkv, bqkv, wo, bo, g2, b2, w1, bf1, w2, bf2 = params
+        t = x.shape[0]
+        if saved is not None:
+            saved[0].copy_(x)
+            st = saved[5]
+            m1, r1, m2, r2 = st[:t], st[t:2 * t], st[2 * t:3 * t], st[3 * t:]
+        else:
+            m1 = r1 = m2 = r2 = None
+        h1, _, _ = _ln_fw(x, g1, b1, m1, r1)
+        qkv = _linear(h1, wqkv, bqkv)
+        del h1
+        o = self._attn_fw(qkv, saved[6] if (saved is not None and self._flash()) else None)
+        x2 = x + _linear(o, wo, bo)
+        h2, _, _ = _ln_fw(x2, g2, b2, m2, r2)
+        f1 = _linear(h2, w1, bf1)
+        del h2
+        y = x2 + _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
+        if saved is not None:
+            saved[1].copy_(qkv)
+            saved[2].copy_(o)
+            saved[3].copy_(x2)
+            saved[4].copy_(f1)
+        return y
+
+    def saved_input(self, saved):
+        return saved[0]
+
+    def backward(self, dy, params, saved, grads):
+        g1, b1, wqkv, bqkv, wo, bo, g2, b2, w1, bf1, w2, bf2 = params
+        x, qkv, o, x2, f1, st = saved[:6]
+        t = x.shape[0]
+        m1, r1, m2, r2 = st[:t], st[t:2 * t], st[2 * t:3 * t], st[3 * t:]
+        gl = F.gelu(f1, approximate="tanh")
+        dg = _linear_bw(dy, gl, w2, grads[10], grads[11])
+        del gl
+        df1 = _aten.gelu_backward(dg, f1, approximate="tanh")
+        del dg
+        h2 = _ln_apply(x2, g2, b2, m2, r2)
+        dh2 = _linear_bw(df1, h2, w1, grads[8], grads[9])
+        del df1, h2
+        dx2 = dy + _ln_bw(dh2, x2, g2, b2, m2, r2, grads[6], grads[7])
+        del dh2
+        do = _linear_bw(dx2, o, wo, grads[4], grads[5])
+        dqkv = self._attn_bw(do, qkv, o, saved[6] if self._flash() else None)
+        del do
+        h1 = _ln_apply(x, g1, b1, m1, r1)
+        dh1 = _linear_bw(dqkv, h1, wqkv, grads[2], grads[3])
+        del dqkv, h1
+        return dx2 + _ln_bw(dh1, x, g1, b1, m1, r1, grads[0], grads[1])
+
+    def fwd_flops(self, n):
+        t = n * self.s
+        return 2.0 * t * 12 * self.h * self.h + 2.0 * n * self.nh * self.s * self.s * self.hd  # + causal attn
+
+    def ir_line(self, lid, batch, analytic=False):
+        grad = 4 * sum(math.prod(p) for p in self.param_specs())
+        return (f"{lid} Conv Wout={self.s} Hout=1 Cin={self.h} Cout={12 * self.h} K=1 elem=2 "
+                f"mem_fwd={self.saved_bytes(batch)} mem_wt=0 mem_grad={grad}")
+
+
+class LMHeadUnit(Unit):
+    """final LayerNorm + LM head (untied) -> logits [T, vocab]."""
+
+    name = "lm_head"
+
+    def __init__(self, hidden, vocab, seq, act_dtype=torch.bfloat16):
+        self.h, self.v, self.s, self.act = hidden, vocab, seq, act_dtype
+
+    def param_specs(self):
+        return [(self.h,), (self.h,), (self.v, self.h)]
+
+    def saved_specs(self, n):
+        t = n * self.s
+        return [SavedSpec((t, self.h), self.act), SavedSpec((2 * t,), torch.float32)]
+
+    def init_params(self, gen):
+        return [torch.ones(self.h), torch.zeros(self.h), torch.randn(self.v, self.h, generator=gen) * 0.02]
+
+    def forward(self, x, params, saved):
+        g, b, w = params
+        t = x.shape[0]
+        if saved is not None:
+            saved[0].copy_(x)
+            m, r = saved[1][:t], saved[1][t:]
+        else:
+            m = r = None
+        h, _, _ = _ln_fw(x, g, b, m, r)
+        return torch.mm(h, w.t())
+
+    def backward(self, dlogits, params, saved, grads):
+        g, b, w = params
+        x, st = saved
+        t = x.shape[0]
+        m, r = st[:t], st[t:]
+        h = _ln_apply(x, g, b, m, r)
+        if dlogits.dtype == torch.float32:
+            torch.mm(dlogits.t(), h, out=grads[2])
+        else:
+            grads[2].copy_(torch.mm(dlogits.t(), h, out_dtype=torch.float32))
+        dh = torch.mm(dlogits, w)
+        return _ln_bw(dh, x, g, b, m, r, grads[0], grads[1])
+
+    def fwd_flops(self, n):
+        return 2.0 * n * self.s * self.h * self.v
+
+    def ir_line(self, lid, batch, analytic=False):
+        return (f"{lid} Conv Wout={self.s} Hout=1 Cin={self.h} Cout={self.v} K=1 elem=2 "
+                f"mem_fwd={self.saved_bytes(batch)} mem_wt=0 mem_grad={4 * (2 * self.h + self.v * self.h)}")
+
+
+def gpt_units(hidden, heads, layers, seq, vocab, act_dtype=torch.bfloat16):
+    return ([EmbeddingUnit(vocab, hidden, seq, act_dtype)]
+            + [TransformerLayerUnit(hidden, heads, seq, act_dtype) for _ in range(layers)]
+            + [LMHeadUnit(hidden, vocab, seq, act_dtype)])
+
+
+def lm_loss(logits, target):
+    """Next-token cross-entropy over all rows; dlogits in the logits dtype."""
+    lf = logits.float()
+    t = target.reshape(-1)
+    loss = F.cross_entropy(lf, t)
+    p = torch.softmax(lf, dim=1)
+    p[torch.arange(p.shape[0], device=p.device), t] -= 1.0
+    return loss, (p * (1.0 / p.shape[0])).to(logits.dtype)

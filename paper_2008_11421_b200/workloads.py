@@ -9,7 +9,7 @@ from pathlib import Path
 import torch
 
 from .plan import PlanBundle
-from .units import resnet1001_units, resnet_units
+from .units import gpt_units, resnet1001_units, resnet_units
 
 PLANS = Path(__file__).with_name("plans")
 
@@ -20,6 +20,9 @@ def load(name: str) -> dict:
 
 def units_for(rec: dict):
     m = rec["meta"]
+    if m["family"] == "gpt":
+        act = torch.float32 if m["act"] == "f32" else torch.bfloat16
+        return gpt_units(m["hidden"], m["heads"], m["layers"], m["seq"], m["vocab"], act_dtype=act)
     if m["family"] == "preact":
         act = torch.float32 if m["act"] == "f32" else torch.bfloat16
         return resnet1001_units(m["res"], m["classes"], m["depth"], act_dtype=act)

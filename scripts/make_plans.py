@@ -28,7 +28,7 @@ from oocsched.plan import plan_string, plan_to_dict  # noqa: E402
 from oocsched.planner import plan_model  # noqa: E402
 from oocsched.simulator import simulate  # noqa: E402
 
-from paper_2008_11421_b200.units import model_text, resnet1001_units, resnet_units  # noqa: E402
+from paper_2008_11421_b200.units import gpt_units, model_text, resnet1001_units, resnet_units  # noqa: E402
 
 OUT = ROOT / "paper_2008_11421_b200" / "plans"
 
@@ -98,6 +98,20 @@ def main():
         make(f"preact29_small_{tag}", units, 4, 0.62 * tot,
              {"family": "preact", "depth": 29, "res": 32, "classes": 10, "act": tag},
              interconnect_bw=1e9, compute_rate=1e11)
+    # GPT decoder family (cfg3/cfg4 shapes), small parity instances
+    for act, tag in ((torch.float32, "f32"), (torch.bfloat16, "bf16")):
+        units = gpt_units(64, 4, 6, 32, 128, act_dtype=act)
+        tot = total_saved(units, 4)
+        make(f"gpt_small_{tag}", units, 4, 0.55 * tot,
+             {"family": "gpt", "hidden": 64, "heads": 4, "layers": 6, "seq": 32, "vocab": 128, "act": tag},
+             interconnect_bw=1e9, compute_rate=1e11)
+    # Megatron 2.5B shape (H1920/A20/L54), seq 1024, vocab 51200:
+    # the largest cfg3-family model whose fp32 master + Adam state fits one
+    # host (the 8.3B shape needs the 8-way shard of cfg3)
+    units = gpt_units(1920, 20, 54, 1024, 51200)
+    make("gpt2p5b_b144", units, 144, 120e9,
+         {"family": "gpt", "hidden": 1920, "heads": 20, "layers": 54, "seq": 1024, "vocab": 51200,
+          "act": "bf16"}, max_blocks=16, compute_rate=5.0e14)
     # cfg2: ResNet-1001 on 2048x2048 images, batch 2 = 314 GB of activations
     units = resnet1001_units(res=2048, classes=10, depth=1001)
     make("resnet1001_2048_b2", units, 2, 150e9,

@@ -1,0 +1,74 @@
+"""GPT decoder units (cfg3/cfg4 model family) under reference-planner plans
+vs the CPU fp32 in-core oracle, and out-of-core vs in-core bitwise."""
+import pytest
+import torch
+
+from oracle import gpt_oracle
+from paper_2008_11421_b200 import workloads as W
+from paper_2008_11421_b200.executor import ExecConfig, Executor
+from paper_2008_11421_b200.units import lm_loss
+
+pytestmark = pytest.mark.gpu
+
+
+def batches(rec, iters, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    m = rec["meta"]
+    xs = [torch.randint(0, m["vocab"], (m["batch"], m["seq"]), generator=g) for _ in range(iters)]
+    ys = [torch.randint(0, m["vocab"], (m["batch"], m["seq"]), generator=g) for _ in range(iters)]
+    return xs, ys
+
+
+def run(rec, plan=None, iters=3, lr=0.1, capacity=None, optimizer="sgd"):
+    units = W.units_for(rec)
+    b = W.bundle_for(rec, plan)
+    if capacity:
+        b.set_capacity(capacity)
+    act = units[1].act
+    ex = Executor(units, b, batch=rec["meta"]["batch"], loss_fn=lm_loss,
+                  cfg=ExecConfig(optimizer=optimizer, lr=lr, weight_dtype=act))
+    gen = torch.Generator().manual_seed(5)
+    init = {i + 1: u.init_params(gen) for i, u in enumerate(units)}
+    ex.load_weights(init)
+    xs, ys = batches(rec, iters)
+    losses = [float(ex.step(x.cuda().int(), y.cuda())) for x, y in zip(xs, ys)]
+    w = ex.unit_weights()
+    st = ex.stats()
+    ex.close()
+    return units, init, losses, w, st
+
+
+@pytest.fixture(autouse=True)
+def strict():
+    old = (torch.backends.cuda.matmul.allow_tf32, torch.are_deterministic_algorithms_enabled())
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.use_deterministic_algorithms(True, warn_only=True)
+    yield
+    torch.backends.cuda.matmul.allow_tf32 = old[0]
+    torch.use_deterministic_algorithms(old[1])
+
+
+def test_gpt_plan_matches_cpu_oracle():
+    rec = W.load("gpt_small_f32")
+    assert any(b["recompute"] for b in rec["plan"]["blocks"]) and "in" in rec["plan_string"]
+    units, init, losses, w, st = run(rec)
+    assert st["iter_bytes_h2d"] > 0
+    xs, ys = batches(rec, 3)
+    ref_losses, ref_w = gpt_oracle.train(units, init, xs, ys, lr=0.1)
+    torch.testing.assert_close(torch.tensor(losses), torch.tensor(ref_losses), rtol=1e-4, atol=1e-5)
+    for k in ref_w:
+        for got, ref in zip(w[k], ref_w[k]):
+            torch.testing.assert_close(got.cpu().float(), ref, rtol=1e-3, atol=1e-5)
+
+
+def test_gpt_bf16_out_of_core_equals_in_core_and_tracks_oracle():
+    rec = W.load("gpt_small_bf16")
+    units, init, l_ooc, w_ooc, s_ooc = run(rec, lr=0.05)
+    _, _, l_inc, w_inc, _ = run(rec, plan=W.incore_plan(rec["plan"]), lr=0.05, capacity=1e12)
+    assert s_ooc["iter_bytes_h2d"] > 0 and l_ooc == l_inc
+    for k in w_inc:
+        for a, b in zip(w_ooc[k], w_inc[k]):
+            assert torch.equal(a, b), k
+    xs, ys = batches(rec, 3)
+    ref_losses, _ = gpt_oracle.train(units, init, xs, ys, lr=0.05)
+    torch.testing.assert_close(torch.tensor(l_ooc), torch.tensor(ref_losses), rtol=2e-2, atol=2e-2)
