@@ -108,44 +108,61 @@ def dist_env():
 # ---------------------------------------------------------------------------
 def cpu_sample_batch(rec):
     # bounded CPU sample: ~10-30 s of host work
-    return 4 if rec["meta"]["res"] <= 256 else 1
+    m = rec["meta"]
+    if m["family"] == "gpt":
+        return 1
+    return 4 if m["res"] <= 256 else 1
 
 
 def cpu_sample_note(rec):
-    return "" if rec["meta"]["res"] <= 256 else " at 512x512, scaled by the pixel ratio 1/16"
+    m = rec["meta"]
+    if m["family"] == "gpt":
+        return " of 256 tokens, scaled to the 1024-token sample by 1/4"
+    return "" if m["res"] <= 256 else " at 512x512, scaled by the pixel ratio 1/16"
 
 
 def cpu_reference(rec, steps, warmup, sample_batch=None):
+    """The in-core fp32 torch-CPU oracle of the same model, all host cores."""
     import torch
 
-    from oracle import resnet_oracle
+    from oracle import gpt_oracle, resnet_oracle
+    from paper_2008_11421_b200 import units as U
     from paper_2008_11421_b200 import workloads as W
 
     torch.set_num_threads(os.cpu_count() or 1)
     sample_batch = sample_batch or cpu_sample_batch(rec)
-    units = W.units_for(rec)
+    m = dict(rec["meta"])
     scale = 1.0
-    if rec["meta"]["res"] > 256:
-        # in-core fp32 at 2048^2 needs ~314 GB of host RAM per image: time the
-        # same network on 512^2 images and scale by the pixel ratio (FLOPs and
-        # bytes of these convnets are linear in the pixel count)
-        from paper_2008_11421_b200 import units as U
-        m = dict(rec["meta"], res=512)
-        scale = (512 / rec["meta"]["res"]) ** 2
-        units = U.resnet1001_units(512, m["classes"], m["depth"], act_dtype=torch.float32)
-        rec = dict(rec, meta=m)
-    m = rec["meta"]
     gen = torch.Generator().manual_seed(0)
+    if m["family"] == "gpt":
+        scale = 256 / m["seq"]
+        m["seq"] = 256
+        units = U.gpt_units(m["hidden"], m["heads"], m["layers"], 256, m["vocab"], act_dtype=torch.float32)
+        x = torch.randint(0, m["vocab"], (sample_batch, 256), generator=gen)
+        y = torch.randint(0, m["vocab"], (sample_batch, 256), generator=gen)
+        fwd = lambda params: gpt_oracle.forward(units, params, x).reshape(-1, m["vocab"])
+        tgt = y.reshape(-1)
+    else:
+        if m["res"] > 256:
+            # in-core fp32 at 2048^2 needs ~314 GB of host RAM per image: time the
+            # same network on 512^2 images and scale by the pixel ratio (FLOPs and
+            # bytes of these convnets are linear in the pixel count)
+            scale = (512 / m["res"]) ** 2
+            m["res"] = 512
+            units = U.resnet1001_units(512, m["classes"], m["depth"], act_dtype=torch.float32)
+        else:
+            units = W.units_for(rec)
+        x = torch.randn(sample_batch, 3, m["res"], m["res"], generator=gen)
+        tgt = torch.randint(0, m["classes"], (sample_batch,), generator=gen)
+        fwd = lambda params: resnet_oracle.forward(units, params, x)
     init = {i + 1: [t.float() for t in u.init_params(gen)] for i, u in enumerate(units)}
     params = {k: [t.requires_grad_(True) for t in ts] for k, ts in init.items()}
     flat = [t for k in sorted(params) for t in params[k]]
     opt = torch.optim.SGD(flat, lr=0.1, foreach=False)
-    x = torch.randn(sample_batch, 3, m["res"], m["res"], generator=gen)
-    y = torch.randint(0, m["classes"], (sample_batch,), generator=gen)
 
     def step():
         opt.zero_grad(set_to_none=True)
-        loss = torch.nn.functional.cross_entropy(resnet_oracle.forward(units, params, x), y)
+        loss = torch.nn.functional.cross_entropy(fwd(params), tgt)
         loss.backward()
         opt.step()
 
@@ -160,13 +177,40 @@ def cpu_reference(rec, steps, warmup, sample_batch=None):
 
 def model_name(rec):
     m = rec["meta"]
+    if m["family"] == "gpt":
+        return f"gpt-h{m['hidden']}-l{m['layers']} ({m['heads']} heads, vocab {m['vocab']})"
     return f"resnet{m['depth']}" if "depth" in m else rec["name"]
 
 
 def metric_name(rec):
     m = rec["meta"]
+    if m["family"] == "gpt":
+        return (f"samples/sec ({model_name(rec)} seq {m['seq']} training step, per-GPU batch beyond HBM)")
     return (f"samples/sec ({model_name(rec)} {m['res']}x{m['res']} training step, per-GPU batch "
             f"beyond HBM)")
+
+
+def workload_inputs(rec, dev, gen, batch=None):
+    import torch
+    m = rec["meta"]
+    n = batch or m["batch"]
+    if m["family"] == "gpt":
+        x = torch.randint(0, m["vocab"], (n, m["seq"]), device=dev, generator=gen, dtype=torch.int32)
+        y = torch.randint(0, m["vocab"], (n, m["seq"]), device=dev, generator=gen)
+        return x, y
+    x = torch.randn(n, 3, m["res"], m["res"], device=dev, generator=gen, dtype=torch.float32).to(
+        torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    y = torch.randint(0, m["classes"], (n,), device=dev, generator=gen)
+    return x, y
+
+
+def workload_exec(rec):
+    """loss function and optimizer per family: SGD-momentum for the convnets,
+    host-side Adam on every block for the transformers."""
+    from paper_2008_11421_b200.units import cross_entropy_loss, lm_loss
+    if rec["meta"]["family"] == "gpt":
+        return lm_loss, dict(optimizer="adam", lr=1e-4, host_path_all=True)
+    return cross_entropy_loss, dict(optimizer="sgd", lr=0.1, momentum=0.9)
 
 
 def run_reference(args, rec):
@@ -184,8 +228,8 @@ def run_reference(args, rec):
         "data": "synthetic", "config": {"workload": rec["name"], "model": model_name(rec),
                                          "per_gpu_batch": m["batch"], "image": m["res"]},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"in-core fp32 torch-CPU {model_name(rec)} step (oracle/resnet_oracle.py) "
-                                   f"on {cpu_sample_batch(rec)} images per step{cpu_sample_note(rec)}"},
+                         "sample": f"in-core fp32 torch-CPU {model_name(rec)} step (oracle/) "
+                                   f"on {cpu_sample_batch(rec)} samples per step{cpu_sample_note(rec)}"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -201,8 +245,6 @@ def run_gpu(args, rec):
 
     from paper_2008_11421_b200 import workloads as W
     from paper_2008_11421_b200.executor import ExecConfig, Executor
-    from paper_2008_11421_b200.units import cross_entropy_loss
-
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     torch.backends.cudnn.benchmark = True
@@ -217,8 +259,9 @@ def run_gpu(args, rec):
         dist.broadcast(idbuf, 0)
         nccl_id = bytes(idbuf.cpu().tolist())
     m = rec["meta"]
-    batch, res, classes = m["batch"], m["res"], m["classes"]
+    batch = m["batch"]
     units = W.units_for(rec)
+    loss_fn, opt_cfg = workload_exec(rec)
     if args.incore:
         bundle = W.bundle_for(rec, W.incore_plan(rec["plan"])).set_capacity(1e12)
         rec = dict(rec, plan=W.incore_plan(rec["plan"]), name=rec["name"] + "_incore",
@@ -226,17 +269,14 @@ def run_gpu(args, rec):
     else:
         bundle = W.bundle_for(rec)
     t_setup = time.perf_counter()
-    ex = Executor(units, bundle, batch=batch, loss_fn=cross_entropy_loss,
+    ex = Executor(units, bundle, batch=batch, loss_fn=loss_fn,
                   cfg=ExecConfig(device=local, world_size=world, rank=rank, nccl_id=nccl_id,
-                                 optimizer="sgd", lr=0.1, weight_dtype=torch.bfloat16,
-                                 momentum=0.9))
+                                 weight_dtype=torch.bfloat16, **opt_cfg))
     ex.init_weights(seed=0)
     setup_s = time.perf_counter() - t_setup
     dev = torch.device("cuda", local)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn(batch, 3, res, res, device=dev, generator=gen, dtype=torch.float32).to(
-        torch.bfloat16).contiguous(memory_format=torch.channels_last)
-    y = torch.randint(0, classes, (batch,), device=dev, generator=gen)
+    x, y = workload_inputs(rec, dev, gen)
     cs = ex.compute_stream
 
     def barrier():
@@ -343,11 +383,11 @@ def run_gpu(args, rec):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": rec["name"], "model": model_name(rec), "per_gpu_batch": batch,
-                   "global_batch": batch * world, "image": res, "parallelism": f"dp{world}",
+                   "global_batch": batch * world, "input": m.get("res", m.get("seq")), "parallelism": f"dp{world}",
                    "plan": rec["plan_string"][:160] + " ...",
                    "activations_bytes": rec["total_bytes"], "hbm_bytes": 183359 * 2 ** 20,
                    "swapped_bytes": rec["swapped_bytes"], "recompute_bytes": rec["recompute_bytes"],
-                   "l2": f"inputs > L2 (batch tensor {x.numel() * 2 / 1e6:.0f} MB; "
+                   "l2": f"inputs > L2 (batch tensor {x.numel() * x.element_size() / 1e6:.0f} MB; "
                          f"{rec['total_bytes'] / 1e9:.0f} GB of activations per step)"},
         "roofline": ({"bound": "hbm", "kernel": dom,
                       "achieved": fam[dom][0] / fam[dom][1] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -381,17 +421,18 @@ def run_gpu(args, rec):
                           "free_total": list(torch.cuda.mem_get_info(dev))},
         "clocks": clocks,
     }
+    if args.trace_out and rank == 0:
+        Path(args.trace_out).write_text(trace)
+    ex.close()
+    del ex
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, dt = cpu_reference(rec, steps=2, warmup=1)
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
                                 "sample": f"in-core fp32 torch-CPU {model_name(rec)} step "
-                                          f"(oracle/resnet_oracle.py), {cpu_sample_batch(rec)} images x 2 steps"
+                                          f"(oracle/), {cpu_sample_batch(rec)} samples x 2 steps"
                                           f"{cpu_sample_note(rec)}"}
-    if args.trace_out and rank == 0:
-        Path(args.trace_out).write_text(trace)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ex.close()
     if world > 1:
         dist.destroy_process_group()
 

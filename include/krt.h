@@ -107,6 +107,8 @@ typedef struct krt_config {
   int host_threads;         /* host update worker threads, 0 = auto */
   size_t arena_slack_bytes; /* extra arena bytes beyond the static assignment */
   void* peer_group;         /* krt_peer_group* for in-process ranks (else NULL: NCCL) */
+  int host_path_all;        /* 1: every block's update on the host even at world_size 1
+                               (distsim.py:134-137 applies this from 2 workers) */
 } krt_config;
 
 /* In-process exchange group: world_size ranks living in one process (threads),

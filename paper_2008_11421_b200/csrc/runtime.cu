@@ -194,7 +194,7 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
   auto groups = assign_groups(nb_, cfg_.dist_groups);
   groups_.clear();
   std::set<int> host_blocks;
-  if (world_ >= 2)
+  if (world_ >= 2 || cfg_.host_path_all)
     for (auto& b : plan.blocks) host_blocks.insert(b.id);
   else
     for (int b : plan.swapped_blocks()) host_blocks.insert(b);

@@ -121,6 +121,7 @@ class ExecConfig:
     host_threads: int = 0
     arena_slack_bytes: int = 0
     peer_group: Optional[object] = None   # _lib.PeerGroup for in-process ranks
+    host_path_all: bool = False           # host update for every block even at world_size 1
 
 
 class Executor:
@@ -149,7 +150,8 @@ class Executor:
                          cfg.dist_groups, wdt, _lib.ADAM if cfg.optimizer == "adam" else _lib.SGD,
                          cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.momentum,
                          1.0 / cfg.world_size, cfg.host_threads, cfg.arena_slack_bytes,
-                         cfg.peer_group.handle if cfg.peer_group is not None else None)
+                         cfg.peer_group.handle if cfg.peer_group is not None else None,
+                         int(cfg.host_path_all))
         h = C.c_void_p()
         _lib.check(L.krt_create(C.byref(kc), C.byref(h)))
         self._ctx = h

@@ -1033,11 +1033,21 @@ def gpt_units(hidden, heads, layers, seq, vocab, act_dtype=torch.bfloat16):
             + [LMHeadUnit(hidden, vocab, seq, act_dtype)])
 
 
-def lm_loss(logits, target):
-    """Next-token cross-entropy over all rows; dlogits in the logits dtype."""
-    lf = logits.float()
+def lm_loss(logits, target, chunk_rows=8192):
+    """Next-token cross-entropy over all rows; dlogits in the logits dtype.
+    Row chunks keep the fp32 softmax transient small (the full [T, vocab]
+    fp32 matrix would be 30 GB at the 2.5B bench shape)."""
     t = target.reshape(-1)
-    loss = F.cross_entropy(lf, t)
-    p = torch.softmax(lf, dim=1)
-    p[torch.arange(p.shape[0], device=p.device), t] -= 1.0
-    return loss, (p * (1.0 / p.shape[0])).to(logits.dtype)
+    n = logits.shape[0]
+    dl = torch.empty_like(logits)
+    total = torch.zeros((), dtype=torch.float32, device=logits.device)
+    inv = 1.0 / n
+    for r0 in range(0, n, chunk_rows):
+        lf = logits[r0:r0 + chunk_rows].float()
+        tc = t[r0:r0 + chunk_rows]
+        lse = torch.logsumexp(lf, dim=1)
+        total += (lse - lf.gather(1, tc.view(-1, 1)).squeeze(1)).sum()
+        p = torch.exp(lf - lse.view(-1, 1))
+        p[torch.arange(p.shape[0], device=p.device), tc] -= 1.0
+        dl[r0:r0 + chunk_rows] = (p * inv).to(logits.dtype)
+    return total * inv, dl
