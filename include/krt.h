@@ -109,6 +109,8 @@ typedef struct krt_config {
   void* peer_group;         /* krt_peer_group* for in-process ranks (else NULL: NCCL) */
   int host_path_all;        /* 1: every block's update on the host even at world_size 1
                                (distsim.py:134-137 applies this from 2 workers) */
+  int force_dp_path;        /* 1: data-parallel op structure (reduce-scatter / shard host
+                               update / all-gather) even at world_size 1 (NCCL, 1 rank) */
 } krt_config;
 
 /* In-process exchange group: world_size ranks living in one process (threads),

@@ -91,16 +91,18 @@ Runtime::Runtime(const krt_config& cfg) : cfg_(cfg) {
   CK(cudaStreamCreateWithPriority(&streams_[0], cudaStreamNonBlocking, lo));
   for (int i = 1; i < 4; ++i) CK(cudaStreamCreateWithPriority(&streams_[i], cudaStreamNonBlocking, hi));
   CK(cudaEventCreate(&ev_base_));
-  if (world_ > 1 && cfg.peer_group) {
+  dp_ = world_ > 1 || cfg.force_dp_path;
+  if (dp_ && cfg.peer_group) {
     peers_ = static_cast<PeerGroup*>(cfg.peer_group);
     if (peers_->world != world_) throw std::invalid_argument("peer group size != world_size");
     std::lock_guard<std::mutex> lk(peers_->mu);
     if (peers_->ranks[rank_]) throw std::invalid_argument("rank already joined the peer group");
     peers_->ranks[rank_] = this;
-  } else if (world_ > 1) {
-    if (!cfg.nccl_id) throw std::invalid_argument("world_size > 1 needs nccl_id or a peer group");
+  } else if (dp_) {
     ncclUniqueId id;
-    std::memcpy(&id, cfg.nccl_id, sizeof(id));
+    if (cfg.nccl_id) std::memcpy(&id, cfg.nccl_id, sizeof(id));
+    else if (world_ == 1) NK(ncclGetUniqueId(&id));   // a one-rank communicator
+    else throw std::invalid_argument("world_size > 1 needs nccl_id or a peer group");
     ncclComm_t comm;
     NK(ncclCommInitRank(&comm, world_, id, rank_));
     nccl_comm_ = comm;
@@ -194,7 +196,7 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
   auto groups = assign_groups(nb_, cfg_.dist_groups);
   groups_.clear();
   std::set<int> host_blocks;
-  if (world_ >= 2 || cfg_.host_path_all)
+  if (dp_ || cfg_.host_path_all)
     for (auto& b : plan.blocks) host_blocks.insert(b.id);
   else
     for (int b : plan.swapped_blocks()) host_blocks.insert(b);
@@ -227,7 +229,7 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
   host_elems_ = 0;
   for (auto& g : groups_) {
     g.host_off = host_elems_;
-    if (world_ >= 2) g.host_n = g.shard_n;
+    if (dp_) g.host_n = g.shard_n;
     else {
       g.host_n = 0;
       for (int b : g.members)
@@ -242,7 +244,7 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
     out.clear();
     std::map<int, int> weight_in_of;  // block -> op
     if (steady) {
-      if (world_ >= 2) {
+      if (dp_) {
         for (size_t gi = 0; gi < groups_.size(); ++gi) {
           XOp x;
           x.e.action = Action::WEIGHT_IN;
@@ -283,7 +285,7 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
       out.push_back(x);
     }
     int out_res = hw.duplex ? R_XFER_OUT : R_XFER;
-    if (world_ >= 2) {
+    if (dp_) {
       for (int gi = (int)groups_.size(); gi >= 1; --gi) {
         auto& g = groups_[gi - 1];
         XOp ex;
@@ -397,7 +399,7 @@ void Runtime::allocate() {
     CK(cudaMalloc((void**)&d_v_, np * 4));
     CK(cudaMemset(d_v_, 0, np * 4));
   }
-  if (world_ > 1) {
+  if (dp_) {
     size_t ns = 0;
     for (auto& g : groups_) ns += (size_t)g.shard_n;
     CK(cudaMalloc((void**)&d_shard_, std::max<size_t>(ns, 64) * 4));
@@ -492,7 +494,7 @@ void Runtime::init_master() {
   std::fill(h_m_.begin(), h_m_.end(), 0.f);
   std::fill(h_v_.begin(), h_v_.end(), 0.f);
   for (auto& g : groups_) {
-    if (world_ >= 2) {
+    if (dp_) {
       fetch_f32(g.p_lo + (int64_t)rank_ * g.shard_n, g.shard_n, h_master_.data() + g.host_off);
     } else {
       for (int b : g.members) {
@@ -553,10 +555,10 @@ void Runtime::host_loop() {
 void Runtime::run_host_task(const HostTask& t) {
   auto& g = groups_.at((size_t)t.group - 1);
   OptimScalars s = make_scalars(cfg_.optimizer, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps, cfg_.weight_decay,
-                                cfg_.momentum, t.step, world_ >= 2 ? cfg_.grad_scale : 1.0f);
+                                cfg_.momentum, t.step, dp_ ? cfg_.grad_scale : 1.0f);
   size_t wb = dtype_bytes(cfg_.weight_dtype);
   auto stage_ptr = [&](size_t host_off) { return static_cast<uint8_t*>(h_wstage_) + host_off * wb; };
-  if (world_ >= 2) {
+  if (dp_) {
     size_t o = g.host_off;
     host_update(pool_.get(), h_master_.data() + o, h_m_.data() + o, h_v_.data() + o, h_grad_ + o, stage_ptr(o),
                 cfg_.weight_dtype, (size_t)g.host_n, s);
@@ -656,7 +658,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
       cudaStream_t s = streams_[2];
       wait_deps(s, x, ops);
       CK(cudaEventRecord(ev_start_[idx], s));
-      if (world_ >= 2) {
+      if (dp_) {
         auto& g = groups_.at((size_t)e.group - 1);
         size_t shard_pos = 0;
         for (int gi = 0; gi < e.group - 1; ++gi) shard_pos += (size_t)groups_[gi].shard_n;
@@ -720,7 +722,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
       cudaStream_t s = streams_[1];
       wait_deps(s, x, ops);
       CK(cudaEventRecord(ev_start_[idx], s));
-      if (world_ >= 2) {
+      if (dp_) {
         auto& g = groups_.at((size_t)e.group - 1);
         void* dst = d_weight(g.p_lo + (int64_t)rank_ * g.shard_n);
         CK(cudaMemcpyAsync(dst, static_cast<uint8_t*>(h_wstage_) + g.host_off * wb, (size_t)g.shard_n * wb,
@@ -853,7 +855,7 @@ void Runtime::flush_weights() {
   size_t wb = dtype_bytes(cfg_.weight_dtype);
   cudaStream_t s = streams_[1];
   for (auto& g : groups_) {
-    if (world_ >= 2) {
+    if (dp_) {
       void* dst = d_weight(g.p_lo + (int64_t)rank_ * g.shard_n);
       CK(cudaMemcpyAsync(dst, static_cast<uint8_t*>(h_wstage_) + g.host_off * wb, (size_t)g.shard_n * wb,
                          cudaMemcpyHostToDevice, s));
@@ -907,7 +909,7 @@ void Runtime::read_master(int block, float* out, size_t numel) {
   if (numel < (size_t)bp.n_params) throw std::invalid_argument("output too small");
   auto& g = groups_.at((size_t)bp.group - 1);
   if (bp.host_path) {
-    if (world_ >= 2) {
+    if (dp_) {
       int64_t lo = g.p_lo + (int64_t)rank_ * g.shard_n, hi = lo + g.shard_n;
       for (int64_t i = 0; i < bp.n_params; ++i) {
         int64_t p = bp.p_off + i;

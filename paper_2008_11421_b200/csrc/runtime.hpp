@@ -127,6 +127,7 @@ class Runtime {
 
   krt_config cfg_;
   int world_ = 1, rank_ = 0;
+  bool dp_ = false;   // data-parallel op structure (exchange / shard host update / all-gather)
   std::map<int, BlockPhys> blocks_;
   std::vector<GroupPhys> groups_;     // index = group-1
   int nb_ = 0;

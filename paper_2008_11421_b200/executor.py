@@ -122,6 +122,7 @@ class ExecConfig:
     arena_slack_bytes: int = 0
     peer_group: Optional[object] = None   # _lib.PeerGroup for in-process ranks
     host_path_all: bool = False           # host update for every block even at world_size 1
+    force_dp_path: bool = False           # DP op structure through a 1-rank NCCL communicator
 
 
 class Executor:
@@ -151,7 +152,7 @@ class Executor:
                          cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.momentum,
                          1.0 / cfg.world_size, cfg.host_threads, cfg.arena_slack_bytes,
                          cfg.peer_group.handle if cfg.peer_group is not None else None,
-                         int(cfg.host_path_all))
+                         int(cfg.host_path_all), int(cfg.force_dp_path))
         h = C.c_void_p()
         _lib.check(L.krt_create(C.byref(kc), C.byref(h)))
         self._ctx = h

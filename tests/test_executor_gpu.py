@@ -211,3 +211,25 @@ def test_cfg0_two_dp_workers_match_oracle(sched_cases, optimizer, lr):
     for ex in exs:
         ex.close()
     pg.close()
+
+
+@pytest.mark.parametrize("optimizer,lr", [("sgd", 1e-2), ("adam", 1e-3)])
+def test_nccl_dp_path_one_rank(sched_cases, optimizer, lr):
+    """The multi-GPU op structure through NCCL (ncclReduceScatter of each
+    group, D2H of the shard, host update of the shard, H2D + ncclAllGather),
+    run with a one-rank communicator: the only NCCL path one GPU can run."""
+    c = cfg0_case(sched_cases)
+    b = PlanBundle(c["model"], c["hardware"], c["plan"])
+    ex = Executor([FCUnit(64, 64) for _ in range(6)], b, batch=2, loss_fn=mse_zero_loss,
+                  cfg=ExecConfig(optimizer=optimizer, lr=lr, force_dp_path=True, dist_groups=2))
+    w0 = orc.init_weights()
+    ex.load_weights({i + 1: [torch.from_numpy(w)] for i, w in enumerate(w0)})
+    losses = [float(ex.step(torch.from_numpy(orc.inputs(0, it)).cuda())) for it in range(1, 4)]
+    w = ex.unit_weights()
+    st = ex.stats()
+    ex.close()
+    ref_losses, ref_w = orc.train(workers=1, iterations=3, optimizer=optimizer, lr=lr, weights=w0)
+    np.testing.assert_allclose(losses, [l[0] for l in ref_losses], rtol=RTOL)
+    for i in range(6):
+        np.testing.assert_allclose(w[i + 1][0].cpu().numpy(), ref_w[i], rtol=RTOL, atol=ATOL)
+    assert st["groups"] == 2 and st["host_elems"] >= 6 * 64 * 64
