@@ -110,8 +110,17 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __
   Map m(C);
   int c0 = m.tx * 8;
   float s[8] = {0}, q[8] = {0};
-#pragma unroll 2
-  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
+  const int64_t step = (int64_t)gridDim.x * m.rb;
+  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
+  for (; r + step < rows; r += 2 * step) {
+    Vec8 v0 = load8(x + r * C + c0), v1 = load8(x + (r + step) * C + c0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      s[k] += v0.v[k] + v1.v[k];
+      q[k] += v0.v[k] * v0.v[k] + v1.v[k] * v1.v[k];
+    }
+  }
+  if (r < rows) {
     Vec8 v = load8(x + r * C + c0);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -264,10 +273,26 @@ __global__ void __launch_bounds__(kThreads) add_relu_bwd_kernel(
 }
 
 // backward reduce: sum(gm) and sum(gm * xhat) with gm = dy * mask
+template <bool RELU>
+__device__ __forceinline__ void bwd_acc(const Vec8& v, const Vec8& d, const float* sc, const float* sh,
+                                        const float* mu, const float* is, float* s1, float* s2) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float gm = d.v[k];
+    if (RELU) {
+      float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
+      gm = yk > 0.0f ? gm : 0.0f;
+    }
+    s1[k] += gm;
+    s2[k] += gm * ((v.v[k] - mu[k]) * is[k]);
+  }
+}
+
+template <bool RELU>
 __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
-    int relu, int64_t rows, int C, float* __restrict__ part) {
+    int64_t rows, int C, float* __restrict__ part) {
   extern __shared__ float smem[];
   Map m(C);
   int c0 = m.tx * 8;
@@ -279,21 +304,19 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
     is[k] = invstd[c0 + k];
   }
   float s1[8] = {0}, s2[8] = {0};
-#pragma unroll 2
-  for (int64_t r = (int64_t)blockIdx.x * m.rb + m.ty; r < rows; r += (int64_t)gridDim.x * m.rb) {
-    Vec8 v = load8(x + r * C + c0);
-    Vec8 d = load8(dy + r * C + c0);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float gm = d.v[k];
-      if (relu) {
-        float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
-        gm = yk > 0.0f ? gm : 0.0f;
-      }
-      float xh = (v.v[k] - mu[k]) * is[k];
-      s1[k] += gm;
-      s2[k] += gm * xh;
-    }
+  const int64_t step = (int64_t)gridDim.x * m.rb;
+  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
+  for (; r + step < rows; r += 2 * step) {
+    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
+    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
+    Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
+    bwd_acc<RELU>(v0, d0, sc, sh, mu, is, s1, s2);
+    bwd_acc<RELU>(v1, d1, sc, sh, mu, is, s1, s2);
+  }
+  if (r < rows) {
+    const int64_t o0 = r * C + c0;
+    Vec8 v0 = load8(x + o0), d0 = load8(dy + o0);
+    bwd_acc<RELU>(v0, d0, sc, sh, mu, is, s1, s2);
   }
   cta_reduce2(s1, s2, smem, m);
   if (m.ty == 0) {
@@ -306,8 +329,6 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
   }
 }
 
-// dbeta = sum(gm), dgamma = sum(gm*xhat)  (fp32, written straight into the
-// gradient region); coef = (dbeta/N, dgamma/N) for the elementwise pass
 __global__ void __launch_bounds__(256) bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
                                                     float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                     float* __restrict__ coef) {
@@ -455,12 +476,17 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
                         const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
                         void* ws, cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
-  int grid = grid_rows(bwd_reduce_kernel, reduce_smem(C), rows, C);
+  int grid = relu ? grid_rows(bwd_reduce_kernel<true>, reduce_smem(C), rows, C)
+                  : grid_rows(bwd_reduce_kernel<false>, reduce_smem(C), rows, C);
   float* part = static_cast<float*>(ws);
   float* coef = part + (size_t)kMaxGrid * 2 * C;
-  bwd_reduce_kernel<<<grid, kThreads, reduce_smem(C), s>>>(
-      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
-      static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), relu, rows, C, part);
+  auto red = [&](auto kernel) {
+    kernel<<<grid, kThreads, reduce_smem(C), s>>>(
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
+        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), rows, C, part);
+  };
+  if (relu) red(bwd_reduce_kernel<true>);
+  else red(bwd_reduce_kernel<false>);
   bwd_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
   if (dx) {
     auto launch = [&](auto kernel) {

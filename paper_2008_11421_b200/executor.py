@@ -285,8 +285,15 @@ class Executor:
         views = self._slot_views(b, slot)
         if action in (_lib.FW, _lib.RECOMPUTE_FW):
             x = self._block_input(b)
+            n = hi - lo + 1
             for k, ui in enumerate(range(lo, hi + 1)):
-                x = self.units[ui - 1].forward(x, self.params[ui], views[k])
+                u = self.units[ui - 1]
+                if k + 1 < n and getattr(u, "writes_out", False):
+                    # write straight into the next unit's saved-input slot
+                    nxt = self.units[ui]
+                    x = u.forward(x, self.params[ui], views[k], out=nxt.saved_input(views[k + 1]))
+                else:
+                    x = u.forward(x, self.params[ui], views[k])
             self.handoff = (b, x)
             if action == _lib.FW and b == self.nb:
                 self.loss, dy = self.loss_fn(x, self.target)

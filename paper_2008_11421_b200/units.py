@@ -100,6 +100,12 @@ def _conv(x, w, stride, pad):
     return _aten.convolution(x, w, None, [stride, stride], [pad, pad], [1, 1], False, [0, 0], 1)
 
 
+def _save_input(dst, x):
+    """Copy the unit input into its slot unless the previous unit wrote it there."""
+    if dst.data_ptr() != x.data_ptr():
+        dst.copy_(x)
+
+
 def _conv_into(x, w, stride, pad, out=None):
     """conv written straight into `out` (an arena-slot view) when given."""
     if out is None:
@@ -281,10 +287,10 @@ class BottleneckUnit(_ConvNetUnit):
     def _fused(self):
         return self.act == torch.bfloat16 and all(bnfused.supported(c) for c in (self.w, self.cout))
 
-    def _forward_fused(self, x, params, saved):
+    def _forward_fused(self, x, params, saved, out=None):
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         if saved is not None:
-            _cl(saved[0]).copy_(x)
+            _save_input(_cl(saved[0]), x)
             st = self._stats_views(saved[-1])
         else:
             st = self._stats_views(torch.empty(self._nstats(), device=x.device))
@@ -304,8 +310,8 @@ class BottleneckUnit(_ConvNetUnit):
             cd = _conv_into(x, _cl(wd), self.s, 0, sv(4))
             bnfused.stats(cd, st[6], st[7])
             return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=cd, rstats=(st[6], st[7]),
-                                 rg=gd, rb=bd)
-        return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=x)
+                                 rg=gd, rb=bd, out=out)
+        return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=x, out=out)
 
     def _backward_fused(self, dy, params, saved, grads):
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
@@ -343,9 +349,13 @@ class BottleneckUnit(_ConvNetUnit):
             dx.add_(dz)
         return dx
 
-    def forward(self, x, params, saved):
+    @property
+    def writes_out(self):
+        return self._fused()
+
+    def forward(self, x, params, saved, out=None):
         if self._fused():
-            return self._forward_fused(x, params, saved)
+            return self._forward_fused(x, params, saved, out)
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         if saved is not None:
             _cl(saved[0]).copy_(x)
@@ -589,10 +599,12 @@ class PreActBottleneckUnit(_ConvNetUnit):
             o += n
         return v
 
-    def forward(self, x, params, saved):
+    writes_out = True
+
+    def forward(self, x, params, saved, out=None):
         g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
         if saved is not None:
-            _cl(saved[0]).copy_(x)
+            _save_input(_cl(saved[0]), x)
             st = self._st(saved[3])
         else:
             st = self._st(torch.empty(self._nstats(), device=x.device))
@@ -609,6 +621,8 @@ class PreActBottleneckUnit(_ConvNetUnit):
         _stats_fw(c2, st[4], st[5])
         a2 = _bn_relu(c2, st[4], st[5], g2, b2)
         y = _conv(a2, _cl(w3), 1, 0)
+        if out is not None:
+            return torch.add(y, sc, out=out)
         return y.add_(sc)
 
     def backward(self, dy, params, saved, grads):
@@ -916,11 +930,13 @@ class TransformerLayerUnit(Unit):
         d = torch.stack([z.transpose(1, 2) for z in (dq, dk, dv)], dim=2)   # [n, s, 3, nh, hd]
         return d.reshape(-1, 3 * self.h)
 
-    def forward(self, x, params, saved):
+    writes_out = True
+
+    def forward(self, x, params, saved, out=None):
         g1, b1, wqkv, bqkv, wo, bo, g2, b2, w1, bf1, w2, bf2 = params
         t = x.shape[0]
         if saved is not None:
-            saved[0].copy_(x)
+            _save_input(saved[0], x)
             st = saved[5]
             m1, r1, m2, r2 = st[:t], st[t:2 * t], st[2 * t:3 * t], st[3 * t:]
         else:
@@ -933,7 +949,9 @@ class TransformerLayerUnit(Unit):
         h2, _, _ = _ln_fw(x2, g2, b2, m2, r2)
         f1 = _linear(h2, w1, bf1)
         del h2
-        y = x2 + _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
+        mlp = _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
+        y = torch.add(x2, mlp, out=out) if out is not None else x2 + mlp
+        del mlp
         if saved is not None:
             saved[1].copy_(qkv)
             saved[2].copy_(o)
