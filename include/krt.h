@@ -111,6 +111,8 @@ typedef struct krt_config {
                                (distsim.py:134-137 applies this from 2 workers) */
   int force_dp_path;        /* 1: data-parallel op structure (reduce-scatter / shard host
                                update / all-gather) even at world_size 1 (NCCL, 1 rank) */
+  int ipc_exchange;         /* 1: exchange over CUDA IPC peer memory between processes
+                               (own reduce kernel + D2D gather, stream-memop flags) */
 } krt_config;
 
 /* In-process exchange group: world_size ranks living in one process (threads),
@@ -184,6 +186,13 @@ int krt_init_master(krt_ctx* ctx);
 int krt_run_iteration(krt_ctx* ctx, krt_compute_cb cb, void* user);
 /* Wait for all device streams and host updates of the last iteration. */
 int krt_synchronize(krt_ctx* ctx);
+
+/* Cross-process exchange over NVLink peer memory (ipc_exchange = 1): after
+ * krt_prepare every rank exports 3 CUDA IPC handles (weights, gradients,
+ * flags; *len = 192 bytes), the ranks all-gather them (torch.distributed) and
+ * each imports the world*192 bytes in rank order. */
+int krt_ipc_export(krt_ctx* ctx, void* out, size_t cap, size_t* len);
+int krt_ipc_import(krt_ctx* ctx, const void* handles, int world);
 
 /* Wait for the last iteration, then return every host-updated weight to the
  * device copy now (the weight_in the next iteration would do), so the device

@@ -46,7 +46,7 @@ class Config(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
                 ("momentum", C.c_float), ("grad_scale", C.c_float), ("host_threads", C.c_int),
                 ("arena_slack_bytes", C.c_size_t), ("peer_group", C.c_void_p),
-                ("host_path_all", C.c_int), ("force_dp_path", C.c_int)]
+                ("host_path_all", C.c_int), ("force_dp_path", C.c_int), ("ipc_exchange", C.c_int)]
 
 
 COMPUTE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -83,6 +83,8 @@ EXPORTS = {
     "krt_run_iteration": (C.c_int, [C.c_void_p, COMPUTE_CB, C.c_void_p]),
     "krt_synchronize": (C.c_int, [C.c_void_p]),
     "krt_flush_weights": (C.c_int, [C.c_void_p]),
+    "krt_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "krt_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "krt_trace_csv": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_read_master": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_float), C.c_size_t]),

@@ -325,6 +325,19 @@ int krt_synchronize(krt_ctx* ctx) {
   return guard([&] { ctx->rt->synchronize(); });
 }
 
+int krt_ipc_export(krt_ctx* ctx, void* out, size_t cap, size_t* len) {
+  return guard([&] {
+    auto h = ctx->rt->ipc_export();
+    if (len) *len = h.size();
+    if (cap < h.size()) throw std::invalid_argument("ipc handle buffer too small");
+    std::memcpy(out, h.data(), h.size());
+  });
+}
+
+int krt_ipc_import(krt_ctx* ctx, const void* handles, int world) {
+  return guard([&] { ctx->rt->ipc_import(static_cast<const uint8_t*>(handles), world); });
+}
+
 int krt_flush_weights(krt_ctx* ctx) {
   return guard([&] { ctx->rt->flush_weights(); });
 }

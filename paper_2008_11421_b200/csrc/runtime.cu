@@ -1,5 +1,7 @@
 #include "runtime.hpp"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -92,7 +94,11 @@ Runtime::Runtime(const krt_config& cfg) : cfg_(cfg) {
   for (int i = 1; i < 4; ++i) CK(cudaStreamCreateWithPriority(&streams_[i], cudaStreamNonBlocking, hi));
   CK(cudaEventCreate(&ev_base_));
   dp_ = world_ > 1 || cfg.force_dp_path;
-  if (dp_ && cfg.peer_group) {
+  ipc_ = dp_ && cfg.ipc_exchange;
+  if (ipc_ && cfg.peer_group) throw std::invalid_argument("choose one of peer_group and ipc_exchange");
+  if (ipc_) {
+    // peers connect after prepare (krt_ipc_export / krt_ipc_import)
+  } else if (dp_ && cfg.peer_group) {
     peers_ = static_cast<PeerGroup*>(cfg.peer_group);
     if (peers_->world != world_) throw std::invalid_argument("peer group size != world_size");
     std::lock_guard<std::mutex> lk(peers_->mu);
@@ -138,6 +144,13 @@ Runtime::~Runtime() {
   cudaFree(d_m_);
   cudaFree(d_v_);
   cudaFree(d_shard_);
+  for (int p = 0; p < (int)ipc_w_.size(); ++p)
+    if (p != rank_) {
+      if (ipc_w_[p]) cudaIpcCloseMemHandle(ipc_w_[p]);
+      if (ipc_g_[p]) cudaIpcCloseMemHandle(ipc_g_[p]);
+      if (ipc_flags_[p]) cudaIpcCloseMemHandle(ipc_flags_[p]);
+    }
+  cudaFree(d_flags_);
   cudaFreeHost(h_swap_);
   cudaFreeHost(h_grad_);
   cudaFreeHost(h_wstage_);
@@ -404,6 +417,11 @@ void Runtime::allocate() {
     for (auto& g : groups_) ns += (size_t)g.shard_n;
     CK(cudaMalloc((void**)&d_shard_, std::max<size_t>(ns, 64) * 4));
   }
+  if (ipc_) {
+    size_t nf = (size_t)3 * groups_.size() * world_;
+    CK(cudaMalloc((void**)&d_flags_, std::max<size_t>(nf, 1) * 4));
+    CK(cudaMemset(d_flags_, 0, std::max<size_t>(nf, 1) * 4));
+  }
   // pinned host: swap area + gradient landing + weight staging
   h_swap_bytes_ = 0;
   for (auto& [id, b] : blocks_)
@@ -622,11 +640,15 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         }
       }
       CK(cudaEventRecord(ev_done_[idx], s));
-      if (peers_ && e.action == Action::BW) {
+      if ((peers_ || ipc_) && e.action == Action::BW) {
         int gi = blocks_.at(e.block).group;
         if (group_first_block_.at(gi) == e.block) {  // last backward of the group
-          CK(cudaEventRecord(peers_->event(rank_, PK_BW, gi), s));
-          peers_->mark(rank_, PK_BW, gi, step);
+          if (ipc_) {
+            ipc_signal(s, PK_BW, gi, (uint32_t)step);
+          } else {
+            CK(cudaEventRecord(peers_->event(rank_, PK_BW, gi), s));
+            peers_->mark(rank_, PK_BW, gi, step);
+          }
         }
       }
       return;
@@ -681,14 +703,20 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
       auto& g = groups_.at((size_t)e.group - 1);
       size_t shard_pos = 0;
       for (int gi = 0; gi < e.group - 1; ++gi) shard_pos += (size_t)groups_[gi].shard_n;
-      if (peers_) {
-        peers_->wait_all(PK_BW, e.group, step);
+      if (peers_ || ipc_) {
         std::vector<const float*> in((size_t)world_);
-        for (int p = 0; p < world_; ++p) {
-          Runtime* peer = peers_->ranks[p];
-          if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
-          CK(cudaStreamWaitEvent(s, peers_->event(p, PK_BW, e.group), 0));
-          in[p] = peer->grads_base() + g.p_lo + (int64_t)rank_ * g.shard_n;
+        if (ipc_) {
+          ipc_wait(s, PK_BW, e.group, (uint32_t)step);
+          for (int p = 0; p < world_; ++p)
+            in[p] = reinterpret_cast<const float*>(ipc_g_[p]) + g.p_lo + (int64_t)rank_ * g.shard_n;
+        } else {
+          peers_->wait_all(PK_BW, e.group, step);
+          for (int p = 0; p < world_; ++p) {
+            Runtime* peer = peers_->ranks[p];
+            if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
+            CK(cudaStreamWaitEvent(s, peers_->event(p, PK_BW, e.group), 0));
+            in[p] = peer->grads_base() + g.p_lo + (int64_t)rank_ * g.shard_n;
+          }
         }
         CK(cudaEventRecord(ev_start_[idx], s));
         CK(launch_reduce_cast(in.data(), world_, d_shard_ + shard_pos, KRT_F32, (size_t)g.shard_n, 1.0f, s));
@@ -732,7 +760,11 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         cudaStream_t ns = streams_[3];
         CK(cudaEventRecord(ev_done_[idx], s));
         CK(cudaStreamWaitEvent(ns, ev_done_[idx], 0));
-        if (peers_) {
+        if (ipc_) {
+          ipc_signal(s, PK_WSHARD, e.group, (uint32_t)step);
+          ipc_wait(ns, PK_WSHARD, e.group, (uint32_t)step);
+          gather_peer_shards(g, e.group, ns, PK_WSHARD);
+        } else if (peers_) {
           CK(cudaEventRecord(peers_->event(rank_, PK_WSHARD, e.group), s));
           peers_->mark(rank_, PK_WSHARD, e.group, step);
           peers_->wait_all(PK_WSHARD, e.group, step);
@@ -859,7 +891,12 @@ void Runtime::flush_weights() {
       void* dst = d_weight(g.p_lo + (int64_t)rank_ * g.shard_n);
       CK(cudaMemcpyAsync(dst, static_cast<uint8_t*>(h_wstage_) + g.host_off * wb, (size_t)g.shard_n * wb,
                          cudaMemcpyHostToDevice, s));
-      if (peers_) {
+      if (ipc_) {
+        int gi = (int)(&g - groups_.data()) + 1;
+        ipc_signal(s, PK_FLUSH, gi, (uint32_t)(flush_count_ + 1));
+        ipc_wait(s, PK_FLUSH, gi, (uint32_t)(flush_count_ + 1));
+        gather_peer_shards(g, gi, s, PK_FLUSH);
+      } else if (peers_) {
         int gi = (int)(&g - groups_.data()) + 1;
         CK(cudaEventRecord(peers_->event(rank_, PK_FLUSH, gi), s));
         peers_->mark(rank_, PK_FLUSH, gi, flush_count_ + 1);
@@ -887,14 +924,101 @@ void Runtime::gather_peer_shards(const GroupPhys& g, int group, cudaStream_t s, 
   size_t wb = dtype_bytes(cfg_.weight_dtype);
   for (int p = 0; p < world_; ++p) {
     if (p == rank_) continue;
-    Runtime* peer = peers_->ranks[p];
-    if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
-    CK(cudaStreamWaitEvent(s, peers_->event(p, kind, group), 0));
+    const uint8_t* src;
+    if (ipc_) {
+      src = ipc_w_[p];
+    } else {
+      Runtime* peer = peers_->ranks[p];
+      if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
+      CK(cudaStreamWaitEvent(s, peers_->event(p, kind, group), 0));
+      src = static_cast<const uint8_t*>(peer->weights_base());
+    }
     size_t off = (size_t)(g.p_lo + (int64_t)p * g.shard_n) * wb;
-    CK(cudaMemcpyAsync(static_cast<uint8_t*>(d_weights_) + off, static_cast<uint8_t*>(peer->weights_base()) + off,
-                       (size_t)g.shard_n * wb, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(d_weights_) + off, src + off, (size_t)g.shard_n * wb,
+                       cudaMemcpyDefault, s));
   }
   bytes_net_ += (size_t)g.shard_n * wb * (world_ - 1);
+}
+
+size_t Runtime::flag_index(int kind, int group, int src) const {
+  return ((size_t)kind * groups_.size() + (size_t)(group - 1)) * (size_t)world_ + (size_t)src;
+}
+
+// driver stream-memory ops, resolved through the runtime (no libcuda link, so
+// the library still loads on a host without the driver)
+namespace {
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteFn g_write32 = nullptr;
+WaitFn g_wait32 = nullptr;
+void load_memops() {
+  if (g_write32 && g_wait32) return;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&g_write32, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !g_write32) throw CudaError("cuStreamWriteValue32 unavailable");
+  CK(cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&g_wait32, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !g_wait32) throw CudaError("cuStreamWaitValue32 unavailable");
+}
+}  // namespace
+
+// flag write into every rank's array: ordered after the stream's prior work,
+// with the default memory barrier (peers then read our data over NVLink)
+void Runtime::ipc_signal(cudaStream_t s, int kind, int group, uint32_t value) {
+  if (!ipc_ready_) throw std::logic_error("IPC exchange used before krt_ipc_import");
+  for (int q = 0; q < world_; ++q) {
+    CUresult r = g_write32((CUstream)s, (CUdeviceptr)(ipc_flags_[q] + flag_index(kind, group, rank_)),
+                                      value, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed: " + std::to_string((int)r));
+  }
+}
+
+void Runtime::ipc_wait(cudaStream_t s, int kind, int group, uint32_t value) {
+  for (int p = 0; p < world_; ++p) {
+    CUresult r = g_wait32((CUstream)s, (CUdeviceptr)(d_flags_ + flag_index(kind, group, p)), value,
+                                     CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed: " + std::to_string((int)r));
+  }
+}
+
+std::vector<uint8_t> Runtime::ipc_export() {
+  if (!prepared_ || !ipc_) throw std::logic_error("ipc_export needs a prepared context with ipc_exchange");
+  CK(cudaSetDevice(cfg_.device));
+  std::vector<uint8_t> out(3 * sizeof(cudaIpcMemHandle_t));
+  cudaIpcMemHandle_t h[3];
+  CK(cudaIpcGetMemHandle(&h[0], d_weights_));
+  CK(cudaIpcGetMemHandle(&h[1], d_grads_));
+  CK(cudaIpcGetMemHandle(&h[2], d_flags_));
+  std::memcpy(out.data(), h, out.size());
+  return out;
+}
+
+void Runtime::ipc_import(const uint8_t* all, int world) {
+  if (!ipc_) throw std::logic_error("context was not created with ipc_exchange");
+  if (world != world_) throw std::invalid_argument("handle count != world_size");
+  CK(cudaSetDevice(cfg_.device));
+  size_t hb = 3 * sizeof(cudaIpcMemHandle_t);
+  ipc_w_.assign(world_, nullptr);
+  ipc_g_.assign(world_, nullptr);
+  ipc_flags_.assign(world_, nullptr);
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) {
+      ipc_w_[p] = static_cast<uint8_t*>(d_weights_);
+      ipc_g_[p] = reinterpret_cast<uint8_t*>(d_grads_);
+      ipc_flags_[p] = d_flags_;
+      continue;
+    }
+    cudaIpcMemHandle_t h[3];
+    std::memcpy(h, all + (size_t)p * hb, hb);
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h[0], cudaIpcMemLazyEnablePeerAccess));
+    ipc_w_[p] = static_cast<uint8_t*>(ptr);
+    CK(cudaIpcOpenMemHandle(&ptr, h[1], cudaIpcMemLazyEnablePeerAccess));
+    ipc_g_[p] = static_cast<uint8_t*>(ptr);
+    CK(cudaIpcOpenMemHandle(&ptr, h[2], cudaIpcMemLazyEnablePeerAccess));
+    ipc_flags_[p] = static_cast<uint32_t*>(ptr);
+  }
+  load_memops();
+  ipc_ready_ = true;
 }
 
 void* Runtime::block_slot(int block) const {

@@ -110,6 +110,8 @@ class Runtime {
   void read_master(int block, float* out, size_t numel);
   void* block_slot(int block) const;
   void flush_weights();
+  std::vector<uint8_t> ipc_export();
+  void ipc_import(const uint8_t* all, int world);
   void* weights_base() const { return d_weights_; }
   float* grads_base() const { return d_grads_; }
 
@@ -158,6 +160,15 @@ class Runtime {
   cudaEvent_t ev_base_ = nullptr;
   void* nccl_comm_ = nullptr;
   PeerGroup* peers_ = nullptr;     // in-process exchange instead of NCCL
+  // cross-process exchange over CUDA IPC peer memory: peers' weight/grad
+  // regions and flag arrays, ordered by stream memory ops on the flags
+  bool ipc_ = false, ipc_ready_ = false;
+  uint32_t* d_flags_ = nullptr;
+  std::vector<uint8_t*> ipc_w_, ipc_g_;
+  std::vector<uint32_t*> ipc_flags_;
+  size_t flag_index(int kind, int group, int src) const;
+  void ipc_signal(cudaStream_t s, int kind, int group, uint32_t value);
+  void ipc_wait(cudaStream_t s, int kind, int group, uint32_t value);
   int flush_count_ = 0;
   std::map<int, int> group_first_block_;  // group -> lowest member (last bw of the group)
 

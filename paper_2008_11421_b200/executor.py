@@ -123,6 +123,7 @@ class ExecConfig:
     peer_group: Optional[object] = None   # _lib.PeerGroup for in-process ranks
     host_path_all: bool = False           # host update for every block even at world_size 1
     force_dp_path: bool = False           # DP op structure through a 1-rank NCCL communicator
+    ipc_exchange: bool = False            # exchange over CUDA IPC peer memory (multi-process)
 
 
 class Executor:
@@ -152,7 +153,7 @@ class Executor:
                          cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.momentum,
                          1.0 / cfg.world_size, cfg.host_threads, cfg.arena_slack_bytes,
                          cfg.peer_group.handle if cfg.peer_group is not None else None,
-                         int(cfg.host_path_all), int(cfg.force_dp_path))
+                         int(cfg.host_path_all), int(cfg.force_dp_path), int(cfg.ipc_exchange))
         h = C.c_void_p()
         _lib.check(L.krt_create(C.byref(kc), C.byref(h)))
         self._ctx = h
@@ -240,6 +241,17 @@ class Executor:
         _lib.check(_lib.lib().krt_read_master(self._ctx, block,
                                               C.cast(out.data_ptr(), C.POINTER(C.c_float)), n))
         return out[:n]
+
+    def ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(256)
+        n = C.c_size_t()
+        _lib.check(_lib.lib().krt_ipc_export(self._ctx, buf, 256, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def ipc_connect(self, all_handles: list):
+        """all_handles: every rank's ipc_handles(), in rank order."""
+        blob = b"".join(all_handles)
+        _lib.check(_lib.lib().krt_ipc_import(self._ctx, blob, len(all_handles)))
 
     def flush_weights(self):
         """Return host-updated weights to the device now (krt_flush_weights)."""
