@@ -246,18 +246,20 @@ def run_gpu(args, rec):
     from paper_2008_11421_b200 import workloads as W
     from paper_2008_11421_b200.executor import ExecConfig, Executor
     world, rank, local = dist_env()
+    if os.environ.get("KRT_BENCH_SHARE_GPU") == "1":
+        local = 0      # test mode: every rank on cuda:0 (IPC still crosses processes)
     torch.cuda.set_device(local)
     torch.backends.cudnn.benchmark = True
     nccl_id = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        from paper_2008_11421_b200 import _lib
-        idbuf = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            idbuf = torch.tensor(list(_lib.nccl_unique_id()), dtype=torch.uint8)
-        idbuf = idbuf.cuda()
-        dist.broadcast(idbuf, 0)
-        nccl_id = bytes(idbuf.cpu().tolist())
+        # control plane (barriers, max-over-ranks, handle exchange) over gloo;
+        # the data-path exchange is the runtime's own (IPC) or NCCL
+        dist.init_process_group("gloo")
+        if args.exchange == "nccl":
+            from paper_2008_11421_b200 import _lib
+            box = [_lib.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            nccl_id = box[0]
     m = rec["meta"]
     batch = m["batch"]
     units = W.units_for(rec)
@@ -271,7 +273,12 @@ def run_gpu(args, rec):
     t_setup = time.perf_counter()
     ex = Executor(units, bundle, batch=batch, loss_fn=loss_fn,
                   cfg=ExecConfig(device=local, world_size=world, rank=rank, nccl_id=nccl_id,
+                                 ipc_exchange=(world > 1 and args.exchange == "ipc"),
                                  weight_dtype=torch.bfloat16, **opt_cfg))
+    if world > 1 and args.exchange == "ipc":
+        handles = [None] * world
+        dist.all_gather_object(handles, ex.ipc_handles())
+        ex.ipc_connect(handles)
     ex.init_weights(seed=0)
     setup_s = time.perf_counter() - t_setup
     dev = torch.device("cuda", local)
@@ -312,7 +319,7 @@ def run_gpu(args, rec):
     launches = st["kernel_launches_total"] - launches0
     h2d_iter = (st["bytes_h2d_total"] - h2d0) / args.steps
     d2h_iter = (st["bytes_d2h_total"] - d2h0) / args.steps
-    t = torch.tensor([ms], device=dev)
+    t = torch.tensor([ms])
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -331,7 +338,7 @@ def run_gpu(args, rec):
     ex.synchronize()
     barrier()
     e2e_s = time.perf_counter() - t0
-    tt = torch.tensor([e2e_s], device=dev)
+    tt = torch.tensor([e2e_s])
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_value = world * batch * e2e_steps / float(tt.item())
@@ -356,7 +363,8 @@ def run_gpu(args, rec):
              "pcie_d2h_s": d2h_iter / PCIE_D2H,
              "nvlink_s": 0.0}
     if world > 1:
-        terms["nvlink_s"] = st["params"] * 4 * (world - 1) / world * 2 / 770e9
+        # reduce-scatter reads (P-1)/P of the fp32 grads, the gather (P-1)/P of the bf16 weights
+        terms["nvlink_s"] = st["params"] * (world - 1) / world * (4 + 2) / 770e9
     bind = max(terms, key=terms.get)
     rows = [r.split(",") for r in trace.strip().splitlines()[1:]]
     comp = [(float(r[0]), float(r[1])) for r in rows if r[2] == "compute"]
@@ -382,7 +390,7 @@ def run_gpu(args, rec):
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": rec["name"], "model": model_name(rec), "per_gpu_batch": batch,
+        "config": {"workload": rec["name"], "exchange": args.exchange if world > 1 else "none", "model": model_name(rec), "per_gpu_batch": batch,
                    "global_batch": batch * world, "input": m.get("res", m.get("seq")), "parallelism": f"dp{world}",
                    "plan": rec["plan_string"][:160] + " ...",
                    "activations_bytes": rec["total_bytes"], "hbm_bytes": 183359 * 2 ** 20,
@@ -446,6 +454,8 @@ def main():
     ap.add_argument("--impl", default="krt", choices=["krt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-out", default=None)
+    ap.add_argument("--exchange", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1 gradient exchange: own reduce-scatter over CUDA IPC peer memory, or NCCL")
     ap.add_argument("--incore", action="store_true",
                     help="same blocks, everything resident (no swap/recompute): the in-core baseline")
     args = ap.parse_args()
