@@ -56,6 +56,13 @@ typedef struct krt_plan krt_plan;
 int krt_plan_load(const char* model_text, const char* hw_text, const char* plan_json,
                   krt_plan** out);
 void krt_plan_free(krt_plan* plan);
+/* plan_model (planner.py:890-912) in C++: partition, recompute flags and the
+ * Algorithm-1 schedule, bit-identical to the reference planner.  strategy:
+ * "eager" | "capacity" | "capacity-recompute"; solver: "auto" | "exhaustive" |
+ * "dp"; max_blocks <= 0 = None.  KRT_INFEASIBLE carries InfeasibleModelError's
+ * reason. */
+int krt_plan_model(const char* model_text, const char* hw_text, const char* strategy,
+                   const char* solver, int max_blocks, krt_plan** out);
 /* Override hardware capacity (bytes) for validation / simulation. */
 int krt_plan_set_capacity(krt_plan* plan, double capacity_bytes);
 

@@ -57,6 +57,8 @@ EXPORTS = {
     "krt_string_free": (None, [C.c_void_p]),
     "krt_plan_load": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
     "krt_plan_free": (None, [C.c_void_p]),
+    "krt_plan_model": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int,
+                                 C.POINTER(C.c_void_p)]),
     "krt_plan_set_capacity": (C.c_int, [C.c_void_p, C.c_double]),
     "krt_plan_string": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_plan_json": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -11,6 +11,7 @@
 
 #include "../../include/krt.h"
 #include "engine.hpp"
+#include "planner.hpp"
 #include "host_optim.hpp"
 #include "bn_kernels.hpp"
 #include "kernels.hpp"
@@ -119,6 +120,30 @@ int krt_plan_load(const char* model_text, const char* hw_text, const char* plan_
 }
 
 void krt_plan_free(krt_plan* p) { delete p; }
+
+int krt_plan_model(const char* model_text, const char* hw_text, const char* strategy, const char* solver,
+                   int max_blocks, krt_plan** out) {
+  return guard([&] {
+    if (!model_text || !hw_text || !out) throw std::invalid_argument("null argument");
+    auto p = std::make_unique<krt_plan>();
+    p->model = parse_model_text(model_text);
+    p->hw = parse_hardware_text(hw_text);
+    std::string st = strategy ? strategy : "capacity-recompute";
+    Strategy s;
+    if (st == "eager") s = Strategy::EAGER;
+    else if (st == "capacity") s = Strategy::CAPACITY;
+    else if (st == "capacity-recompute") s = Strategy::CAPACITY_RECOMPUTE;
+    else throw std::invalid_argument("'" + st + "' is not a valid Strategy");
+    try {
+      p->plan = plan_model(p->model, p->hw, s, solver ? solver : "auto", max_blocks);
+    } catch (const InfeasibleModel& e) {
+      throw Infeasible(e.what());
+    } catch (const PlannerMisuse& e) {
+      throw std::invalid_argument(e.what());
+    }
+    *out = p.release();
+  });
+}
 
 int krt_plan_set_capacity(krt_plan* p, double cap) {
   return guard([&] {

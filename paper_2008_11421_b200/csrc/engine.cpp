@@ -19,19 +19,6 @@ int queue_rank(Action a) {
     default: return 0;
   }
 }
-// Python >= 3.12 builtin sum() over floats: Neumaier-compensated
-// (bltinmodule.c builtin_sum_impl).  Used wherever the reference calls sum().
-struct PySum {
-  double f = 0.0, c = 0.0;
-  void add(double x) {
-    double t = f + x;
-    if (std::fabs(f) >= std::fabs(x)) c += (f - t) + x;
-    else c += (x - t) + f;
-    f = t;
-  }
-  double value() const { return (c != 0.0 && std::isfinite(c)) ? f + c : f; }
-};
-
 bool is_compute(Action a) { return a == Action::FW || a == Action::BW || a == Action::RECOMPUTE_FW; }
 }  // namespace
 
@@ -298,6 +285,20 @@ SimResult simulate(const Plan& p, const Model& g, const Hardware& hw, bool enfor
   sr.total_stall = er.makespan - busy;
   sr.peak = er.peak;
   return sr;
+}
+
+bool plan_metrics(const Plan& p, const Model& g, const Hardware& hw, const std::map<int, BlockCost>& costs,
+                  double* makespan, double* stall, double* peak) {
+  auto ops = build_engine_ops(p, g, hw, costs);
+  EngineResult er = run_engine(ops, base_resources(hw), hw.capacity_bytes, true);
+  if (er.deadlock) return false;
+  PySum busy;
+  for (auto& e : er.events)   // raw events in op order (simulator.py:359-360)
+    if (e.res == R_COMPUTE) busy.add(e.t_end - e.t_start);
+  *makespan = er.makespan;
+  *stall = er.makespan - busy.value();
+  *peak = er.peak;
+  return true;
 }
 
 std::vector<std::string> residency_memory_walk(const Plan& p, const Model& g, const Hardware& hw,

@@ -14,6 +14,19 @@
 
 namespace krt {
 
+// Python >= 3.12 builtin sum() over floats: Neumaier-compensated
+// (bltinmodule.c builtin_sum_impl).  Used wherever the reference calls sum().
+struct PySum {
+  double f = 0.0, c = 0.0;
+  void add(double x) {
+    double t = f + x;
+    if ((f < 0 ? -f : f) >= (x < 0 ? -x : x)) c += (f - t) + x;
+    else c += (x - t) + f;
+    f = t;
+  }
+  double value() const { return (c != 0.0 && c - c == 0.0) ? f + c : f; }
+};
+
 enum Res : int { R_COMPUTE = 0, R_XFER_IN, R_XFER_OUT, R_XFER, R_NETWORK, R_HOST, R_COUNT };
 const char* res_name(int r);
 
@@ -65,6 +78,10 @@ struct SimResult {
   std::string csv() const;          // SimTrace.to_csv schema
 };
 SimResult simulate(const Plan& p, const Model& g, const Hardware& hw, bool enforce);
+// simulator.py:352-361 plan_metrics with caller-supplied costs:
+// returns false on deadlock; makespan, stall (= makespan - busy), peak
+bool plan_metrics(const Plan& p, const Model& g, const Hardware& hw, const std::map<int, BlockCost>& costs,
+                  double* makespan, double* stall, double* peak);
 
 std::vector<std::string> validate_plan(const Plan& p, const Model& g, const Hardware& hw);
 std::vector<std::string> residency_memory_walk(const Plan& p, const Model& g, const Hardware& hw,

@@ -123,6 +123,19 @@ class PlanBundle:
         return res
 
 
+def plan_model(model_text: str, hw_text: str, strategy: str = "capacity-recompute",
+               solver: str = "auto", max_blocks: Optional[int] = None) -> PlanBundle:
+    """planner.py:890-912 in C++ (csrc/planner.cpp): same plan, bit for bit."""
+    h = C.c_void_p()
+    _lib.check(_lib.lib().krt_plan_model(model_text.encode(), hw_text.encode(), strategy.encode(),
+                                         solver.encode(), int(max_blocks or 0), C.byref(h)))
+    b = PlanBundle.__new__(PlanBundle)
+    b.model_text, b.hw_text = model_text, hw_text
+    b._h = h
+    b.plan_json = None
+    return b
+
+
 # reference-named module functions -------------------------------------------------
 
 def read_plan(json_path, model_text: str, hw_text: str) -> PlanBundle:
