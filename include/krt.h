@@ -247,8 +247,10 @@ int krt_bn_apply(const void* x, const float* mean, const float* invstd, const vo
                  const void* beta, const void* res, const float* rmean, const float* rinvstd,
                  const void* rgamma, const void* rbeta, int relu, void* y, int64_t rows, int C,
                  void* stream);
-/* dz = dy * ( bn(x) + (res | bn'(res)) > 0 ): backward of the residual add + ReLU */
-int krt_bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd,
+/* dz = (dy [+ dy2]) * ( bn(x) + (res | bn'(res)) > 0 ): backward of the residual
+ * add + ReLU; dy2 (may be NULL) is a second incoming gradient, summed and
+ * rounded to bf16 first, so the producer never materialises dy + dy2 */
+int krt_bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const float* mean, const float* invstd,
                         const void* gamma, const void* beta, const void* res, const float* rmean,
                         const float* rinvstd, const void* rgamma, const void* rbeta, void* dz,
                         int64_t rows, int C, void* stream);

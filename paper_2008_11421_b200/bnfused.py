@@ -83,13 +83,16 @@ def apply(c, mean, invstd, g, b, relu, res=None, rstats=None, rg=None, rb=None, 
     return y
 
 
-def add_relu_bwd(dy, c, mean, invstd, g, b, res, rstats=None, rg=None, rb=None):
+def add_relu_bwd(dy, c, mean, invstd, g, b, res, rstats=None, rg=None, rb=None, dy2=None):
+    """dz = (dy [+ dy2]) * mask; dy2 is summed in-kernel (never materialised)."""
     c, dy, res = _nhwc(c), _nhwc(dy), _nhwc(res)
+    if dy2 is not None:
+        dy2 = _nhwc(dy2)
     rows, C = _rows_c(c)
     dz = torch.empty_like(c, memory_format=torch.channels_last)
     rm, ri = (rstats if rstats is not None else (None, None))
-    with _timed("bn_add_relu_bwd", rows * C * 2 * 4):
-        _lib.check(_lib.lib().krt_bn_add_relu_bwd(dy.data_ptr(), c.data_ptr(), mean.data_ptr(),
+    with _timed("bn_add_relu_bwd", rows * C * 2 * (4 if dy2 is None else 5)):
+        _lib.check(_lib.lib().krt_bn_add_relu_bwd(dy.data_ptr(), _ptr(dy2), c.data_ptr(), mean.data_ptr(),
                                               invstd.data_ptr(), g.data_ptr(), b.data_ptr(),
                                               res.data_ptr(), _ptr(rm), _ptr(ri), _ptr(rg), _ptr(rb),
                                               dz.data_ptr(), rows, C, _stream()))

@@ -139,17 +139,18 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __
   }
 }
 
-// Sum CTA partials for 32 channels per block: lane = channel, the 8 warps
-// stride over the partial rows, then a fixed-order tree over the warps
+// Sum CTA partials for 32 channels per block: lane = channel, the 32 warps
+// stride over the partial rows, then a fixed-order pass over the warps
 // (deterministic).  Returns the two double sums in lane c of warp 0.
+constexpr int kFinWarps = 32;
 __device__ __forceinline__ bool sum_partials(const float* __restrict__ part, int nblk, int C, double& s1,
                                              double& s2) {
-  __shared__ double sh[2][8][32];
+  __shared__ double sh[2][kFinWarps][33];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int c = blockIdx.x * 32 + lane;
   double a = 0, q = 0;
   if (c < C)
-    for (int b = w; b < nblk; b += 8) {
+    for (int b = w; b < nblk; b += kFinWarps) {
       a += part[(size_t)b * 2 * C + c];
       q += part[(size_t)b * 2 * C + C + c];
     }
@@ -159,14 +160,14 @@ __device__ __forceinline__ bool sum_partials(const float* __restrict__ part, int
   if (w != 0 || c >= C) return false;
   s1 = 0;
   s2 = 0;
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < kFinWarps; ++k) {
     s1 += sh[0][k][lane];
     s2 += sh[1][k][lane];
   }
   return true;
 }
 
-__global__ void __launch_bounds__(256) stats_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
+__global__ void __launch_bounds__(1024) stats_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
                                                       float eps, float* __restrict__ mean, float* __restrict__ invstd) {
   double s, q;
   if (!sum_partials(part, nblk, C, s, q)) return;
@@ -243,9 +244,19 @@ __device__ __forceinline__ Vec8 add_relu_row(const Vec8& v, const Vec8& rv, cons
   return o;
 }
 
-template <int MODE>
+// dy = bf16(dy + dy2): the residual-gradient sum the next unit handed over
+// unmaterialised, rounded exactly like a separate bf16 add would
+__device__ __forceinline__ Vec8 add_grad(const Vec8& a, const Vec8& b) {
+  Vec8 o;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o.v[k] = __bfloat162float(__float2bfloat16_rn(__fadd_rn(a.v[k], b.v[k])));
+  return o;
+}
+
+template <int MODE, bool DY2>
 __global__ void __launch_bounds__(kThreads) add_relu_bwd_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dy2, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
     const __nv_bfloat16* __restrict__ res, const float* __restrict__ rmean, const float* __restrict__ rinvstd,
     const __nv_bfloat16* __restrict__ rg, const __nv_bfloat16* __restrict__ rb_, __nv_bfloat16* __restrict__ dz,
@@ -262,12 +273,18 @@ __global__ void __launch_bounds__(kThreads) add_relu_bwd_kernel(
     Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
     Vec8 q0 = load8(res + o0), q1 = load8(res + o1);
     Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
+    if (DY2) {
+      Vec8 e0 = load8(dy2 + o0), e1 = load8(dy2 + o1);
+      d0 = add_grad(d0, e0);
+      d1 = add_grad(d1, e1);
+    }
     store8(dz + o0, add_relu_row<MODE>(v0, q0, d0, sc, sh, rsc, rsh));
     store8(dz + o1, add_relu_row<MODE>(v1, q1, d1, sc, sh, rsc, rsh));
   }
   if (r < rows) {
     const int64_t o0 = r * C + c0;
     Vec8 v0 = load8(x + o0), q0 = load8(res + o0), d0 = load8(dy + o0);
+    if (DY2) d0 = add_grad(d0, load8(dy2 + o0));
     store8(dz + o0, add_relu_row<MODE>(v0, q0, d0, sc, sh, rsc, rsh));
   }
 }
@@ -329,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
   }
 }
 
-__global__ void __launch_bounds__(256) bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
+__global__ void __launch_bounds__(1024) bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
                                                     float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                     float* __restrict__ coef) {
   double s1, s2;
@@ -430,7 +447,7 @@ cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean,
   int grid = grid_rows(stats_kernel, reduce_smem(C), rows, C);
   float* part = static_cast<float*>(ws);
   stats_kernel<<<grid, kThreads, reduce_smem(C), s>>>(static_cast<const __nv_bfloat16*>(x), rows, C, part);
-  stats_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, grid, rows, C, eps, mean, invstd);
+  stats_finalize<<<(C + 31) / 32, 32 * kFinWarps, 0, s>>>(part, grid, rows, C, eps, mean, invstd);
   return cudaGetLastError();
 }
 
@@ -456,19 +473,25 @@ cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, cons
   return cudaGetLastError();
 }
 
-cudaError_t bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
-                            const void* b, const void* res, const float* rmean, const float* rinvstd,
+cudaError_t bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const float* mean, const float* invstd,
+                            const void* g, const void* b, const void* res, const float* rmean, const float* rinvstd,
                             const void* rg, const void* rb, void* dz, int64_t rows, int C, cudaStream_t s) {
   if (!shape_ok(rows, C) || res == nullptr) return cudaErrorInvalidValue;
   auto args = [&](auto kernel) {
     kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
-        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b),
-        static_cast<const __nv_bfloat16*>(res), rmean, rinvstd, static_cast<const __nv_bfloat16*>(rg),
-        static_cast<const __nv_bfloat16*>(rb), static_cast<__nv_bfloat16*>(dz), rows, C);
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(dy2),
+        static_cast<const __nv_bfloat16*>(x), mean, invstd, static_cast<const __nv_bfloat16*>(g),
+        static_cast<const __nv_bfloat16*>(b), static_cast<const __nv_bfloat16*>(res), rmean, rinvstd,
+        static_cast<const __nv_bfloat16*>(rg), static_cast<const __nv_bfloat16*>(rb),
+        static_cast<__nv_bfloat16*>(dz), rows, C);
   };
-  if (rmean == nullptr) args(add_relu_bwd_kernel<1>);
-  else args(add_relu_bwd_kernel<2>);
+  if (rmean == nullptr) {
+    if (dy2) args(add_relu_bwd_kernel<1, true>);
+    else args(add_relu_bwd_kernel<1, false>);
+  } else {
+    if (dy2) args(add_relu_bwd_kernel<2, true>);
+    else args(add_relu_bwd_kernel<2, false>);
+  }
   return cudaGetLastError();
 }
 
@@ -487,7 +510,7 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
   };
   if (relu) red(bwd_reduce_kernel<true>);
   else red(bwd_reduce_kernel<false>);
-  bwd_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
+  bwd_finalize<<<(C + 31) / 32, 32 * kFinWarps, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
   if (dx) {
     auto launch = [&](auto kernel) {
       kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(

@@ -11,7 +11,7 @@ cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean,
 cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, const void* g, const void* b,
                      const void* res, const float* rmean, const float* rinvstd, const void* rg, const void* rb,
                      int relu, void* y, int64_t rows, int C, cudaStream_t s);
-cudaError_t bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+cudaError_t bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const float* mean, const float* invstd, const void* g,
                             const void* b, const void* res, const float* rmean, const float* rinvstd,
                             const void* rg, const void* rb, void* dz, int64_t rows, int C, cudaStream_t s);
 cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,

@@ -406,10 +406,10 @@ int krt_bn_apply(const void* x, const float* mean, const float* invstd, const vo
                  "bn_apply");
 }
 
-int krt_bn_add_relu_bwd(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
-                        const void* b, const void* res, const float* rmean, const float* rinvstd, const void* rg,
-                        const void* rb, void* dz, int64_t rows, int C, void* stream) {
-  KRT_CUDA_GUARD(bn_add_relu_bwd(dy, x, mean, invstd, g, b, res, rmean, rinvstd, rg, rb, dz, rows, C,
+int krt_bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const float* mean, const float* invstd,
+                        const void* g, const void* b, const void* res, const float* rmean, const float* rinvstd,
+                        const void* rg, const void* rb, void* dz, int64_t rows, int C, void* stream) {
+  KRT_CUDA_GUARD(bn_add_relu_bwd(dy, dy2, x, mean, invstd, g, b, res, rmean, rinvstd, rg, rb, dz, rows, C,
                                  (cudaStream_t)stream),
                  "bn_add_relu_bwd");
 }

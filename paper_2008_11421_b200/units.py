@@ -48,6 +48,7 @@ class FCUnit(Unit):
         return torch.mm(x, w.t())
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         (w,) = params
         x = saved[0]
         if dy.dtype == torch.float32 and x.dtype == torch.float32:
@@ -98,6 +99,18 @@ def _cl(t):
 
 def _conv(x, w, stride, pad):
     return _aten.convolution(x, w, None, [stride, stride], [pad, pad], [1, 1], False, [0, 0], 1)
+
+
+class GradPair(tuple):
+    """(a, b) standing for the gradient a + b, handed unsummed to the previous
+    unit so a fused kernel can add it on the fly (bn_add_relu_bwd dy2)."""
+
+
+def _dense(dy):
+    """Materialise a GradPair (bf16 a + b, rounded like a fused add would)."""
+    if isinstance(dy, GradPair):
+        return dy[0] + dy[1]
+    return dy
 
 
 def _save_input(dst, x):
@@ -199,6 +212,7 @@ class StemUnit(_ConvNetUnit):
         return y
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         w, g, b = params
         x, c = _cl(saved[0]), _cl(saved[1])
         m, i = saved[2][:self.cout], saved[2][self.cout:]
@@ -317,12 +331,15 @@ class BottleneckUnit(_ConvNetUnit):
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         x, c1, c2, c3 = (_cl(t) for t in saved[:4])
         st = self._stats_views(saved[-1])
+        dy, dy2 = (dy[0], dy[1]) if isinstance(dy, GradPair) else (dy, None)
         if self.down:
             wd, gd, bd = params[9:12]
             cd = _cl(saved[4])
-            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, cd, rstats=(st[6], st[7]), rg=gd, rb=bd)
+            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, cd, rstats=(st[6], st[7]), rg=gd, rb=bd,
+                                      dy2=dy2)
         else:
-            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, x)
+            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, x, dy2=dy2)
+        del dy, dy2
         dc3 = bnfused.backward(dz, c3, st[4], st[5], g3, b3, relu=False, dgamma=grads[7], dbeta=grads[8])
         a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
         da2, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0)
@@ -344,10 +361,8 @@ class BottleneckUnit(_ConvNetUnit):
                                    dbeta=grads[11])
             dxd, dwd, _ = _conv_bw(dcd, x, _cl(wd), self.s, 0)
             _cl(grads[9]).copy_(dwd)
-            dx.add_(dxd)
-        else:
-            dx.add_(dz)
-        return dx
+            return GradPair((dx, dxd))
+        return GradPair((dx, dz))
 
     @property
     def writes_out(self):
@@ -389,6 +404,7 @@ class BottleneckUnit(_ConvNetUnit):
     def backward(self, dy, params, saved, grads):
         if self._fused():
             return self._backward_fused(dy, params, saved, grads)
+        dy = _dense(dy)
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         x, c1, c2, c3 = (_cl(t) for t in saved[:4])
         st = self._stats_views(saved[-1])
@@ -470,6 +486,7 @@ class HeadUnit(_ConvNetUnit):
         return torch.addmm(b, p, w.t())
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         w, b = params
         x = _cl(saved[0])
         p = x.mean(dim=(2, 3))
@@ -626,6 +643,7 @@ class PreActBottleneckUnit(_ConvNetUnit):
         return y.add_(sc)
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
         x, c1, c2 = (_cl(t) for t in saved[:3])
         st = self._st(saved[3])
@@ -690,6 +708,7 @@ class CifarStemUnit(_ConvNetUnit):
         return _conv(x, _cl(params[0]), 1, 1)
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         _, dw, _ = _conv_bw(dy, _cl(saved[0]), _cl(params[0]), 1, 1, need_dx=False)
         _cl(grads[0]).copy_(dw)
         return None
@@ -733,6 +752,7 @@ class PreActHeadUnit(_ConvNetUnit):
         return torch.addmm(bias, p, w.t())
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         g, b, w, bias = params
         x, st = _cl(saved[0]), saved[1]
         a = _bn_relu(x, st[:self.cin], st[self.cin:], g, b)
@@ -843,6 +863,7 @@ class EmbeddingUnit(Unit):
         return x.view(-1, self.h)
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         t = saved[0].long()
         grads[0].zero_().index_add_(0, t, dy.float())
         grads[1].copy_(dy.float().view(-1, self.s, self.h).sum(0))
@@ -963,6 +984,7 @@ class TransformerLayerUnit(Unit):
         return saved[0]
 
     def backward(self, dy, params, saved, grads):
+        dy = _dense(dy)
         g1, b1, wqkv, bqkv, wo, bo, g2, b2, w1, bf1, w2, bf2 = params
         x, qkv, o, x2, f1, st = saved[:6]
         t = x.shape[0]
