@@ -99,3 +99,15 @@ def test_add_relu_backward_mask():
     y1 = bnfused.apply(x, m, i, g, b, relu=True, res=r)
     dz1 = bnfused.add_relu_bwd(dy, x, m, i, g, b, r)
     assert torch.equal(dz1, torch.where(y1 > 0, dy, torch.zeros_like(dy)))
+
+
+def test_add_relu_backward_second_gradient():
+    shape = (8, 256, 14, 14)
+    x, r, dy, dy2 = (rand(*shape, seed=s) for s in (21, 22, 23, 24))
+    g, b = params(256)
+    m, i = torch.empty(256, device="cuda"), torch.empty(256, device="cuda")
+    bnfused.stats(x, m, i)
+    y = bnfused.apply(x, m, i, g, b, relu=True, res=r)
+    dz = bnfused.add_relu_bwd(dy, x, m, i, g, b, r, dy2=dy2)
+    ref = torch.where(y > 0, dy + dy2, torch.zeros_like(dy))
+    assert torch.equal(dz, ref)
