@@ -242,6 +242,12 @@ size_t krt_bn_workspace_bytes(int C);
 /* batch statistics: mean[c], invstd[c] = 1/sqrt(var_biased + eps) */
 int krt_bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws,
                  void* stream);
+/* krt_bn_stats then y = relu?( bn(x) [+ res] ) in one kernel (res NULL: none,
+ * else identity residual); the apply pass walks the rows in reverse so the
+ * tail the stats pass read last is still in L2 */
+int krt_bn_stats_apply(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd,
+                       const void* gamma, const void* beta, const void* res, int relu, void* y, void* ws,
+                       void* stream);
 /* y = relu?( bn(x) [+ res | + bn'(res)] ); res NULL: no residual, rmean NULL: identity residual */
 int krt_bn_apply(const void* x, const float* mean, const float* invstd, const void* gamma,
                  const void* beta, const void* res, const float* rmean, const float* rinvstd,
@@ -259,6 +265,14 @@ int krt_bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const fl
 int krt_bn_backward(const void* dy, const void* x, const float* mean, const float* invstd,
                     const void* gamma, const void* beta, int relu, void* dx, float* dgamma,
                     float* dbeta, int64_t rows, int C, void* ws, void* stream);
+/* krt_bn_add_relu_bwd (identity residual) and krt_bn_backward (no ReLU) of the
+ * same BN in one kernel: dz = (dy [+ dy2]) * (bn(x) + res > 0) is written and
+ * reduced in the same pass, then dx.  dz and dx required; dgamma/dbeta may be
+ * NULL. */
+int krt_bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean,
+                             const float* invstd, const void* gamma, const void* beta, const void* res,
+                             void* dz, void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
+                             void* stream);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,20 @@ def stats(c, mean, invstd):
                                            invstd.data_ptr(), ws.data_ptr(), _stream()))
 
 
+def stats_apply(c, mean, invstd, g, b, relu, res=None, out=None):
+    """stats() then relu?(bn(c) [+ res]) in one cooperative kernel."""
+    c = _nhwc(c)
+    rows, C = _rows_c(c)
+    y = out if out is not None else torch.empty_like(c, memory_format=torch.channels_last)
+    ws = _ws(C, c.device)
+    with _timed("bn_stats_apply", rows * C * 2 * (3 if res is None else 4)):
+        _lib.check(_lib.lib().krt_bn_stats_apply(c.data_ptr(), rows, C, EPS, mean.data_ptr(), invstd.data_ptr(),
+                                                 g.data_ptr(), b.data_ptr(),
+                                                 _ptr(None if res is None else _nhwc(res)), int(relu),
+                                                 y.data_ptr(), ws.data_ptr(), _stream()))
+    return y
+
+
 def apply(c, mean, invstd, g, b, relu, res=None, rstats=None, rg=None, rb=None, out=None):
     """relu?(bn(c) [+ res | + bn'(res)]) -> new bf16 channels_last tensor (or out)."""
     c = _nhwc(c)
@@ -110,3 +124,22 @@ def backward(dy, c, mean, invstd, g, b, relu, dgamma=None, dbeta=None, need_dx=T
                                           g.data_ptr(), b.data_ptr(), int(relu), _ptr(dx), _ptr(dgamma),
                                           _ptr(dbeta), rows, C, ws.data_ptr(), _stream()))
     return dx
+
+
+def add_relu_backward(dy, c, mean, invstd, g, b, res, dgamma=None, dbeta=None, dy2=None):
+    """add_relu_bwd (identity residual) + backward(relu=False) of the same BN in
+    one cooperative kernel: returns (dz, dx)."""
+    c, dy, res = _nhwc(c), _nhwc(dy), _nhwc(res)
+    if dy2 is not None:
+        dy2 = _nhwc(dy2)
+    rows, C = _rows_c(c)
+    dz = torch.empty_like(c, memory_format=torch.channels_last)
+    dx = torch.empty_like(c, memory_format=torch.channels_last)
+    ws = _ws(C, c.device)
+    with _timed("bn_add_relu_backward", rows * C * 2 * (7 if dy2 is None else 8)):
+        _lib.check(_lib.lib().krt_bn_add_relu_backward(dy.data_ptr(), _ptr(dy2), c.data_ptr(), mean.data_ptr(),
+                                                       invstd.data_ptr(), g.data_ptr(), b.data_ptr(),
+                                                       res.data_ptr(), dz.data_ptr(), dx.data_ptr(),
+                                                       _ptr(dgamma), _ptr(dbeta), rows, C, ws.data_ptr(),
+                                                       _stream()))
+    return dz, dx

@@ -4,37 +4,61 @@
 // elementwise/norm kernels elsewhere").  All are HBM-bound streaming kernels
 // over a [rows, C] matrix (rows = N*H*W, C contiguous, C % 8 == 0):
 //
-//   stats     : per-channel mean / invstd (batch statistics)       1R
-//   apply     : y = relu?(bn(x) [+ res | + bn'(res)])               1-2R + 1W
-//   add_relu_bwd_mask : dz = dy * (bn(x) + (res | bn'(res)) > 0)    2-3R + 1W
-//   bwd       : dgamma, dbeta (reduce) and dx (elementwise), with the
-//               ReLU mask recomputed from x when the BN feeds a ReLU   2R + 2R+1W
+//   stats        : per-channel mean / invstd (batch statistics)          1R
+//   stats_apply  : stats, then y = relu?(bn(x) [+ res])                  1R | 1R + 1W (+1R)
+//   apply        : y = relu?(bn(x) [+ res | + bn'(res)])                  1-2R + 1W
+//   add_relu_bwd : dz = dy * (bn(x) + (res | bn'(res)) > 0)               2-3R + 1W
+//   backward     : dgamma, dbeta (reduce) and dx (elementwise), with the
+//                  ReLU mask recomputed from x when the BN feeds a ReLU   2R + 2R+1W
+//   add_relu_backward : add_relu_bwd and backward of the same BN; the
+//                  reduce runs on dz while it is produced                 3R+1W | 2R+1W
 //
 // Thread mapping: a thread owns 8 consecutive channels (one 16-byte vector)
-// for its whole life, so per-channel scale/shift stay in registers; the rows
-// are grid-strided.  Reductions: per-thread fp32 partials -> shared-memory
-// tree over the rows of a CTA -> one fp32 partial per CTA and channel ->
-// a finalize kernel sums the CTA partials in double (fixed order:
-// deterministic, so in-core and out-of-core runs stay bitwise equal).
+// for its whole life, so per-channel coefficients stay in registers; rows are
+// grid-strided with kU rows in flight per thread and tensor (the bytes in
+// flight per SM, not the instruction count, set the achieved HBM rate).
+//
+// Reductions are one cooperative kernel (grid = one wave of resident CTAs):
+//   pass   per-thread fp32 partials -> CTA fixed-order sum -> one partial per CTA
+//   sync   grid barrier
+//   final  CTA k sums the partials of channel octets k, k+grid, ... in double
+//          (fixed order: deterministic, so in-core and out-of-core runs stay
+//          bitwise equal) with coalesced 32-byte sector reads, and writes the
+//          per-channel results (mean/invstd, or dgamma/dbeta + dx coefficients)
+// so the separate finalize launch and its latency are gone.  The elementwise
+// pass that follows a reduction is its own kernel: measured on B200, a second
+// streaming pass inside the cooperative kernel after the barrier ran at 4.5
+// TB/s against 5.8 TB/s as a fresh launch (scripts/bench_bn.py, round 1).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 #include "bn_kernels.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace krt {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxGrid = 148 * 4;
+constexpr int kMaxGrid = 148 * 8;  // partial rows the workspace holds
+constexpr int kU = 4;              // rows in flight per thread and tensor
 
 struct Vec8 {
   float v[8];
 };
 
-__device__ __forceinline__ Vec8 load8(const __nv_bfloat16* p) {
-  uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+__device__ __forceinline__ uint4 ld16(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+// streaming load: the data is touched once more at most (evict-first in L1)
+__device__ __forceinline__ uint4 ld16s(const __nv_bfloat16* p) { return __ldcs(reinterpret_cast<const uint4*>(p)); }
+
+__device__ __forceinline__ Vec8 unpack(const uint4& u) {
   Vec8 r;
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -46,17 +70,19 @@ __device__ __forceinline__ Vec8 load8(const __nv_bfloat16* p) {
   return r;
 }
 
-__device__ __forceinline__ void store8(__nv_bfloat16* p, const Vec8& x) {
+__device__ __forceinline__ uint4 pack(const Vec8& x) {
   uint4 u;
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
   for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(x.v[2 * k], x.v[2 * k + 1]);
-  *reinterpret_cast<uint4*>(p) = u;
+  return u;
 }
+
+__device__ __forceinline__ void st16(__nv_bfloat16* p, const Vec8& x) { *reinterpret_cast<uint4*>(p) = pack(x); }
 
 __device__ __forceinline__ float bf(const __nv_bfloat16* p, int i) { return __bfloat162float(p[i]); }
 
-// threads of a CTA: tx = channel group (C/8 of them), ty = row lane
+// threads of a CTA: tx = channel octet (C/8 of them), ty = row lane
 struct Map {
   int tc, rb, tx, ty;
   __device__ Map(int C) {
@@ -64,6 +90,15 @@ struct Map {
     rb = kThreads / tc;  // rows per CTA sweep (>= 1 since C <= 2048)
     tx = threadIdx.x % tc;
     ty = threadIdx.x / tc;
+  }
+};
+
+// Row iteration: thread rows are r0 + k*step; one "group" is kU of them.
+struct Rows {
+  int64_t first, step, rows;
+  __device__ Rows(const Map& m, int64_t rows_) : rows(rows_) {
+    first = (int64_t)blockIdx.x * m.rb + m.ty;
+    step = (int64_t)gridDim.x * m.rb;
   }
 };
 
@@ -78,110 +113,110 @@ __device__ __forceinline__ void bn_coeffs(const float* mean, const float* invstd
   }
 }
 
-// reduce two 8-vectors over the ty dimension of the CTA; result in ty == 0
-__device__ __forceinline__ void cta_reduce2(float* a, float* b, float* smem, const Map& m) {
-  // smem: [rb][tc][16]
-  float* mine = smem + ((size_t)m.ty * m.tc + m.tx) * 16;
+// Reduce the per-thread partials (a: sum, b: second sum; 8 channels each)
+// over the CTA's rows and write one partial row [2][C] for this CTA:
+//   1) butterfly shuffles over the rows one warp holds (C < 256: 32/tc rows)
+//   2) the remaining row groups (warps, or rows of tc >= 32 threads) are added
+//      in fixed group order through a C-float shared buffer, sum then second
+// Deterministic, and at most C floats of shared memory: the streaming passes
+// need the L1 the shared-memory carve-out would otherwise take.
+__device__ __forceinline__ void cta_partial(float* a, float* b, float* smem, const Map& m, float* part, int C,
+                                            int c0) {
+  const int lane = threadIdx.x & 31;
+  int groups, gid;
+  bool leader;
+  if (m.tc < 32) {
+    for (int off = m.tc; off < 32; off <<= 1) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    mine[k] = a[k];
-    mine[8 + k] = b[k];
+      for (int k = 0; k < 8; ++k) {
+        a[k] += __shfl_xor_sync(0xffffffffu, a[k], off);
+        b[k] += __shfl_xor_sync(0xffffffffu, b[k], off);
+      }
+    }
+    groups = kThreads / 32;
+    gid = threadIdx.x >> 5;
+    leader = lane < m.tc;
+  } else {
+    groups = m.rb;
+    gid = m.ty;
+    leader = true;
+  }
+  float* out = part + (size_t)blockIdx.x * 2 * C;
+  for (int half = 0; half < 2; ++half) {
+    const float* v = half ? b : a;
+    for (int g = 0; g < groups; ++g) {
+      if (leader && gid == g) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float t = g == 0 ? v[k] : smem[c0 + k] + v[k];
+          if (g == groups - 1) out[half * C + c0 + k] = t;
+          else smem[c0 + k] = t;
+        }
+      }
+      if (groups > 1) __syncthreads();
+    }
+  }
+}
+
+// Sum the gridDim.x CTA partials of channel octet `oct`: thread = (row lane
+// 0..31, channel 0..7), so a warp reads four full 32-byte sectors per step
+// (eight loads in flight per thread); then butterfly shuffles over the four
+// row lanes of a warp and a fixed-order pass over the eight warps.  Threads
+// 0..7 return the sums of channel oct*8+threadIdx.x.
+__device__ __forceinline__ bool sum_octet(const float* part, int nblk, int C, int oct, double* sh, double& s1,
+                                          double& s2) {
+  const int lr = threadIdx.x >> 3, ch = threadIdx.x & 7;
+  const int c = oct * 8 + ch;
+  constexpr int L = kThreads / 8;  // row lanes
+  double a[4] = {0, 0, 0, 0}, q[4] = {0, 0, 0, 0};
+  int b = lr;
+  for (; b + 3 * L < nblk; b += 4 * L) {
+    float x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = __ldcg(part + (size_t)(b + u * L) * 2 * C + c);
+      y[u] = __ldcg(part + (size_t)(b + u * L) * 2 * C + C + c);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] += (double)x[u];
+      q[u] += (double)y[u];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    if (b + u * L < nblk) {
+      a[u] += (double)__ldcg(part + (size_t)(b + u * L) * 2 * C + c);
+      q[u] += (double)__ldcg(part + (size_t)(b + u * L) * 2 * C + C + c);
+    }
+  }
+  double sa = (a[0] + a[1]) + (a[2] + a[3]);
+  double sq = (q[0] + q[1]) + (q[2] + q[3]);
+  sa += __shfl_xor_sync(0xffffffffu, sa, 8);
+  sq += __shfl_xor_sync(0xffffffffu, sq, 8);
+  sa += __shfl_xor_sync(0xffffffffu, sa, 16);
+  sq += __shfl_xor_sync(0xffffffffu, sq, 16);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane < 8) {
+    sh[w * 16 + lane] = sa;
+    sh[w * 16 + 8 + lane] = sq;
   }
   __syncthreads();
-  for (int s = 1; s < m.rb; s <<= 1) {
-    if ((m.ty % (2 * s)) == 0 && m.ty + s < m.rb) {
-      float* other = smem + ((size_t)(m.ty + s) * m.tc + m.tx) * 16;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) mine[k] += other[k];
+  if (threadIdx.x < 8) {
+    s1 = 0;
+    s2 = 0;
+    for (int k = 0; k < kThreads / 32; ++k) {
+      s1 += sh[k * 16 + threadIdx.x];
+      s2 += sh[k * 16 + 8 + threadIdx.x];
     }
-    __syncthreads();
   }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    a[k] = mine[k];
-    b[k] = mine[8 + k];
-  }
+  __syncthreads();  // sh reused by the next octet
+  return threadIdx.x < 8;
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
-                                                         float* __restrict__ part) {
-  extern __shared__ float smem[];
-  Map m(C);
-  int c0 = m.tx * 8;
-  float s[8] = {0}, q[8] = {0};
-  const int64_t step = (int64_t)gridDim.x * m.rb;
-  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
-  for (; r + step < rows; r += 2 * step) {
-    Vec8 v0 = load8(x + r * C + c0), v1 = load8(x + (r + step) * C + c0);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      s[k] += v0.v[k] + v1.v[k];
-      q[k] += v0.v[k] * v0.v[k] + v1.v[k] * v1.v[k];
-    }
-  }
-  if (r < rows) {
-    Vec8 v = load8(x + r * C + c0);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      s[k] += v.v[k];
-      q[k] += v.v[k] * v.v[k];
-    }
-  }
-  cta_reduce2(s, q, smem, m);
-  if (m.ty == 0) {
-    float* out = part + (size_t)blockIdx.x * 2 * C;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      out[c0 + k] = s[k];
-      out[C + c0 + k] = q[k];
-    }
-  }
-}
-
-// Sum CTA partials for 32 channels per block: lane = channel, the 32 warps
-// stride over the partial rows, then a fixed-order pass over the warps
-// (deterministic).  Returns the two double sums in lane c of warp 0.
-constexpr int kFinWarps = 32;
-__device__ __forceinline__ bool sum_partials(const float* __restrict__ part, int nblk, int C, double& s1,
-                                             double& s2) {
-  __shared__ double sh[2][kFinWarps][33];
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int c = blockIdx.x * 32 + lane;
-  double a = 0, q = 0;
-  if (c < C)
-    for (int b = w; b < nblk; b += kFinWarps) {
-      a += part[(size_t)b * 2 * C + c];
-      q += part[(size_t)b * 2 * C + C + c];
-    }
-  sh[0][w][lane] = a;
-  sh[1][w][lane] = q;
-  __syncthreads();
-  if (w != 0 || c >= C) return false;
-  s1 = 0;
-  s2 = 0;
-  for (int k = 0; k < kFinWarps; ++k) {
-    s1 += sh[0][k][lane];
-    s2 += sh[1][k][lane];
-  }
-  return true;
-}
-
-__global__ void __launch_bounds__(1024) stats_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
-                                                      float eps, float* __restrict__ mean, float* __restrict__ invstd) {
-  double s, q;
-  if (!sum_partials(part, nblk, C, s, q)) return;
-  int c = blockIdx.x * 32 + (threadIdx.x & 31);
-  double mu = s / (double)rows;
-  double var = q / (double)rows - mu * mu;
-  if (var < 0) var = 0;
-  mean[c] = (float)mu;
-  invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
-}
-
-// ---------------------------------------------------------------------------
-// mode: 0 none, 1 identity residual, 2 bn(residual).  Two rows in flight
-// per thread (all loads issued before the math) for memory-level parallelism.
+// forward: stats [+ apply]
+//   MODE: 0 none, 1 identity residual, 2 bn(residual)
 template <int MODE, bool RELU>
 __device__ __forceinline__ Vec8 apply_row(const Vec8& v, const Vec8& rv, const float* sc, const float* sh,
                                           const float* rsc, const float* rsh) {
@@ -196,6 +231,77 @@ __device__ __forceinline__ Vec8 apply_row(const Vec8& v, const Vec8& rv, const f
   return o;
 }
 
+// the apply pass over one group of kU rows (rows >= rows_ skipped)
+template <int MODE, bool RELU>
+__device__ __forceinline__ void apply_group(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
+                                            __nv_bfloat16* __restrict__ y, int64_t r0, int64_t step, int64_t rows,
+                                            int C, int c0, const float* sc, const float* sh, const float* rsc,
+                                            const float* rsh) {
+  uint4 v[kU], q[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t r = r0 + u * step;
+    if (r < rows) {
+      v[u] = ld16s(x + r * C + c0);
+      if (MODE != 0) q[u] = ld16s(res + r * C + c0);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t r = r0 + u * step;
+    if (r < rows) {
+      Vec8 rv{};
+      if (MODE != 0) rv = unpack(q[u]);
+      st16(y + r * C + c0, apply_row<MODE, RELU>(unpack(v[u]), rv, sc, sh, rsc, rsh));
+    }
+  }
+}
+
+// stats pass-1 accumulation of one group
+__device__ __forceinline__ void stats_group(const __nv_bfloat16* __restrict__ x, int64_t r0, int64_t step,
+                                            int64_t rows, int C, int c0, float* s, float* q) {
+  uint4 v[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t r = r0 + u * step;
+    v[u] = r < rows ? ld16(x + r * C + c0) : make_uint4(0, 0, 0, 0);  // bf16 zero bits
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    Vec8 f = unpack(v[u]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      s[k] += f.v[k];
+      q[k] += f.v[k] * f.v[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
+                                                         float eps, float* __restrict__ part,
+                                                         float* __restrict__ mean, float* __restrict__ invstd) {
+  extern __shared__ float smem[];
+  Map m(C);
+  Rows rw(m, rows);
+  const int c0 = m.tx * 8;
+  float s[8] = {0}, q[8] = {0};
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) stats_group(x, r0, rw.step, rows, C, c0, s, q);
+  cta_partial(s, q, smem, m, part, C, c0);
+  cg::this_grid().sync();
+  double* shd = reinterpret_cast<double*>(smem);
+  for (int oct = blockIdx.x; oct < C / 8; oct += gridDim.x) {
+    double s1, s2;
+    if (sum_octet(part, gridDim.x, C, oct, shd, s1, s2)) {
+      const int c = oct * 8 + threadIdx.x;
+      double mu = s1 / (double)rows;
+      double var = s2 / (double)rows - mu * mu;
+      if (var < 0) var = 0;
+      mean[c] = (float)mu;
+      invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
+    }
+  }
+}
+
 template <int MODE, bool RELU>
 __global__ void __launch_bounds__(kThreads) apply_kernel(
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ invstd,
@@ -203,32 +309,18 @@ __global__ void __launch_bounds__(kThreads) apply_kernel(
     const float* __restrict__ rmean, const float* __restrict__ rinvstd, const __nv_bfloat16* __restrict__ rg,
     const __nv_bfloat16* __restrict__ rb_, __nv_bfloat16* __restrict__ y, int64_t rows, int C) {
   Map m(C);
-  int c0 = m.tx * 8;
+  Rows rw(m, rows);
+  const int c0 = m.tx * 8;
   float sc[8], sh[8], rsc[8], rsh[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
   if (MODE == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
-  const int64_t step = (int64_t)gridDim.x * m.rb;
-  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
-  Vec8 z{};
-  for (; r + step < rows; r += 2 * step) {
-    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
-    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
-    Vec8 q0 = z, q1 = z;
-    if (MODE != 0) {
-      q0 = load8(res + o0);
-      q1 = load8(res + o1);
-    }
-    store8(y + o0, apply_row<MODE, RELU>(v0, q0, sc, sh, rsc, rsh));
-    store8(y + o1, apply_row<MODE, RELU>(v1, q1, sc, sh, rsc, rsh));
-  }
-  if (r < rows) {
-    const int64_t o0 = r * C + c0;
-    Vec8 v0 = load8(x + o0), q0 = z;
-    if (MODE != 0) q0 = load8(res + o0);
-    store8(y + o0, apply_row<MODE, RELU>(v0, q0, sc, sh, rsc, rsh));
-  }
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU)
+    apply_group<MODE, RELU>(x, res, y, r0, rw.step, rows, C, c0, sc, sh, rsc, rsh);
 }
 
+// ---------------------------------------------------------------------------
+// backward
+//
 // dz = dy * ( bn(x) [+ res | + bn'(res)] > 0 )   (backward of the add + ReLU);
 // the forward sum is re-rounded to bf16 exactly as apply_kernel stored it
 template <int MODE>
@@ -256,199 +348,338 @@ __device__ __forceinline__ Vec8 add_grad(const Vec8& a, const Vec8& b) {
 template <int MODE, bool DY2>
 __global__ void __launch_bounds__(kThreads) add_relu_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dy2, const __nv_bfloat16* __restrict__ x,
-    const float* __restrict__ mean,
-    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
-    const __nv_bfloat16* __restrict__ res, const float* __restrict__ rmean, const float* __restrict__ rinvstd,
-    const __nv_bfloat16* __restrict__ rg, const __nv_bfloat16* __restrict__ rb_, __nv_bfloat16* __restrict__ dz,
-    int64_t rows, int C) {
+    const float* __restrict__ mean, const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g,
+    const __nv_bfloat16* __restrict__ b, const __nv_bfloat16* __restrict__ res, const float* __restrict__ rmean,
+    const float* __restrict__ rinvstd, const __nv_bfloat16* __restrict__ rg, const __nv_bfloat16* __restrict__ rb_,
+    __nv_bfloat16* __restrict__ dz, int64_t rows, int C) {
   Map m(C);
-  int c0 = m.tx * 8;
+  Rows rw(m, rows);
+  const int c0 = m.tx * 8;
   float sc[8], sh[8], rsc[8], rsh[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
   if (MODE == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
-  const int64_t step = (int64_t)gridDim.x * m.rb;
-  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
-  for (; r + step < rows; r += 2 * step) {
-    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
-    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
-    Vec8 q0 = load8(res + o0), q1 = load8(res + o1);
-    Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
-    if (DY2) {
-      Vec8 e0 = load8(dy2 + o0), e1 = load8(dy2 + o1);
-      d0 = add_grad(d0, e0);
-      d1 = add_grad(d1, e1);
+  constexpr int U = 2;  // 3-4 tensors per row: two rows already saturate HBM
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {
+    uint4 v[U], q[U], d[U], e[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      if (r < rows) {
+        const int64_t o = r * C + c0;
+        v[u] = ld16s(x + o);
+        q[u] = ld16s(res + o);
+        d[u] = ld16s(dy + o);
+        if (DY2) e[u] = ld16s(dy2 + o);
+      }
     }
-    store8(dz + o0, add_relu_row<MODE>(v0, q0, d0, sc, sh, rsc, rsh));
-    store8(dz + o1, add_relu_row<MODE>(v1, q1, d1, sc, sh, rsc, rsh));
-  }
-  if (r < rows) {
-    const int64_t o0 = r * C + c0;
-    Vec8 v0 = load8(x + o0), q0 = load8(res + o0), d0 = load8(dy + o0);
-    if (DY2) d0 = add_grad(d0, load8(dy2 + o0));
-    store8(dz + o0, add_relu_row<MODE>(v0, q0, d0, sc, sh, rsc, rsh));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      if (r < rows) {
+        Vec8 dd = unpack(d[u]);
+        if (DY2) dd = add_grad(dd, unpack(e[u]));
+        st16(dz + r * C + c0, add_relu_row<MODE>(unpack(v[u]), unpack(q[u]), dd, sc, sh, rsc, rsh));
+      }
+    }
   }
 }
 
-// backward reduce: sum(gm) and sum(gm * xhat) with gm = dy * mask
+// Backward coefficients.  With gm = dy * mask, xhat = (x - mean) * invstd:
+//   dbeta = sum gm, dgamma = sum gm * xhat
+//   dx = gamma*invstd * (gm - dbeta/n - xhat * dgamma/n)  =  A*gm + B*x + D
+struct BwdCoef {
+  float sc[8], sh[8];  // forward affine (ReLU mask)
+  float a[8], bx[8], d[8];
+};
+
+template <bool RELU>
+__device__ __forceinline__ float relu_mask(float v, float sc, float sh, float gm) {
+  if (!RELU) return gm;
+  float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v, sc, sh)));
+  return yk > 0.0f ? gm : 0.0f;
+}
+
+// pass-1 accumulation: s1 += gm, s2 += gm * xhat
 template <bool RELU>
 __device__ __forceinline__ void bwd_acc(const Vec8& v, const Vec8& d, const float* sc, const float* sh,
                                         const float* mu, const float* is, float* s1, float* s2) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    float gm = d.v[k];
-    if (RELU) {
-      float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
-      gm = yk > 0.0f ? gm : 0.0f;
-    }
+    float gm = relu_mask<RELU>(v.v[k], sc[k], sh[k], d.v[k]);
     s1[k] += gm;
     s2[k] += gm * ((v.v[k] - mu[k]) * is[k]);
   }
 }
 
 template <bool RELU>
-__global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
-    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
-    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
-    int64_t rows, int C, float* __restrict__ part) {
-  extern __shared__ float smem[];
-  Map m(C);
-  int c0 = m.tx * 8;
-  float sc[8], sh[8], mu[8], is[8];
-  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    mu[k] = mean[c0 + k];
-    is[k] = invstd[c0 + k];
-  }
-  float s1[8] = {0}, s2[8] = {0};
-  const int64_t step = (int64_t)gridDim.x * m.rb;
-  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
-  for (; r + step < rows; r += 2 * step) {
-    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
-    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
-    Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
-    bwd_acc<RELU>(v0, d0, sc, sh, mu, is, s1, s2);
-    bwd_acc<RELU>(v1, d1, sc, sh, mu, is, s1, s2);
-  }
-  if (r < rows) {
-    const int64_t o0 = r * C + c0;
-    Vec8 v0 = load8(x + o0), d0 = load8(dy + o0);
-    bwd_acc<RELU>(v0, d0, sc, sh, mu, is, s1, s2);
-  }
-  cta_reduce2(s1, s2, smem, m);
-  if (m.ty == 0) {
-    float* out = part + (size_t)blockIdx.x * 2 * C;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      out[c0 + k] = s1[k];
-      out[C + c0 + k] = s2[k];
-    }
-  }
-}
-
-__global__ void __launch_bounds__(1024) bwd_finalize(const float* __restrict__ part, int nblk, int64_t rows, int C,
-                                                    float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                    float* __restrict__ coef) {
-  double s1, s2;
-  if (!sum_partials(part, nblk, C, s1, s2)) return;
-  int c = blockIdx.x * 32 + (threadIdx.x & 31);
-  if (dbeta) dbeta[c] = (float)s1;
-  if (dgamma) dgamma[c] = (float)s2;
-  coef[c] = (float)(s1 / (double)rows);
-  coef[C + c] = (float)(s2 / (double)rows);
-}
-
-// dx = gamma*invstd * (gm - mean(gm) - xhat * mean(gm*xhat))
-template <bool RELU>
-__device__ __forceinline__ Vec8 bwd_row(const Vec8& v, const Vec8& d, const float* sc, const float* sh,
-                                        const float* mu, const float* is, const float* k1, const float* k2,
-                                        const float* gs) {
+__device__ __forceinline__ Vec8 bwd_row(const Vec8& v, const Vec8& d, const BwdCoef& k) {
   Vec8 o;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    float gm = d.v[k];
-    if (RELU) {
-      float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v.v[k], sc[k], sh[k])));
-      gm = yk > 0.0f ? gm : 0.0f;
-    }
-    float xh = (v.v[k] - mu[k]) * is[k];
-    o.v[k] = gs[k] * (gm - k1[k] - xh * k2[k]);
+  for (int j = 0; j < 8; ++j) {
+    float gm = relu_mask<RELU>(v.v[j], k.sc[j], k.sh[j], d.v[j]);
+    o.v[j] = __fmaf_rn(k.a[j], gm, __fmaf_rn(k.bx[j], v.v[j], k.d[j]));
   }
   return o;
 }
 
+// finalize: dgamma/dbeta and the dx coefficients (coef: [3][C] = A, B, D)
+__device__ __forceinline__ void bwd_finalize(const float* part, int64_t rows, int C, const float* mean,
+                                             const float* invstd, const __nv_bfloat16* g, float* dgamma,
+                                             float* dbeta, float* coef, double* shd) {
+  for (int oct = blockIdx.x; oct < C / 8; oct += gridDim.x) {
+    double s1, s2;
+    if (sum_octet(part, gridDim.x, C, oct, shd, s1, s2)) {
+      const int c = oct * 8 + threadIdx.x;
+      if (dbeta) dbeta[c] = (float)s1;
+      if (dgamma) dgamma[c] = (float)s2;
+      const double is = invstd[c], mu = mean[c];
+      const double gs = (double)bf(g, c) * is;
+      const double k1 = s1 / (double)rows, k2 = s2 / (double)rows;
+      // dx = gs*(gm - k1 - (x - mu)*is*k2)
+      coef[c] = (float)gs;
+      coef[C + c] = (float)(-gs * is * k2);
+      coef[2 * C + c] = (float)(gs * (mu * is * k2 - k1));
+    }
+  }
+}
+
+// reduce + finalize (dgamma, dbeta, dx coefficients), one cooperative kernel
+template <bool RELU>
+__global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
+    int64_t rows, int C, float* __restrict__ part, float* __restrict__ coef, float* __restrict__ dgamma,
+    float* __restrict__ dbeta) {
+  extern __shared__ float smem[];
+  Map m(C);
+  Rows rw(m, rows);
+  const int c0 = m.tx * 8;
+  float sc[8], sh[8], mu[8], is[8];
+  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    mu[j] = mean[c0 + j];
+    is[j] = invstd[c0 + j];
+  }
+  float s1[8] = {0}, s2[8] = {0};
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) {
+    uint4 v[kU], d[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      v[u] = r < rows ? ld16s(x + r * C + c0) : make_uint4(0, 0, 0, 0);
+      d[u] = r < rows ? ld16s(dy + r * C + c0) : make_uint4(0, 0, 0, 0);  // gm = 0 on padding
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) bwd_acc<RELU>(unpack(v[u]), unpack(d[u]), sc, sh, mu, is, s1, s2);
+  }
+  cta_partial(s1, s2, smem, m, part, C, c0);
+  cg::this_grid().sync();
+  bwd_finalize(part, rows, C, mean, invstd, g, dgamma, dbeta, coef, reinterpret_cast<double*>(smem));
+}
+
+// add_relu_bwd of the residual sum and the reduce of the BN (no ReLU of its
+// own) that produced x, in one pass: dz = (dy [+ dy2]) * mask(bn(x) + res) is
+// written out and accumulated from registers; then the finalize
+template <bool DY2>
+__global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dy2, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ mean, const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g,
+    const __nv_bfloat16* __restrict__ b, const __nv_bfloat16* __restrict__ res, __nv_bfloat16* __restrict__ dz,
+    int64_t rows, int C, float* __restrict__ part, float* __restrict__ coef, float* __restrict__ dgamma,
+    float* __restrict__ dbeta) {
+  extern __shared__ float smem[];
+  Map m(C);
+  Rows rw(m, rows);
+  const int c0 = m.tx * 8;
+  float sc[8], sh[8], mu[8], is[8];
+  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    mu[j] = mean[c0 + j];
+    is[j] = invstd[c0 + j];
+  }
+  float s1[8] = {0}, s2[8] = {0};
+  constexpr int U = 2;  // 3-4 tensors per row
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {
+    uint4 v[U], q[U], d[U], e[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      if (r < rows) {
+        const int64_t o = r * C + c0;
+        v[u] = ld16s(x + o);
+        q[u] = ld16s(res + o);
+        d[u] = ld16s(dy + o);
+        if (DY2) e[u] = ld16s(dy2 + o);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      if (r < rows) {
+        Vec8 dd = unpack(d[u]);
+        if (DY2) dd = add_grad(dd, unpack(e[u]));
+        Vec8 xv = unpack(v[u]);
+        Vec8 z = add_relu_row<1>(xv, unpack(q[u]), dd, sc, sh, nullptr, nullptr);
+        st16(dz + r * C + c0, z);
+        bwd_acc<false>(xv, z, sc, sh, mu, is, s1, s2);
+      }
+    }
+  }
+  cta_partial(s1, s2, smem, m, part, C, c0);
+  cg::this_grid().sync();
+  bwd_finalize(part, rows, C, mean, invstd, g, dgamma, dbeta, coef, reinterpret_cast<double*>(smem));
+}
+
+// dx = A*gm + B*x + D with gm = dy * mask (coefficients from the reduce)
 template <bool RELU>
 __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
     const float* __restrict__ coef, __nv_bfloat16* __restrict__ dx, int64_t rows, int C) {
   Map m(C);
-  int c0 = m.tx * 8;
-  float sc[8], sh[8], mu[8], is[8], k1[8], k2[8], gs[8];
-  bn_coeffs(mean, invstd, g, b, c0, sc, sh);
+  Rows rw(m, rows);
+  const int c0 = m.tx * 8;
+  BwdCoef k;
+  if (RELU) bn_coeffs(mean, invstd, g, b, c0, k.sc, k.sh);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    mu[k] = mean[c0 + k];
-    is[k] = invstd[c0 + k];
-    k1[k] = coef[c0 + k];
-    k2[k] = coef[C + c0 + k];
-    gs[k] = bf(g, c0 + k) * is[k];
+  for (int j = 0; j < 8; ++j) {
+    k.a[j] = coef[c0 + j];
+    k.bx[j] = coef[C + c0 + j];
+    k.d[j] = coef[2 * C + c0 + j];
   }
-  const int64_t step = (int64_t)gridDim.x * m.rb;
-  int64_t r = (int64_t)blockIdx.x * m.rb + m.ty;
-  for (; r + step < rows; r += 2 * step) {
-    const int64_t o0 = r * C + c0, o1 = (r + step) * C + c0;
-    Vec8 v0 = load8(x + o0), v1 = load8(x + o1);
-    Vec8 d0 = load8(dy + o0), d1 = load8(dy + o1);
-    store8(dx + o0, bwd_row<RELU>(v0, d0, sc, sh, mu, is, k1, k2, gs));
-    store8(dx + o1, bwd_row<RELU>(v1, d1, sc, sh, mu, is, k1, k2, gs));
-  }
-  if (r < rows) {
-    const int64_t o0 = r * C + c0;
-    Vec8 v0 = load8(x + o0), d0 = load8(dy + o0);
-    store8(dx + o0, bwd_row<RELU>(v0, d0, sc, sh, mu, is, k1, k2, gs));
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) {
+    uint4 v[kU], d[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      if (r < rows) {
+        v[u] = ld16s(x + r * C + c0);
+        d[u] = ld16s(dy + r * C + c0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t r = r0 + u * rw.step;
+      if (r < rows) st16(dx + r * C + c0, bwd_row<RELU>(unpack(v[u]), unpack(d[u]), k));
+    }
   }
 }
 
-size_t reduce_smem(int C);
+// ---------------------------------------------------------------------------
+// launch helpers
 
-// persistent grid: one full wave of resident CTAs (148 SMs x occupancy),
-// capped at kMaxGrid so the reduction partials fit the workspace
-template <class K>
-int grid_rows(K kernel, size_t smem, int64_t rows, int C) {
-  static int resident = 0;  // per kernel instantiation
-  if (resident == 0) {
-    int per_sm = 0, sms = 148, dev = 0;
+size_t reduce_smem(int C) {
+  size_t tree = C >= 8 * kThreads ? 0 : (size_t)C * sizeof(float);  // rb == 1: no cross-row step
+  size_t fin = (size_t)(kThreads / 32) * 16 * sizeof(double);
+  return tree > fin ? tree : fin;
+}
+
+bool shape_ok(int64_t rows, int C) {
+  return rows > 0 && C >= 8 && C % 8 == 0 && C <= 8 * kThreads && (kThreads % (C / 8)) == 0;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
-    resident = sms * (per_sm < 1 ? 1 : per_sm);
+    if (sms < 1) sms = 148;
   }
+  return sms;
+}
+
+// one full wave of resident CTAs (148 SMs x occupancy), capped at kMaxGrid
+// so the reduction partials fit the workspace; never more CTAs than row
+// sweeps.  Cooperative kernels need every CTA resident, which this grants.
+// Resident CTAs per kernel instantiation and shared-memory size.  Kernels
+// that use shared memory get the smallest carve-out that still holds their
+// full occupancy: the rest stays L1, which is what keeps enough streaming
+// loads in flight (measured: the default carve-out for 16 KB/CTA cost 30% of
+// the apply pass's bandwidth).
+int resident_ctas(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, std::unordered_map<size_t, int>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& per = cache[kernel];
+  auto it = per.find(smem);
+  if (it != per.end()) return it->second;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  if (smem > 0) {
+    int dev = 0, max_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    size_t need = (size_t)per_sm * (smem + 1024);  // + the per-CTA reservation
+    int pct = (int)((need * 100 + max_smem - 1) / max_smem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 100 ? pct : 100);
+    int again = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&again, kernel, kThreads, smem);
+    if (again >= 1 && again < per_sm) per_sm = again;
+  }
+  int r = num_sms() * per_sm;
+  per[smem] = r;
+  return r;
+}
+
+template <class K>
+int grid_rows(K kernel, size_t smem, int64_t rows, int C) {
+  const int resident = resident_ctas(reinterpret_cast<const void*>(kernel), smem);
   int rb = kThreads / (C / 8);
   int64_t want = (rows + rb - 1) / rb;
   int cap = resident < kMaxGrid ? resident : kMaxGrid;
   return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
-size_t reduce_smem(int C) {
-  int tc = C / 8, rb = kThreads / tc;
-  return (size_t)rb * tc * 16 * sizeof(float);
+template <class T>
+struct Id {
+  using type = T;
+};
+
+// cooperative launch; every argument converted to the kernel's exact parameter type
+template <class... P>
+cudaError_t coop(void (*kernel)(P...), int64_t rows, int C, cudaStream_t s, typename Id<P>::type... args) {
+  size_t smem = reduce_smem(C);
+  int grid = grid_rows(kernel, smem, rows, C);
+  void* argv[] = {static_cast<void*>(&args)...};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid), dim3(kThreads), argv, smem,
+                                     s);
 }
 
-bool shape_ok(int64_t rows, int C) { return rows > 0 && C >= 8 && C % 8 == 0 && C <= 8 * kThreads && (kThreads % (C / 8)) == 0; }
+using bf16 = __nv_bfloat16;
+inline const bf16* B(const void* p) { return static_cast<const bf16*>(p); }
+inline bf16* BW_(void* p) { return static_cast<bf16*>(p); }
+
+cudaError_t bwd_elemt(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                      const void* b, const float* coef, void* dx, int64_t rows, int C, int relu, cudaStream_t s) {
+  auto go = [&](auto kernel) {
+    kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(B(dy), B(x), mean, invstd, B(g), B(b), coef, BW_(dx),
+                                                              rows, C);
+  };
+  if (relu) go(bwd_elemt_kernel<true>);
+  else go(bwd_elemt_kernel<false>);
+  return cudaGetLastError();
+}
 
 }  // namespace
 
-size_t bn_workspace_bytes(int C) { return (size_t)kMaxGrid * 2 * C * sizeof(float) + 2 * C * sizeof(float); }
+size_t bn_workspace_bytes(int C) { return (size_t)kMaxGrid * 2 * C * sizeof(float) + 3 * C * sizeof(float); }
 
 cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws,
                      cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
-  int grid = grid_rows(stats_kernel, reduce_smem(C), rows, C);
-  float* part = static_cast<float*>(ws);
-  stats_kernel<<<grid, kThreads, reduce_smem(C), s>>>(static_cast<const __nv_bfloat16*>(x), rows, C, part);
-  stats_finalize<<<(C + 31) / 32, 32 * kFinWarps, 0, s>>>(part, grid, rows, C, eps, mean, invstd);
-  return cudaGetLastError();
+  return coop(stats_kernel, rows, C, s, B(x), rows, C, eps, static_cast<float*>(ws), mean, invstd);
+}
+
+cudaError_t bn_stats_apply(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd,
+                           const void* g, const void* b, const void* res, int relu, void* y, void* ws,
+                           cudaStream_t s) {
+  cudaError_t e = bn_stats(x, rows, C, eps, mean, invstd, ws, s);
+  if (e != cudaSuccess) return e;
+  return bn_apply(x, mean, invstd, g, b, res, nullptr, nullptr, nullptr, nullptr, relu, y, rows, C, s);
 }
 
 cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, const void* g, const void* b,
@@ -456,16 +687,9 @@ cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, cons
                      int relu, void* y, int64_t rows, int C, cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
   int mode = res == nullptr ? 0 : (rmean == nullptr ? 1 : 2);
-  auto X = static_cast<const __nv_bfloat16*>(x);
-  auto G = static_cast<const __nv_bfloat16*>(g);
-  auto B = static_cast<const __nv_bfloat16*>(b);
-  auto R = static_cast<const __nv_bfloat16*>(res);
-  auto RG = static_cast<const __nv_bfloat16*>(rg);
-  auto RB = static_cast<const __nv_bfloat16*>(rb);
-  auto Y = static_cast<__nv_bfloat16*>(y);
-#define KRT_APPLY(M, RL)                                                                              \
-  apply_kernel<M, RL><<<grid_rows(apply_kernel<M, RL>, 0, rows, C), kThreads, 0, s>>>(X, mean, invstd, G, B, R, \
-                                                                                      rmean, rinvstd, RG, RB, Y, rows, C)
+#define KRT_APPLY(M, RL)                                                                                        \
+  apply_kernel<M, RL><<<grid_rows(apply_kernel<M, RL>, 0, rows, C), kThreads, 0, s>>>(                          \
+      B(x), mean, invstd, B(g), B(b), B(res), rmean, rinvstd, B(rg), B(rb), BW_(y), rows, C)
   if (mode == 0) { if (relu) KRT_APPLY(0, true); else KRT_APPLY(0, false); }
   else if (mode == 1) { if (relu) KRT_APPLY(1, true); else KRT_APPLY(1, false); }
   else { if (relu) KRT_APPLY(2, true); else KRT_APPLY(2, false); }
@@ -478,12 +702,8 @@ cudaError_t bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, cons
                             const void* rg, const void* rb, void* dz, int64_t rows, int C, cudaStream_t s) {
   if (!shape_ok(rows, C) || res == nullptr) return cudaErrorInvalidValue;
   auto args = [&](auto kernel) {
-    kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(dy2),
-        static_cast<const __nv_bfloat16*>(x), mean, invstd, static_cast<const __nv_bfloat16*>(g),
-        static_cast<const __nv_bfloat16*>(b), static_cast<const __nv_bfloat16*>(res), rmean, rinvstd,
-        static_cast<const __nv_bfloat16*>(rg), static_cast<const __nv_bfloat16*>(rb),
-        static_cast<__nv_bfloat16*>(dz), rows, C);
+    kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(B(dy), B(dy2), B(x), mean, invstd, B(g), B(b), B(res),
+                                                              rmean, rinvstd, B(rg), B(rb), BW_(dz), rows, C);
   };
   if (rmean == nullptr) {
     if (dy2) args(add_relu_bwd_kernel<1, true>);
@@ -499,29 +719,30 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
                         const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
                         void* ws, cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
-  int grid = relu ? grid_rows(bwd_reduce_kernel<true>, reduce_smem(C), rows, C)
-                  : grid_rows(bwd_reduce_kernel<false>, reduce_smem(C), rows, C);
   float* part = static_cast<float*>(ws);
   float* coef = part + (size_t)kMaxGrid * 2 * C;
   auto red = [&](auto kernel) {
-    kernel<<<grid, kThreads, reduce_smem(C), s>>>(
-        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
-        static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), rows, C, part);
+    return coop(kernel, rows, C, s, B(dy), B(x), mean, invstd, B(g), B(b), rows, C, part, coef, dgamma, dbeta);
   };
-  if (relu) red(bwd_reduce_kernel<true>);
-  else red(bwd_reduce_kernel<false>);
-  bwd_finalize<<<(C + 31) / 32, 32 * kFinWarps, 0, s>>>(part, grid, rows, C, dgamma, dbeta, coef);
-  if (dx) {
-    auto launch = [&](auto kernel) {
-      kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(
-          static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), mean, invstd,
-          static_cast<const __nv_bfloat16*>(g), static_cast<const __nv_bfloat16*>(b), coef,
-          static_cast<__nv_bfloat16*>(dx), rows, C);
-    };
-    if (relu) launch(bwd_elemt_kernel<true>);
-    else launch(bwd_elemt_kernel<false>);
-  }
-  return cudaGetLastError();
+  cudaError_t e = relu ? red(bwd_reduce_kernel<true>) : red(bwd_reduce_kernel<false>);
+  if (e != cudaSuccess || dx == nullptr) return e;
+  return bwd_elemt(dy, x, mean, invstd, g, b, coef, dx, rows, C, relu, s);
+}
+
+cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean,
+                                 const float* invstd, const void* g, const void* b, const void* res, void* dz,
+                                 void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
+                                 cudaStream_t s) {
+  if (!shape_ok(rows, C) || res == nullptr || dz == nullptr || dx == nullptr) return cudaErrorInvalidValue;
+  float* part = static_cast<float*>(ws);
+  float* coef = part + (size_t)kMaxGrid * 2 * C;
+  auto red = [&](auto kernel) {
+    return coop(kernel, rows, C, s, B(dy), B(dy2), B(x), mean, invstd, B(g), B(b), B(res), BW_(dz), rows, C, part,
+                coef, dgamma, dbeta);
+  };
+  cudaError_t e = dy2 ? red(add_relu_reduce_kernel<true>) : red(add_relu_reduce_kernel<false>);
+  if (e != cudaSuccess) return e;
+  return bwd_elemt(dz, x, mean, invstd, g, b, coef, dx, rows, C, 0, s);
 }
 
 }  // namespace krt

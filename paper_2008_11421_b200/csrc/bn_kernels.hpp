@@ -8,6 +8,9 @@ namespace krt {
 size_t bn_workspace_bytes(int C);
 cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws,
                      cudaStream_t s);
+cudaError_t bn_stats_apply(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd,
+                           const void* g, const void* b, const void* res, int relu, void* y, void* ws,
+                           cudaStream_t s);
 cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, const void* g, const void* b,
                      const void* res, const float* rmean, const float* rinvstd, const void* rg, const void* rb,
                      int relu, void* y, int64_t rows, int C, cudaStream_t s);
@@ -17,4 +20,8 @@ cudaError_t bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, cons
 cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
                         const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
                         void* ws, cudaStream_t s);
+cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean,
+                                 const float* invstd, const void* g, const void* b, const void* res, void* dz,
+                                 void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
+                                 cudaStream_t s);
 }  // namespace krt

@@ -399,6 +399,12 @@ int krt_bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, flo
   KRT_CUDA_GUARD(bn_stats(x, rows, C, eps, mean, invstd, ws, (cudaStream_t)stream), "bn_stats");
 }
 
+int krt_bn_stats_apply(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, const void* g,
+                       const void* b, const void* res, int relu, void* y, void* ws, void* stream) {
+  KRT_CUDA_GUARD(bn_stats_apply(x, rows, C, eps, mean, invstd, g, b, res, relu, y, ws, (cudaStream_t)stream),
+                 "bn_stats_apply");
+}
+
 int krt_bn_apply(const void* x, const float* mean, const float* invstd, const void* g, const void* b,
                  const void* res, const float* rmean, const float* rinvstd, const void* rg, const void* rb, int relu,
                  void* y, int64_t rows, int C, void* stream) {
@@ -419,6 +425,14 @@ int krt_bn_backward(const void* dy, const void* x, const float* mean, const floa
                     void* stream) {
   KRT_CUDA_GUARD(bn_backward(dy, x, mean, invstd, g, b, relu, dx, dgamma, dbeta, rows, C, ws, (cudaStream_t)stream),
                  "bn_backward");
+}
+
+int krt_bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean, const float* invstd,
+                             const void* g, const void* b, const void* res, void* dz, void* dx, float* dgamma,
+                             float* dbeta, int64_t rows, int C, void* ws, void* stream) {
+  KRT_CUDA_GUARD(bn_add_relu_backward(dy, dy2, x, mean, invstd, g, b, res, dz, dx, dgamma, dbeta, rows, C, ws,
+                                      (cudaStream_t)stream),
+                 "bn_add_relu_backward");
 }
 
 int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,

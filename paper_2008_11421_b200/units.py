@@ -197,8 +197,7 @@ class StemUnit(_ConvNetUnit):
             c = _conv_into(x, wv, 2, 3, None if saved is None else _cl(saved[1]))
             st = saved[2] if saved is not None else torch.empty(2 * self.cout, device=x.device)
             m, i = st[:self.cout], st[self.cout:]
-            bnfused.stats(c, m, i)
-            a = bnfused.apply(c, m, i, g, b, relu=True)
+            a = bnfused.stats_apply(c, m, i, g, b, relu=True)
             y, _ = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
             return y
         c = _conv(x, wv, 2, 3)
@@ -310,22 +309,20 @@ class BottleneckUnit(_ConvNetUnit):
             st = self._stats_views(torch.empty(self._nstats(), device=x.device))
         sv = (lambda k: None) if saved is None else (lambda k: _cl(saved[k]))
         c1 = _conv_into(x, _cl(w1), 1, 0, sv(1))
-        bnfused.stats(c1, st[0], st[1])
-        a1 = bnfused.apply(c1, st[0], st[1], g1, b1, relu=True)
+        a1 = bnfused.stats_apply(c1, st[0], st[1], g1, b1, relu=True)
         c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
         del a1
-        bnfused.stats(c2, st[2], st[3])
-        a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
+        a2 = bnfused.stats_apply(c2, st[2], st[3], g2, b2, relu=True)
         c3 = _conv_into(a2, _cl(w3), 1, 0, sv(3))
         del a2
-        bnfused.stats(c3, st[4], st[5])
         if self.down:
             wd, gd, bd = params[9:12]
+            bnfused.stats(c3, st[4], st[5])
             cd = _conv_into(x, _cl(wd), self.s, 0, sv(4))
             bnfused.stats(cd, st[6], st[7])
             return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=cd, rstats=(st[6], st[7]),
                                  rg=gd, rb=bd, out=out)
-        return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=x, out=out)
+        return bnfused.stats_apply(c3, st[4], st[5], g3, b3, relu=True, res=x, out=out)
 
     def _backward_fused(self, dy, params, saved, grads):
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
@@ -337,10 +334,11 @@ class BottleneckUnit(_ConvNetUnit):
             cd = _cl(saved[4])
             dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, cd, rstats=(st[6], st[7]), rg=gd, rb=bd,
                                       dy2=dy2)
+            dc3 = bnfused.backward(dz, c3, st[4], st[5], g3, b3, relu=False, dgamma=grads[7], dbeta=grads[8])
         else:
-            dz = bnfused.add_relu_bwd(dy, c3, st[4], st[5], g3, b3, x, dy2=dy2)
+            dz, dc3 = bnfused.add_relu_backward(dy, c3, st[4], st[5], g3, b3, x, dgamma=grads[7],
+                                                dbeta=grads[8], dy2=dy2)
         del dy, dy2
-        dc3 = bnfused.backward(dz, c3, st[4], st[5], g3, b3, relu=False, dgamma=grads[7], dbeta=grads[8])
         a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
         da2, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0)
         del dc3, a2
@@ -555,6 +553,14 @@ def _stats_fw(c, st_m, st_i):
         st_i.copy_(torch.rsqrt(v + BN_EPS))
 
 
+def _stats_bn_relu(c, st_m, st_i, g, b):
+    """_stats_fw then _bn_relu; one cooperative kernel for bf16."""
+    if c.dtype == torch.bfloat16 and bnfused.supported(c.shape[1]):
+        return bnfused.stats_apply(c, st_m, st_i, g, b, relu=True)
+    _stats_fw(c, st_m, st_i)
+    return _bn_relu(c, st_m, st_i, g, b)
+
+
 def _bn_relu(c, m, i, g, b):
     if c.dtype == torch.bfloat16 and bnfused.supported(c.shape[1]):
         return bnfused.apply(c, m, i, g, b, relu=True)
@@ -626,17 +632,14 @@ class PreActBottleneckUnit(_ConvNetUnit):
         else:
             st = self._st(torch.empty(self._nstats(), device=x.device))
         sv = (lambda k: None) if saved is None else (lambda k: _cl(saved[k]))
-        _stats_fw(x, st[0], st[1])
-        a0 = _bn_relu(x, st[0], st[1], g0, b0)
+        a0 = _stats_bn_relu(x, st[0], st[1], g0, b0)
         c1 = _conv_into(a0, _cl(w1), 1, 0, sv(1))
         sc = _conv(a0, _cl(params[9]), self.s, 0) if self.down else x
         del a0
-        _stats_fw(c1, st[2], st[3])
-        a1 = _bn_relu(c1, st[2], st[3], g1, b1)
+        a1 = _stats_bn_relu(c1, st[2], st[3], g1, b1)
         c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
         del a1
-        _stats_fw(c2, st[4], st[5])
-        a2 = _bn_relu(c2, st[4], st[5], g2, b2)
+        a2 = _stats_bn_relu(c2, st[4], st[5], g2, b2)
         y = _conv(a2, _cl(w3), 1, 0)
         if out is not None:
             return torch.add(y, sc, out=out)
@@ -746,8 +749,7 @@ class PreActHeadUnit(_ConvNetUnit):
         st = saved[1] if saved is not None else torch.empty(2 * self.cin, device=x.device)
         if saved is not None:
             _cl(saved[0]).copy_(x)
-        _stats_fw(x, st[:self.cin], st[self.cin:])
-        a = _bn_relu(x, st[:self.cin], st[self.cin:], g, b)
+        a = _stats_bn_relu(x, st[:self.cin], st[self.cin:], g, b)
         p = a.float().mean(dim=(2, 3)).to(a.dtype)
         return torch.addmm(bias, p, w.t())
 

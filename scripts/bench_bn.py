@@ -1,0 +1,64 @@
+"""CUDA-event timing of the fused BN kernels at the ResNet-200 layer shapes
+(batch 512 slices of the b3072 bench workload), algorithmic bytes / time.
+
+    python scripts/bench_bn.py [--batch 512] [--json out.json]
+"""
+import argparse
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2008_11421_b200 import bnfused  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batch", type=int, default=512)
+ap.add_argument("--json", default=None)
+args = ap.parse_args()
+
+# (C, H): bottleneck widths and outputs of the four ResNet-200 stages
+SHAPES = [(64, 56), (256, 56), (128, 28), (512, 28), (256, 14), (1024, 14), (512, 7), (2048, 7)]
+
+
+def t(fn, reps=10):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps * 1e-3
+
+
+rows_out = []
+for c, hw in SHAPES:
+    n = args.batch
+    mk = lambda: torch.randn(n, c, hw, hw, device="cuda").to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    x, r, dy = mk(), mk(), mk()
+    g = torch.ones(c, device="cuda", dtype=torch.bfloat16)
+    b = torch.zeros(c, device="cuda", dtype=torch.bfloat16)
+    m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    dg, db = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    bnfused.stats(x, m, i)
+    nb = x.numel() * 2
+    cases = [("stats", lambda: bnfused.stats(x, m, i), nb),
+             ("stats_apply", lambda: bnfused.stats_apply(x, m, i, g, b, relu=True), 3 * nb),
+             ("stats_apply_res", lambda: bnfused.stats_apply(x, m, i, g, b, relu=True, res=r), 4 * nb),
+             ("apply", lambda: bnfused.apply(x, m, i, g, b, relu=True), 2 * nb),
+             ("apply_res", lambda: bnfused.apply(x, m, i, g, b, relu=True, res=r), 3 * nb),
+             ("add_relu_bwd", lambda: bnfused.add_relu_bwd(dy, x, m, i, g, b, r), 4 * nb),
+             ("backward_relu", lambda: bnfused.backward(dy, x, m, i, g, b, relu=True, dgamma=dg, dbeta=db), 5 * nb),
+             ("add_relu_backward", lambda: bnfused.add_relu_backward(dy, x, m, i, g, b, r, dgamma=dg, dbeta=db),
+              7 * nb)]
+    for name, fn, traffic in cases:
+        sec = t(fn)
+        rows_out.append({"C": c, "HW": hw, "batch": n, "kernel": name, "us": sec * 1e6,
+                         "GBps": traffic / sec / 1e9})
+        print(f"C={c:5d} {hw:3d}x{hw:<3d} {name:18s} {sec*1e6:9.1f} us {traffic/sec/1e9:8.1f} GB/s")
+    del x, r, dy
+    torch.cuda.empty_cache()
+if args.json:
+    json.dump(rows_out, open(args.json, "w"), indent=1)

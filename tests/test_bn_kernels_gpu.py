@@ -111,3 +111,79 @@ def test_add_relu_backward_second_gradient():
     dz = bnfused.add_relu_bwd(dy, x, m, i, g, b, r, dy2=dy2)
     ref = torch.where(y > 0, dy + dy2, torch.zeros_like(dy))
     assert torch.equal(dz, ref)
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 28, 28), (8, 2048, 7, 7), (3, 128, 5, 7), (1, 8, 1, 3), (2, 256, 1, 1)])
+@pytest.mark.parametrize("residual", [False, True])
+def test_stats_apply_fused(shape, residual):
+    """stats + apply in one cooperative kernel == the torch fp32 reference,
+    and equal to the two separate kernels up to the last bit of the stats."""
+    n, c, h, w = shape
+    x = rand(*shape, scale=2.0, shift=0.5, seed=31)
+    r = rand(*shape, seed=32) if residual else None
+    g, b = params(c, seed=33)
+    m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    y = bnfused.stats_apply(x, m, i, g, b, relu=True, res=r)
+    rm, ri = ref_stats(x)
+    torch.testing.assert_close(m, rm, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(i, ri, rtol=1e-4, atol=1e-5)
+    pre = ((x.float() - rm[None, :, None, None]) * ri[None, :, None, None] * g.float()[None, :, None, None]
+           + b.float()[None, :, None, None])
+    if residual:
+        pre = pre + r.float()
+    torch.testing.assert_close(y.float(), F.relu(pre), **BF16_TOL)
+    m2, i2 = torch.empty_like(m), torch.empty_like(i)
+    bnfused.stats(x, m2, i2)
+    torch.testing.assert_close(m2, m, rtol=1e-6, atol=1e-7)
+    y2 = bnfused.apply(x, m, i, g, b, relu=True, res=r)
+    assert torch.equal(y, y2)  # same stats -> the apply pass is bit-identical
+    # deterministic: a second launch is bitwise equal
+    m3, i3 = torch.empty_like(m), torch.empty_like(i)
+    y3 = bnfused.stats_apply(x, m3, i3, g, b, relu=True, res=r)
+    assert torch.equal(m3, m) and torch.equal(i3, i) and torch.equal(y3, y)
+
+
+@pytest.mark.parametrize("shape", [(8, 256, 14, 14), (4, 2048, 7, 7), (3, 64, 5, 7)])
+@pytest.mark.parametrize("two", [False, True])
+def test_add_relu_backward_fused(shape, two):
+    """add_relu_bwd + backward(relu=False) fused == the two kernels: dz bitwise,
+    dgamma/dbeta/dx within fp32-reduction / bf16 resolution."""
+    n, c, h, w = shape
+    x, r, dy, dy2 = (rand(*shape, seed=s) for s in (41, 42, 43, 44))
+    dy2 = dy2 if two else None
+    g, b = params(c, seed=45)
+    m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    bnfused.stats(x, m, i)
+    dg, db = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    dz, dx = bnfused.add_relu_backward(dy, x, m, i, g, b, r, dgamma=dg, dbeta=db, dy2=dy2)
+    dz_ref = bnfused.add_relu_bwd(dy, x, m, i, g, b, r, dy2=dy2)
+    assert torch.equal(dz, dz_ref)
+    dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+    dx2 = bnfused.backward(dz_ref, x, m, i, g, b, relu=False, dgamma=dg2, dbeta=db2)
+    torch.testing.assert_close(db, db2, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(dg, dg2, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(dx.float(), dx2.float(), **BF16_TOL)
+    # against autograd of bn (no relu) on dz
+    xr = x.float().requires_grad_(True)
+    gr, br = g.float().requires_grad_(True), b.float().requires_grad_(True)
+    bn_ref_fwd(xr, gr, br).backward(dz.float())
+    torch.testing.assert_close(db, br.grad, rtol=1e-3, atol=1e-2)
+    torch.testing.assert_close(dg, gr.grad, rtol=1e-3, atol=1e-2)
+    err = (dx.float() - xr.grad).abs().max() / xr.grad.abs().max()
+    assert err < 2e-2, float(err)
+
+
+def test_backward_no_dx_and_tiny_rows():
+    """dx=None path (reduce only) and rows smaller than one CTA sweep."""
+    for shape in [(1, 64, 1, 1), (2, 8, 1, 1), (1, 2048, 1, 2)]:
+        n, c, h, w = shape
+        x, dy = rand(*shape, seed=51), rand(*shape, seed=52)
+        g, b = params(c, seed=53)
+        m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+        bnfused.stats(x, m, i)
+        dg, db = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+        assert bnfused.backward(dy, x, m, i, g, b, relu=True, dgamma=dg, dbeta=db, need_dx=False) is None
+        dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+        bnfused.backward(dy, x, m, i, g, b, relu=True, dgamma=dg2, dbeta=db2)
+        torch.testing.assert_close(dg, dg2, rtol=1e-5, atol=1e-5)
+        torch.testing.assert_close(db, db2, rtol=1e-5, atol=1e-5)
