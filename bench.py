@@ -327,17 +327,21 @@ def run_gpu(args, rec):
     # ---- e2e: host (pinned) inputs copied in, loss read back, every step --------
     xh = x.cpu().pin_memory()
     yh = y.cpu().pin_memory()
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, args.steps)
+    retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     barrier()
     t0 = time.perf_counter()
+    e2e_marks = []
     for _ in range(e2e_steps):
         xd = xh.to(dev, non_blocking=True)
         yd = yh.to(dev, non_blocking=True)
         loss = ex.step(xd, yd)
         float(loss)    # D2H of the step's loss
+        e2e_marks.append(time.perf_counter() - t0)
     ex.synchronize()
     barrier()
     e2e_s = time.perf_counter() - t0
+    e2e_retries = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0) - retries0
     tt = torch.tensor([e2e_s])
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -420,7 +424,9 @@ def run_gpu(args, rec):
                     "swap_in_busy_s": sum(b - a for a, b in xin),
                     "swap_out_busy_s": sum(b - a for a, b in xout)},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_in,
-                "d2h_bytes_per_step": 4},
+                "d2h_bytes_per_step": 4, "steps": e2e_steps,
+                "loss_ready_s": [round(t, 4) for t in e2e_marks], "total_s": round(e2e_s, 4),
+                "alloc_retries": e2e_retries},
         "gpu_launches": launches + sum(v[2] for v in fam.values()) * args.steps,
         "runtime": {k: st[k] for k in ("arena_bytes", "ledger_peak_bytes", "host_swap_bytes",
                                        "swapped_blocks", "ops_per_iteration", "params")},

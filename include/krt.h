@@ -274,6 +274,21 @@ int krt_bn_add_relu_backward(const void* dy, const void* dy2, const void* x, con
                              void* dz, void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
                              void* stream);
 
+/* ResNet stem: y = maxpool_{k,s,p}( relu(bn(x)) ), x NHWC bf16 [n,h,w,c], c % 8 == 0;
+ * the post-BN activation is never written.  Bitwise equal to krt_bn_apply (relu)
+ * followed by aten max_pool2d_with_indices. */
+int krt_bn_relu_maxpool(const void* x, const float* mean, const float* invstd, const void* gamma,
+                        const void* beta, void* y, int n, int h, int w, int c, int k, int s, int p,
+                        void* stream);
+/* Backward of the max-pool above: dx = d(pool)/d(relu(bn(x))) given dy, window
+ * argmaxes recomputed from x (ws: krt_bn_relu_maxpool_bwd_workspace bytes);
+ * bitwise equal to aten max_pool2d_with_indices_backward.  The ReLU/BN backward
+ * follows with krt_bn_backward(relu=1). */
+size_t krt_bn_relu_maxpool_bwd_workspace(int n, int h, int w, int c, int k, int s, int p);
+int krt_bn_relu_maxpool_bwd(const void* dy, const void* x, const float* mean, const float* invstd,
+                            const void* gamma, const void* beta, void* dx, void* ws, int n, int h, int w,
+                            int c, int k, int s, int p, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

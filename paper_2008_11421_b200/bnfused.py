@@ -143,3 +143,30 @@ def add_relu_backward(dy, c, mean, invstd, g, b, res, dgamma=None, dbeta=None, d
                                                        _ptr(dgamma), _ptr(dbeta), rows, C, ws.data_ptr(),
                                                        _stream()))
     return dz, dx
+
+
+def relu_maxpool(c, mean, invstd, g, b, k=3, s=2, p=1):
+    """maxpool_{k,s,p}(relu(bn(c))) without materialising relu(bn(c))."""
+    c = _nhwc(c)
+    n, C, h, w = c.shape
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    y = torch.empty((n, C, oh, ow), dtype=c.dtype, device=c.device, memory_format=torch.channels_last)
+    with _timed("bn_relu_maxpool", c.numel() * 2 + y.numel() * 2):
+        _lib.check(_lib.lib().krt_bn_relu_maxpool(c.data_ptr(), mean.data_ptr(), invstd.data_ptr(), g.data_ptr(),
+                                                  b.data_ptr(), y.data_ptr(), n, h, w, C, k, s, p, _stream()))
+    return y
+
+
+def relu_maxpool_backward(dy, c, mean, invstd, g, b, k=3, s=2, p=1):
+    """Gradient w.r.t. relu(bn(c)) of maxpool_{k,s,p}; argmaxes recomputed from c."""
+    c, dy = _nhwc(c), _nhwc(dy)
+    n, C, h, w = c.shape
+    ws = torch.empty(_lib.lib().krt_bn_relu_maxpool_bwd_workspace(n, h, w, C, k, s, p), dtype=torch.uint8,
+                     device=c.device)
+    dx = torch.empty_like(c, memory_format=torch.channels_last)
+    # bytes: c read for the argmax pass, argmax bytes written + read, dy read, dx written
+    with _timed("bn_relu_maxpool_bwd", c.numel() * 2 * 2 + ws.numel() * 2 + dy.numel() * 2):
+        _lib.check(_lib.lib().krt_bn_relu_maxpool_bwd(dy.data_ptr(), c.data_ptr(), mean.data_ptr(),
+                                                      invstd.data_ptr(), g.data_ptr(), b.data_ptr(), dx.data_ptr(),
+                                                      ws.data_ptr(), n, h, w, C, k, s, p, _stream()))
+    return dx

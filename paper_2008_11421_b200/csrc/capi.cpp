@@ -14,6 +14,7 @@
 #include "planner.hpp"
 #include "host_optim.hpp"
 #include "bn_kernels.hpp"
+#include "pool_kernels.hpp"
 #include "kernels.hpp"
 #include "runtime.hpp"
 
@@ -433,6 +434,23 @@ int krt_bn_add_relu_backward(const void* dy, const void* dy2, const void* x, con
   KRT_CUDA_GUARD(bn_add_relu_backward(dy, dy2, x, mean, invstd, g, b, res, dz, dx, dgamma, dbeta, rows, C, ws,
                                       (cudaStream_t)stream),
                  "bn_add_relu_backward");
+}
+
+int krt_bn_relu_maxpool(const void* x, const float* mean, const float* invstd, const void* g, const void* b, void* y,
+                        int n, int h, int w, int c, int k, int s, int p, void* stream) {
+  KRT_CUDA_GUARD(bn_relu_maxpool(x, mean, invstd, g, b, y, n, h, w, c, k, s, p, (cudaStream_t)stream),
+                 "bn_relu_maxpool");
+}
+
+size_t krt_bn_relu_maxpool_bwd_workspace(int n, int h, int w, int c, int k, int s, int p) {
+  return bn_relu_maxpool_bwd_workspace(n, h, w, c, k, s, p);
+}
+
+int krt_bn_relu_maxpool_bwd(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                            const void* b, void* dx, void* ws, int n, int h, int w, int c, int k, int s, int p,
+                            void* stream) {
+  KRT_CUDA_GUARD(bn_relu_maxpool_bwd(dy, x, mean, invstd, g, b, dx, ws, n, h, w, c, k, s, p, (cudaStream_t)stream),
+                 "bn_relu_maxpool_bwd");
 }
 
 int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,

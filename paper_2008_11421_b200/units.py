@@ -197,9 +197,8 @@ class StemUnit(_ConvNetUnit):
             c = _conv_into(x, wv, 2, 3, None if saved is None else _cl(saved[1]))
             st = saved[2] if saved is not None else torch.empty(2 * self.cout, device=x.device)
             m, i = st[:self.cout], st[self.cout:]
-            a = bnfused.stats_apply(c, m, i, g, b, relu=True)
-            y, _ = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
-            return y
+            bnfused.stats(c, m, i)
+            return bnfused.relu_maxpool(c, m, i, g, b, 3, 2, 1)   # relu(bn(c)) never materialised
         c = _conv(x, wv, 2, 3)
         o, m, i = _bn_fw(c, g, b)
         if saved is not None:
@@ -216,10 +215,7 @@ class StemUnit(_ConvNetUnit):
         x, c = _cl(saved[0]), _cl(saved[1])
         m, i = saved[2][:self.cout], saved[2][self.cout:]
         if self._fused():
-            a = bnfused.apply(c, m, i, g, b, relu=True)
-            _, idx = _aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
-            da = _aten.max_pool2d_with_indices_backward(dy, a, [3, 3], [2, 2], [1, 1], [1, 1], False, idx)
-            del a, idx
+            da = bnfused.relu_maxpool_backward(dy, c, m, i, g, b, 3, 2, 1)
             dc = bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=grads[1], dbeta=grads[2])
             _, dw, _ = _conv_bw(dc, x, _cl(w), 2, 3, need_dx=False)
             _cl(grads[0]).copy_(dw)

@@ -60,5 +60,36 @@ for c, hw in SHAPES:
         print(f"C={c:5d} {hw:3d}x{hw:<3d} {name:18s} {sec*1e6:9.1f} us {traffic/sec/1e9:8.1f} GB/s")
     del x, r, dy
     torch.cuda.empty_cache()
+# ResNet stem: relu(bn(c)) -> maxpool 3x3/s2 fused vs apply + aten max-pool (fwd and bwd)
+n, c, hw = args.batch, 64, 112
+x = torch.randn(n, c, hw, hw, device="cuda").to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
+g = torch.ones(c, device="cuda", dtype=torch.bfloat16)
+b = torch.zeros(c, device="cuda", dtype=torch.bfloat16)
+m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+bnfused.stats(x, m, i)
+y = bnfused.relu_maxpool(x, m, i, g, b)
+dy = torch.randn_like(y).contiguous(memory_format=torch.channels_last)
+
+
+def aten_fw():
+    a = bnfused.apply(x, m, i, g, b, relu=True)
+    return torch.ops.aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
+
+
+def aten_bw():
+    a = bnfused.apply(x, m, i, g, b, relu=True)
+    _, idx = torch.ops.aten.max_pool2d_with_indices(a, [3, 3], [2, 2], [1, 1])
+    return torch.ops.aten.max_pool2d_with_indices_backward(dy, a, [3, 3], [2, 2], [1, 1], [1, 1], False, idx)
+
+
+nb_in, nb_out = x.numel() * 2, y.numel() * 2
+for name, fn, traffic in [("relu_maxpool", lambda: bnfused.relu_maxpool(x, m, i, g, b), nb_in + nb_out),
+                          ("apply+aten_maxpool", aten_fw, nb_in + nb_out),
+                          ("relu_maxpool_bwd", lambda: bnfused.relu_maxpool_backward(dy, x, m, i, g, b),
+                           2 * nb_in + nb_out),
+                          ("apply+aten_maxpool_bwd", aten_bw, 2 * nb_in + nb_out)]:
+    sec = t(fn)
+    rows_out.append({"C": c, "HW": hw, "batch": n, "kernel": name, "us": sec * 1e6, "GBps": traffic / sec / 1e9})
+    print(f"C={c:5d} {hw:3d}x{hw:<3d} {name:22s} {sec*1e6:9.1f} us {traffic/sec/1e9:8.1f} GB/s (vs fused-min bytes)")
 if args.json:
     json.dump(rows_out, open(args.json, "w"), indent=1)

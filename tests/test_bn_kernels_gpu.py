@@ -187,3 +187,26 @@ def test_backward_no_dx_and_tiny_rows():
         bnfused.backward(dy, x, m, i, g, b, relu=True, dgamma=dg2, dbeta=db2)
         torch.testing.assert_close(dg, dg2, rtol=1e-5, atol=1e-5)
         torch.testing.assert_close(db, db2, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("shape,ksp", [((4, 64, 112, 112), (3, 2, 1)), ((3, 16, 9, 7), (3, 2, 1)),
+                                       ((2, 8, 6, 6), (2, 2, 0)), ((2, 32, 11, 13), (3, 1, 1)), ((2, 64, 10, 10), (5, 3, 2))])
+def test_relu_maxpool_matches_aten_bitwise(shape, ksp):
+    """maxpool(relu(bn(c))) fused, forward and backward, == apply -> aten
+    max_pool2d_with_indices -> max_pool2d_with_indices_backward, bitwise
+    (ties included: a coarse input makes equal maxima common)."""
+    k, s, p = ksp
+    n, c, h, w = shape
+    x = (rand(*shape, scale=2.0, seed=61).float() * 4).round().div(4).to(torch.bfloat16)
+    x = x.contiguous(memory_format=torch.channels_last)
+    g, b = params(c, seed=62)
+    m, i = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    bnfused.stats(x, m, i)
+    a = bnfused.apply(x, m, i, g, b, relu=True)
+    y_ref, idx = torch.ops.aten.max_pool2d_with_indices(a, [k, k], [s, s], [p, p])
+    y = bnfused.relu_maxpool(x, m, i, g, b, k, s, p)
+    assert y.shape == y_ref.shape and torch.equal(y, y_ref)
+    dy = rand(*y.shape, seed=63).contiguous(memory_format=torch.channels_last)
+    da_ref = torch.ops.aten.max_pool2d_with_indices_backward(dy, a, [k, k], [s, s], [p, p], [1, 1], False, idx)
+    da = bnfused.relu_maxpool_backward(dy, x, m, i, g, b, k, s, p)
+    assert torch.equal(da, da_ref)
