@@ -380,15 +380,34 @@ def run_gpu(args, rec):
     swap_out_bytes = st["iter_bytes_d2h"]
     # live roofline of our dominant kernel family (CUDA events on the compute stream)
     fam = {}
-    for kind, nbytes, a, b in prof or []:
+    for kind, nbytes, a, b, flops in prof or []:
         t = a.elapsed_time(b) * 1e-3
-        f = fam.setdefault(kind, [0, 0.0, 0])
+        f = fam.setdefault(kind, [0, 0.0, 0, 0.0])
         f[0] += nbytes
         f[1] += t
         f[2] += 1
-    kernels = {k: {"launches": v[2], "ms_per_step": v[1] * 1e3, "achieved_GBps": v[0] / v[1] / 1e9,
-                   "frac_of_hbm": v[0] / v[1] / 1e9 / pk["hbm_gbs"]} for k, v in fam.items() if v[1] > 0}
+        f[3] += flops
+    kernels = {}
+    for k, v in fam.items():
+        if v[1] <= 0:
+            continue
+        kernels[k] = {"launches": v[2], "ms_per_step": v[1] * 1e3, "achieved_GBps": v[0] / v[1] / 1e9,
+                      "frac_of_hbm": v[0] / v[1] / 1e9 / pk["hbm_gbs"]}
+        if v[3] > 0:   # tensor-core family: also against the dense bf16 peak
+            kernels[k]["achieved_TFLOPs"] = v[3] / v[1] / 1e12
+            kernels[k]["frac_of_tensor"] = v[3] / v[1] / 1e12 / pk["bf16_tflops"]
     dom = max(fam, key=lambda k: fam[k][1]) if fam else None
+
+    def dom_roofline(k):
+        v = fam[k]
+        hbm = {"bound": "hbm", "kernel": k, "achieved": v[0] / v[1] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+               "frac": v[0] / v[1] / 1e9 / pk["hbm_gbs"], "traffic": None,
+               "peak_kind": f"{pk_kind} HBM copy (burst)"}
+        if v[3] > 0 and v[3] / v[1] / 1e12 / pk["bf16_tflops"] > hbm["frac"]:
+            return {"bound": "tensor", "kernel": k, "achieved": v[3] / v[1] / 1e12, "peak": pk["bf16_tflops"],
+                    "unit": "TFLOP/s", "frac": v[3] / v[1] / 1e12 / pk["bf16_tflops"], "traffic": None,
+                    "peak_kind": f"{pk_kind} dense bf16 (burst)", "hbm_frac": hbm["frac"]}
+        return hbm
     line = {
         "metric": metric_name(rec),
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -401,13 +420,10 @@ def run_gpu(args, rec):
                    "swapped_bytes": rec["swapped_bytes"], "recompute_bytes": rec["recompute_bytes"],
                    "l2": f"inputs > L2 (batch tensor {x.numel() * x.element_size() / 1e6:.0f} MB; "
                          f"{rec['total_bytes'] / 1e9:.0f} GB of activations per step)"},
-        "roofline": ({"bound": "hbm", "kernel": dom,
-                      "achieved": fam[dom][0] / fam[dom][1] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                      "frac": fam[dom][0] / fam[dom][1] / 1e9 / pk["hbm_gbs"],
-                      "traffic": None, "peak_kind": f"{pk_kind} HBM copy (burst)",
-                      "note": "our dominant kernel family in the step (sum of algorithmic bytes / sum of "
-                              "CUDA-event durations over one timed step); DRAM traffic == algorithmic "
-                              "bytes per profiles/ ncu capture"} if dom else None),
+        "roofline": (dict(dom_roofline(dom),
+                          note="our dominant kernel family in the step (sum of algorithmic bytes or flops / sum "
+                               "of CUDA-event durations over one timed step, on the compute stream)")
+                     if dom else None),
         "kernels": kernels,
         "step_roofline": {"bound": "tensor", "achieved": alg_flops / iter_s / 1e12,
                           "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",

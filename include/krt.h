@@ -289,6 +289,23 @@ int krt_bn_relu_maxpool_bwd(const void* dy, const void* x, const float* mean, co
                             const void* gamma, const void* beta, void* dx, void* ws, int n, int h, int w,
                             int c, int k, int s, int p, void* stream);
 
+/* 1x1 convolution of NHWC bf16 activations as a tcgen05 GEMM (sm_100a):
+ * C[M,N] = f(A)[M,K] . B[N,K]^T with A = activations [rows, Cin], B = weights
+ * [Cout, Cin], C bf16.  f(A) = A, or relu(bn(A)) per input channel when pmean
+ * is non-NULL (pmean/pinvstd fp32, pgamma/pbeta bf16; K <= 1024): the previous
+ * BN's output is never written.  With part non-NULL (krt_conv1x1_partials_bytes
+ * of device scratch) the epilogue also reduces the per-output-channel sums of
+ * the stored C and C^2 into *part_rows partial rows, which
+ * krt_bn_partials_finalize turns into mean/invstd: no statistics pass re-reads C.
+ * Requirements: K % 64 == 0, N in {64, 128} or N % 256 == 0,
+ * 16-byte aligned pointers. */
+size_t krt_conv1x1_partials_bytes(int N);
+int krt_conv1x1_bn(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                   const float* pinvstd, const void* pgamma, const void* pbeta, float* part, int* part_rows,
+                   void* stream);
+int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
+                             float* invstd, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

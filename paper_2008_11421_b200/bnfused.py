@@ -11,13 +11,14 @@ from . import _lib
 EPS = 1e-5
 
 # When a list, every launch appends (kind, algorithmic_bytes, start_event,
-# end_event) recorded on the launching stream — bench.py's live roofline.
+# end_event, algorithmic_flops) recorded on the launching stream — bench.py's
+# live roofline.
 PROFILE = None
 
 
 class _timed:
-    def __init__(self, kind, nbytes):
-        self.kind, self.nbytes = kind, nbytes
+    def __init__(self, kind, nbytes, flops=0.0):
+        self.kind, self.nbytes, self.flops = kind, nbytes, flops
 
     def __enter__(self):
         if PROFILE is not None:
@@ -29,7 +30,7 @@ class _timed:
     def __exit__(self, *exc):
         if PROFILE is not None:
             self.e1.record()
-            PROFILE.append((self.kind, self.nbytes, self.e0, self.e1))
+            PROFILE.append((self.kind, self.nbytes, self.e0, self.e1, self.flops))
         return False
 
 
@@ -170,3 +171,40 @@ def relu_maxpool_backward(dy, c, mean, invstd, g, b, k=3, s=2, p=1):
                                                       invstd.data_ptr(), g.data_ptr(), b.data_ptr(), dx.data_ptr(),
                                                       ws.data_ptr(), n, h, w, C, k, s, p, _stream()))
     return dx
+
+
+def conv1x1_supported(cin, cout, pre=False):
+    return cin % 64 == 0 and (cout in (64, 128) or cout % 256 == 0) and (not pre or cin <= 1024)
+
+
+def conv1x1(x, w, out=None, pre=None, stats=None):
+    """Stride-1 1x1 convolution on the sm_100a tcgen05 GEMM (csrc/gemm_sm100.cu).
+
+    x: (N, Cin, H, W) channels_last bf16; w: (Cout, Cin, 1, 1) bf16.
+    pre=(mean, invstd, gamma, beta): convolve relu(bn(x)) instead of x, without
+    writing relu(bn(x)).  stats=(mean, invstd): fp32 outputs, the batch
+    statistics of the (bf16) result, reduced in the GEMM epilogue.
+    """
+    import ctypes as C
+    x = _nhwc(x)
+    n, cin, h, ww = x.shape
+    cout = w.shape[0]
+    wm = w.reshape(cout, cin)
+    if not wm.is_contiguous():
+        wm = wm.contiguous()
+    y = out if out is not None else torch.empty((n, cout, h, ww), dtype=x.dtype, device=x.device,
+                                                memory_format=torch.channels_last)
+    M = n * h * ww
+    part = None
+    rows = C.c_int(0)
+    if stats is not None:
+        part = torch.empty(_lib.lib().krt_conv1x1_partials_bytes(cout) // 4, dtype=torch.float32, device=x.device)
+    pm, pi, pg, pb = pre if pre is not None else (None, None, None, None)
+    # bytes: A read, C written (the statistics pass this replaces would re-read C)
+    with _timed("conv1x1_bn", M * (cin + cout) * 2, 2.0 * M * cin * cout):
+        _lib.check(_lib.lib().krt_conv1x1_bn(x.data_ptr(), wm.data_ptr(), y.data_ptr(), M, cout, cin, _ptr(pm),
+                                             _ptr(pi), _ptr(pg), _ptr(pb), _ptr(part), C.byref(rows), _stream()))
+        if stats is not None:
+            _lib.check(_lib.lib().krt_bn_partials_finalize(part.data_ptr(), rows.value, cout, M, EPS,
+                                                           stats[0].data_ptr(), stats[1].data_ptr(), _stream()))
+    return y

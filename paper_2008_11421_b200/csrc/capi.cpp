@@ -15,6 +15,7 @@
 #include "host_optim.hpp"
 #include "bn_kernels.hpp"
 #include "pool_kernels.hpp"
+#include "gemm_sm100.hpp"
 #include "kernels.hpp"
 #include "runtime.hpp"
 
@@ -451,6 +452,20 @@ int krt_bn_relu_maxpool_bwd(const void* dy, const void* x, const float* mean, co
                             void* stream) {
   KRT_CUDA_GUARD(bn_relu_maxpool_bwd(dy, x, mean, invstd, g, b, dx, ws, n, h, w, c, k, s, p, (cudaStream_t)stream),
                  "bn_relu_maxpool_bwd");
+}
+
+size_t krt_conv1x1_partials_bytes(int N) { return conv1x1_partials_bytes(N); }
+
+int krt_conv1x1_bn(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                   const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows, void* stream) {
+  KRT_CUDA_GUARD(conv1x1_bn_fprop(A, B, C, M, N, K, pmean, pinvstd, pg, pb, part, part_rows, (cudaStream_t)stream),
+                 "conv1x1_bn");
+}
+
+int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
+                             float* invstd, void* stream) {
+  KRT_CUDA_GUARD(bn_partials_finalize(part, part_rows, N, M, eps, mean, invstd, (cudaStream_t)stream),
+                 "bn_partials_finalize");
 }
 
 int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,

@@ -1,0 +1,582 @@
+// 1x1 convolution of NHWC activations as a tcgen05 GEMM, fused with the
+// batch-norm work around it (sm_100a):
+//
+//   C[M, N] = f(A)[M, K] . B[N, K]^T        (A = activations [rows, Cin],
+//                                            B = weights [Cout, Cin], both K-major)
+//   f(A)    = A, or relu(A*scale + shift) per K channel (the BN + ReLU of the
+//             previous layer applied in shared memory: its output is never
+//             written to HBM)
+//   epilogue: C rounded to bf16 and stored, and per-channel partial sums of
+//             C and C^2 (the next BN's batch statistics) reduced on chip, so
+//             no separate statistics pass re-reads C.
+//
+// Structure (one CTA per SM, persistent, static tile schedule):
+//   warp 0        TMA producer: A and B k-blocks (64 x bf16 = 128 B rows,
+//                 SWIZZLE_128B) into a kStages-deep shared-memory ring
+//   warp 1        TMEM allocator + MMA issuer: one elected thread issues
+//                 tcgen05.mma (M=128, N=BN, K=16) into one of two TMEM
+//                 accumulators, tcgen05.commit frees the smem stage / hands the
+//                 accumulator to the epilogue
+//   warps 2..17   epilogue, four warps per TMEM lane quarter (32 rows), each
+//                 a quarter of the tile's columns: tcgen05.ld 32 columns at a time,
+//                 bf16 round, staged through shared memory and written by TMA
+//                 bulk stores; lane j then sums column j of the staged chunk
+//   warps 18..21  prologue only: transform each A stage in place (one tile row
+//                 per thread) between the TMA landing and the MMA
+// Statistics are deterministic: fixed tile schedule, fixed summation order,
+// per-warp partial rows summed in double by bn_partials_finalize.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "gemm_sm100.hpp"
+
+namespace krt {
+namespace {
+
+constexpr int kBM = 128;       // tile rows (UMMA M, TMEM lanes)
+constexpr int kBK = 64;        // k-block: 64 bf16 = one 128-byte swizzle row
+constexpr int kUmmaK = 16;     // K per tcgen05.mma (bf16)
+constexpr int kEpiWarps = 16;  // four per TMEM lane quarter, each a quarter of the columns
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kXfWarp0 = 2 + kEpiWarps;        // prologue transform warps (4: one row per thread)
+constexpr int kThreads = 64 + kEpiThreads + 128;  // producer, MMA, epilogue, transform
+constexpr int kEpiWarp0 = 2;
+constexpr int kMaxProK = 1024;  // prologue channels held in shared memory
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns: thread = lane = row, v[j] = column j
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart
+// (cute/arch/mma_sm100_desc.hpp SmemDescriptor: start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version 1 [46,48), base offset [49,52), layout [61,64) = 2)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;               // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;     // SBO: next 8-row group
+  d |= (uint64_t)1 << 46;               // version
+  d |= (uint64_t)2 << 61;               // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M=128, N
+__host__ __device__ constexpr uint32_t instr_desc(int n) {
+  return (1u << 4)                      // c_format F32
+         | (1u << 7)                    // a_format BF16
+         | (1u << 10)                   // b_format BF16
+         | ((uint32_t)(n >> 3) << 17)   // n_dim
+         | ((uint32_t)(kBM >> 4) << 24);  // m_dim
+}
+
+// ---------------------------------------------------------------------------
+struct Params {
+  int64_t M;
+  int N, K, BN;
+  int n_tiles, m_tiles;
+  __nv_bfloat16* C;
+  float* part;  // [gridDim.x / n_tiles * 4][2][N] or nullptr: one row per (m-group, lane quarter)
+  // prologue (nullptr: none): a = relu(A*sc + sh), sc = invstd*g, sh = b - mean*sc
+  const float* pmean;
+  const float* pinvstd;
+  const __nv_bfloat16* pg;
+  const __nv_bfloat16* pb;
+};
+
+template <int BN, int STAGES, bool PRO>
+struct Smem {
+  alignas(1024) uint8_t a[STAGES][kBM * kBK * 2];
+  alignas(1024) uint8_t b[STAGES][BN * kBK * 2];
+  uint64_t full[STAGES], ready[STAGES], empty[STAGES];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+  float sc[PRO ? kMaxProK : 1], sh[PRO ? kMaxProK : 1];
+  // per-warp C staging for the TMA store: 32 rows x 64 B, SWIZZLE_64B (16-byte
+  // chunk c of row r at c ^ ((r >> 1) & 3)), so row-per-lane writes and
+  // column-per-lane reads are both free of bank conflicts
+  alignas(1024) uint8_t cstage[kEpiWarps][2][32 * 64];
+};
+
+template <int BN, int STAGES, bool PRO, bool STATS>
+__global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
+                                                              const __grid_constant__ CUtensorMap map_b,
+                                                              const __grid_constant__ CUtensorMap map_c, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kblocks = p.K / kBK;
+  // this CTA's tiles: fixed n-tile, m-tiles strided (grid is a multiple of n_tiles)
+  const int n_tile = blockIdx.x % p.n_tiles;
+  const int m_first = blockIdx.x / p.n_tiles, m_step = gridDim.x / p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.ready[s], 128);
+      mbar_init(&S.empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.tfull[i], 1);
+      mbar_init(&S.tempty[i], 128 * (BN >= 128 ? 4 : BN / 32));  // active epilogue threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(&S.tmem_base, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&S.empty[stage], phase ^ 1);
+          mbar_expect_tx(&S.full[stage], (kBM + BN) * kBK * 2);
+          tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * kBK, mt * kBM);
+          tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * kBK, n_tile * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = instr_desc(BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+      mbar_wait(&S.tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * BN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        if (PRO) mbar_wait(&S.ready[stage], phase);  // transformed by the epilogue warps
+        else mbar_wait(&S.full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(S.a[stage]), b0 = smem_u32(S.b[stage]);
+#pragma unroll
+          for (int k = 0; k < kBK / kUmmaK; ++k)
+            umma_bf16(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2), idesc,
+                      (kb | k) != 0);
+          umma_commit(&S.empty[stage]);                   // smem stage free when these MMAs finish
+          if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= kXfWarp0) {
+    // ------------------------------------------------------------ prologue transform
+    if (PRO) {
+      const int r = threadIdx.x - kXfWarp0 * 32;  // tile row 0..127
+      // the previous BN's affine, exactly as bn_apply computes it
+      for (int c = r; c < p.K; c += 128) {
+        float sc = p.pinvstd[c] * __bfloat162float(p.pg[c]);
+        S.sc[c] = sc;
+        S.sh[c] = __bfloat162float(p.pb[c]) - p.pmean[c] * sc;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // transform warps only
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+        // a = bf16(relu(a*sc + sh)) in place.  SWIZZLE_128B: logical 16-byte
+        // chunk jj of row r (channels kb*64 + 8*jj .. +8) is physical chunk jj ^ (r & 7)
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&S.full[stage], phase);
+          uint4* rowp = reinterpret_cast<uint4*>(S.a[stage] + r * 128);
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            // logical chunk jj sits at physical chunk jj ^ (r & 7): consecutive
+            // rows hit different 16-byte columns (no bank conflicts)
+            const int j = jj ^ (r & 7);
+            const int c0 = kb * kBK + 8 * jj;
+            uint4 u = rowp[j];
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float2 f = __bfloat1622float2(h[e]);
+              const int c = c0 + 2 * e;
+              h[e] = __floats2bfloat162_rn(fmaxf(__fmaf_rn(f.x, S.sc[c], S.sh[c]), 0.f),
+                                           fmaxf(__fmaf_rn(f.y, S.sc[c + 1], S.sh[c + 1]), 0.f));
+            }
+            rowp[j] = u;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+          mbar_arrive(&S.ready[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue warps
+    const int q = warp & 3;                       // TMEM lane quarter this warp may access
+    const int ew = warp - kEpiWarp0;              // 0..15
+    constexpr int kParts = BN >= 128 ? 4 : BN / 32;  // column parts (one warp per part and quarter)
+    const int half = ew >> 2;                     // this warp's column part
+    constexpr int kChunks = BN / 32 / kParts;     // 32-column chunks per part
+    if (half < kParts) {                          // BN = 64: two parts only
+    float acc_s[kChunks], acc_q[kChunks];
+#pragma unroll
+    for (int c = 0; c < kChunks; ++c) acc_s[c] = acc_q[c] = 0.f;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int sbuf = 0;
+    for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+      mbar_wait(&S.tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row0 = (int64_t)mt * kBM + q * 32;
+      const bool valid = row0 + lane < p.M;
+#pragma unroll 1
+      for (int c = 0; c < kChunks; ++c) {
+        const int col = half * (BN / kParts) + c * 32;  // within the tile
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
+        // this warp's staging buffer must be free: the TMA store issued two chunks ago has read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * 64);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 u;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            h[e] = valid ? __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1])
+                         : __floats2bfloat162_rn(0.f, 0.f);
+          }
+          st[j ^ ((lane >> 1) & 3)] = u;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          // rows beyond M are clipped by the TMA unit
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&map_c)),
+              "r"(n_tile * BN + col), "r"((int)row0), "r"(smem_u32(S.cstage[ew][sbuf]))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (STATS) {
+          // column `lane` of the staged (stored) bf16 chunk, rows in order;
+          // rows beyond M were staged as zeros
+          const __nv_bfloat16* stg = reinterpret_cast<const __nv_bfloat16*>(S.cstage[ew][sbuf]);
+          const int cc = lane >> 3, ce = lane & 7;  // logical chunk, element
+          float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            float x = __bfloat162float(stg[r * 32 + 8 * (cc ^ ((r >> 1) & 3)) + ce]);
+            s1[r & 3] += x;
+            s2[r & 3] = __fmaf_rn(x, x, s2[r & 3]);
+          }
+          acc_s[c] += (s1[0] + s1[1]) + (s1[2] + s1[3]);
+          acc_q[c] += (s2[0] + s2[1]) + (s2[2] + s2[3]);
+        }
+        sbuf ^= 1;
+      }
+      tc_fence_before();
+      mbar_arrive(&S.tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+    if (STATS) {
+      // lane l holds column part*BN/kParts + c*32 + l of this warp's 32 rows;
+      // one partial row per lane quarter, the parts fill disjoint columns
+      float* out = p.part + ((size_t)m_first * 4 + q) * 2 * p.N + (size_t)n_tile * BN + half * (BN / kParts);
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c) {
+        out[c * 32 + lane] = acc_s[c];
+        out[p.N + c * 32 + lane] = acc_q[c];
+      }
+    }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+}
+
+// per-channel mean / invstd from the partial rows: CTA = 32 channels, 32 warps
+// stride the rows (4 loads in flight each), then a fixed-order pass over the
+// warps in double (deterministic)
+__global__ void __launch_bounds__(1024) partials_finalize_kernel(const float* __restrict__ part, int rows_part, int N,
+                                                                 int64_t M, float eps, float* __restrict__ mean,
+                                                                 float* __restrict__ invstd) {
+  __shared__ double sh[2][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double s = 0, q = 0;
+  if (c < N) {
+    int r = w;
+    for (; r + 96 < rows_part; r += 128) {
+      float a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = part[(size_t)(r + 32 * u) * 2 * N + c];
+        b[u] = part[(size_t)(r + 32 * u) * 2 * N + N + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += (double)a[u];
+        q += (double)b[u];
+      }
+    }
+    for (; r < rows_part; r += 32) {
+      s += (double)part[(size_t)r * 2 * N + c];
+      q += (double)part[(size_t)r * 2 * N + N + c];
+    }
+  }
+  sh[0][w][lane] = s;
+  sh[1][w][lane] = q;
+  __syncthreads();
+  if (w != 0 || c >= N) return;
+  s = 0;
+  q = 0;
+  for (int k = 0; k < 32; ++k) {
+    s += sh[0][k][lane];
+    q += sh[1][k][lane];
+  }
+  const double mu = s / (double)M;
+  double var = q / (double)M - mu * mu;
+  if (var < 0) var = 0;
+  mean[c] = (float)mu;
+  invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
+}
+
+// ---------------------------------------------------------------------------
+// host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// [rows, cols] bf16 row-major, box [box_rows, box_cols]
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows, int box_cols,
+              CUtensorMapSwizzle sw) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+template <int BN, int STAGES, bool PRO, bool STATS>
+cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, int grid,
+                   cudaStream_t s) {
+  auto k = conv1x1_kernel<BN, STAGES, PRO, STATS>;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO>) + 1024;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k<<<grid, kThreads, smem, s>>>(ma, mb, mc, p);
+  return cudaGetLastError();
+}
+
+template <int BN, bool PRO, bool STATS>
+cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p,
+                            int grid, cudaStream_t s) {
+  // deepest ring that fits next to the barriers (227 KB per CTA)
+  constexpr int stage_bytes = (kBM + BN) * kBK * 2;
+  constexpr int avail = 220 * 1024 - (PRO ? 2 * kMaxProK * 4 : 0) - kEpiWarps * 2 * 32 * 64;
+  constexpr int stages = avail / stage_bytes > 8 ? 8 : avail / stage_bytes;
+  return launch<BN, stages, PRO, STATS>(ma, mb, mc, p, grid, s);
+}
+
+}  // namespace
+
+size_t conv1x1_partials_bytes(int N) { return (size_t)num_sms() * 4 * 2 * N * sizeof(float); }
+
+bool conv1x1_supported(int64_t M, int N, int K) {
+  return M > 0 && K >= kBK && K % kBK == 0 && K <= 65536 && (N == 64 || N == 128 || N % 256 == 0);
+}
+
+cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                             const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
+                             cudaStream_t s) {
+  if (!conv1x1_supported(M, N, K) || (pmean != nullptr && K > kMaxProK)) return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return cudaErrorMisalignedAddress;
+  const int BN = N <= 256 ? N : 256;
+  Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.BN = BN;
+  p.n_tiles = N / BN;
+  p.m_tiles = (int)((M + kBM - 1) / kBM);
+  p.C = static_cast<__nv_bfloat16*>(C);
+  p.part = part;
+  p.pmean = pmean;
+  p.pinvstd = pinvstd;
+  p.pg = static_cast<const __nv_bfloat16*>(pg);
+  p.pb = static_cast<const __nv_bfloat16*>(pb);
+  CUtensorMap ma, mb, mc;
+  if (!make_map(&ma, A, M, K, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mb, B, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorInvalidValue;
+  // whole n-tile groups, at most one CTA per SM and no more m-tiles than exist
+  int per = num_sms() / p.n_tiles;
+  if (per < 1) per = 1;
+  if (per > p.m_tiles) per = p.m_tiles;
+  const int grid = per * p.n_tiles;
+  if (part_rows) *part_rows = per * 4;  // every row and column written exactly once
+  const bool pro = pmean != nullptr, st = part != nullptr;
+#define KRT_GEMM_BN(BNV)                                                               \
+  if (BN == BNV) {                                                                     \
+    if (pro && st) return dispatch_stages<BNV, true, true>(ma, mb, mc, p, grid, s);   \
+    if (pro) return dispatch_stages<BNV, true, false>(ma, mb, mc, p, grid, s);        \
+    if (st) return dispatch_stages<BNV, false, true>(ma, mb, mc, p, grid, s);         \
+    return dispatch_stages<BNV, false, false>(ma, mb, mc, p, grid, s);                \
+  }
+  KRT_GEMM_BN(64)
+  KRT_GEMM_BN(128)
+  KRT_GEMM_BN(256)
+#undef KRT_GEMM_BN
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
+                                 float* invstd, cudaStream_t s) {
+  partials_finalize_kernel<<<(N + 31) / 32, 1024, 0, s>>>(part, part_rows, N, M, eps, mean, invstd);
+  return cudaGetLastError();
+}
+
+}  // namespace krt

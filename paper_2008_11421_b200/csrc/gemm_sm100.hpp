@@ -1,0 +1,16 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace krt {
+// tcgen05 1x1-convolution GEMM with fused BN prologue / statistics epilogue (gemm_sm100.cu)
+bool conv1x1_supported(int64_t M, int N, int K);
+size_t conv1x1_partials_bytes(int N);
+cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                             const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
+                             cudaStream_t s);
+cudaError_t bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
+                                 float* invstd, cudaStream_t s);
+}  // namespace krt

@@ -13,6 +13,7 @@ unit, ``mem_grad`` = its fp32 gradient bytes.
 from __future__ import annotations
 
 import math
+import os
 from typing import Optional
 
 import torch
@@ -90,6 +91,9 @@ def model_text(units, batch, analytic=False) -> str:
 # ---------------------------------------------------------------------------
 _aten = torch.ops.aten
 BN_EPS = 1e-5
+# bottleneck 1x1 convolutions on the own tcgen05 GEMM (csrc/gemm_sm100.cu) with
+# the BN work fused in; KRT_TC_CONV1X1=0 selects cuDNN + separate BN kernels
+TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
 
 
 def _cl(t):
@@ -296,6 +300,11 @@ class BottleneckUnit(_ConvNetUnit):
     def _fused(self):
         return self.act == torch.bfloat16 and all(bnfused.supported(c) for c in (self.w, self.cout))
 
+    def _tc1x1(self):
+        # both 1x1 convolutions (stride 1 in this bottleneck) fit the tcgen05 GEMM
+        return (self._fused() and TC_CONV1X1 and bnfused.conv1x1_supported(self.cin, self.w)
+                and bnfused.conv1x1_supported(self.w, self.cout, pre=True))
+
     def _forward_fused(self, x, params, saved, out=None):
         w1, g1, b1, w2, g2, b2, w3, g3, b3 = params[:9]
         if saved is not None:
@@ -304,20 +313,33 @@ class BottleneckUnit(_ConvNetUnit):
         else:
             st = self._stats_views(torch.empty(self._nstats(), device=x.device))
         sv = (lambda k: None) if saved is None else (lambda k: _cl(saved[k]))
-        c1 = _conv_into(x, _cl(w1), 1, 0, sv(1))
-        a1 = bnfused.stats_apply(c1, st[0], st[1], g1, b1, relu=True)
-        c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
-        del a1
-        a2 = bnfused.stats_apply(c2, st[2], st[3], g2, b2, relu=True)
-        c3 = _conv_into(a2, _cl(w3), 1, 0, sv(3))
-        del a2
+        if self._tc1x1():
+            # 1x1 convolutions on the tcgen05 GEMM: BN statistics of c1 and c3
+            # reduced in its epilogue, relu(bn2(c2)) applied in its prologue
+            c1 = bnfused.conv1x1(x, _cl(w1), out=sv(1), stats=(st[0], st[1]))
+            a1 = bnfused.apply(c1, st[0], st[1], g1, b1, relu=True)
+            c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
+            del a1
+            bnfused.stats(c2, st[2], st[3])
+            c3 = bnfused.conv1x1(c2, _cl(w3), out=sv(3), pre=(st[2], st[3], g2, b2), stats=(st[4], st[5]))
+        else:
+            c1 = _conv_into(x, _cl(w1), 1, 0, sv(1))
+            a1 = bnfused.stats_apply(c1, st[0], st[1], g1, b1, relu=True)
+            c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
+            del a1
+            a2 = bnfused.stats_apply(c2, st[2], st[3], g2, b2, relu=True)
+            c3 = _conv_into(a2, _cl(w3), 1, 0, sv(3))
+            del a2
         if self.down:
             wd, gd, bd = params[9:12]
-            bnfused.stats(c3, st[4], st[5])
+            if not self._tc1x1():
+                bnfused.stats(c3, st[4], st[5])
             cd = _conv_into(x, _cl(wd), self.s, 0, sv(4))
             bnfused.stats(cd, st[6], st[7])
             return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=cd, rstats=(st[6], st[7]),
                                  rg=gd, rb=bd, out=out)
+        if self._tc1x1():
+            return bnfused.apply(c3, st[4], st[5], g3, b3, relu=True, res=x, out=out)
         return bnfused.stats_apply(c3, st[4], st[5], g3, b3, relu=True, res=x, out=out)
 
     def _backward_fused(self, dy, params, saved, grads):

@@ -1,0 +1,63 @@
+"""tcgen05 1x1-convolution GEMM (csrc/gemm_sm100.cu) vs torch: the GEMM in fp32
+(tolerance: bf16 output rounding, one ulp = 2^-8 relative, plus fp32
+accumulation-order differences), the fused BN+ReLU prologue and the fused
+statistics epilogue (vs the stats kernel on the stored output: rtol 1e-4)."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2008_11421_b200 import bnfused
+
+pytestmark = pytest.mark.gpu
+
+
+def rand(shape, seed, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(*shape, device="cuda", generator=g) * scale).to(torch.bfloat16)
+
+
+def cl(t):
+    return t.contiguous(memory_format=torch.channels_last)
+
+
+@pytest.mark.parametrize("n,cin,cout,hw", [(2, 64, 64, 8), (4, 256, 64, 14), (2, 64, 256, 7), (3, 128, 512, 5),
+                                           (1, 512, 2048, 3), (2, 1024, 256, 6)])
+@pytest.mark.parametrize("pre", [False, True])
+def test_conv1x1_matches_torch(n, cin, cout, hw, pre):
+    x = cl(rand((n, cin, hw, hw), 1, 2.0))
+    w = cl(rand((cout, cin, 1, 1), 2, cin ** -0.5))
+    if pre:
+        g = (1 + 0.2 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+        b = (0.1 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+        m, i = torch.empty(cin, device="cuda"), torch.empty(cin, device="cuda")
+        bnfused.stats(x, m, i)
+        a = bnfused.apply(x, m, i, g, b, relu=True)   # what the prologue must reproduce
+        pre_t = (m, i, g, b)
+    else:
+        a, pre_t = x, None
+    sm, si = torch.empty(cout, device="cuda"), torch.empty(cout, device="cuda")
+    y = bnfused.conv1x1(x, w, pre=pre_t, stats=(sm, si))
+    torch.cuda.synchronize()
+    ref = F.conv2d(a.float(), w.float())
+    err = (y.float() - ref).abs().max() / ref.abs().max()
+    assert err < 1e-2, float(err)
+    # fused statistics == statistics of the stored bf16 output
+    rm, ri = torch.empty_like(sm), torch.empty_like(si)
+    bnfused.stats(y, rm, ri)
+    torch.testing.assert_close(sm, rm, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(si, ri, rtol=1e-4, atol=1e-5)
+    # deterministic
+    sm2, si2 = torch.empty_like(sm), torch.empty_like(si)
+    y2 = bnfused.conv1x1(x, w, pre=pre_t, stats=(sm2, si2))
+    assert torch.equal(y, y2) and torch.equal(sm, sm2) and torch.equal(si, si2)
+
+
+def test_conv1x1_ragged_rows_and_out():
+    """M not a multiple of the 128-row tile, output into a preallocated view."""
+    x = cl(rand((1, 128, 13, 11), 3))      # M = 143
+    w = cl(rand((256, 128, 1, 1), 4, 0.1))
+    out = torch.empty((1, 256, 13, 11), dtype=torch.bfloat16, device="cuda", memory_format=torch.channels_last)
+    y = bnfused.conv1x1(x, w, out=out)
+    assert y.data_ptr() == out.data_ptr()
+    ref = F.conv2d(x.float(), w.float())
+    assert ((y.float() - ref).abs().max() / ref.abs().max()) < 1e-2
