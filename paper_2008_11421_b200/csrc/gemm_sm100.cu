@@ -21,8 +21,8 @@
 //                 a quarter of the tile's columns: tcgen05.ld 32 columns at a time,
 //                 bf16 round, staged through shared memory and written by TMA
 //                 bulk stores; lane j then sums column j of the staged chunk
-//   warps 18..21  prologue only: transform each A stage in place (one tile row
-//                 per thread) between the TMA landing and the MMA
+//   warps 18..25  prologue only: transform each A stage in place (half a tile
+//                 row per thread) between the TMA landing and the MMA
 // Statistics are deterministic: fixed tile schedule, fixed summation order,
 // per-warp partial rows summed in double by bn_partials_finalize.
 #include <cuda.h>
@@ -43,8 +43,9 @@ constexpr int kBK = 64;        // k-block: 64 bf16 = one 128-byte swizzle row
 constexpr int kUmmaK = 16;     // K per tcgen05.mma (bf16)
 constexpr int kEpiWarps = 16;  // four per TMEM lane quarter, each a quarter of the columns
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kXfWarp0 = 2 + kEpiWarps;        // prologue transform warps (4: one row per thread)
-constexpr int kThreads = 64 + kEpiThreads + 128;  // producer, MMA, epilogue, transform
+constexpr int kXfWarp0 = 2 + kEpiWarps;        // prologue transform warps
+constexpr int kXfThreads = 256;                 // two threads per tile row, four 16-byte chunks each
+constexpr int kThreads = 64 + kEpiThreads + kXfThreads;  // producer, MMA, epilogue, transform
 constexpr int kEpiWarp0 = 2;
 constexpr int kMaxProK = 1024;  // prologue channels held in shared memory
 
@@ -176,7 +177,8 @@ struct Smem {
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
-  float sc[PRO ? kMaxProK : 1], sh[PRO ? kMaxProK : 1];
+  alignas(16) float sc[PRO ? kMaxProK : 4];
+  alignas(16) float sh[PRO ? kMaxProK : 4];
   // per-warp C staging for the TMA store: 32 rows x 64 B, SWIZZLE_64B (16-byte
   // chunk c of row r at c ^ ((r >> 1) & 3)), so row-per-lane writes and
   // column-per-lane reads are both free of bank conflicts
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.ready[s], 128);
+      mbar_init(&S.ready[s], kXfThreads);
       mbar_init(&S.empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -270,14 +272,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   } else if (warp >= kXfWarp0) {
     // ------------------------------------------------------------ prologue transform
     if (PRO) {
-      const int r = threadIdx.x - kXfWarp0 * 32;  // tile row 0..127
+      const int xt = threadIdx.x - kXfWarp0 * 32;  // 0..255
+      const int r = xt & 127, jh = 4 * (xt >> 7);  // tile row, first logical chunk
       // the previous BN's affine, exactly as bn_apply computes it
-      for (int c = r; c < p.K; c += 128) {
+      for (int c = xt; c < p.K; c += kXfThreads) {
         float sc = p.pinvstd[c] * __bfloat162float(p.pg[c]);
         S.sc[c] = sc;
         S.sh[c] = __bfloat162float(p.pb[c]) - p.pmean[c] * sc;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // transform warps only
+      asm volatile("bar.sync 1, %0;" ::"n"(kXfThreads) : "memory");  // transform warps only
       int stage = 0;
       uint32_t phase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
@@ -286,22 +289,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&S.full[stage], phase);
           uint4* rowp = reinterpret_cast<uint4*>(S.a[stage] + r * 128);
+          uint4 u[4];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            // logical chunk jj sits at physical chunk jj ^ (r & 7): consecutive
-            // rows hit different 16-byte columns (no bank conflicts)
-            const int j = jj ^ (r & 7);
-            const int c0 = kb * kBK + 8 * jj;
-            uint4 u = rowp[j];
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+          for (int i = 0; i < 4; ++i) u[i] = rowp[(jh + i) ^ (r & 7)];  // consecutive rows: distinct columns
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c0 = kb * kBK + 8 * (jh + i);
+            const float4 sa = *reinterpret_cast<const float4*>(&S.sc[c0]);
+            const float4 sb = *reinterpret_cast<const float4*>(&S.sc[c0 + 4]);
+            const float4 ha = *reinterpret_cast<const float4*>(&S.sh[c0]);
+            const float4 hb = *reinterpret_cast<const float4*>(&S.sh[c0 + 4]);
+            const float sc[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+            const float sh[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u[i]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               float2 f = __bfloat1622float2(h[e]);
-              const int c = c0 + 2 * e;
-              h[e] = __floats2bfloat162_rn(fmaxf(__fmaf_rn(f.x, S.sc[c], S.sh[c]), 0.f),
-                                           fmaxf(__fmaf_rn(f.y, S.sc[c + 1], S.sh[c + 1]), 0.f));
+              h[e] = __floats2bfloat162_rn(fmaxf(__fmaf_rn(f.x, sc[2 * e], sh[2 * e]), 0.f),
+                                           fmaxf(__fmaf_rn(f.y, sc[2 * e + 1], sh[2 * e + 1]), 0.f));
             }
-            rowp[j] = u;
+            rowp[(jh + i) ^ (r & 7)] = u[i];
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
           mbar_arrive(&S.ready[stage]);
