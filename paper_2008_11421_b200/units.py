@@ -833,7 +833,10 @@ def _ln_fw(x, g, b, mean, rstd):
 
 
 def _ln_apply(x, g, b, mean, rstd):
-    return ((x.float() - mean.view(-1, 1)) * rstd.view(-1, 1) * g.float() + b.float()).to(x.dtype)
+    """The forward's LayerNorm output again: one native_layer_norm pass (its
+    statistics are recomputed bit-identically from the same input), instead
+    of an fp32 formula that materialised four [T, H] fp32 temporaries."""
+    return _aten.native_layer_norm(x, [x.shape[-1]], g, b, LN_EPS)[0]
 
 
 def _ln_bw(dy, x, g, b, mean, rstd, dg, db):
@@ -844,17 +847,24 @@ def _ln_bw(dy, x, g, b, mean, rstd, dg, db):
     return dx
 
 
-def _linear(x, w, b):
-    return torch.addmm(b, x, w.t())
+def _linear(x, w, b, out=None):
+    return torch.addmm(b, x, w.t(), out=out) if out is not None else torch.addmm(b, x, w.t())
+
+
+def _mm_f32_into(a, b, out):
+    """out (fp32) = a @ b: cuBLAS writes fp32 straight into the gradient region."""
+    if a.dtype == torch.float32:
+        torch.mm(a, b, out=out)
+    elif a.is_cuda:
+        torch.mm(a, b, out_dtype=torch.float32, out=out)
+    else:
+        out.copy_(torch.mm(a, b).float())
 
 
 def _linear_bw(dy, x, w, gw, gb, need_dx=True):
     """y = x W^T + b: writes fp32 dW, db; returns dx."""
-    if dy.dtype == torch.float32:
-        torch.mm(dy.t(), x, out=gw)
-    else:
-        gw.copy_(torch.mm(dy.t(), x, out_dtype=torch.float32))
-    gb.copy_(dy.float().sum(0))
+    _mm_f32_into(dy.t(), x, gw)
+    torch.sum(dy, 0, dtype=torch.float32, out=gb)   # fp32 accumulation, no fp32 copy of dy
     return torch.mm(dy, w) if need_dx else None
 
 
@@ -982,22 +992,20 @@ class TransformerLayerUnit(Unit):
             m1, r1, m2, r2 = st[:t], st[t:2 * t], st[2 * t:3 * t], st[3 * t:]
         else:
             m1 = r1 = m2 = r2 = None
+        sv = (lambda k: None) if saved is None else (lambda k: saved[k])
         h1, _, _ = _ln_fw(x, g1, b1, m1, r1)
-        qkv = _linear(h1, wqkv, bqkv)
+        qkv = _linear(h1, wqkv, bqkv, out=sv(1))          # GEMMs write straight into the saved slots
         del h1
         o = self._attn_fw(qkv, saved[6] if (saved is not None and self._flash()) else None)
-        x2 = x + _linear(o, wo, bo)
+        if saved is not None:
+            saved[2].copy_(o)
+        x2 = torch.add(x, _linear(o, wo, bo), out=sv(3)) if saved is not None else x + _linear(o, wo, bo)
         h2, _, _ = _ln_fw(x2, g2, b2, m2, r2)
-        f1 = _linear(h2, w1, bf1)
+        f1 = _linear(h2, w1, bf1, out=sv(4))
         del h2
         mlp = _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
         y = torch.add(x2, mlp, out=out) if out is not None else x2 + mlp
         del mlp
-        if saved is not None:
-            saved[1].copy_(qkv)
-            saved[2].copy_(o)
-            saved[3].copy_(x2)
-            saved[4].copy_(f1)
         return y
 
     def saved_input(self, saved):
@@ -1072,10 +1080,7 @@ class LMHeadUnit(Unit):
         t = x.shape[0]
         m, r = st[:t], st[t:]
         h = _ln_apply(x, g, b, m, r)
-        if dlogits.dtype == torch.float32:
-            torch.mm(dlogits.t(), h, out=grads[2])
-        else:
-            grads[2].copy_(torch.mm(dlogits.t(), h, out_dtype=torch.float32))
+        _mm_f32_into(dlogits.t(), h, grads[2])
         dh = torch.mm(dlogits, w)
         return _ln_bw(dh, x, g, b, m, r, grads[0], grads[1])
 
