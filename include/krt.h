@@ -261,10 +261,11 @@ int krt_bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const fl
                         const float* rinvstd, const void* rgamma, const void* rbeta, void* dz,
                         int64_t rows, int C, void* stream);
 /* BN backward with the optional ReLU mask recomputed from x: dgamma/dbeta (fp32,
- * may be NULL) and dx (bf16, may be NULL) */
+ * may be NULL) and dx (bf16, may be NULL); addend (may be NULL) is a residual
+ * gradient added to dx before its single bf16 rounding */
 int krt_bn_backward(const void* dy, const void* x, const float* mean, const float* invstd,
                     const void* gamma, const void* beta, int relu, void* dx, float* dgamma,
-                    float* dbeta, int64_t rows, int C, void* ws, void* stream);
+                    float* dbeta, int64_t rows, int C, void* ws, const void* addend, void* stream);
 /* krt_bn_add_relu_bwd (identity residual) and krt_bn_backward (no ReLU) of the
  * same BN in one kernel: dz = (dy [+ dy2]) * (bn(x) + res > 0) is written and
  * reduced in the same pass, then dx.  dz and dx required; dgamma/dbeta may be

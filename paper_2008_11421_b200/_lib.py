@@ -112,7 +112,7 @@ EXPORTS = {
     "krt_bn_apply": (C.c_int, [C.c_void_p] * 10 + [C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),
     "krt_bn_add_relu_bwd": (C.c_int, [C.c_void_p] * 13 + [C.c_int64, C.c_int, C.c_void_p]),
     "krt_bn_backward": (C.c_int, [C.c_void_p] * 6 + [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
-                                                   C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
+                                                   C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "krt_host_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_int, C.c_size_t, C.c_int, C.c_float, C.c_float, C.c_float,
                                   C.c_float, C.c_float, C.c_float, C.c_int, C.c_int]),

@@ -114,16 +114,20 @@ def add_relu_bwd(dy, c, mean, invstd, g, b, res, rstats=None, rg=None, rb=None, 
     return dz
 
 
-def backward(dy, c, mean, invstd, g, b, relu, dgamma=None, dbeta=None, need_dx=True):
-    """BN backward (ReLU mask recomputed from c when relu); dgamma/dbeta fp32 outputs."""
+def backward(dy, c, mean, invstd, g, b, relu, dgamma=None, dbeta=None, need_dx=True, addend=None):
+    """BN backward (ReLU mask recomputed from c when relu); dgamma/dbeta fp32
+    outputs; addend (a residual gradient) is summed into dx in the same pass."""
     c, dy = _nhwc(c), _nhwc(dy)
+    if addend is not None:
+        addend = _nhwc(addend)
     rows, C = _rows_c(c)
     dx = torch.empty_like(c, memory_format=torch.channels_last) if need_dx else None
     ws = _ws(C, c.device)
-    with _timed("bn_backward", rows * C * 2 * (5 if need_dx else 2)):
+    nb = rows * C * 2 * ((5 if need_dx else 2) + (1 if addend is not None else 0))
+    with _timed("bn_backward", nb):
         _lib.check(_lib.lib().krt_bn_backward(dy.data_ptr(), c.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
-                                          g.data_ptr(), b.data_ptr(), int(relu), _ptr(dx), _ptr(dgamma),
-                                          _ptr(dbeta), rows, C, ws.data_ptr(), _stream()))
+                                              g.data_ptr(), b.data_ptr(), int(relu), _ptr(dx), _ptr(dgamma),
+                                              _ptr(dbeta), rows, C, ws.data_ptr(), _ptr(addend), _stream()))
     return dx
 
 

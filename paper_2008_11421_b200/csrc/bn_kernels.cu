@@ -532,12 +532,15 @@ __global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
   bwd_finalize(part, rows, C, mean, invstd, g, dgamma, dbeta, coef, reinterpret_cast<double*>(smem));
 }
 
-// dx = A*gm + B*x + D with gm = dy * mask (coefficients from the reduce)
-template <bool RELU>
+// dx = A*gm + B*x + D [+ addend] with gm = dy * mask (coefficients from the
+// reduce); the optional addend (a residual gradient) is summed before the one
+// bf16 rounding, so no separate add pass re-reads dx
+template <bool RELU, bool ADD>
 __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
-    const float* __restrict__ coef, __nv_bfloat16* __restrict__ dx, int64_t rows, int C) {
+    const float* __restrict__ coef, const __nv_bfloat16* __restrict__ addend, __nv_bfloat16* __restrict__ dx,
+    int64_t rows, int C) {
   Map m(C);
   Rows rw(m, rows);
   const int c0 = m.tx * 8;
@@ -550,19 +553,28 @@ __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     k.d[j] = coef[2 * C + c0 + j];
   }
   for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) {
-    uint4 v[kU], d[kU];
+    uint4 v[kU], d[kU], e[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int64_t r = r0 + u * rw.step;
       if (r < rows) {
         v[u] = ld16s(x + r * C + c0);
         d[u] = ld16s(dy + r * C + c0);
+        if (ADD) e[u] = ld16s(addend + r * C + c0);
       }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int64_t r = r0 + u * rw.step;
-      if (r < rows) st16(dx + r * C + c0, bwd_row<RELU>(unpack(v[u]), unpack(d[u]), k));
+      if (r < rows) {
+        Vec8 o = bwd_row<RELU>(unpack(v[u]), unpack(d[u]), k);
+        if (ADD) {
+          Vec8 a = unpack(e[u]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o.v[j] = __fadd_rn(o.v[j], a.v[j]);
+        }
+        st16(dx + r * C + c0, o);
+      }
     }
   }
 }
@@ -654,13 +666,19 @@ inline const bf16* B(const void* p) { return static_cast<const bf16*>(p); }
 inline bf16* BW_(void* p) { return static_cast<bf16*>(p); }
 
 cudaError_t bwd_elemt(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
-                      const void* b, const float* coef, void* dx, int64_t rows, int C, int relu, cudaStream_t s) {
+                      const void* b, const float* coef, const void* addend, void* dx, int64_t rows, int C, int relu,
+                      cudaStream_t s) {
   auto go = [&](auto kernel) {
-    kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(B(dy), B(x), mean, invstd, B(g), B(b), coef, BW_(dx),
-                                                              rows, C);
+    kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(B(dy), B(x), mean, invstd, B(g), B(b), coef,
+                                                              B(addend), BW_(dx), rows, C);
   };
-  if (relu) go(bwd_elemt_kernel<true>);
-  else go(bwd_elemt_kernel<false>);
+  if (addend) {
+    if (relu) go(bwd_elemt_kernel<true, true>);
+    else go(bwd_elemt_kernel<false, true>);
+  } else {
+    if (relu) go(bwd_elemt_kernel<true, false>);
+    else go(bwd_elemt_kernel<false, false>);
+  }
   return cudaGetLastError();
 }
 
@@ -717,7 +735,7 @@ cudaError_t bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, cons
 
 cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
                         const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
-                        void* ws, cudaStream_t s) {
+                        void* ws, const void* addend, cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
   float* part = static_cast<float*>(ws);
   float* coef = part + (size_t)kMaxGrid * 2 * C;
@@ -726,7 +744,7 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
   };
   cudaError_t e = relu ? red(bwd_reduce_kernel<true>) : red(bwd_reduce_kernel<false>);
   if (e != cudaSuccess || dx == nullptr) return e;
-  return bwd_elemt(dy, x, mean, invstd, g, b, coef, dx, rows, C, relu, s);
+  return bwd_elemt(dy, x, mean, invstd, g, b, coef, addend, dx, rows, C, relu, s);
 }
 
 cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean,
@@ -742,7 +760,7 @@ cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x,
   };
   cudaError_t e = dy2 ? red(add_relu_reduce_kernel<true>) : red(add_relu_reduce_kernel<false>);
   if (e != cudaSuccess) return e;
-  return bwd_elemt(dz, x, mean, invstd, g, b, coef, dx, rows, C, 0, s);
+  return bwd_elemt(dz, x, mean, invstd, g, b, coef, nullptr, dx, rows, C, 0, s);
 }
 
 }  // namespace krt

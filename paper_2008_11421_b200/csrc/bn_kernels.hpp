@@ -19,7 +19,7 @@ cudaError_t bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, cons
                             const void* rg, const void* rb, void* dz, int64_t rows, int C, cudaStream_t s);
 cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
                         const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C,
-                        void* ws, cudaStream_t s);
+                        void* ws, const void* addend, cudaStream_t s);
 cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean,
                                  const float* invstd, const void* g, const void* b, const void* res, void* dz,
                                  void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,

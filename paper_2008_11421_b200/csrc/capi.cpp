@@ -424,8 +424,9 @@ int krt_bn_add_relu_bwd(const void* dy, const void* dy2, const void* x, const fl
 
 int krt_bn_backward(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
                     const void* b, int relu, void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
-                    void* stream) {
-  KRT_CUDA_GUARD(bn_backward(dy, x, mean, invstd, g, b, relu, dx, dgamma, dbeta, rows, C, ws, (cudaStream_t)stream),
+                    const void* addend, void* stream) {
+  KRT_CUDA_GUARD(bn_backward(dy, x, mean, invstd, g, b, relu, dx, dgamma, dbeta, rows, C, ws, addend,
+                             (cudaStream_t)stream),
                  "bn_backward");
 }
 

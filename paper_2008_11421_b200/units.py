@@ -585,16 +585,17 @@ def _bn_relu(c, m, i, g, b):
     return _bn_apply(c, g, b, m, i).relu_()
 
 
-def _bn_relu_bw(da, c, m, i, g, b, dg, db):
-    """Backward through relu(bn(c)) given d(relu output); writes dgamma/dbeta."""
+def _bn_relu_bw(da, c, m, i, g, b, dg, db, addend=None):
+    """Backward through relu(bn(c)) given d(relu output); writes dgamma/dbeta.
+    addend: a residual gradient summed into the result (fused for bf16)."""
     if c.dtype == torch.bfloat16 and bnfused.supported(c.shape[1]):
-        return bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=dg, dbeta=db)
+        return bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=dg, dbeta=db, addend=addend)
     a = _bn_apply(c, g, b, m, i).relu_()
     dpre = _aten.threshold_backward(da, a, 0)
     dc, dgg, dbb = _bn_bw(dpre, c, g, m, i)
     dg.copy_(dgg)
     db.copy_(dbb)
-    return dc
+    return dc if addend is None else dc.add_(addend)
 
 
 class PreActBottleneckUnit(_ConvNetUnit):
@@ -689,9 +690,8 @@ class PreActBottleneckUnit(_ConvNetUnit):
             _cl(grads[9]).copy_(dws)
             da0.add_(das)
             dx = _bn_relu_bw(da0, x, st[0], st[1], g0, b0, grads[0], grads[1])
-        else:
-            dx = _bn_relu_bw(da0, x, st[0], st[1], g0, b0, grads[0], grads[1])
-            dx.add_(dy)
+        else:   # identity shortcut: its gradient dy is added inside the BN backward pass
+            dx = _bn_relu_bw(da0, x, st[0], st[1], g0, b0, grads[0], grads[1], addend=dy)
         return dx
 
     def fwd_flops(self, n):

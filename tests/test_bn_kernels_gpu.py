@@ -210,3 +210,19 @@ def test_relu_maxpool_matches_aten_bitwise(shape, ksp):
     da_ref = torch.ops.aten.max_pool2d_with_indices_backward(dy, a, [k, k], [s, s], [p, p], [1, 1], False, idx)
     da = bnfused.relu_maxpool_backward(dy, x, m, i, g, b, k, s, p)
     assert torch.equal(da, da_ref)
+
+
+def test_backward_with_addend():
+    """bn backward + residual-gradient addend in one pass == backward then add,
+    within one bf16 rounding (the fused version rounds once)."""
+    shape = (4, 64, 16, 16)
+    x, dy, r = rand(*shape, seed=71), rand(*shape, seed=72), rand(*shape, seed=73)
+    g, b = params(64, seed=74)
+    m, i = torch.empty(64, device="cuda"), torch.empty(64, device="cuda")
+    bnfused.stats(x, m, i)
+    dg, db = torch.empty(64, device="cuda"), torch.empty(64, device="cuda")
+    dx = bnfused.backward(dy, x, m, i, g, b, relu=True, dgamma=dg, dbeta=db, addend=r)
+    dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+    ref = bnfused.backward(dy, x, m, i, g, b, relu=True, dgamma=dg2, dbeta=db2).float() + r.float()
+    assert torch.equal(dg, dg2) and torch.equal(db, db2)
+    torch.testing.assert_close(dx.float(), ref, **BF16_TOL)
