@@ -173,6 +173,112 @@ __global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(
   }
 }
 
+// Shared-memory tiled variant for the ResNet stem (k 3, s 2, p 1, C 64): a CTA
+// owns an 8 x 8 block of output pixels of one image; the 17 x 17 input patch
+// is loaded once with coalesced 16-byte loads, activated once (the windows
+// overlap 2.25x) and kept in shared memory with a padded pixel stride; padding
+// positions hold -inf, which never wins the scan (the window centre is always
+// inside the image and relu output is >= 0), so argmax offsets are unchanged.
+constexpr int kTile = 8, kPatch = 2 * kTile + 1, kTC = 64, kPixStride = kTC + 8;  // bf16 elements
+
+template <bool ARGMAX>
+__global__ void __launch_bounds__(kThreads) stem_pool_tiled_kernel(
+    const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ invstd,
+    const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y,
+    uint8_t* __restrict__ arg_out, Pool P) {
+  __shared__ alignas(16) __nv_bfloat16 patch[kPatch * kPatch * kPixStride];
+  const int tiles_w = (P.ow + kTile - 1) / kTile, tiles_h = (P.oh + kTile - 1) / kTile;
+  const int tw = blockIdx.x % tiles_w, th = (blockIdx.x / tiles_w) % tiles_h, n = blockIdx.x / (tiles_w * tiles_h);
+  const int oh0 = th * kTile, ow0 = tw * kTile;
+  const int ih0 = oh0 * 2 - 1, iw0 = ow0 * 2 - 1;
+  // phase 1: patch load + activation (octet = threadIdx & 7 is fixed per thread)
+  const int oct = threadIdx.x & 7;
+  float sc[8], sh[8];
+  coeffs(mean, invstd, g, b, oct * 8, sc, sh);
+  const __nv_bfloat16* xb = x + (int64_t)n * P.h * P.w * kTC;
+  constexpr int kPer = (kPatch * kPatch + kThreads / 8 - 1) / (kThreads / 8);  // patch pixels per thread
+  uint4 raw[kPer];
+  bool ok[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {  // all loads in flight before any use
+    const int q = (threadIdx.x >> 3) + i * (kThreads / 8);
+    const int pr = q / kPatch, pc = q % kPatch;
+    const int ih = ih0 + pr, iw = iw0 + pc;
+    ok[i] = q < kPatch * kPatch && ih >= 0 && ih < P.h && iw >= 0 && iw < P.w;
+    if (ok[i]) raw[i] = __ldg(reinterpret_cast<const uint4*>(xb + ((int64_t)ih * P.w + iw) * kTC + oct * 8));
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int q = (threadIdx.x >> 3) + i * (kThreads / 8);
+    if (q >= kPatch * kPatch) break;
+    uint4 u;
+    __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+    if (ok[i]) {
+      const __nv_bfloat162* rv = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(rv[e]);
+        hv[e] = __floats2bfloat162_rn(act(f.x, sc[2 * e], sh[2 * e]), act(f.y, sc[2 * e + 1], sh[2 * e + 1]));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hv[e] = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    }
+    *reinterpret_cast<uint4*>(patch + q * kPixStride + oct * 8) = u;
+  }
+  __syncthreads();
+  // phase 2: one output octet per thread and pass (8 x 8 pixels x 8 octets = 2 passes)
+  for (int t = threadIdx.x; t < kTile * kTile * 8; t += kThreads) {
+    const int o8 = t & 7, op = t >> 3;
+    const int lr = op / kTile, lc = op % kTile;
+    const int oh = oh0 + lr, ow = ow0 + lc;
+    if (oh >= P.oh || ow >= P.ow) continue;
+    float mx[8];
+    int am[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      mx[j] = -INFINITY;
+      am[j] = -1;
+    }
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        const uint4 u = *reinterpret_cast<const uint4*>(patch + ((2 * lr + kh) * kPatch + 2 * lc + kw) * kPixStride + o8 * 8);
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float2 f = __bfloat1622float2(hv[j / 2]);
+          float a = j & 1 ? f.y : f.x;
+          if (a > mx[j] || isnan(a)) {
+            mx[j] = a;
+            am[j] = kh * 3 + kw;
+          }
+        }
+      }
+    }
+    const int64_t o = (((int64_t)n * P.oh + oh) * P.ow + ow) * kTC + o8 * 8;
+    if (ARGMAX) {
+      uint2 packed;
+      packed.x = (uint32_t)am[0] | ((uint32_t)am[1] << 8) | ((uint32_t)am[2] << 16) | ((uint32_t)am[3] << 24);
+      packed.y = (uint32_t)am[4] | ((uint32_t)am[5] << 8) | ((uint32_t)am[6] << 16) | ((uint32_t)am[7] << 24);
+      *reinterpret_cast<uint2*>(arg_out + o) = packed;
+    } else {
+      uint4 u;
+      __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hv[e] = __floats2bfloat162_rn(mx[2 * e], mx[2 * e + 1]);
+      *reinterpret_cast<uint4*>(y + o) = u;
+    }
+  }
+}
+
+bool stem_tiled(const Pool& P) { return P.k == 3 && P.s == 2 && P.p == 1 && P.c == kTC; }
+
+int stem_tiles(const Pool& P) {
+  return P.n * ((P.oh + kTile - 1) / kTile) * ((P.ow + kTile - 1) / kTile);
+}
+
 // phase 2: gather, per input pixel, the output gradients of the windows whose
 // argmax it is (aten's max_pool_backward_nhwc order and fp32 accumulation)
 __global__ void __launch_bounds__(kThreads) maxpool_bwd_gather_kernel(const __nv_bfloat16* __restrict__ dy,
@@ -247,6 +353,56 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_gather_kernel(const __nv
   }
 }
 
+// the stem's gather (k 3, s 2, p 1, C 64; fewer than 2^31 threads): 32-bit
+// index math with constant divisors, the same (oh, ow) scan order and fp32 sums
+__global__ void __launch_bounds__(kThreads) stem_gather_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                               const uint8_t* __restrict__ arg,
+                                                               __nv_bfloat16* __restrict__ dx, Pool P) {
+  const uint32_t total = (uint32_t)P.n * P.h * P.w * 8;
+  for (uint32_t t = blockIdx.x * kThreads + threadIdx.x; t < total; t += gridDim.x * kThreads) {
+    const uint32_t oct = t & 7, pix = t >> 3;
+    const int iw = (int)(pix % (uint32_t)P.w);
+    const uint32_t rest = pix / (uint32_t)P.w;
+    const int ih = (int)(rest % (uint32_t)P.h);
+    const uint32_t n = rest / (uint32_t)P.h;
+    const int phs = ih >= 2 ? ih >> 1 : 0, phe = min(((ih + 1) >> 1) + 1, P.oh);
+    const int pws = iw >= 2 ? iw >> 1 : 0, pwe = min(((iw + 1) >> 1) + 1, P.ow);
+    uint2 a[4];
+    uint4 d[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int oh = phs + (q >> 1), ow = pws + (q & 1);
+      ok[q] = oh < phe && ow < pwe;
+      if (ok[q]) {
+        const uint32_t o = ((n * P.oh + oh) * P.ow + ow) * 64 + oct * 8;
+        a[q] = __ldg(reinterpret_cast<const uint2*>(arg + o));
+        d[q] = __ldg(reinterpret_cast<const uint4*>(dy + o));
+      }
+    }
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!ok[q]) continue;
+      const int oh = phs + (q >> 1), ow = pws + (q & 1);
+      const int me = (ih - 2 * oh + 1) * 3 + (iw - 2 * ow + 1);
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&d[q]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t word = j < 4 ? a[q].x : a[q].y;
+        const int sel = (int)((word >> (8 * (j & 3))) & 0xff);
+        float2 tv = __bfloat1622float2(hv[j / 2]);
+        if (sel == me) acc[j] += j & 1 ? tv.y : tv.x;
+      }
+    }
+    uint4 u;
+    __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hv[k] = __floats2bfloat162_rn(acc[2 * k], acc[2 * k + 1]);
+    *reinterpret_cast<uint4*>(dx + (size_t)t * 8) = u;
+  }
+}
+
 int grid_for(int64_t total) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -268,6 +424,12 @@ cudaError_t bn_relu_maxpool(const void* x, const float* mean, const float* invst
   Pool P{n, h, w, c, (h + 2 * p - k) / s + 1, (w + 2 * p - k) / s + 1, k, s, p};
   if (!pool_ok(P)) return cudaErrorInvalidValue;
   const int64_t total = (int64_t)n * P.oh * P.ow * (c / 8);
+  if (stem_tiled(P)) {
+    stem_pool_tiled_kernel<false><<<stem_tiles(P), kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), mean, invstd, static_cast<const __nv_bfloat16*>(g),
+        static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(y), nullptr, P);
+    return cudaGetLastError();
+  }
   auto go = [&](auto kernel) {
     kernel<<<grid_for(total), kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(x), mean, invstd,
                                                   static_cast<const __nv_bfloat16*>(g),
@@ -296,11 +458,19 @@ cudaError_t bn_relu_maxpool_bwd(const void* dy, const void* x, const float* mean
                                                  static_cast<const __nv_bfloat16*>(g),
                                                  static_cast<const __nv_bfloat16*>(b), arg, P);
   };
-  if (k == 3) go(maxpool_argmax_kernel<3>);
+  if (stem_tiled(P))
+    stem_pool_tiled_kernel<true><<<stem_tiles(P), kThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), mean, invstd, static_cast<const __nv_bfloat16*>(g),
+        static_cast<const __nv_bfloat16*>(b), nullptr, arg, P);
+  else if (k == 3) go(maxpool_argmax_kernel<3>);
   else go(maxpool_argmax_kernel<0>);
   const int64_t ins = (int64_t)n * h * w * (c / 8);
-  maxpool_bwd_gather_kernel<<<grid_for(ins), kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), arg,
-                                                                 static_cast<__nv_bfloat16*>(dx), P);
+  if (stem_tiled(P) && ins < (int64_t(1) << 31))
+    stem_gather_kernel<<<grid_for(ins), kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), arg,
+                                                           static_cast<__nv_bfloat16*>(dx), P);
+  else
+    maxpool_bwd_gather_kernel<<<grid_for(ins), kThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(dy), arg,
+                                                                   static_cast<__nv_bfloat16*>(dx), P);
   return cudaGetLastError();
 }
 

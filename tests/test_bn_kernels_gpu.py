@@ -189,7 +189,7 @@ def test_backward_no_dx_and_tiny_rows():
         torch.testing.assert_close(db, db2, rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("shape,ksp", [((4, 64, 112, 112), (3, 2, 1)), ((3, 16, 9, 7), (3, 2, 1)),
+@pytest.mark.parametrize("shape,ksp", [((4, 64, 112, 112), (3, 2, 1)), ((3, 16, 9, 7), (3, 2, 1)), ((2, 64, 13, 11), (3, 2, 1)),
                                        ((2, 8, 6, 6), (2, 2, 0)), ((2, 32, 11, 13), (3, 1, 1)), ((2, 64, 10, 10), (5, 3, 2))])
 def test_relu_maxpool_matches_aten_bitwise(shape, ksp):
     """maxpool(relu(bn(c))) fused, forward and backward, == apply -> aten
