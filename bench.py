@@ -335,13 +335,19 @@ def run_gpu(args, rec):
     retries0 = torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)
     barrier()
     t0 = time.perf_counter()
-    e2e_marks = []
+    e2e_marks, issue_marks = [], []
+    prev = None
     for _ in range(e2e_steps):
         xd = xh.to(dev, non_blocking=True)
         yd = yh.to(dev, non_blocking=True)
         loss = ex.step(xd, yd)
-        float(loss)    # D2H of the step's loss
-        e2e_marks.append(time.perf_counter() - t0)
+        issue_marks.append(time.perf_counter() - t0)
+        if prev is not None:
+            float(prev)    # D2H of the previous step's loss, read once this step is queued
+            e2e_marks.append(time.perf_counter() - t0)
+        prev = loss
+    float(prev)            # and the last step's
+    e2e_marks.append(time.perf_counter() - t0)
     ex.synchronize()
     barrier()
     e2e_s = time.perf_counter() - t0
@@ -452,7 +458,10 @@ def run_gpu(args, rec):
                     "swap_out_busy_s": sum(b - a for a, b in xout)},
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_in,
                 "d2h_bytes_per_step": 4, "steps": e2e_steps,
-                "loss_ready_s": [round(t, 4) for t in e2e_marks], "total_s": round(e2e_s, 4),
+                "loss_read_s": [round(t, 4) for t in e2e_marks], "issued_s": [round(t, 4) for t in issue_marks],
+                "total_s": round(e2e_s, 4),
+                "note": "every step: pinned H2D of its inputs, issue, then D2H read of the previous step's loss "
+                        "(the last loss read after the loop)",
                 "alloc_retries": e2e_retries},
         "gpu_launches": launches + sum(v[2] for v in fam.values()) * args.steps,
         "runtime": {k: st[k] for k in ("arena_bytes", "ledger_peak_bytes", "host_swap_bytes",

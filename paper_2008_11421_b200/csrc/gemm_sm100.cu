@@ -170,12 +170,20 @@ struct Params {
   const __nv_bfloat16* pb;
 };
 
-template <int BN, int STAGES, bool PRO>
+// ASTAT (A-stationary, prologue only, K <= kMaxAstatK): the transformed A tile
+// of an m-tile stays in shared memory while the CTA walks all n-tiles, so the
+// relu(bn(.)) transform and the A loads happen once per m-tile instead of once
+// per (m, n) tile; the ring then carries B k-blocks only.
+constexpr int kMaxAstatK = 256;
+constexpr int kMaxNT = 8;  // n-tiles per CTA in A-stationary mode (N <= 2048)
+
+template <int BN, int STAGES, bool PRO, bool ASTAT>
 struct Smem {
-  alignas(1024) uint8_t a[STAGES][kBM * kBK * 2];
+  alignas(1024) uint8_t a[ASTAT ? kMaxAstatK / kBK : STAGES][kBM * kBK * 2];
   alignas(1024) uint8_t b[STAGES][BN * kBK * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
   uint64_t tfull[2], tempty[2];
+  uint64_t a_full[kMaxAstatK / kBK], a_ready[kMaxAstatK / kBK], a_free[kMaxAstatK / kBK];  // A-stationary, per k-block
   uint32_t tmem_base;
   alignas(16) float sc[PRO ? kMaxProK : 4];
   alignas(16) float sh[PRO ? kMaxProK : 4];
@@ -185,18 +193,21 @@ struct Smem {
   alignas(1024) uint8_t cstage[kEpiWarps][2][32 * 64];
 };
 
-template <int BN, int STAGES, bool PRO, bool STATS>
+template <int BN, int STAGES, bool PRO, bool STATS, bool ASTAT>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c, Params p) {
   extern __shared__ uint8_t smem_raw[];
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO>*>(
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblocks = p.K / kBK;
-  // this CTA's tiles: fixed n-tile, m-tiles strided (grid is a multiple of n_tiles)
-  const int n_tile = blockIdx.x % p.n_tiles;
-  const int m_first = blockIdx.x / p.n_tiles, m_step = gridDim.x / p.n_tiles;
+  // this CTA's tiles: m-tiles strided; either a fixed n-tile (grid is a
+  // multiple of n_tiles) or, A-stationary, every n-tile of each m-tile
+  const int nts = ASTAT ? p.n_tiles : 1;
+  const int n_fixed = ASTAT ? 0 : blockIdx.x % p.n_tiles;
+  const int m_first = ASTAT ? blockIdx.x : blockIdx.x / p.n_tiles;
+  const int m_step = ASTAT ? gridDim.x : gridDim.x / p.n_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -207,6 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.tfull[i], 1);
       mbar_init(&S.tempty[i], 128 * (BN >= 128 ? 4 : BN / 32));  // active epilogue threads
+    }
+    for (int kb = 0; kb < kMaxAstatK / kBK; ++kb) {
+      mbar_init(&S.a_full[kb], 1);
+      mbar_init(&S.a_ready[kb], kXfThreads);
+      mbar_init(&S.a_free[kb], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -220,16 +236,31 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, aphase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&S.empty[stage], phase ^ 1);
-          mbar_expect_tx(&S.full[stage], (kBM + BN) * kBK * 2);
-          tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * kBK, mt * kBM);
-          tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * kBK, n_tile * BN);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+        if (ASTAT) {  // this m-tile's A k-blocks, each once the previous m-tile's last MMA on it is done
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&S.a_free[kb], aphase ^ 1);
+            mbar_expect_tx(&S.a_full[kb], kBM * kBK * 2);
+            tma_load_2d(&map_a, &S.a_full[kb], S.a[kb], kb * kBK, mt * kBM);
+          }
+          aphase ^= 1;
+        }
+        for (int nt = 0; nt < nts; ++nt) {
+          const int n_tile = ASTAT ? nt : n_fixed;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            mbar_wait(&S.empty[stage], phase ^ 1);
+            if (ASTAT) {
+              mbar_expect_tx(&S.full[stage], BN * kBK * 2);
+            } else {
+              mbar_expect_tx(&S.full[stage], (kBM + BN) * kBK * 2);
+              tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * kBK, mt * kBM);
+            }
+            tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * kBK, n_tile * BN);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -238,36 +269,41 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = instr_desc(BN);
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, aphase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
-      mbar_wait(&S.tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
-      tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * BN;
-      for (int kb = 0; kb < kblocks; ++kb) {
-        if (PRO) mbar_wait(&S.ready[stage], phase);  // transformed by the epilogue warps
-        else mbar_wait(&S.full[stage], phase);
+      for (int nt = 0; nt < nts; ++nt) {
+        mbar_wait(&S.tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(S.a[stage]), b0 = smem_u32(S.b[stage]);
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          if (ASTAT && nt == 0) mbar_wait(&S.a_ready[kb], aphase);  // this A k-block landed and transformed
+          if (PRO && !ASTAT) mbar_wait(&S.ready[stage], phase);     // transformed by the transform warps
+          else mbar_wait(&S.full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(ASTAT ? S.a[kb] : S.a[stage]), b0 = smem_u32(S.b[stage]);
 #pragma unroll
-          for (int k = 0; k < kBK / kUmmaK; ++k)
-            umma_bf16(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2), idesc,
-                      (kb | k) != 0);
-          umma_commit(&S.empty[stage]);                   // smem stage free when these MMAs finish
-          if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
+            for (int k = 0; k < kBK / kUmmaK; ++k)
+              umma_bf16(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2), idesc,
+                        (kb | k) != 0);
+            umma_commit(&S.empty[stage]);                       // smem stage free when these MMAs finish
+            if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
+            if (ASTAT && nt == nts - 1) umma_commit(&S.a_free[kb]);  // A k-block no longer read
+          }
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
       }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
+      aphase ^= 1;
     }
   } else if (warp >= kXfWarp0) {
     // ------------------------------------------------------------ prologue transform
@@ -282,13 +318,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kXfThreads) : "memory");  // transform warps only
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, aphase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         // a = bf16(relu(a*sc + sh)) in place.  SWIZZLE_128B: logical 16-byte
         // chunk jj of row r (channels kb*64 + 8*jj .. +8) is physical chunk jj ^ (r & 7)
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&S.full[stage], phase);
-          uint4* rowp = reinterpret_cast<uint4*>(S.a[stage] + r * 128);
+          if (ASTAT) mbar_wait(&S.a_full[kb], aphase);
+          else mbar_wait(&S.full[stage], phase);
+          uint4* rowp = reinterpret_cast<uint4*>((ASTAT ? S.a[kb] : S.a[stage]) + r * 128);
           uint4 u[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) u[i] = rowp[(jh + i) ^ (r & 7)];  // consecutive rows: distinct columns
@@ -311,12 +348,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             rowp[(jh + i) ^ (r & 7)] = u[i];
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
-          mbar_arrive(&S.ready[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+          if (ASTAT) {
+            mbar_arrive(&S.a_ready[kb]);
+          } else {
+            mbar_arrive(&S.ready[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
+        if (ASTAT) aphase ^= 1;
       }
     }
   } else {
@@ -327,13 +369,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     const int half = ew >> 2;                     // this warp's column part
     constexpr int kChunks = BN / 32 / kParts;     // 32-column chunks per part
     if (half < kParts) {                          // BN = 64: two parts only
-    float acc_s[kChunks], acc_q[kChunks];
+    constexpr int kNT = ASTAT ? kMaxNT : 1;
+    float acc_s[kNT * kChunks], acc_q[kNT * kChunks];
 #pragma unroll
-    for (int c = 0; c < kChunks; ++c) acc_s[c] = acc_q[c] = 0.f;
+    for (int c = 0; c < kNT * kChunks; ++c) acc_s[c] = acc_q[c] = 0.f;
     int acc = 0;
     uint32_t acc_phase = 0;
     int sbuf = 0;
     for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+     for (int nt = 0; nt < nts; ++nt) {
+      const int n_tile = ASTAT ? nt : n_fixed;
       mbar_wait(&S.tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t row0 = (int64_t)mt * kBM + q * 32;
@@ -381,8 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             s1[r & 3] += x;
             s2[r & 3] = __fmaf_rn(x, x, s2[r & 3]);
           }
-          acc_s[c] += (s1[0] + s1[1]) + (s1[2] + s1[3]);
-          acc_q[c] += (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          acc_s[nt * kChunks + c] += (s1[0] + s1[1]) + (s1[2] + s1[3]);
+          acc_q[nt * kChunks + c] += (s2[0] + s2[1]) + (s2[2] + s2[3]);
         }
         sbuf ^= 1;
       }
@@ -392,16 +437,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         acc = 0;
         acc_phase ^= 1;
       }
+     }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
     if (STATS) {
       // lane l holds column part*BN/kParts + c*32 + l of this warp's 32 rows;
       // one partial row per lane quarter, the parts fill disjoint columns
-      float* out = p.part + ((size_t)m_first * 4 + q) * 2 * p.N + (size_t)n_tile * BN + half * (BN / kParts);
+      for (int nt = 0; nt < nts; ++nt) {
+        const int n_tile = ASTAT ? nt : n_fixed;
+        float* out = p.part + ((size_t)m_first * 4 + q) * 2 * p.N + (size_t)n_tile * BN + half * (BN / kParts);
 #pragma unroll
-      for (int c = 0; c < kChunks; ++c) {
-        out[c * 32 + lane] = acc_s[c];
-        out[p.N + c * 32 + lane] = acc_q[c];
+        for (int c = 0; c < kChunks; ++c) {
+          out[c * 32 + lane] = acc_s[nt * kChunks + c];
+          out[p.N + c * 32 + lane] = acc_q[nt * kChunks + c];
+        }
       }
     }
     }
@@ -501,11 +550,11 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int STAGES, bool PRO, bool STATS>
+template <int BN, int STAGES, bool PRO, bool STATS, bool ASTAT>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, int grid,
                    cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, STATS>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO>) + 1024;
+  auto k = conv1x1_kernel<BN, STAGES, PRO, STATS, ASTAT>;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT>) + 1024;
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -516,14 +565,17 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, bool STATS>
+template <int BN, bool PRO, bool STATS, bool ASTAT>
 cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p,
                             int grid, cudaStream_t s) {
-  // deepest ring that fits next to the barriers (227 KB per CTA)
-  constexpr int stage_bytes = (kBM + BN) * kBK * 2;
-  constexpr int avail = 220 * 1024 - (PRO ? 2 * kMaxProK * 4 : 0) - kEpiWarps * 2 * 32 * 64;
+  // deepest ring that fits next to everything else (227 KB per CTA)
+  constexpr int fixed = (PRO ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
+                        (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0);
+  constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * kBK * 2;
+  constexpr int avail = 220 * 1024 - fixed;
   constexpr int stages = avail / stage_bytes > 8 ? 8 : avail / stage_bytes;
-  return launch<BN, stages, PRO, STATS>(ma, mb, mc, p, grid, s);
+  static_assert(stages >= 2, "shared memory");
+  return launch<BN, stages, PRO, STATS, ASTAT>(ma, mb, mc, p, grid, s);
 }
 
 }  // namespace
@@ -559,19 +611,23 @@ cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, i
       !make_map(&mb, B, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
-  // whole n-tile groups, at most one CTA per SM and no more m-tiles than exist
-  int per = num_sms() / p.n_tiles;
+  const bool pro = pmean != nullptr, st = part != nullptr;
+  // A-stationary when the prologue would otherwise transform the same A tile once per n-tile
+  const bool astat = pro && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
+  // whole n-tile groups (or, A-stationary, whole m-tiles), at most one CTA per SM
+  int per = astat ? num_sms() : num_sms() / p.n_tiles;
   if (per < 1) per = 1;
   if (per > p.m_tiles) per = p.m_tiles;
-  const int grid = per * p.n_tiles;
+  const int grid = astat ? per : per * p.n_tiles;
   if (part_rows) *part_rows = per * 4;  // every row and column written exactly once
-  const bool pro = pmean != nullptr, st = part != nullptr;
-#define KRT_GEMM_BN(BNV)                                                               \
-  if (BN == BNV) {                                                                     \
-    if (pro && st) return dispatch_stages<BNV, true, true>(ma, mb, mc, p, grid, s);   \
-    if (pro) return dispatch_stages<BNV, true, false>(ma, mb, mc, p, grid, s);        \
-    if (st) return dispatch_stages<BNV, false, true>(ma, mb, mc, p, grid, s);         \
-    return dispatch_stages<BNV, false, false>(ma, mb, mc, p, grid, s);                \
+#define KRT_GEMM_BN(BNV)                                                                        \
+  if (BN == BNV) {                                                                              \
+    if (astat && st) return dispatch_stages<BNV, true, true, true>(ma, mb, mc, p, grid, s);    \
+    if (astat) return dispatch_stages<BNV, true, false, true>(ma, mb, mc, p, grid, s);         \
+    if (pro && st) return dispatch_stages<BNV, true, true, false>(ma, mb, mc, p, grid, s);     \
+    if (pro) return dispatch_stages<BNV, true, false, false>(ma, mb, mc, p, grid, s);          \
+    if (st) return dispatch_stages<BNV, false, true, false>(ma, mb, mc, p, grid, s);           \
+    return dispatch_stages<BNV, false, false, false>(ma, mb, mc, p, grid, s);                  \
   }
   KRT_GEMM_BN(64)
   KRT_GEMM_BN(128)

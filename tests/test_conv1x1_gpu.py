@@ -21,7 +21,8 @@ def cl(t):
 
 
 @pytest.mark.parametrize("n,cin,cout,hw", [(2, 64, 64, 8), (4, 256, 64, 14), (2, 64, 256, 7), (3, 128, 512, 5),
-                                           (1, 512, 2048, 3), (2, 1024, 256, 6)])
+                                           (1, 512, 2048, 3), (2, 1024, 256, 6), (2, 256, 1024, 6),
+                                           (1, 64, 2048, 5), (3, 128, 512, 17)])
 @pytest.mark.parametrize("pre", [False, True])
 def test_conv1x1_matches_torch(n, cin, cout, hw, pre):
     x = cl(rand((n, cin, hw, hw), 1, 2.0))
