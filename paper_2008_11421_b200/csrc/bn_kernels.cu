@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
 // add_relu_bwd of the residual sum and the reduce of the BN (no ReLU of its
 // own) that produced x, in one pass: dz = (dy [+ dy2]) * mask(bn(x) + res) is
 // written out and accumulated from registers; then the finalize
-template <bool DY2>
+template <bool DY2, int U>
 __global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ dy2, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean, const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g,
@@ -500,8 +500,7 @@ __global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
     is[j] = invstd[c0 + j];
   }
   float s1[8] = {0}, s2[8] = {0};
-  constexpr int U = 2;  // 3-4 tensors per row
-  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {  // U rows x 3-4 tensors in flight
     uint4 v[U], q[U], d[U], e[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -758,7 +757,12 @@ cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x,
     return coop(kernel, rows, C, s, B(dy), B(dy2), B(x), mean, invstd, B(g), B(b), B(res), BW_(dz), rows, C, part,
                 coef, dgamma, dbeta);
   };
-  cudaError_t e = dy2 ? red(add_relu_reduce_kernel<true>) : red(add_relu_reduce_kernel<false>);
+  // two rows in flight per thread, four at C = 1024 (measured: the ResNet-200
+  // stage-3 output width, 13% faster there and slower at every other width)
+  static const int force_u = getenv("KRT_BN_ADDRELU_U") ? atoi(getenv("KRT_BN_ADDRELU_U")) : 0;
+  const bool u4 = force_u ? force_u == 4 : C == 1024;
+  cudaError_t e = u4 ? (dy2 ? red(add_relu_reduce_kernel<true, 4>) : red(add_relu_reduce_kernel<false, 4>))
+                     : (dy2 ? red(add_relu_reduce_kernel<true, 2>) : red(add_relu_reduce_kernel<false, 2>));
   if (e != cudaSuccess) return e;
   return bwd_elemt(dz, x, mean, invstd, g, b, coef, nullptr, dx, rows, C, 0, s);
 }
