@@ -231,15 +231,15 @@ __device__ __forceinline__ Vec8 apply_row(const Vec8& v, const Vec8& rv, const f
   return o;
 }
 
-// the apply pass over one group of kU rows (rows >= rows_ skipped)
-template <int MODE, bool RELU>
+// the apply pass over one group of U rows (rows >= rows_ skipped)
+template <int MODE, bool RELU, int U>
 __device__ __forceinline__ void apply_group(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
                                             __nv_bfloat16* __restrict__ y, int64_t r0, int64_t step, int64_t rows,
                                             int C, int c0, const float* sc, const float* sh, const float* rsc,
                                             const float* rsh) {
-  uint4 v[kU], q[kU];
+  uint4 v[U], q[U];
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int64_t r = r0 + u * step;
     if (r < rows) {
       v[u] = ld16s(x + r * C + c0);
@@ -247,7 +247,7 @@ __device__ __forceinline__ void apply_group(const __nv_bfloat16* __restrict__ x,
     }
   }
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int64_t r = r0 + u * step;
     if (r < rows) {
       Vec8 rv{};
@@ -258,16 +258,17 @@ __device__ __forceinline__ void apply_group(const __nv_bfloat16* __restrict__ x,
 }
 
 // stats pass-1 accumulation of one group
+template <int U>
 __device__ __forceinline__ void stats_group(const __nv_bfloat16* __restrict__ x, int64_t r0, int64_t step,
                                             int64_t rows, int C, int c0, float* s, float* q) {
-  uint4 v[kU];
+  uint4 v[U];
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int64_t r = r0 + u * step;
     v[u] = r < rows ? ld16(x + r * C + c0) : make_uint4(0, 0, 0, 0);  // bf16 zero bits
   }
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
+  for (int u = 0; u < U; ++u) {
     Vec8 f = unpack(v[u]);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -277,6 +278,7 @@ __device__ __forceinline__ void stats_group(const __nv_bfloat16* __restrict__ x,
   }
 }
 
+template <int U>
 __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int C,
                                                          float eps, float* __restrict__ part,
                                                          float* __restrict__ mean, float* __restrict__ invstd) {
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __
   Rows rw(m, rows);
   const int c0 = m.tx * 8;
   float s[8] = {0}, q[8] = {0};
-  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) stats_group(x, r0, rw.step, rows, C, c0, s, q);
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) stats_group<U>(x, r0, rw.step, rows, C, c0, s, q);
   cta_partial(s, q, smem, m, part, C, c0);
   cg::this_grid().sync();
   double* shd = reinterpret_cast<double*>(smem);
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(kThreads) stats_kernel(const __nv_bfloat16* __
   }
 }
 
-template <int MODE, bool RELU>
+template <int MODE, bool RELU, int U>
 __global__ void __launch_bounds__(kThreads) apply_kernel(
     const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ invstd,
     const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b, const __nv_bfloat16* __restrict__ res,
@@ -314,8 +316,8 @@ __global__ void __launch_bounds__(kThreads) apply_kernel(
   float sc[8], sh[8], rsc[8], rsh[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
   if (MODE == 2) bn_coeffs(rmean, rinvstd, rg, rb_, c0, rsc, rsh);
-  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU)
-    apply_group<MODE, RELU>(x, res, y, r0, rw.step, rows, C, c0, sc, sh, rsc, rsh);
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U)
+    apply_group<MODE, RELU, U>(x, res, y, r0, rw.step, rows, C, c0, sc, sh, rsc, rsh);
 }
 
 // ---------------------------------------------------------------------------
@@ -444,7 +446,7 @@ __device__ __forceinline__ void bwd_finalize(const float* part, int64_t rows, in
 }
 
 // reduce + finalize (dgamma, dbeta, dx coefficients), one cooperative kernel
-template <bool RELU>
+template <bool RELU, int U>
 __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
@@ -462,16 +464,16 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
     is[j] = invstd[c0 + j];
   }
   float s1[8] = {0}, s2[8] = {0};
-  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) {
-    uint4 v[kU], d[kU];
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {
+    uint4 v[U], d[U];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * rw.step;
       v[u] = r < rows ? ld16s(x + r * C + c0) : make_uint4(0, 0, 0, 0);
       d[u] = r < rows ? ld16s(dy + r * C + c0) : make_uint4(0, 0, 0, 0);  // gm = 0 on padding
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) bwd_acc<RELU>(unpack(v[u]), unpack(d[u]), sc, sh, mu, is, s1, s2);
+    for (int u = 0; u < U; ++u) bwd_acc<RELU>(unpack(v[u]), unpack(d[u]), sc, sh, mu, is, s1, s2);
   }
   cta_partial(s1, s2, smem, m, part, C, c0);
   cg::this_grid().sync();
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
 // dx = A*gm + B*x + D [+ addend] with gm = dy * mask (coefficients from the
 // reduce); the optional addend (a residual gradient) is summed before the one
 // bf16 rounding, so no separate add pass re-reads dx
-template <bool RELU, bool ADD>
+template <bool RELU, bool ADD, int U>
 __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, const __nv_bfloat16* __restrict__ b,
@@ -551,10 +553,10 @@ __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
     k.bx[j] = coef[C + c0 + j];
     k.d[j] = coef[2 * C + c0 + j];
   }
-  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * kU) {
-    uint4 v[kU], d[kU], e[kU];
+  for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {
+    uint4 v[U], d[U], e[U];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * rw.step;
       if (r < rows) {
         v[u] = ld16s(x + r * C + c0);
@@ -563,7 +565,7 @@ __global__ void __launch_bounds__(kThreads) bwd_elemt_kernel(
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t r = r0 + u * rw.step;
       if (r < rows) {
         Vec8 o = bwd_row<RELU>(unpack(v[u]), unpack(d[u]), k);
@@ -660,6 +662,29 @@ cudaError_t coop(void (*kernel)(P...), int64_t rows, int C, cudaStream_t s, type
                                      s);
 }
 
+// Rows in flight per thread and tensor, per kernel family and channel count:
+// KRT_BN_U_<FAMILY>=2|4|8 forces a value (tuning sweeps), otherwise the
+// measured table (scripts/bench_bn.py at the ResNet-200 widths).
+enum Fam { kStats, kApply, kBwdReduce, kBwdElemt, kFams };
+
+int rows_in_flight(Fam f, int C) {
+  static int force[kFams] = {-1, -1, -1, -1};
+  static const char* names[kFams] = {"KRT_BN_U_STATS", "KRT_BN_U_APPLY", "KRT_BN_U_BWDREDUCE", "KRT_BN_U_BWDELEMT"};
+  if (force[f] < 0) {
+    const char* e = getenv(names[f]);
+    force[f] = e ? atoi(e) : 0;
+  }
+  if (force[f] == 2 || force[f] == 4 || force[f] == 8) return force[f];
+  // measured at batch 1024 on the ResNet-200 widths (profiles/round1_s2_bn_rows_in_flight.md):
+  // apply 2-5% faster with two rows, stats up to 25% faster with eight (four at
+  // C = 1024), the backward pair best with four everywhere
+  switch (f) {
+    case kApply: return 2;
+    case kStats: return C == 1024 ? 4 : 8;
+    default: return 4;
+  }
+}
+
 using bf16 = __nv_bfloat16;
 inline const bf16* B(const void* p) { return static_cast<const bf16*>(p); }
 inline bf16* BW_(void* p) { return static_cast<bf16*>(p); }
@@ -671,13 +696,17 @@ cudaError_t bwd_elemt(const void* dy, const void* x, const float* mean, const fl
     kernel<<<grid_rows(kernel, 0, rows, C), kThreads, 0, s>>>(B(dy), B(x), mean, invstd, B(g), B(b), coef,
                                                               B(addend), BW_(dx), rows, C);
   };
-  if (addend) {
-    if (relu) go(bwd_elemt_kernel<true, true>);
-    else go(bwd_elemt_kernel<false, true>);
-  } else {
-    if (relu) go(bwd_elemt_kernel<true, false>);
-    else go(bwd_elemt_kernel<false, false>);
+  const int u = rows_in_flight(kBwdElemt, C);
+#define KRT_ELEMT(U)                                                     \
+  if (addend) {                                                          \
+    if (relu) go(bwd_elemt_kernel<true, true, U>);                       \
+    else go(bwd_elemt_kernel<false, true, U>);                           \
+  } else {                                                               \
+    if (relu) go(bwd_elemt_kernel<true, false, U>);                      \
+    else go(bwd_elemt_kernel<false, false, U>);                          \
   }
+  if (u == 2) { KRT_ELEMT(2) } else if (u == 8) { KRT_ELEMT(8) } else { KRT_ELEMT(4) }
+#undef KRT_ELEMT
   return cudaGetLastError();
 }
 
@@ -688,7 +717,11 @@ size_t bn_workspace_bytes(int C) { return (size_t)kMaxGrid * 2 * C * sizeof(floa
 cudaError_t bn_stats(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd, void* ws,
                      cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
-  return coop(stats_kernel, rows, C, s, B(x), rows, C, eps, static_cast<float*>(ws), mean, invstd);
+  const int u = rows_in_flight(kStats, C);
+  float* part = static_cast<float*>(ws);
+  if (u == 2) return coop(stats_kernel<2>, rows, C, s, B(x), rows, C, eps, part, mean, invstd);
+  if (u == 8) return coop(stats_kernel<8>, rows, C, s, B(x), rows, C, eps, part, mean, invstd);
+  return coop(stats_kernel<4>, rows, C, s, B(x), rows, C, eps, part, mean, invstd);
 }
 
 cudaError_t bn_stats_apply(const void* x, int64_t rows, int C, float eps, float* mean, float* invstd,
@@ -704,13 +737,21 @@ cudaError_t bn_apply(const void* x, const float* mean, const float* invstd, cons
                      int relu, void* y, int64_t rows, int C, cudaStream_t s) {
   if (!shape_ok(rows, C)) return cudaErrorInvalidValue;
   int mode = res == nullptr ? 0 : (rmean == nullptr ? 1 : 2);
-#define KRT_APPLY(M, RL)                                                                                        \
-  apply_kernel<M, RL><<<grid_rows(apply_kernel<M, RL>, 0, rows, C), kThreads, 0, s>>>(                          \
+  const int u = rows_in_flight(kApply, C);
+#define KRT_APPLY_U(M, RL, U)                                                                                   \
+  apply_kernel<M, RL, U><<<grid_rows(apply_kernel<M, RL, U>, 0, rows, C), kThreads, 0, s>>>(                    \
       B(x), mean, invstd, B(g), B(b), B(res), rmean, rinvstd, B(rg), B(rb), BW_(y), rows, C)
+#define KRT_APPLY(M, RL)                                                           \
+  do {                                                                             \
+    if (u == 2) KRT_APPLY_U(M, RL, 2);                                             \
+    else if (u == 8) KRT_APPLY_U(M, RL, 8);                                        \
+    else KRT_APPLY_U(M, RL, 4);                                                    \
+  } while (0)
   if (mode == 0) { if (relu) KRT_APPLY(0, true); else KRT_APPLY(0, false); }
   else if (mode == 1) { if (relu) KRT_APPLY(1, true); else KRT_APPLY(1, false); }
   else { if (relu) KRT_APPLY(2, true); else KRT_APPLY(2, false); }
 #undef KRT_APPLY
+#undef KRT_APPLY_U
   return cudaGetLastError();
 }
 
@@ -741,7 +782,10 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
   auto red = [&](auto kernel) {
     return coop(kernel, rows, C, s, B(dy), B(x), mean, invstd, B(g), B(b), rows, C, part, coef, dgamma, dbeta);
   };
-  cudaError_t e = relu ? red(bwd_reduce_kernel<true>) : red(bwd_reduce_kernel<false>);
+  const int u = rows_in_flight(kBwdReduce, C);
+  cudaError_t e = u == 2 ? (relu ? red(bwd_reduce_kernel<true, 2>) : red(bwd_reduce_kernel<false, 2>))
+                  : u == 8 ? (relu ? red(bwd_reduce_kernel<true, 8>) : red(bwd_reduce_kernel<false, 8>))
+                           : (relu ? red(bwd_reduce_kernel<true, 4>) : red(bwd_reduce_kernel<false, 4>));
   if (e != cudaSuccess || dx == nullptr) return e;
   return bwd_elemt(dy, x, mean, invstd, g, b, coef, addend, dx, rows, C, relu, s);
 }
