@@ -206,6 +206,16 @@ int krt_ipc_import(krt_ctx* ctx, const void* handles, int world);
  * weights equal the masters — for evaluation and checkpoints. */
 int krt_flush_weights(krt_ctx* ctx);
 
+/* Checkpoint / restart of this rank's training state: after
+ * the last iteration completes, write the device weights, device-path fp32
+ * masters and moments, host-path masters/moments/weight staging and the
+ * iteration counter to `path` (atomically: temp file + rename).  Load into a
+ * context prepared with the same model, plan, dtype, world size and rank;
+ * training then continues bitwise as if uninterrupted.  Errors: KRT_USAGE for
+ * a mismatched or foreign file, KRT_INTERNAL for I/O failures. */
+int krt_checkpoint_save(krt_ctx* ctx, const char* path);
+int krt_checkpoint_load(krt_ctx* ctx, const char* path);
+
 /* Measured trace of the last iteration in the SimTrace CSV schema
  * (simulator.py:225-230) extended with the DP ops; caller frees. */
 int krt_trace_csv(krt_ctx* ctx, char** out);

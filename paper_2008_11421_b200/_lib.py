@@ -95,6 +95,8 @@ EXPORTS = {
     "krt_device_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int, C.c_size_t, C.c_int, C.c_float, C.c_float, C.c_float,
                                     C.c_float, C.c_float, C.c_float, C.c_int, C.c_void_p]),
+    "krt_checkpoint_save": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "krt_checkpoint_load": (C.c_int, [C.c_void_p, C.c_char_p]),
     "krt_bn_workspace_bytes": (C.c_size_t, [C.c_int]),
     "krt_bn_stats": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_float, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p]),

@@ -377,6 +377,14 @@ int krt_stats(krt_ctx* ctx, char** out) {
   return guard([&] { *out = dup(ctx->rt->stats_json()); });
 }
 
+int krt_checkpoint_save(krt_ctx* ctx, const char* path) {
+  return guard([&] { ctx->rt->checkpoint_save(path); });
+}
+
+int krt_checkpoint_load(krt_ctx* ctx, const char* path) {
+  return guard([&] { ctx->rt->checkpoint_load(path); });
+}
+
 int krt_read_master(krt_ctx* ctx, int block, float* out, size_t numel) {
   return guard([&] { ctx->rt->read_master(block, out, numel); });
 }

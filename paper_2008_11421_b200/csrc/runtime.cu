@@ -1,5 +1,8 @@
 #include "runtime.hpp"
 
+#include <cstdio>
+#include <cstring>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <nccl.h>
@@ -1025,6 +1028,135 @@ void* Runtime::block_slot(int block) const {
   auto it = cur_slot_.find(block);
   if (it == cur_slot_.end()) throw std::invalid_argument("block " + std::to_string(block) + " has no resident slot");
   return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// checkpoint / restart of the training state this rank owns (PAPER.md:567:
+// epochs split across runs with C/R of the model state).  Written after the
+// last iteration completes: device weights, device-path fp32 masters and
+// optimizer moments, the host-path fp32 masters and moments (this rank's
+// shards) and the weight staging the next weight_in copies from, plus the
+// iteration counter (Adam bias correction).  A restored context continues
+// bitwise where the saved one stopped.
+// ---------------------------------------------------------------------------
+namespace {
+struct CkptHeader {
+  char magic[8];
+  uint32_t version, world, rank, weight_dtype;
+  uint64_t params, host_elems, step;
+  uint32_t has_dev_master, has_dev_moments;
+};
+
+void write_all(std::FILE* f, const void* p, size_t n) {
+  if (n && std::fwrite(p, 1, n, f) != n) throw std::runtime_error("checkpoint: short write");
+}
+void read_all(std::FILE* f, void* p, size_t n) {
+  if (n && std::fread(p, 1, n, f) != n) throw std::runtime_error("checkpoint: short read (truncated file?)");
+}
+
+// device buffer <-> file through a bounded pinned bounce buffer
+void dev_to_file(std::FILE* f, const void* d, size_t n) {
+  const size_t chunk = (size_t)64 << 20;
+  std::vector<uint8_t> buf(std::min(n, chunk));
+  for (size_t o = 0; o < n; o += chunk) {
+    size_t k = std::min(chunk, n - o);
+    CK(cudaMemcpy(buf.data(), static_cast<const uint8_t*>(d) + o, k, cudaMemcpyDeviceToHost));
+    write_all(f, buf.data(), k);
+  }
+}
+void file_to_dev(std::FILE* f, void* d, size_t n) {
+  const size_t chunk = (size_t)64 << 20;
+  std::vector<uint8_t> buf(std::min(n, chunk));
+  for (size_t o = 0; o < n; o += chunk) {
+    size_t k = std::min(chunk, n - o);
+    read_all(f, buf.data(), k);
+    CK(cudaMemcpy(static_cast<uint8_t*>(d) + o, buf.data(), k, cudaMemcpyHostToDevice));
+  }
+}
+}  // namespace
+
+void Runtime::checkpoint_save(const std::string& path) {
+  if (!prepared_) throw std::logic_error("checkpoint_save before prepare");
+  synchronize();
+  CK(cudaSetDevice(cfg_.device));
+  const size_t wb = dtype_bytes(cfg_.weight_dtype);
+  const size_t np = (size_t)std::max<int64_t>(total_params_, 64);
+  const size_t he = std::max<size_t>(host_elems_, 64);
+  CkptHeader h{};
+  std::memcpy(h.magic, "KRTCKPT1", 8);
+  h.version = 1;
+  h.world = (uint32_t)world_;
+  h.rank = (uint32_t)rank_;
+  h.weight_dtype = (uint32_t)cfg_.weight_dtype;
+  h.params = np;
+  h.host_elems = he;
+  h.step = (uint64_t)step_;
+  h.has_dev_master = d_master_ != nullptr;
+  h.has_dev_moments = d_m_ != nullptr;
+  std::string tmp = path + ".tmp";
+  std::FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) throw std::runtime_error("checkpoint: cannot open " + tmp);
+  try {
+    write_all(f, &h, sizeof(h));
+    dev_to_file(f, d_weights_, np * wb);
+    if (d_master_) dev_to_file(f, d_master_, np * 4);
+    if (d_m_) {
+      dev_to_file(f, d_m_, np * 4);
+      dev_to_file(f, d_v_, np * 4);
+    }
+    write_all(f, h_master_.data(), he * 4);
+    write_all(f, h_m_.data(), he * 4);
+    write_all(f, h_v_.data(), he * 4);
+    write_all(f, h_wstage_, he * wb);
+  } catch (...) {
+    std::fclose(f);
+    std::remove(tmp.c_str());
+    throw;
+  }
+  if (std::fclose(f) != 0) throw std::runtime_error("checkpoint: close failed");
+  if (std::rename(tmp.c_str(), path.c_str()) != 0) throw std::runtime_error("checkpoint: rename failed");
+}
+
+void Runtime::checkpoint_load(const std::string& path) {
+  if (!prepared_) throw std::logic_error("checkpoint_load before prepare");
+  synchronize();
+  CK(cudaSetDevice(cfg_.device));
+  const size_t wb = dtype_bytes(cfg_.weight_dtype);
+  const size_t np = (size_t)std::max<int64_t>(total_params_, 64);
+  const size_t he = std::max<size_t>(host_elems_, 64);
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw std::runtime_error("checkpoint: cannot open " + path);
+  try {
+    CkptHeader h{};
+    read_all(f, &h, sizeof(h));
+    if (std::memcmp(h.magic, "KRTCKPT1", 8) != 0 || h.version != 1)
+      throw std::invalid_argument("checkpoint: not a krt checkpoint (bad magic/version)");
+    if (h.world != (uint32_t)world_ || h.rank != (uint32_t)rank_ || h.weight_dtype != (uint32_t)cfg_.weight_dtype ||
+        h.params != np || h.host_elems != he || h.has_dev_master != (d_master_ != nullptr) ||
+        h.has_dev_moments != (d_m_ != nullptr))
+      throw std::invalid_argument("checkpoint: saved for a different model, plan, dtype or rank");
+    file_to_dev(f, d_weights_, np * wb);
+    if (d_master_) file_to_dev(f, d_master_, np * 4);
+    if (d_m_) {
+      file_to_dev(f, d_m_, np * 4);
+      file_to_dev(f, d_v_, np * 4);
+    }
+    read_all(f, h_master_.data(), he * 4);
+    read_all(f, h_m_.data(), he * 4);
+    read_all(f, h_v_.data(), he * 4);
+    read_all(f, h_wstage_, he * wb);
+    std::fclose(f);
+    f = nullptr;
+    // continue as the iteration after the saved one: steady-state ops, whose
+    // weight_in then finds the saved staging and a completed host update
+    step_ = (int)h.step;
+    last_first_ = step_ <= 1;
+    std::lock_guard<std::mutex> lk(hmu_);
+    for (size_t gi = 0; gi < groups_.size(); ++gi) host_done_step_[(int)gi + 1] = step_;
+  } catch (...) {
+    if (f) std::fclose(f);
+    throw;
+  }
 }
 
 void Runtime::read_master(int block, float* out, size_t numel) {

@@ -110,6 +110,8 @@ class Runtime {
   void read_master(int block, float* out, size_t numel);
   void* block_slot(int block) const;
   void flush_weights();
+  void checkpoint_save(const std::string& path);
+  void checkpoint_load(const std::string& path);
   std::vector<uint8_t> ipc_export();
   void ipc_import(const uint8_t* all, int world);
   void* weights_base() const { return d_weights_; }

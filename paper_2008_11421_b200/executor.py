@@ -253,6 +253,17 @@ class Executor:
         blob = b"".join(all_handles)
         _lib.check(_lib.lib().krt_ipc_import(self._ctx, blob, len(all_handles)))
 
+    def save_checkpoint(self, path):
+        """Write this rank's training state (weights, fp32 masters, optimizer
+        moments, iteration counter) to `path` once the last step completed."""
+        _lib.check(_lib.lib().krt_checkpoint_save(self._ctx, str(path).encode()))
+
+    def load_checkpoint(self, path):
+        """Restore a state saved by save_checkpoint into this prepared executor
+        (same units, plan, dtype, world size and rank); the next step continues
+        exactly where the saved run stopped."""
+        _lib.check(_lib.lib().krt_checkpoint_load(self._ctx, str(path).encode()))
+
     def flush_weights(self):
         """Return host-updated weights to the device now (krt_flush_weights)."""
         _lib.check(_lib.lib().krt_flush_weights(self._ctx))
