@@ -386,6 +386,21 @@ def run_gpu(args, rec):
     span = (max(b for _, b in comp) - min(a for a, _ in comp)) if comp else 0.0
     xin = [(float(r[0]), float(r[1])) for r in rows if r[4] in ("swap_in", "weight_in")]
     xout = [(float(r[0]), float(r[1])) for r in rows if r[4] in ("swap_out", "grad_out")]
+    # occupancy of the backward phase against the analytic model (occupancy.py:178-237):
+    # steps = the compute ops from the first bw on (bw and recompute_fw), busy =
+    # duration, idle = measured stall before it; theta = 0-based index of the
+    # first step that waited (None: the backward phase never waited)
+    comp_ops = sorted(((float(r[0]), float(r[1]), r[4], float(r[6])) for r in rows if r[2] == "compute"))
+    first_bw = next((i for i, o in enumerate(comp_ops) if o[2] == "bw"), None)
+    bsteps = comp_ops[first_bw:] if first_bw is not None else []
+    theta_meas = next((j for j, o in enumerate(bsteps) if o[3] > 1e-3), None)
+    b_busy = sum(o[1] - o[0] for o in bsteps)
+    b_idle = sum(o[3] for o in bsteps)
+    occupancy = {"theta_predicted": rec["plan"].get("theta"), "theta_measured": theta_meas,
+                 "backward_steps": len(bsteps),
+                 "backward_mean_occupancy_measured": b_busy / (b_busy + b_idle) if bsteps else None,
+                 "note": "reference find_theta / report_from_steps semantics on the measured trace; "
+                         "idle = stall_before > 1 ms counts as waiting"}
     swap_in_bytes = st["iter_bytes_h2d"]
     swap_out_bytes = st["iter_bytes_d2h"]
     # live roofline of our dominant kernel family (CUDA events on the compute stream)
@@ -456,6 +471,7 @@ def run_gpu(args, rec):
                     "exposed_stall_frac": 1 - busy / span if span else None,
                     "swap_in_busy_s": sum(b - a for a, b in xin),
                     "swap_out_busy_s": sum(b - a for a, b in xout)},
+        "occupancy": occupancy,
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_in,
                 "d2h_bytes_per_step": 4, "steps": e2e_steps,
                 "loss_read_s": [round(t, 4) for t in e2e_marks], "issued_s": [round(t, 4) for t in issue_marks],
