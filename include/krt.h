@@ -316,6 +316,24 @@ int krt_conv1x1_bn(const void* A, const void* B, void* C, int64_t M, int N, int 
                    void* stream);
 int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
                              float* invstd, void* stream);
+/* Backward of a 1x1 convolution fused with the reduce of the BN (+ ReLU) in
+ * front of it: dX[M,N] = dY[M,K] . Wt[N,K]^T (Wt = weights transposed, K-major)
+ * is stored, and with x = that BN's input the epilogue reduces sum(gm) and
+ * sum(gm * xhat), gm = dX * (relu(bn(x)) > 0), into *part_rows partial rows;
+ * krt_bn_partials_bwd_finalize turns them into dgamma, dbeta and the dx
+ * coefficients (coef [3][N]) that krt_bn_backward_elemt applies: the
+ * separate reduce pass over (dX, x) is gone.  Shape rules as krt_conv1x1_bn. */
+int krt_conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
+                         const float* mean, const float* invstd, const void* gamma, const void* beta,
+                         float* part, int* part_rows, void* stream);
+int krt_bn_partials_bwd_finalize(const float* part, int part_rows, int N, int64_t M, const float* mean,
+                                 const float* invstd, const void* gamma, float* dgamma, float* dbeta,
+                                 float* coef, void* stream);
+/* dx = A*gm + B*x + D [+ addend] with gm = dy * (relu ? mask(x) : 1) and
+ * coef [3][C] = A, B, D (from krt_bn_partials_bwd_finalize) */
+int krt_bn_backward_elemt(const void* dy, const void* x, const float* mean, const float* invstd,
+                          const void* gamma, const void* beta, const float* coef, const void* addend, int relu,
+                          void* dx, int64_t rows, int C, void* stream);
 
 #ifdef __cplusplus
 }

@@ -212,3 +212,34 @@ def conv1x1(x, w, out=None, pre=None, stats=None):
             _lib.check(_lib.lib().krt_bn_partials_finalize(part.data_ptr(), rows.value, cout, M, EPS,
                                                            stats[0].data_ptr(), stats[1].data_ptr(), _stream()))
     return y
+
+
+def conv1x1_dgrad_bn_backward(dy, w, x, mean, invstd, g, b, dgamma=None, dbeta=None, relu=True):
+    """d(input of relu(bn(x)))-chain through a stride-1 1x1 convolution:
+    da = dy . W (tcgen05 GEMM, W transposed to K-major) with the BN backward
+    reduce of (da, x) in its epilogue, then the BN backward elementwise pass.
+    dy: (N, Cout, H, W) grad of the conv output; w: (Cout, Cin, 1, 1); x: the
+    BN input (N, Cin, H, W).  Returns dx = d/dx of conv(relu(bn(x)))."""
+    import ctypes as C
+    dy, x = _nhwc(dy), _nhwc(x)
+    n, cout, h, ww = dy.shape
+    cin = w.shape[1]
+    wt = w.reshape(cout, cin).t().contiguous()          # [Cin, Cout]: the K-major B operand
+    M = n * h * ww
+    da = torch.empty((n, cin, h, ww), dtype=dy.dtype, device=dy.device, memory_format=torch.channels_last)
+    part = torch.empty(_lib.lib().krt_conv1x1_partials_bytes(cin) // 4, dtype=torch.float32, device=dy.device)
+    coef = torch.empty(3 * cin, dtype=torch.float32, device=dy.device)
+    rows = C.c_int(0)
+    with _timed("conv1x1_dgrad_bn", M * (cout + 2 * cin) * 2, 2.0 * M * cin * cout):
+        _lib.check(_lib.lib().krt_conv1x1_bn_dgrad(dy.data_ptr(), wt.data_ptr(), da.data_ptr(), M, cin, cout,
+                                                   x.data_ptr(), mean.data_ptr(), invstd.data_ptr(), g.data_ptr(),
+                                                   b.data_ptr(), part.data_ptr(), C.byref(rows), _stream()))
+        _lib.check(_lib.lib().krt_bn_partials_bwd_finalize(part.data_ptr(), rows.value, cin, M, mean.data_ptr(),
+                                                           invstd.data_ptr(), g.data_ptr(), _ptr(dgamma),
+                                                           _ptr(dbeta), coef.data_ptr(), _stream()))
+    dx = torch.empty_like(x, memory_format=torch.channels_last)
+    with _timed("bn_backward_elemt", M * cin * 2 * 3):
+        _lib.check(_lib.lib().krt_bn_backward_elemt(da.data_ptr(), x.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                                                    g.data_ptr(), b.data_ptr(), coef.data_ptr(), None, int(relu),
+                                                    dx.data_ptr(), M, cin, _stream()))
+    return dx

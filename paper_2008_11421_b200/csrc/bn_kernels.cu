@@ -790,6 +790,13 @@ cudaError_t bn_backward(const void* dy, const void* x, const float* mean, const 
   return bwd_elemt(dy, x, mean, invstd, g, b, coef, addend, dx, rows, C, relu, s);
 }
 
+cudaError_t bn_backward_elemt(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                              const void* b, const float* coef, const void* addend, int relu, void* dx, int64_t rows,
+                              int C, cudaStream_t s) {
+  if (!shape_ok(rows, C) || coef == nullptr || dx == nullptr) return cudaErrorInvalidValue;
+  return bwd_elemt(dy, x, mean, invstd, g, b, coef, addend, dx, rows, C, relu, s);
+}
+
 cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x, const float* mean,
                                  const float* invstd, const void* g, const void* b, const void* res, void* dz,
                                  void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,

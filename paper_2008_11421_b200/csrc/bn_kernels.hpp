@@ -24,4 +24,9 @@ cudaError_t bn_add_relu_backward(const void* dy, const void* dy2, const void* x,
                                  const float* invstd, const void* g, const void* b, const void* res, void* dz,
                                  void* dx, float* dgamma, float* dbeta, int64_t rows, int C, void* ws,
                                  cudaStream_t s);
+// the elementwise half of bn_backward with coefficients from elsewhere
+// (coef [3][C] = A, B, D: dx = A*gm + B*x + D [+ addend], gm = dy*mask)
+cudaError_t bn_backward_elemt(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                              const void* b, const float* coef, const void* addend, int relu, void* dx, int64_t rows,
+                              int C, cudaStream_t s);
 }  // namespace krt

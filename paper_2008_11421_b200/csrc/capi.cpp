@@ -471,6 +471,28 @@ int krt_conv1x1_bn(const void* A, const void* B, void* C, int64_t M, int N, int 
                  "conv1x1_bn");
 }
 
+int krt_conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
+                         const float* mean, const float* invstd, const void* g, const void* b, float* part,
+                         int* part_rows, void* stream) {
+  KRT_CUDA_GUARD(conv1x1_bn_dgrad(dY, Wt, dX, M, N, K, x, mean, invstd, g, b, part, part_rows, (cudaStream_t)stream),
+                 "conv1x1_bn_dgrad");
+}
+
+int krt_bn_partials_bwd_finalize(const float* part, int part_rows, int N, int64_t M, const float* mean,
+                                 const float* invstd, const void* g, float* dgamma, float* dbeta, float* coef,
+                                 void* stream) {
+  KRT_CUDA_GUARD(bn_partials_bwd_finalize(part, part_rows, N, M, mean, invstd, g, dgamma, dbeta, coef,
+                                          (cudaStream_t)stream),
+                 "bn_partials_bwd_finalize");
+}
+
+int krt_bn_backward_elemt(const void* dy, const void* x, const float* mean, const float* invstd, const void* g,
+                          const void* b, const float* coef, const void* addend, int relu, void* dx, int64_t rows,
+                          int C, void* stream) {
+  KRT_CUDA_GUARD(bn_backward_elemt(dy, x, mean, invstd, g, b, coef, addend, relu, dx, rows, C, (cudaStream_t)stream),
+                 "bn_backward_elemt");
+}
+
 int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
                              float* invstd, void* stream) {
   KRT_CUDA_GUARD(bn_partials_finalize(part, part_rows, N, M, eps, mean, invstd, (cudaStream_t)stream),

@@ -168,6 +168,13 @@ struct Params {
   const float* pinvstd;
   const __nv_bfloat16* pg;
   const __nv_bfloat16* pb;
+  // BN-backward epilogue (EPI 2): x of the BN whose output gradient C is, and
+  // its statistics/affine; partials = sum gm, sum gm*xhat with gm = C*mask(x)
+  const __nv_bfloat16* bx;
+  const float* bmean;
+  const float* binvstd;
+  const __nv_bfloat16* bg;
+  const __nv_bfloat16* bb;
 };
 
 // ASTAT (A-stationary, prologue only, K <= kMaxAstatK): the transformed A tile
@@ -193,7 +200,8 @@ struct Smem {
   alignas(1024) uint8_t cstage[kEpiWarps][2][32 * 64];
 };
 
-template <int BN, int STAGES, bool PRO, bool STATS, bool ASTAT>
+// EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c, Params p) {
@@ -414,7 +422,33 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (STATS) {
+        if (EPI == 2) {
+          // BN backward reduce on the stored (rounded) gradient: lane = column,
+          // rows in order; x read straight from global (a warp reads 64
+          // contiguous bytes per row), the mask recomputed as bn_backward does
+          const __nv_bfloat16* stg = reinterpret_cast<const __nv_bfloat16*>(S.cstage[ew][sbuf]);
+          const int cc = lane >> 3, ce = lane & 7;
+          const int gc = n_tile * BN + col + lane;  // global column
+          const float is = __ldg(p.binvstd + gc), mu = __ldg(p.bmean + gc);
+          const float sc = is * __bfloat162float(p.bg[gc]);
+          const float sh = __bfloat162float(p.bb[gc]) - mu * sc;
+          float xv[32];
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            xv[r] = row0 + r < p.M ? __bfloat162float(p.bx[(row0 + r) * p.N + gc]) : 0.f;
+          float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            float gm = __bfloat162float(stg[r * 32 + 8 * (cc ^ ((r >> 1) & 3)) + ce]);
+            const float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(xv[r], sc, sh)));
+            gm = yk > 0.0f ? gm : 0.0f;   // rows beyond M: staged gm = 0
+            s1[r & 3] += gm;
+            s2[r & 3] += gm * ((xv[r] - mu) * is);
+          }
+          acc_s[nt * kChunks + c] += (s1[0] + s1[1]) + (s1[2] + s1[3]);
+          acc_q[nt * kChunks + c] += (s2[0] + s2[1]) + (s2[2] + s2[3]);
+        }
+        if (EPI == 1) {
           // column `lane` of the staged (stored) bf16 chunk, rows in order;
           // rows beyond M were staged as zeros
           const __nv_bfloat16* stg = reinterpret_cast<const __nv_bfloat16*>(S.cstage[ew][sbuf]);
@@ -440,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-    if (STATS) {
+    if (EPI != 0) {
       // lane l holds column part*BN/kParts + c*32 + l of this warp's 32 rows;
       // one partial row per lane quarter, the parts fill disjoint columns
       for (int nt = 0; nt < nts; ++nt) {
@@ -507,6 +541,41 @@ __global__ void __launch_bounds__(1024) partials_finalize_kernel(const float* __
   invstd[c] = (float)(1.0 / sqrt(var + (double)eps));
 }
 
+// BN backward from the partial rows (EPI 2): dbeta = sum gm, dgamma = sum
+// gm*xhat, and the dx coefficients A, B, D of bn_kernels.cu (dx = A*gm + B*x + D)
+__global__ void __launch_bounds__(1024) partials_bwd_finalize_kernel(
+    const float* __restrict__ part, int rows_part, int N, int64_t M, const float* __restrict__ mean,
+    const float* __restrict__ invstd, const __nv_bfloat16* __restrict__ g, float* __restrict__ dgamma,
+    float* __restrict__ dbeta, float* __restrict__ coef) {
+  __shared__ double sh[2][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double s = 0, q = 0;
+  if (c < N)
+    for (int r = w; r < rows_part; r += 32) {
+      s += (double)part[(size_t)r * 2 * N + c];
+      q += (double)part[(size_t)r * 2 * N + N + c];
+    }
+  sh[0][w][lane] = s;
+  sh[1][w][lane] = q;
+  __syncthreads();
+  if (w != 0 || c >= N) return;
+  s = 0;
+  q = 0;
+  for (int k = 0; k < 32; ++k) {
+    s += sh[0][k][lane];
+    q += sh[1][k][lane];
+  }
+  if (dbeta) dbeta[c] = (float)s;
+  if (dgamma) dgamma[c] = (float)q;
+  const double is = invstd[c], mu = mean[c];
+  const double gs = (double)__bfloat162float(g[c]) * is;
+  const double k1 = s / (double)M, k2 = q / (double)M;
+  coef[c] = (float)gs;
+  coef[N + c] = (float)(-gs * is * k2);
+  coef[2 * N + c] = (float)(gs * (mu * is * k2 - k1));
+}
+
 // ---------------------------------------------------------------------------
 // host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -550,10 +619,10 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int STAGES, bool PRO, bool STATS, bool ASTAT>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, int grid,
                    cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, STATS, ASTAT>;
+  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT>;
   const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT>) + 1024;
   static bool configured = false;  // per instantiation
   if (!configured) {
@@ -565,7 +634,7 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, bool STATS, bool ASTAT>
+template <int BN, bool PRO, int EPI, bool ASTAT>
 cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p,
                             int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
@@ -575,7 +644,7 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int stages = avail / stage_bytes > 8 ? 8 : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, STATS, ASTAT>(ma, mb, mc, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT>(ma, mb, mc, p, grid, s);
 }
 
 }  // namespace
@@ -586,9 +655,11 @@ bool conv1x1_supported(int64_t M, int N, int K) {
   return M > 0 && K >= kBK && K % kBK == 0 && K <= 65536 && (N == 64 || N == 128 || N % 256 == 0);
 }
 
-cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
-                             const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
-                             cudaStream_t s) {
+namespace {
+cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                         const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
+                         const void* bx, const float* bmean, const float* binvstd, const void* bg, const void* bb,
+                         cudaStream_t s) {
   if (!conv1x1_supported(M, N, K) || (pmean != nullptr && K > kMaxProK)) return cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return cudaErrorMisalignedAddress;
@@ -606,6 +677,13 @@ cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, i
   p.pinvstd = pinvstd;
   p.pg = static_cast<const __nv_bfloat16*>(pg);
   p.pb = static_cast<const __nv_bfloat16*>(pb);
+  p.bx = static_cast<const __nv_bfloat16*>(bx);
+  p.bmean = bmean;
+  p.binvstd = binvstd;
+  p.bg = static_cast<const __nv_bfloat16*>(bg);
+  p.bb = static_cast<const __nv_bfloat16*>(bb);
+  const bool bwd = bx != nullptr;
+  if (bwd && (pmean != nullptr || part == nullptr)) return cudaErrorInvalidValue;
   CUtensorMap ma, mb, mc;
   if (!make_map(&ma, A, M, K, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mb, B, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -622,18 +700,45 @@ cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, i
   if (part_rows) *part_rows = per * 4;  // every row and column written exactly once
 #define KRT_GEMM_BN(BNV)                                                                        \
   if (BN == BNV) {                                                                              \
-    if (astat && st) return dispatch_stages<BNV, true, true, true>(ma, mb, mc, p, grid, s);    \
-    if (astat) return dispatch_stages<BNV, true, false, true>(ma, mb, mc, p, grid, s);         \
-    if (pro && st) return dispatch_stages<BNV, true, true, false>(ma, mb, mc, p, grid, s);     \
-    if (pro) return dispatch_stages<BNV, true, false, false>(ma, mb, mc, p, grid, s);          \
-    if (st) return dispatch_stages<BNV, false, true, false>(ma, mb, mc, p, grid, s);           \
-    return dispatch_stages<BNV, false, false, false>(ma, mb, mc, p, grid, s);                  \
+    if (bwd) return dispatch_stages<BNV, false, 2, false>(ma, mb, mc, p, grid, s);             \
+    if (astat && st) return dispatch_stages<BNV, true, 1, true>(ma, mb, mc, p, grid, s);       \
+    if (astat) return dispatch_stages<BNV, true, 0, true>(ma, mb, mc, p, grid, s);             \
+    if (pro && st) return dispatch_stages<BNV, true, 1, false>(ma, mb, mc, p, grid, s);        \
+    if (pro) return dispatch_stages<BNV, true, 0, false>(ma, mb, mc, p, grid, s);              \
+    if (st) return dispatch_stages<BNV, false, 1, false>(ma, mb, mc, p, grid, s);              \
+    return dispatch_stages<BNV, false, 0, false>(ma, mb, mc, p, grid, s);                     \
   }
   KRT_GEMM_BN(64)
   KRT_GEMM_BN(128)
   KRT_GEMM_BN(256)
 #undef KRT_GEMM_BN
   return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                             const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
+                             cudaStream_t s) {
+  return conv1x1_impl(A, B, C, M, N, K, pmean, pinvstd, pg, pb, part, part_rows, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, s);
+}
+
+cudaError_t conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
+                             const float* mean, const float* invstd, const void* g, const void* b, float* part,
+                             int* part_rows, cudaStream_t s) {
+  if (x == nullptr || mean == nullptr || invstd == nullptr || g == nullptr || b == nullptr)
+    return cudaErrorInvalidValue;
+  return conv1x1_impl(dY, Wt, dX, M, N, K, nullptr, nullptr, nullptr, nullptr, part, part_rows, x, mean, invstd, g,
+                      b, s);
+}
+
+cudaError_t bn_partials_bwd_finalize(const float* part, int part_rows, int N, int64_t M, const float* mean,
+                                     const float* invstd, const void* g, float* dgamma, float* dbeta, float* coef,
+                                     cudaStream_t s) {
+  partials_bwd_finalize_kernel<<<(N + 31) / 32, 1024, 0, s>>>(part, part_rows, N, M, mean, invstd,
+                                                              static_cast<const __nv_bfloat16*>(g), dgamma, dbeta,
+                                                              coef);
+  return cudaGetLastError();
 }
 
 cudaError_t bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,

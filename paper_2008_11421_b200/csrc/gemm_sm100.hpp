@@ -11,6 +11,14 @@ size_t conv1x1_partials_bytes(int N);
 cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                              const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
                              cudaStream_t s);
+// dX[M,N] = dY[M,K] . Wt[N,K]^T (1x1 dgrad, Wt = the weights transposed) with
+// the backward reduce of the BN (+ReLU) whose input is x fused in the epilogue
+cudaError_t conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
+                             const float* mean, const float* invstd, const void* g, const void* b, float* part,
+                             int* part_rows, cudaStream_t s);
+cudaError_t bn_partials_bwd_finalize(const float* part, int part_rows, int N, int64_t M, const float* mean,
+                                     const float* invstd, const void* g, float* dgamma, float* dbeta, float* coef,
+                                     cudaStream_t s);
 cudaError_t bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
                                  float* invstd, cudaStream_t s);
 }  // namespace krt

@@ -94,6 +94,10 @@ BN_EPS = 1e-5
 # bottleneck 1x1 convolutions on the own tcgen05 GEMM (csrc/gemm_sm100.cu) with
 # the BN work fused in; KRT_TC_CONV1X1=0 selects cuDNN + separate BN kernels
 TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
+# conv3's backward data gradient on the same GEMM with BN2's reduce fused.  Off
+# by default: measured 3% slower per step than cuDNN dgrad + the bwd_reduce
+# kernel (3540 vs 3653 samples/s, same box); KRT_TC_DGRAD=1 selects it
+TC_DGRAD = os.environ.get("KRT_TC_DGRAD", "0") == "1"
 
 
 def _cl(t):
@@ -358,11 +362,21 @@ class BottleneckUnit(_ConvNetUnit):
                                                 dbeta=grads[8], dy2=dy2)
         del dy, dy2
         a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
-        da2, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0)
-        del dc3, a2
-        _cl(grads[6]).copy_(dw3)
-        dc2 = bnfused.backward(da2, c2, st[2], st[3], g2, b2, relu=True, dgamma=grads[4], dbeta=grads[5])
-        del da2
+        if self._tc1x1() and TC_DGRAD:
+            # conv3 dgrad on the tcgen05 GEMM with BN2's backward reduce in its
+            # epilogue; cuDNN keeps the weight gradient
+            _, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0, need_dx=False)
+            del a2
+            _cl(grads[6]).copy_(dw3)
+            dc2 = bnfused.conv1x1_dgrad_bn_backward(dc3, _cl(w3), c2, st[2], st[3], g2, b2,
+                                                    dgamma=grads[4], dbeta=grads[5])
+            del dc3
+        else:
+            da2, dw3, _ = _conv_bw(dc3, a2, _cl(w3), 1, 0)
+            del dc3, a2
+            _cl(grads[6]).copy_(dw3)
+            dc2 = bnfused.backward(da2, c2, st[2], st[3], g2, b2, relu=True, dgamma=grads[4], dbeta=grads[5])
+            del da2
         a1 = bnfused.apply(c1, st[0], st[1], g1, b1, relu=True)
         da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
         del dc2, a1

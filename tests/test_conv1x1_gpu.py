@@ -62,3 +62,32 @@ def test_conv1x1_ragged_rows_and_out():
     assert y.data_ptr() == out.data_ptr()
     ref = F.conv2d(x.float(), w.float())
     assert ((y.float() - ref).abs().max() / ref.abs().max()) < 1e-2
+
+
+@pytest.mark.parametrize("n,cin,cout,hw", [(2, 64, 256, 8), (3, 128, 512, 7), (1, 256, 1024, 6), (2, 512, 2048, 3),
+                                           (1, 64, 256, 13)])
+def test_conv1x1_dgrad_bn_backward(n, cin, cout, hw):
+    """dgrad of conv(relu(bn(x))) through the tcgen05 GEMM with the BN reduce in
+    its epilogue == torch conv dgrad + the standalone BN backward kernels:
+    dgamma/dbeta at fp32-reduction tolerance, dx at bf16 resolution."""
+    x = cl(rand((n, cin, hw, hw), 11, 1.5))
+    dy = cl(rand((n, cout, hw, hw), 12))
+    w = cl(rand((cout, cin, 1, 1), 13, cin ** -0.5))
+    g = (1 + 0.2 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+    b = (0.1 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+    m, i = torch.empty(cin, device="cuda"), torch.empty(cin, device="cuda")
+    bnfused.stats(x, m, i)
+    dg, db = torch.empty(cin, device="cuda"), torch.empty(cin, device="cuda")
+    dx = bnfused.conv1x1_dgrad_bn_backward(dy, w, x, m, i, g, b, dgamma=dg, dbeta=db)
+    # reference: torch dgrad in fp32, rounded to bf16 like the stored gradient, then the BN kernels
+    da = torch.nn.grad.conv2d_input(x.shape, w.float(), dy.float()).to(torch.bfloat16)
+    da = cl(da)
+    dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+    dx2 = bnfused.backward(da, x, m, i, g, b, relu=True, dgamma=dg2, dbeta=db2)
+    torch.testing.assert_close(db, db2, rtol=2e-3, atol=2e-2)
+    torch.testing.assert_close(dg, dg2, rtol=2e-3, atol=2e-2)
+    err = (dx.float() - dx2.float()).abs().max() / dx2.float().abs().max()
+    assert err < 2e-2, float(err)
+    # deterministic
+    dx3 = bnfused.conv1x1_dgrad_bn_backward(dy, w, x, m, i, g, b)
+    assert torch.equal(dx, dx3)

@@ -119,3 +119,16 @@ def test_preact_bf16_out_of_core_equals_in_core_and_tracks_oracle():
     xs, ys = batches(rec, 3)
     ref_losses, _ = resnet_oracle.train(units, init, xs, ys, lr=0.05)
     torch.testing.assert_close(torch.tensor(l_ooc), torch.tensor(ref_losses), rtol=3e-2, atol=3e-2)
+
+
+def test_resnet_fused_dgrad_path_matches_default(monkeypatch):
+    """The optional conv3 dgrad + BN2-reduce GEMM path (KRT_TC_DGRAD=1) trains
+    the bf16 ResNet plan to the same losses as the default path, within bf16
+    resolution."""
+    from paper_2008_11421_b200 import units as U
+    rec = W.load("resnet_small_bf16")
+    _, _, ref, _, _ = run(rec, iters=2)
+    monkeypatch.setattr(U, "TC_DGRAD", True)
+    _, _, got, _, _ = run(rec, iters=2)
+    for a, b in zip(got, ref):
+        assert abs(a - b) <= 2e-2 * abs(b), (got, ref)
