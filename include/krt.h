@@ -335,6 +335,19 @@ int krt_bn_backward_elemt(const void* dy, const void* x, const float* mean, cons
                           const void* gamma, const void* beta, const float* coef, const void* addend, int relu,
                           void* dx, int64_t rows, int C, void* stream);
 
+/* GPT layers (bf16 rows [T, H], H % 8 == 0).  h = LayerNorm(x [+ r]) with
+ * gamma/beta bf16 and the row mean/rstd (fp32) written; with r non-NULL the
+ * sum x2 = bf16(x + r) is stored too (residual add fused in front of the
+ * norm).  Deterministic: the backward recompute reproduces h bitwise. */
+int krt_ln_fwd(const void* x, const void* r, void* x2, const void* gamma, const void* beta, void* h,
+               float* mean, float* rstd, int64_t T, int H, float eps, void* stream);
+/* dx = gelu_tanh'(f) * dy and colsum[n] = sum_t dx[t, n] (fp32, the bias
+ * gradient of the layer that produced f) in one pass over the activations;
+ * ws: krt_gelu_bwd_colsum_workspace bytes. */
+size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N);
+int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@
 #include "bn_kernels.hpp"
 #include "pool_kernels.hpp"
 #include "gemm_sm100.hpp"
+#include "ln_kernels.hpp"
 #include "kernels.hpp"
 #include "runtime.hpp"
 
@@ -497,6 +498,18 @@ int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M,
                              float* invstd, void* stream) {
   KRT_CUDA_GUARD(bn_partials_finalize(part, part_rows, N, M, eps, mean, invstd, (cudaStream_t)stream),
                  "bn_partials_finalize");
+}
+
+int krt_ln_fwd(const void* x, const void* r, void* x2, const void* g, const void* b, void* h, float* mean, float* rstd,
+               int64_t T, int H, float eps, void* stream) {
+  KRT_CUDA_GUARD(ln_fwd(x, r, x2, g, b, h, mean, rstd, T, H, eps, (cudaStream_t)stream), "ln_fwd");
+}
+
+size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N) { return gelu_bwd_colsum_workspace(T, N); }
+
+int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,
+                        void* stream) {
+  KRT_CUDA_GUARD(gelu_bwd_colsum(dy, f, dx, colsum, ws, T, N, (cudaStream_t)stream), "gelu_bwd_colsum");
 }
 
 int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,

@@ -1,0 +1,40 @@
+"""Thin torch-facing wrappers of libkrt's GPT-layer kernels (csrc/ln_kernels.cu):
+LayerNorm with the residual add fused in front, and GELU backward with the
+bias-gradient column sums fused.  bf16 rows [T, H]; issued on torch's current
+stream (libkrt's compute stream inside the executor)."""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .bnfused import _timed, _ptr, _stream
+
+
+def supported(t: torch.Tensor) -> bool:
+    return t.is_cuda and t.dtype == torch.bfloat16 and t.shape[-1] % 8 == 0
+
+
+def ln_fwd(x, g, b, eps, mean, rstd, residual=None, x2_out=None):
+    """h = LayerNorm(x [+ residual]); with a residual the sum x2 is written to
+    x2_out (required).  mean/rstd: fp32 [T] outputs.  Returns h."""
+    T, H = x.shape
+    x = x.contiguous()
+    h = torch.empty_like(x)
+    nb = T * H * 2 * (4 if residual is not None else 2)
+    with _timed("ln_fwd", nb):
+        _lib.check(_lib.lib().krt_ln_fwd(x.data_ptr(), _ptr(residual), _ptr(x2_out), g.data_ptr(), b.data_ptr(),
+                                         h.data_ptr(), mean.data_ptr(), rstd.data_ptr(), T, H, float(eps),
+                                         _stream()))
+    return h
+
+
+def gelu_bwd_colsum(dy, f, colsum):
+    """dx = gelu_tanh'(f) * dy; colsum (fp32 [N]) = column sums of dx."""
+    T, N = f.shape
+    dy, f = dy.contiguous(), f.contiguous()
+    dx = torch.empty_like(f)
+    ws = torch.empty(_lib.lib().krt_gelu_bwd_colsum_workspace(T, N), dtype=torch.uint8, device=f.device)
+    with _timed("gelu_bwd_colsum", T * N * 2 * 3):
+        _lib.check(_lib.lib().krt_gelu_bwd_colsum(dy.data_ptr(), f.data_ptr(), dx.data_ptr(), colsum.data_ptr(),
+                                                  ws.data_ptr(), T, N, _stream()))
+    return dx

@@ -19,7 +19,7 @@ from typing import Optional
 import torch
 import torch.nn.functional as F
 
-from . import bnfused
+from . import bnfused, lnfused
 from .executor import SavedSpec, Unit, _align
 
 
@@ -838,18 +838,32 @@ def resnet1001_units(res: int = 2048, classes: int = 10, depth: int = 1001, act_
 LN_EPS = 1e-5
 
 
-def _ln_fw(x, g, b, mean, rstd):
+def _ln_fw(x, g, b, mean, rstd, residual=None, x2_out=None):
+    """LayerNorm(x [+ residual]); bf16 on the fused kernel (x2 = x + residual
+    written to x2_out), otherwise aten.  Returns the normalised rows."""
+    if lnfused.supported(x):
+        t = x.shape[0]
+        m = mean if mean is not None else torch.empty(t, device=x.device)
+        r = rstd if rstd is not None else torch.empty(t, device=x.device)
+        if residual is not None and x2_out is None:
+            x2_out = torch.empty_like(x)
+        h = lnfused.ln_fwd(x, g, b, LN_EPS, m, r, residual=residual, x2_out=x2_out)
+        return h, (x2_out if residual is not None else x)
+    if residual is not None:
+        x = torch.add(x, residual, out=x2_out) if x2_out is not None else x + residual
     y, m, r = _aten.native_layer_norm(x, [x.shape[-1]], g, b, LN_EPS)
     if mean is not None:
         mean.copy_(m.view(-1))
         rstd.copy_(r.view(-1))
-    return y, m, r
+    return y, x
 
 
 def _ln_apply(x, g, b, mean, rstd):
-    """The forward's LayerNorm output again: one native_layer_norm pass (its
-    statistics are recomputed bit-identically from the same input), instead
-    of an fp32 formula that materialised four [T, H] fp32 temporaries."""
+    """The forward's LayerNorm output again (deterministic recompute from the
+    same input: bitwise the forward's), one pass."""
+    if lnfused.supported(x):
+        t = x.shape[0]
+        return lnfused.ln_fwd(x, g, b, LN_EPS, torch.empty(t, device=x.device), torch.empty(t, device=x.device))
     return _aten.native_layer_norm(x, [x.shape[-1]], g, b, LN_EPS)[0]
 
 
@@ -876,9 +890,10 @@ def _mm_f32_into(a, b, out):
 
 
 def _linear_bw(dy, x, w, gw, gb, need_dx=True):
-    """y = x W^T + b: writes fp32 dW, db; returns dx."""
+    """y = x W^T + b: writes fp32 dW, db (gb None: already written); returns dx."""
     _mm_f32_into(dy.t(), x, gw)
-    torch.sum(dy, 0, dtype=torch.float32, out=gb)   # fp32 accumulation, no fp32 copy of dy
+    if gb is not None:
+        torch.sum(dy, 0, dtype=torch.float32, out=gb)   # fp32 accumulation, no fp32 copy of dy
     return torch.mm(dy, w) if need_dx else None
 
 
@@ -1007,14 +1022,14 @@ class TransformerLayerUnit(Unit):
         else:
             m1 = r1 = m2 = r2 = None
         sv = (lambda k: None) if saved is None else (lambda k: saved[k])
-        h1, _, _ = _ln_fw(x, g1, b1, m1, r1)
+        h1, _ = _ln_fw(x, g1, b1, m1, r1)
         qkv = _linear(h1, wqkv, bqkv, out=sv(1))          # GEMMs write straight into the saved slots
         del h1
         o = self._attn_fw(qkv, saved[6] if (saved is not None and self._flash()) else None)
         if saved is not None:
             saved[2].copy_(o)
-        x2 = torch.add(x, _linear(o, wo, bo), out=sv(3)) if saved is not None else x + _linear(o, wo, bo)
-        h2, _, _ = _ln_fw(x2, g2, b2, m2, r2)
+        # x2 = x + attn-proj and LN2(x2) in one kernel; x2 lands in its saved slot
+        h2, x2 = _ln_fw(x, g2, b2, m2, r2, residual=_linear(o, wo, bo), x2_out=sv(3))
         f1 = _linear(h2, w1, bf1, out=sv(4))
         del h2
         mlp = _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
@@ -1034,10 +1049,15 @@ class TransformerLayerUnit(Unit):
         gl = F.gelu(f1, approximate="tanh")
         dg = _linear_bw(dy, gl, w2, grads[10], grads[11])
         del gl
-        df1 = _aten.gelu_backward(dg, f1, approximate="tanh")
+        if lnfused.supported(f1):   # GELU backward + fc1's bias gradient in one pass
+            df1 = lnfused.gelu_bwd_colsum(dg, f1, grads[9])
+            gb1 = None
+        else:
+            df1 = _aten.gelu_backward(dg, f1, approximate="tanh")
+            gb1 = grads[9]
         del dg
         h2 = _ln_apply(x2, g2, b2, m2, r2)
-        dh2 = _linear_bw(df1, h2, w1, grads[8], grads[9])
+        dh2 = _linear_bw(df1, h2, w1, grads[8], gb1)
         del df1, h2
         dx2 = dy + _ln_bw(dh2, x2, g2, b2, m2, r2, grads[6], grads[7])
         del dh2
@@ -1085,7 +1105,7 @@ class LMHeadUnit(Unit):
             m, r = saved[1][:t], saved[1][t:]
         else:
             m = r = None
-        h, _, _ = _ln_fw(x, g, b, m, r)
+        h, _ = _ln_fw(x, g, b, m, r)
         return torch.mm(h, w.t())
 
     def backward(self, dlogits, params, saved, grads):
