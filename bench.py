@@ -401,6 +401,8 @@ def run_gpu(args, rec):
                  "backward_mean_occupancy_measured": b_busy / (b_busy + b_idle) if bsteps else None,
                  "note": "reference find_theta / report_from_steps semantics on the measured trace; "
                          "idle = stall_before > 1 ms counts as waiting"}
+    busy_in = sum(b - a for a, b in xin)
+    busy_out = sum(b - a for a, b in xout)
     swap_in_bytes = st["iter_bytes_h2d"]
     swap_out_bytes = st["iter_bytes_d2h"]
     # live roofline of our dominant kernel family (CUDA events on the compute stream)
@@ -466,7 +468,14 @@ def run_gpu(args, rec):
         "iteration_roofline": dict(terms, binding=bind, bound_s=terms[bind],
                                    frac=terms[bind] / iter_s,
                                    pcie_h2d_GBps=swap_in_bytes / iter_s / 1e9,
-                                   pcie_d2h_GBps=swap_out_bytes / iter_s / 1e9),
+                                   pcie_d2h_GBps=swap_out_bytes / iter_s / 1e9,
+                                   # while a transfer is in flight, against the probed link rate
+                                   pcie_h2d_active_GBps=(swap_in_bytes / busy_in / 1e9) if busy_in else None,
+                                   pcie_d2h_active_GBps=(swap_out_bytes / busy_out / 1e9) if busy_out else None,
+                                   pcie_h2d_active_frac_of_link=(swap_in_bytes / busy_in / PCIE_H2D) if busy_in else None,
+                                   pcie_d2h_active_frac_of_link=(swap_out_bytes / busy_out / PCIE_D2H) if busy_out else None,
+                                   pcie_link_GBps={"h2d": PCIE_H2D / 1e9, "d2h": PCIE_D2H / 1e9,
+                                                   "source": "scripts/probe_box.py (pinned cudaMemcpyAsync)"}),
         "overlap": {"compute_busy_frac": busy / span if span else None,
                     "exposed_stall_frac": 1 - busy / span if span else None,
                     "swap_in_busy_s": sum(b - a for a, b in xin),
