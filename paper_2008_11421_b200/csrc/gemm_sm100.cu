@@ -184,7 +184,7 @@ struct Params {
 constexpr int kMaxAstatK = 256;
 constexpr int kMaxNT = 8;  // n-tiles per CTA in A-stationary mode (N <= 2048)
 
-template <int BN, int STAGES, bool PRO, bool ASTAT>
+template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI>
 struct Smem {
   alignas(1024) uint8_t a[ASTAT ? kMaxAstatK / kBK : STAGES][kBM * kBK * 2];
   alignas(1024) uint8_t b[STAGES][BN * kBK * 2];
@@ -198,15 +198,20 @@ struct Smem {
   // chunk c of row r at c ^ ((r >> 1) & 3)), so row-per-lane writes and
   // column-per-lane reads are both free of bank conflicts
   alignas(1024) uint8_t cstage[kEpiWarps][2][32 * 64];
+  // EPI 2: the BN input x of the current tile pair, TMA-loaded by the producer
+  // ahead of the epilogue (row-major [128][BN]); one buffer per accumulator
+  alignas(128) uint8_t xt[EPI == 2 ? 2 : 1][EPI == 2 ? kBM * BN * 2 : 16];
+  uint64_t x_full[2], x_empty[2];
 };
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C
 template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
-                                                              const __grid_constant__ CUtensorMap map_c, Params p) {
+                                                              const __grid_constant__ CUtensorMap map_c,
+                                                              const __grid_constant__ CUtensorMap map_x, Params p) {
   extern __shared__ uint8_t smem_raw[];
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT>*>(
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblocks = p.K / kBK;
@@ -226,6 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.tfull[i], 1);
       mbar_init(&S.tempty[i], 128 * (BN >= 128 ? 4 : BN / 32));  // active epilogue threads
+      mbar_init(&S.x_full[i], 1);
+      mbar_init(&S.x_empty[i], 128 * (BN >= 128 ? 4 : BN / 32));
     }
     for (int kb = 0; kb < kMaxAstatK / kBK; ++kb) {
       mbar_init(&S.a_full[kb], 1);
@@ -243,8 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0, aphase = 0;
+      int stage = 0, xb = 0;
+      uint32_t phase = 0, aphase = 0, xphase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         if (ASTAT) {  // this m-tile's A k-blocks, each once the previous m-tile's last MMA on it is done
           for (int kb = 0; kb < kblocks; ++kb) {
@@ -256,6 +263,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         }
         for (int nt = 0; nt < nts; ++nt) {
           const int n_tile = ASTAT ? nt : n_fixed;
+          if (EPI == 2) {  // the BN input tile the epilogue of this (m, n) tile reads
+            mbar_wait(&S.x_empty[xb], xphase ^ 1);
+            mbar_expect_tx(&S.x_full[xb], kBM * BN * 2);
+            tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb], n_tile * BN, mt * kBM);
+            if (++xb == 2) {
+              xb = 0;
+              xphase ^= 1;
+            }
+          }
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&S.empty[stage], phase ^ 1);
             if (ASTAT) {
@@ -388,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
      for (int nt = 0; nt < nts; ++nt) {
       const int n_tile = ASTAT ? nt : n_fixed;
       mbar_wait(&S.tfull[acc], acc_phase);
+      if (EPI == 2) mbar_wait(&S.x_full[acc], acc_phase);  // x tiles alternate with the accumulators
       tc_fence_after();
       const int64_t row0 = (int64_t)mt * kBM + q * 32;
       const bool valid = row0 + lane < p.M;
@@ -432,10 +449,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           const float is = __ldg(p.binvstd + gc), mu = __ldg(p.bmean + gc);
           const float sc = is * __bfloat162float(p.bg[gc]);
           const float sh = __bfloat162float(p.bb[gc]) - mu * sc;
+          // x of this (row, column) from the TMA-loaded tile (OOB rows are zeros)
+          const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(S.xt[acc]) + (q * 32) * BN + col + lane;
           float xv[32];
 #pragma unroll
-          for (int r = 0; r < 32; ++r)
-            xv[r] = row0 + r < p.M ? __bfloat162float(p.bx[(row0 + r) * p.N + gc]) : 0.f;
+          for (int r = 0; r < 32; ++r) xv[r] = __bfloat162float(xs[r * BN]);
           float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
@@ -467,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(&S.tempty[acc]);
+      if (EPI == 2) mbar_arrive(&S.x_empty[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -620,31 +639,31 @@ int num_sms() {
 }
 
 template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
-cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p, int grid,
-                   cudaStream_t s) {
+cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
+                   const Params& p, int grid, cudaStream_t s) {
   auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT>) + 1024;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT, EPI>) + 1024;
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k<<<grid, kThreads, smem, s>>>(ma, mb, mc, p);
+  k<<<grid, kThreads, smem, s>>>(ma, mb, mc, mx, p);
   return cudaGetLastError();
 }
 
 template <int BN, bool PRO, int EPI, bool ASTAT>
-cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Params& p,
-                            int grid, cudaStream_t s) {
+cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                            const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
   constexpr int fixed = (PRO ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
-                        (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0);
+                        (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * kBK * 2;
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int stages = avail / stage_bytes > 8 ? 8 : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, EPI, ASTAT>(ma, mb, mc, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT>(ma, mb, mc, mx, p, grid, s);
 }
 
 }  // namespace
@@ -663,7 +682,9 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   if (!conv1x1_supported(M, N, K) || (pmean != nullptr && K > kMaxProK)) return cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return cudaErrorMisalignedAddress;
-  const int BN = N <= 256 ? N : 256;
+  const bool bwd_mode = bx != nullptr;
+  // the BN-backward epilogue keeps two x tiles in shared memory: 128-column tiles
+  const int BN = bwd_mode ? (N < 128 ? N : 128) : (N <= 256 ? N : 256);
   Params p{};
   p.M = M;
   p.N = N;
@@ -684,11 +705,16 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   p.bb = static_cast<const __nv_bfloat16*>(bb);
   const bool bwd = bx != nullptr;
   if (bwd && (pmean != nullptr || part == nullptr)) return cudaErrorInvalidValue;
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb, mc, mx;
   if (!make_map(&ma, A, M, K, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mb, B, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
+  if (bwd_mode) {
+    if (!make_map(&mx, bx, M, N, kBM, BN, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  } else {
+    mx = mc;  // unused
+  }
   const bool pro = pmean != nullptr, st = part != nullptr;
   // A-stationary when the prologue would otherwise transform the same A tile once per n-tile
   const bool astat = pro && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
@@ -698,15 +724,19 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   if (per > p.m_tiles) per = p.m_tiles;
   const int grid = astat ? per : per * p.n_tiles;
   if (part_rows) *part_rows = per * 4;  // every row and column written exactly once
-#define KRT_GEMM_BN(BNV)                                                                        \
-  if (BN == BNV) {                                                                              \
-    if (bwd) return dispatch_stages<BNV, false, 2, false>(ma, mb, mc, p, grid, s);             \
-    if (astat && st) return dispatch_stages<BNV, true, 1, true>(ma, mb, mc, p, grid, s);       \
-    if (astat) return dispatch_stages<BNV, true, 0, true>(ma, mb, mc, p, grid, s);             \
-    if (pro && st) return dispatch_stages<BNV, true, 1, false>(ma, mb, mc, p, grid, s);        \
-    if (pro) return dispatch_stages<BNV, true, 0, false>(ma, mb, mc, p, grid, s);              \
-    if (st) return dispatch_stages<BNV, false, 1, false>(ma, mb, mc, p, grid, s);              \
-    return dispatch_stages<BNV, false, 0, false>(ma, mb, mc, p, grid, s);                     \
+  if (bwd) {
+    if (BN == 64) return dispatch_stages<64, false, 2, false>(ma, mb, mc, mx, p, grid, s);
+    if (BN == 128) return dispatch_stages<128, false, 2, false>(ma, mb, mc, mx, p, grid, s);
+    return cudaErrorInvalidValue;
+  }
+#define KRT_GEMM_BN(BNV)                                                                          \
+  if (BN == BNV) {                                                                                \
+    if (astat && st) return dispatch_stages<BNV, true, 1, true>(ma, mb, mc, mx, p, grid, s);     \
+    if (astat) return dispatch_stages<BNV, true, 0, true>(ma, mb, mc, mx, p, grid, s);           \
+    if (pro && st) return dispatch_stages<BNV, true, 1, false>(ma, mb, mc, mx, p, grid, s);      \
+    if (pro) return dispatch_stages<BNV, true, 0, false>(ma, mb, mc, mx, p, grid, s);            \
+    if (st) return dispatch_stages<BNV, false, 1, false>(ma, mb, mc, mx, p, grid, s);            \
+    return dispatch_stages<BNV, false, 0, false>(ma, mb, mc, mx, p, grid, s);                   \
   }
   KRT_GEMM_BN(64)
   KRT_GEMM_BN(128)

@@ -95,8 +95,9 @@ BN_EPS = 1e-5
 # the BN work fused in; KRT_TC_CONV1X1=0 selects cuDNN + separate BN kernels
 TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
 # conv3's backward data gradient on the same GEMM with BN2's reduce fused.  Off
-# by default: measured 3% slower per step than cuDNN dgrad + the bwd_reduce
-# kernel (3540 vs 3653 samples/s, same box); KRT_TC_DGRAD=1 selects it
+# by default: measured 1% slower per step than cuDNN dgrad + the bwd_reduce
+# kernel (3643-3655 vs 3685-3689 samples/s, same box, with the x tile
+# TMA-prefetched); KRT_TC_DGRAD=1 selects it
 TC_DGRAD = os.environ.get("KRT_TC_DGRAD", "0") == "1"
 
 
