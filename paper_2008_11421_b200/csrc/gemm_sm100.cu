@@ -210,9 +210,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c,
                                                               const __grid_constant__ CUtensorMap map_x, Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // the dynamic shared-memory window starts 1024-aligned (no static shared
+  // memory in this kernel); using it directly keeps every access in the shared
+  // address space (an integer round-up made them generic LD.E/ST.E)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI>*>(smem_raw);
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblocks = p.K / kBK;
   // this CTA's tiles: m-tiles strided; either a fixed n-tile (grid is a
@@ -393,10 +396,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     const int half = ew >> 2;                     // this warp's column part
     constexpr int kChunks = BN / 32 / kParts;     // 32-column chunks per part
     if (half < kParts) {                          // BN = 64: two parts only
-    constexpr int kNT = ASTAT ? kMaxNT : 1;
-    float acc_s[kNT * kChunks], acc_q[kNT * kChunks];
+    // statistics: one partial row per (m-group, lane quarter); lane = column.
+    // Fixed n-tile: accumulated in registers, written once at the end.
+    // A-stationary (the n-tile varies per tile): accumulated in the thread's
+    // own slots of the partial rows, written on the first m-tile and
+    // read-modify-written (L2) after it (no dynamically indexed local arrays)
+    float* part_row = EPI != 0 ? p.part + ((size_t)m_first * 4 + q) * 2 * p.N : nullptr;
+    float acc_s[kChunks], acc_q[kChunks];
 #pragma unroll
-    for (int c = 0; c < kNT * kChunks; ++c) acc_s[c] = acc_q[c] = 0.f;
+    for (int c = 0; c < kChunks; ++c) acc_s[c] = acc_q[c] = 0.f;
     int acc = 0;
     uint32_t acc_phase = 0;
     int sbuf = 0;
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       tc_fence_after();
       const int64_t row0 = (int64_t)mt * kBM + q * 32;
       const bool valid = row0 + lane < p.M;
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < kChunks; ++c) {
         const int col = half * (BN / kParts) + c * 32;  // within the tile
         float v[32];
@@ -463,8 +471,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             s1[r & 3] += gm;
             s2[r & 3] += gm * ((xv[r] - mu) * is);
           }
-          acc_s[nt * kChunks + c] += (s1[0] + s1[1]) + (s1[2] + s1[3]);
-          acc_q[nt * kChunks + c] += (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          const float t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          if (ASTAT) {
+            float* slot = part_row + (size_t)n_tile * BN + col + lane;
+            if (mt == m_first) {
+              slot[0] = t1;
+              slot[p.N] = t2;
+            } else {
+              slot[0] += t1;
+              slot[p.N] += t2;
+            }
+          } else {
+            acc_s[c] += t1;
+            acc_q[c] += t2;
+          }
         }
         if (EPI == 1) {
           // column `lane` of the staged (stored) bf16 chunk, rows in order;
@@ -478,8 +498,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             s1[r & 3] += x;
             s2[r & 3] = __fmaf_rn(x, x, s2[r & 3]);
           }
-          acc_s[nt * kChunks + c] += (s1[0] + s1[1]) + (s1[2] + s1[3]);
-          acc_q[nt * kChunks + c] += (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          const float t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          if (ASTAT) {
+            float* slot = part_row + (size_t)n_tile * BN + col + lane;
+            if (mt == m_first) {
+              slot[0] = t1;
+              slot[p.N] = t2;
+            } else {
+              slot[0] += t1;
+              slot[p.N] += t2;
+            }
+          } else {
+            acc_s[c] += t1;
+            acc_q[c] += t2;
+          }
         }
         sbuf ^= 1;
       }
@@ -493,17 +525,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-    if (EPI != 0) {
-      // lane l holds column part*BN/kParts + c*32 + l of this warp's 32 rows;
-      // one partial row per lane quarter, the parts fill disjoint columns
-      for (int nt = 0; nt < nts; ++nt) {
-        const int n_tile = ASTAT ? nt : n_fixed;
-        float* out = p.part + ((size_t)m_first * 4 + q) * 2 * p.N + (size_t)n_tile * BN + half * (BN / kParts);
+    if (EPI != 0 && !ASTAT) {
+      float* out = part_row + (size_t)n_fixed * BN + half * (BN / kParts);
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c) {
-          out[c * 32 + lane] = acc_s[nt * kChunks + c];
-          out[p.N + c * 32 + lane] = acc_q[nt * kChunks + c];
-        }
+      for (int c = 0; c < kChunks; ++c) {
+        out[c * 32 + lane] = acc_s[c];
+        out[p.N + c * 32 + lane] = acc_q[c];
       }
     }
     }
@@ -642,7 +669,7 @@ template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
   auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT, EPI>) + 1024;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT, EPI>);
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
