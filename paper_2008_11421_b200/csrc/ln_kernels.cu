@@ -115,68 +115,80 @@ __global__ void __launch_bounds__(32 * kRowsPerCta) ln_fwd_reg_kernel(
     float* __restrict__ mean, float* __restrict__ rstd, int64_t T, int H, float eps) {
   const int lane = threadIdx.x & 31;
   const int oct = H / 8;
-  // persistent: warps stride the rows (a CTA per 8 rows made launch overhead a
-  // large share of a 60 KB CTA)
+  // persistent: warps stride the rows.  The row stays packed (bf16, 4
+  // registers per octet) and is unpacked per pass: half the registers of an
+  // fp32 copy, so twice the warps (rows in flight) per SM.
   for (int64_t row = (int64_t)blockIdx.x * kRowsPerCta + (threadIdx.x >> 5); row < T;
        row += (int64_t)gridDim.x * kRowsPerCta) {
-  uint4 ux[J], ur[J];
+    uint4 ux[J];
 #pragma unroll
-  for (int i = 0; i < J; ++i) {
-    const int j = lane + 32 * i;
-    if (j < oct) {
-      ux[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * H) + j);
-      if (RES) ur[i] = __ldcs(reinterpret_cast<const uint4*>(r + row * H) + j);
+    for (int i = 0; i < J; ++i) {
+      const int j = lane + 32 * i;
+      if (j < oct) ux[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * H) + j);
     }
-  }
-  float a[J][8];
-  float s = 0.f;
+    if (RES) {
+      uint4 ur[J];
 #pragma unroll
-  for (int i = 0; i < J; ++i) {
-    const int j = lane + 32 * i;
-    if (j < oct) {
-      unpack8(ux[i], a[i]);
-      if (RES) {
-        float c[8];
-        unpack8(ur[i], c);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) a[i][k] = __fadd_rn(a[i][k], c[k]);
-        const uint4 u = pack8(a[i]);
-        reinterpret_cast<uint4*>(x2 + row * H)[j] = u;
-        unpack8(u, a[i]);
+      for (int i = 0; i < J; ++i) {
+        const int j = lane + 32 * i;
+        if (j < oct) ur[i] = __ldcs(reinterpret_cast<const uint4*>(r + row * H) + j);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += a[i][k];
-    }
-  }
-  const float mu = warp_sum(s) / (float)H;
-  float q = 0.f;
+      for (int i = 0; i < J; ++i) {
+        const int j = lane + 32 * i;
+        if (j < oct) {
+          float a[8], c[8];
+          unpack8(ux[i], a);
+          unpack8(ur[i], c);
 #pragma unroll
-  for (int i = 0; i < J; ++i) {
-    if (lane + 32 * i < oct) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float d = a[i][k] - mu;
-        q = __fmaf_rn(d, d, q);
+          for (int k = 0; k < 8; ++k) a[k] = __fadd_rn(a[k], c[k]);
+          ux[i] = pack8(a);  // the stored, rounded sum
+          reinterpret_cast<uint4*>(x2 + row * H)[j] = ux[i];
+        }
       }
     }
-  }
-  const float rs = rsqrtf(warp_sum(q) / (float)H + eps);
-  if (lane == 0) {
-    mean[row] = mu;
-    rstd[row] = rs;
-  }
+    float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < J; ++i) {
-    const int j = lane + 32 * i;
-    if (j < oct) {
-      float gg[8], bb[8];
-      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
-      unpack8(__ldg(reinterpret_cast<const uint4*>(b) + j), bb);
+    for (int i = 0; i < J; ++i) {
+      if (lane + 32 * i < oct) {
+        float a[8];
+        unpack8(ux[i], a);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) a[i][k] = __fmaf_rn((a[i][k] - mu) * rs, gg[k], bb[k]);
-      reinterpret_cast<uint4*>(h + row * H)[j] = pack8(a[i]);
+        for (int k = 0; k < 8; ++k) s += a[k];
+      }
     }
-  }
+    const float mu = warp_sum(s) / (float)H;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      if (lane + 32 * i < oct) {
+        float a[8];
+        unpack8(ux[i], a);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float d = a[k] - mu;
+          q = __fmaf_rn(d, d, q);
+        }
+      }
+    }
+    const float rs = rsqrtf(warp_sum(q) / (float)H + eps);
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const int j = lane + 32 * i;
+      if (j < oct) {
+        float a[8], gg[8], bb[8];
+        unpack8(ux[i], a);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(b) + j), bb);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __fmaf_rn((a[k] - mu) * rs, gg[k], bb[k]);
+        reinterpret_cast<uint4*>(h + row * H)[j] = pack8(a);
+      }
+    }
   }
 }
 
@@ -275,7 +287,7 @@ cudaError_t ln_fwd(const void* x, const void* r, void* x2, const void* g, const 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = (T + kRowsPerCta - 1) / kRowsPerCta, cap = (int64_t)sms * 4;
+    const int64_t want = (T + kRowsPerCta - 1) / kRowsPerCta, cap = (int64_t)sms * 8;
     const dim3 pgrid((unsigned)(want < cap ? want : cap));
     if (r) ln_fwd_reg_kernel<true, 8><<<pgrid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
     else ln_fwd_reg_kernel<false, 8><<<pgrid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
