@@ -134,17 +134,30 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart
+// UMMA shared-memory descriptor, K-major, for a k-block of BKT bf16 per row
+// (row = 2*BKT bytes = the swizzle span: 128 B -> SWIZZLE_128B, 64 B ->
+// SWIZZLE_64B, 32 B -> SWIZZLE_32B), 8-row atoms 8 rows apart
 // (cute/arch/mma_sm100_desc.hpp SmemDescriptor: start>>4 [0,14), LBO>>4 [16,30),
-// SBO>>4 [32,46), version 1 [46,48), base offset [49,52), layout [61,64) = 2)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+// SBO>>4 [32,46), version 1 [46,48), base offset [49,52), layout [61,64))
+template <int BKT>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t smem_addr) {
+  constexpr uint64_t layout = BKT == 64 ? 2 : (BKT == 32 ? 4 : 6);  // SW128 / SW64 / SW32
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;               // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;     // SBO: next 8-row group
-  d |= (uint64_t)1 << 46;               // version
-  d |= (uint64_t)2 << 61;               // SWIZZLE_128B
+  d |= (uint64_t)1 << 16;                         // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((8 * BKT * 2) >> 4) << 32;      // SBO: next 8-row group
+  d |= (uint64_t)1 << 46;                         // version
+  d |= layout << 61;
   return d;
+}
+
+// physical 16-byte chunk of logical chunk jj in row r under the TMA swizzle
+// matching a BKT-wide row (address bits [4,..) ^= bits [7,..))
+template <int BKT>
+__device__ __forceinline__ int swz_chunk(int jj, int r) {
+  if constexpr (BKT == 64) return jj ^ (r & 7);
+  else if constexpr (BKT == 32) return jj ^ ((r >> 1) & 3);
+  else return jj ^ ((r >> 2) & 1);
 }
 
 // instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M=128, N
@@ -184,10 +197,10 @@ struct Params {
 constexpr int kMaxAstatK = 256;
 constexpr int kMaxNT = 8;  // n-tiles per CTA in A-stationary mode (N <= 2048)
 
-template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI>
+template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT>
 struct Smem {
-  alignas(1024) uint8_t a[ASTAT ? kMaxAstatK / kBK : STAGES][kBM * kBK * 2];
-  alignas(1024) uint8_t b[STAGES][BN * kBK * 2];
+  alignas(1024) uint8_t a[ASTAT ? kMaxAstatK / kBK : STAGES][kBM * BKT * 2];
+  alignas(1024) uint8_t b[STAGES][BN * BKT * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
   uint64_t tfull[2], tempty[2];
   uint64_t a_full[kMaxAstatK / kBK], a_ready[kMaxAstatK / kBK], a_free[kMaxAstatK / kBK];  // A-stationary, per k-block
@@ -205,7 +218,7 @@ struct Smem {
 };
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c,
@@ -214,10 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // memory in this kernel); using it directly keeps every access in the shared
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI>*>(smem_raw);
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI, BKT>*>(smem_raw);
+  static_assert(!ASTAT || BKT == kBK, "A-stationary uses 64-wide k-blocks");
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kblocks = p.K / kBK;
+  const int kblocks = p.K / BKT;
   // this CTA's tiles: m-tiles strided; either a fixed n-tile (grid is a
   // multiple of n_tiles) or, A-stationary, every n-tile of each m-tile
   const int nts = ASTAT ? p.n_tiles : 1;
@@ -259,8 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         if (ASTAT) {  // this m-tile's A k-blocks, each once the previous m-tile's last MMA on it is done
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&S.a_free[kb], aphase ^ 1);
-            mbar_expect_tx(&S.a_full[kb], kBM * kBK * 2);
-            tma_load_2d(&map_a, &S.a_full[kb], S.a[kb], kb * kBK, mt * kBM);
+            mbar_expect_tx(&S.a_full[kb], kBM * BKT * 2);
+            tma_load_2d(&map_a, &S.a_full[kb], S.a[kb], kb * BKT, mt * kBM);
           }
           aphase ^= 1;
         }
@@ -278,12 +292,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&S.empty[stage], phase ^ 1);
             if (ASTAT) {
-              mbar_expect_tx(&S.full[stage], BN * kBK * 2);
+              mbar_expect_tx(&S.full[stage], BN * BKT * 2);
             } else {
-              mbar_expect_tx(&S.full[stage], (kBM + BN) * kBK * 2);
-              tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * kBK, mt * kBM);
+              mbar_expect_tx(&S.full[stage], (kBM + BN) * BKT * 2);
+              tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, mt * kBM);
             }
-            tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * kBK, n_tile * BN);
+            tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -312,9 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           if (lane == 0) {
             const uint32_t a0 = smem_u32(ASTAT ? S.a[kb] : S.a[stage]), b0 = smem_u32(S.b[stage]);
 #pragma unroll
-            for (int k = 0; k < kBK / kUmmaK; ++k)
-              umma_bf16(d_tmem, sw128_desc(a0 + k * kUmmaK * 2), sw128_desc(b0 + k * kUmmaK * 2), idesc,
-                        (kb | k) != 0);
+            for (int k = 0; k < BKT / kUmmaK; ++k)
+              umma_bf16(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
+                        idesc, (kb | k) != 0);
             umma_commit(&S.empty[stage]);                       // smem stage free when these MMAs finish
             if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
             if (ASTAT && nt == nts - 1) umma_commit(&S.a_free[kb]);  // A k-block no longer read
@@ -336,7 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // ------------------------------------------------------------ prologue transform
     if (PRO) {
       const int xt = threadIdx.x - kXfWarp0 * 32;  // 0..255
-      const int r = xt & 127, jh = 4 * (xt >> 7);  // tile row, first logical chunk
+      constexpr int kPer = BKT / 16;                // 16-byte chunks per thread (two threads per row)
+      const int r = xt & 127, jh = kPer * (xt >> 7);  // tile row, first logical chunk
       // the previous BN's affine, exactly as bn_apply computes it
       for (int c = xt; c < p.K; c += kXfThreads) {
         float sc = p.pinvstd[c] * __bfloat162float(p.pg[c]);
@@ -347,18 +362,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       int stage = 0;
       uint32_t phase = 0, aphase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
-        // a = bf16(relu(a*sc + sh)) in place.  SWIZZLE_128B: logical 16-byte
-        // chunk jj of row r (channels kb*64 + 8*jj .. +8) is physical chunk jj ^ (r & 7)
+        // a = bf16(relu(a*sc + sh)) in place.  Logical 16-byte chunk jj of row r
+        // (channels kb*BKT + 8*jj .. +8) is physical chunk swz_chunk(jj, r)
         for (int kb = 0; kb < kblocks; ++kb) {
           if (ASTAT) mbar_wait(&S.a_full[kb], aphase);
           else mbar_wait(&S.full[stage], phase);
-          uint4* rowp = reinterpret_cast<uint4*>((ASTAT ? S.a[kb] : S.a[stage]) + r * 128);
-          uint4 u[4];
+          uint4* rowp = reinterpret_cast<uint4*>((ASTAT ? S.a[kb] : S.a[stage]) + r * BKT * 2);
+          uint4 u[kPer];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) u[i] = rowp[(jh + i) ^ (r & 7)];  // consecutive rows: distinct columns
+          for (int i = 0; i < kPer; ++i) u[i] = rowp[swz_chunk<BKT>(jh + i, r)];  // consecutive rows: distinct columns
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int c0 = kb * kBK + 8 * (jh + i);
+          for (int i = 0; i < kPer; ++i) {
+            const int c0 = kb * BKT + 8 * (jh + i);
             const float4 sa = *reinterpret_cast<const float4*>(&S.sc[c0]);
             const float4 sb = *reinterpret_cast<const float4*>(&S.sc[c0 + 4]);
             const float4 ha = *reinterpret_cast<const float4*>(&S.sh[c0]);
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
               h[e] = __floats2bfloat162_rn(fmaxf(__fmaf_rn(f.x, sc[2 * e], sh[2 * e]), 0.f),
                                            fmaxf(__fmaf_rn(f.y, sc[2 * e + 1], sh[2 * e + 1]), 0.f));
             }
-            rowp[(jh + i) ^ (r & 7)] = u[i];
+            rowp[swz_chunk<BKT>(jh + i, r)] = u[i];
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
           if (ASTAT) {
@@ -665,11 +680,11 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT, EPI>);
+  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT>;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT, EPI, BKT>);
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -680,17 +695,18 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, int EPI, bool ASTAT>
+template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK>
 cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                             const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
   constexpr int fixed = (PRO ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
                         (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0);
-  constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * kBK * 2;
+  constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
-  constexpr int stages = avail / stage_bytes > 8 ? 8 : avail / stage_bytes;
+  constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
+  constexpr int stages = avail / stage_bytes > max_stages ? max_stages : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, EPI, ASTAT>(ma, mb, mc, mx, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT, BKT>(ma, mb, mc, mx, p, grid, s);
 }
 
 }  // namespace
@@ -698,7 +714,7 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
 size_t conv1x1_partials_bytes(int N) { return (size_t)num_sms() * 4 * 2 * N * sizeof(float); }
 
 bool conv1x1_supported(int64_t M, int N, int K) {
-  return M > 0 && K >= kBK && K % kBK == 0 && K <= 65536 && (N == 64 || N == 128 || N % 256 == 0);
+  return M > 0 && (K == 16 || K == 32 || K % kBK == 0) && K <= 65536 && (N == 64 || N == 128 || N % 256 == 0);
 }
 
 namespace {
@@ -732,9 +748,13 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   p.bb = static_cast<const __nv_bfloat16*>(bb);
   const bool bwd = bx != nullptr;
   if (bwd && (pmean != nullptr || part == nullptr)) return cudaErrorInvalidValue;
+  // narrow reductions (K = 16, 32: the first stages of ResNet-1001) use one
+  // K-wide k-block whose row is the 32/64-byte swizzle span
+  const int bkt = K < kBK ? K : kBK;
+  const CUtensorMapSwizzle ksw = bkt == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                           : (bkt == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   CUtensorMap ma, mb, mc, mx;
-  if (!make_map(&ma, A, M, K, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&mb, B, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
+  if (!make_map(&ma, A, M, K, kBM, bkt, ksw) || !make_map(&mb, B, N, K, BN, bkt, ksw) ||
       !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
   if (bwd_mode) {
@@ -744,13 +764,31 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   }
   const bool pro = pmean != nullptr, st = part != nullptr;
   // A-stationary when the prologue would otherwise transform the same A tile once per n-tile
-  const bool astat = pro && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
+  const bool astat = pro && bkt == kBK && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
   // whole n-tile groups (or, A-stationary, whole m-tiles), at most one CTA per SM
   int per = astat ? num_sms() : num_sms() / p.n_tiles;
   if (per < 1) per = 1;
   if (per > p.m_tiles) per = p.m_tiles;
   const int grid = astat ? per : per * p.n_tiles;
   if (part_rows) *part_rows = per * 4;  // every row and column written exactly once
+  if (bkt != kBK) {  // no A-stationary / BN-backward instantiations for narrow k-blocks
+    if (bwd) return cudaErrorInvalidValue;
+#define KRT_GEMM_NARROW(BNV, BKV)                                                                  \
+  if (BN == BNV && bkt == BKV) {                                                                  \
+    if (pro && st) return dispatch_stages<BNV, true, 1, false, BKV>(ma, mb, mc, mx, p, grid, s); \
+    if (pro) return dispatch_stages<BNV, true, 0, false, BKV>(ma, mb, mc, mx, p, grid, s);       \
+    if (st) return dispatch_stages<BNV, false, 1, false, BKV>(ma, mb, mc, mx, p, grid, s);       \
+    return dispatch_stages<BNV, false, 0, false, BKV>(ma, mb, mc, mx, p, grid, s);               \
+  }
+    KRT_GEMM_NARROW(64, 16)
+    KRT_GEMM_NARROW(128, 16)
+    KRT_GEMM_NARROW(256, 16)
+    KRT_GEMM_NARROW(64, 32)
+    KRT_GEMM_NARROW(128, 32)
+    KRT_GEMM_NARROW(256, 32)
+#undef KRT_GEMM_NARROW
+    return cudaErrorInvalidValue;
+  }
   if (bwd) {
     if (BN == 64) return dispatch_stages<64, false, 2, false>(ma, mb, mc, mx, p, grid, s);
     if (BN == 128) return dispatch_stages<128, false, 2, false>(ma, mb, mc, mx, p, grid, s);
