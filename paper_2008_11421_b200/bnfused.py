@@ -178,7 +178,7 @@ def relu_maxpool_backward(dy, c, mean, invstd, g, b, k=3, s=2, p=1):
 
 
 def conv1x1_supported(cin, cout, pre=False):
-    return (cin in (16, 32) or cin % 64 == 0) and (cout in (64, 128) or cout % 256 == 0) and (not pre or cin <= 1024)
+    return (cin in (16, 32) or cin % 64 == 0) and (cout in (16, 32, 64, 128) or cout % 256 == 0) and (not pre or cin <= 1024)
 
 
 def conv1x1(x, w, out=None, pre=None, stats=None):

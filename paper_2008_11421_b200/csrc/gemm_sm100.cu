@@ -134,6 +134,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// 32 lanes x 16 consecutive fp32 columns (narrow n-tiles)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 // UMMA shared-memory descriptor, K-major, for a k-block of BKT bf16 per row
 // (row = 2*BKT bytes = the swizzle span: 128 B -> SWIZZLE_128B, 64 B ->
 // SWIZZLE_64B, 32 B -> SWIZZLE_32B), 8-row atoms 8 rows apart
@@ -228,10 +242,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI, BKT>*>(smem_raw);
-  static_assert(!ASTAT || BKT == kBK, "A-stationary uses 64-wide k-blocks");
+  static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblocks = p.K / BKT;
+  // epilogue column parts: one warp per (part, TMEM lane quarter)
+  constexpr int kEpiParts = BN >= 128 ? 4 : (BN >= 64 ? BN / 32 : 1);
   // this CTA's tiles: m-tiles strided; either a fixed n-tile (grid is a
   // multiple of n_tiles) or, A-stationary, every n-tile of each m-tile
   const int nts = ASTAT ? p.n_tiles : 1;
@@ -247,9 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.tfull[i], 1);
-      mbar_init(&S.tempty[i], 128 * (BN >= 128 ? 4 : BN / 32));  // active epilogue threads
+      mbar_init(&S.tempty[i], 128 * kEpiParts);  // active epilogue threads
       mbar_init(&S.x_full[i], 1);
-      mbar_init(&S.x_empty[i], 128 * (BN >= 128 ? 4 : BN / 32));
+      mbar_init(&S.x_empty[i], 128 * kEpiParts);
     }
     for (int kb = 0; kb < kMaxAstatK / kBK; ++kb) {
       mbar_init(&S.a_full[kb], 1);
@@ -407,9 +423,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // ------------------------------------------------------------ epilogue warps
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
     const int ew = warp - kEpiWarp0;              // 0..15
-    constexpr int kParts = BN >= 128 ? 4 : BN / 32;  // column parts (one warp per part and quarter)
+    constexpr int kCW = BN < 32 ? BN : 32;        // chunk width: 32 columns (16 for BN = 16)
+    constexpr int kParts = kEpiParts;
     const int half = ew >> 2;                     // this warp's column part
-    constexpr int kChunks = BN / 32 / kParts;     // 32-column chunks per part
+    constexpr int kChunks = BN / kCW / kParts;    // chunks per part
     if (half < kParts) {                          // BN = 64: two parts only
     // statistics: one partial row per (m-group, lane quarter); lane = column.
     // Fixed n-tile: accumulated in registers, written once at the end.
@@ -433,15 +450,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       const bool valid = row0 + lane < p.M;
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
-        const int col = half * (BN / kParts) + c * 32;  // within the tile
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
+        const int col = half * (BN / kParts) + c * kCW;  // within the tile
+        float v[kCW];
+        if constexpr (kCW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
+        else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
         // this warp's staging buffer must be free: the TMA store issued two chunks ago has read it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
-        uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * 64);
+        uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * kCW * 2);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kCW / 8; ++j) {
           uint4 u;
           __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
@@ -449,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             h[e] = valid ? __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1])
                          : __floats2bfloat162_rn(0.f, 0.f);
           }
-          st[j ^ ((lane >> 1) & 3)] = u;
+          st[swz_chunk<kCW>(j, lane)] = u;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -503,17 +521,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         }
         if (EPI == 1) {
           // column `lane` of the staged (stored) bf16 chunk, rows in order;
-          // rows beyond M were staged as zeros
+          // rows beyond M were staged as zeros.  16-wide chunks: lanes 16..31
+          // take rows 16..31 of the same columns, folded in with one shuffle
           const __nv_bfloat16* stg = reinterpret_cast<const __nv_bfloat16*>(S.cstage[ew][sbuf]);
-          const int cc = lane >> 3, ce = lane & 7;  // logical chunk, element
+          const int cl = lane % kCW, cc = cl >> 3, ce = cl & 7;  // column, logical chunk, element
+          constexpr int kRows = kCW == 32 ? 32 : 16;
+          const int rb = lane / kCW * kRows;
           float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent chains
 #pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            float x = __bfloat162float(stg[r * 32 + 8 * (cc ^ ((r >> 1) & 3)) + ce]);
-            s1[r & 3] += x;
-            s2[r & 3] = __fmaf_rn(x, x, s2[r & 3]);
+          for (int i = 0; i < kRows; ++i) {
+            const int r = rb + i;
+            float x = __bfloat162float(stg[r * kCW + 8 * swz_chunk<kCW>(cc, r) + ce]);
+            s1[i & 3] += x;
+            s2[i & 3] = __fmaf_rn(x, x, s2[i & 3]);
           }
-          const float t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          float t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+          if constexpr (kCW == 16) {
+            t1 += __shfl_down_sync(0xffffffffu, t1, 16);
+            t2 += __shfl_down_sync(0xffffffffu, t2, 16);
+          }
           if (ASTAT) {
             float* slot = part_row + (size_t)n_tile * BN + col + lane;
             if (mt == m_first) {
@@ -544,8 +570,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       float* out = part_row + (size_t)n_fixed * BN + half * (BN / kParts);
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
-        out[c * 32 + lane] = acc_s[c];
-        out[p.N + c * 32 + lane] = acc_q[c];
+        if (lane < kCW) {
+          out[c * kCW + lane] = acc_s[c];
+          out[p.N + c * kCW + lane] = acc_q[c];
+        }
       }
     }
     }
@@ -714,7 +742,8 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
 size_t conv1x1_partials_bytes(int N) { return (size_t)num_sms() * 4 * 2 * N * sizeof(float); }
 
 bool conv1x1_supported(int64_t M, int N, int K) {
-  return M > 0 && (K == 16 || K == 32 || K % kBK == 0) && K <= 65536 && (N == 64 || N == 128 || N % 256 == 0);
+  return M > 0 && (K == 16 || K == 32 || K % kBK == 0) && K <= 65536 &&
+         (N == 16 || N == 32 || N == 64 || N == 128 || N % 256 == 0);
 }
 
 namespace {
@@ -747,7 +776,7 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   p.bg = static_cast<const __nv_bfloat16*>(bg);
   p.bb = static_cast<const __nv_bfloat16*>(bb);
   const bool bwd = bx != nullptr;
-  if (bwd && (pmean != nullptr || part == nullptr)) return cudaErrorInvalidValue;
+  if (bwd && (pmean != nullptr || part == nullptr || N < 64)) return cudaErrorInvalidValue;
   // narrow reductions (K = 16, 32: the first stages of ResNet-1001) use one
   // K-wide k-block whose row is the 32/64-byte swizzle span
   const int bkt = K < kBK ? K : kBK;
@@ -755,7 +784,7 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
                                            : (bkt == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   CUtensorMap ma, mb, mc, mx;
   if (!make_map(&ma, A, M, K, kBM, bkt, ksw) || !make_map(&mb, B, N, K, BN, bkt, ksw) ||
-      !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      !make_map(&mc, C, M, N, 32, N < 32 ? N : 32, N < 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
   if (bwd_mode) {
     if (!make_map(&mx, bx, M, N, kBM, BN, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
@@ -780,9 +809,13 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
     if (st) return dispatch_stages<BNV, false, 1, false, BKV>(ma, mb, mc, mx, p, grid, s);       \
     return dispatch_stages<BNV, false, 0, false, BKV>(ma, mb, mc, mx, p, grid, s);               \
   }
+    KRT_GEMM_NARROW(16, 16)
+    KRT_GEMM_NARROW(32, 16)
     KRT_GEMM_NARROW(64, 16)
     KRT_GEMM_NARROW(128, 16)
     KRT_GEMM_NARROW(256, 16)
+    KRT_GEMM_NARROW(16, 32)
+    KRT_GEMM_NARROW(32, 32)
     KRT_GEMM_NARROW(64, 32)
     KRT_GEMM_NARROW(128, 32)
     KRT_GEMM_NARROW(256, 32)
@@ -802,6 +835,17 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
     if (pro) return dispatch_stages<BNV, true, 0, false>(ma, mb, mc, mx, p, grid, s);            \
     if (st) return dispatch_stages<BNV, false, 1, false>(ma, mb, mc, mx, p, grid, s);            \
     return dispatch_stages<BNV, false, 0, false>(ma, mb, mc, mx, p, grid, s);                   \
+  }
+  if (BN < 64) {  // one n-tile: never A-stationary
+    if (BN == 16) return pro ? (st ? dispatch_stages<16, true, 1, false>(ma, mb, mc, mx, p, grid, s)
+                                   : dispatch_stages<16, true, 0, false>(ma, mb, mc, mx, p, grid, s))
+                             : (st ? dispatch_stages<16, false, 1, false>(ma, mb, mc, mx, p, grid, s)
+                                   : dispatch_stages<16, false, 0, false>(ma, mb, mc, mx, p, grid, s));
+    if (BN == 32) return pro ? (st ? dispatch_stages<32, true, 1, false>(ma, mb, mc, mx, p, grid, s)
+                                   : dispatch_stages<32, true, 0, false>(ma, mb, mc, mx, p, grid, s))
+                             : (st ? dispatch_stages<32, false, 1, false>(ma, mb, mc, mx, p, grid, s)
+                                   : dispatch_stages<32, false, 0, false>(ma, mb, mc, mx, p, grid, s));
+    return cudaErrorInvalidValue;
   }
   KRT_GEMM_BN(64)
   KRT_GEMM_BN(128)

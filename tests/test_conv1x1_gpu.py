@@ -24,7 +24,10 @@ def cl(t):
                                            (1, 512, 2048, 3), (2, 1024, 256, 6), (2, 256, 1024, 6),
                                            (1, 64, 2048, 5), (3, 128, 512, 17),
                                            # narrow reductions: one 16/32-wide k-block (SWIZZLE_32B/64B)
-                                           (2, 16, 64, 8), (3, 32, 128, 9), (2, 16, 256, 7), (1, 32, 64, 17)])
+                                           (2, 16, 64, 8), (3, 32, 128, 9), (2, 16, 256, 7), (1, 32, 64, 17),
+                                           # narrow n-tiles: 16/32-column accumulators and epilogue
+                                           (2, 64, 16, 8), (3, 128, 32, 9), (1, 16, 16, 17), (2, 32, 32, 13),
+                                           (2, 256, 64, 11)])
 @pytest.mark.parametrize("pre", [False, True])
 def test_conv1x1_matches_torch(n, cin, cout, hw, pre):
     x = cl(rand((n, cin, hw, hw), 1, 2.0))
