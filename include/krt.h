@@ -308,14 +308,21 @@ int krt_bn_relu_maxpool_bwd(const void* dy, const void* x, const float* mean, co
  * of device scratch) the epilogue also reduces the per-output-channel sums of
  * the stored C and C^2 into *part_rows partial rows, which
  * krt_bn_partials_finalize turns into mean/invstd: no statistics pass re-reads C.
- * Requirements: K % 64 == 0, N in {64, 128} or N % 256 == 0,
- * 16-byte aligned pointers. */
+ * Requirements: K in {16, 32} or K % 64 == 0, N in {16, 32, 64, 128} or
+ * N % 256 == 0, 16-byte aligned pointers. */
 size_t krt_conv1x1_partials_bytes(int N);
 int krt_conv1x1_bn(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                    const float* pinvstd, const void* pgamma, const void* pbeta, float* part, int* part_rows,
                    void* stream);
 int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M, float eps, float* mean,
                              float* invstd, void* stream);
+/* krt_conv1x1_bn plus a residual read in the epilogue: C = f(A) . B^T + res
+ * (res [M, N] bf16, summed in fp32 before the one bf16 rounding; the partial
+ * statistics are those of the stored sum).  The pre-activation bottleneck's
+ * last convolution and shortcut add in one pass. */
+int krt_conv1x1_bn_res(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                       const float* pinvstd, const void* pgamma, const void* pbeta, const void* res, float* part,
+                       int* part_rows, void* stream);
 /* Backward of a 1x1 convolution fused with the reduce of the BN (+ ReLU) in
  * front of it: dX[M,N] = dY[M,K] . Wt[N,K]^T (Wt = weights transposed, K-major)
  * is stored, and with x = that BN's input the epilogue reduces sum(gm) and

@@ -181,13 +181,15 @@ def conv1x1_supported(cin, cout, pre=False):
     return (cin in (16, 32) or cin % 64 == 0) and (cout in (16, 32, 64, 128) or cout % 256 == 0) and (not pre or cin <= 1024)
 
 
-def conv1x1(x, w, out=None, pre=None, stats=None):
+def conv1x1(x, w, out=None, pre=None, stats=None, res=None):
     """Stride-1 1x1 convolution on the sm_100a tcgen05 GEMM (csrc/gemm_sm100.cu).
 
     x: (N, Cin, H, W) channels_last bf16; w: (Cout, Cin, 1, 1) bf16.
     pre=(mean, invstd, gamma, beta): convolve relu(bn(x)) instead of x, without
     writing relu(bn(x)).  stats=(mean, invstd): fp32 outputs, the batch
     statistics of the (bf16) result, reduced in the GEMM epilogue.
+    res: (N, Cout, H, W) channels_last bf16 added to the result in the
+    epilogue (fp32 sum, one rounding).
     """
     import ctypes as C
     x = _nhwc(x)
@@ -205,9 +207,17 @@ def conv1x1(x, w, out=None, pre=None, stats=None):
         part = torch.empty(_lib.lib().krt_conv1x1_partials_bytes(cout) // 4, dtype=torch.float32, device=x.device)
     pm, pi, pg, pb = pre if pre is not None else (None, None, None, None)
     # bytes: A read, C written (the statistics pass this replaces would re-read C)
-    with _timed("conv1x1_bn", M * (cin + cout) * 2, 2.0 * M * cin * cout):
-        _lib.check(_lib.lib().krt_conv1x1_bn(x.data_ptr(), wm.data_ptr(), y.data_ptr(), M, cout, cin, _ptr(pm),
-                                             _ptr(pi), _ptr(pg), _ptr(pb), _ptr(part), C.byref(rows), _stream()))
+    if res is not None:
+        res = _nhwc(res)
+        assert res.shape == y.shape and res.dtype == y.dtype
+    with _timed("conv1x1_bn", M * (cin + cout * (1 if res is None else 2)) * 2, 2.0 * M * cin * cout):
+        if res is None:
+            _lib.check(_lib.lib().krt_conv1x1_bn(x.data_ptr(), wm.data_ptr(), y.data_ptr(), M, cout, cin, _ptr(pm),
+                                                 _ptr(pi), _ptr(pg), _ptr(pb), _ptr(part), C.byref(rows), _stream()))
+        else:
+            _lib.check(_lib.lib().krt_conv1x1_bn_res(x.data_ptr(), wm.data_ptr(), y.data_ptr(), M, cout, cin,
+                                                     _ptr(pm), _ptr(pi), _ptr(pg), _ptr(pb), res.data_ptr(),
+                                                     _ptr(part), C.byref(rows), _stream()))
         if stats is not None:
             _lib.check(_lib.lib().krt_bn_partials_finalize(part.data_ptr(), rows.value, cout, M, EPS,
                                                            stats[0].data_ptr(), stats[1].data_ptr(), _stream()))

@@ -472,6 +472,14 @@ int krt_conv1x1_bn(const void* A, const void* B, void* C, int64_t M, int N, int 
                  "conv1x1_bn");
 }
 
+int krt_conv1x1_bn_res(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                       const float* pinvstd, const void* pg, const void* pb, const void* res, float* part,
+                       int* part_rows, void* stream) {
+  KRT_CUDA_GUARD(
+      conv1x1_bn_res_fprop(A, B, C, M, N, K, pmean, pinvstd, pg, pb, res, part, part_rows, (cudaStream_t)stream),
+      "conv1x1_bn_res");
+}
+
 int krt_conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
                          const float* mean, const float* invstd, const void* g, const void* b, float* part,
                          int* part_rows, void* stream) {

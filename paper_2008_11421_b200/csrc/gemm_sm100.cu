@@ -202,6 +202,9 @@ struct Params {
   const float* binvstd;
   const __nv_bfloat16* bg;
   const __nv_bfloat16* bb;
+  // residual (nullptr: none): C = acc + res, res [M, N] bf16 row-major,
+  // added in fp32 before the single bf16 rounding (EPI 0/1)
+  const __nv_bfloat16* res;
 };
 
 // ASTAT (A-stationary, prologue only, K <= kMaxAstatK): the transformed A tile
@@ -451,6 +454,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
         const int col = half * (BN / kParts) + c * kCW;  // within the tile
+        uint4 rv[kCW / 8];
+        if (EPI != 2 && p.res != nullptr) {  // in flight while the accumulator is read
+          const uint4* rp = reinterpret_cast<const uint4*>(p.res + (row0 + lane) * p.N + n_tile * BN + col);
+#pragma unroll
+          for (int j = 0; j < kCW / 8; ++j) rv[j] = valid ? __ldg(rp + j) : make_uint4(0, 0, 0, 0);
+        }
         float v[kCW];
         if constexpr (kCW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
         else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
@@ -460,6 +469,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * kCW * 2);
 #pragma unroll
         for (int j = 0; j < kCW / 8; ++j) {
+          if (EPI != 2 && p.res != nullptr) {
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[j]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(rh[e]);
+              v[8 * j + 2 * e] += f.x;
+              v[8 * j + 2 * e + 1] += f.y;
+            }
+          }
           uint4 u;
           __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
@@ -750,7 +768,7 @@ namespace {
 cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                          const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
                          const void* bx, const float* bmean, const float* binvstd, const void* bg, const void* bb,
-                         cudaStream_t s) {
+                         const void* res, cudaStream_t s) {
   if (!conv1x1_supported(M, N, K) || (pmean != nullptr && K > kMaxProK)) return cudaErrorInvalidValue;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return cudaErrorMisalignedAddress;
@@ -775,8 +793,10 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   p.binvstd = binvstd;
   p.bg = static_cast<const __nv_bfloat16*>(bg);
   p.bb = static_cast<const __nv_bfloat16*>(bb);
+  p.res = static_cast<const __nv_bfloat16*>(res);
+  if (res != nullptr && (reinterpret_cast<uintptr_t>(res) & 15)) return cudaErrorMisalignedAddress;
   const bool bwd = bx != nullptr;
-  if (bwd && (pmean != nullptr || part == nullptr || N < 64)) return cudaErrorInvalidValue;
+  if (bwd && (pmean != nullptr || part == nullptr || N < 64 || res != nullptr)) return cudaErrorInvalidValue;
   // narrow reductions (K = 16, 32: the first stages of ResNet-1001) use one
   // K-wide k-block whose row is the 32/64-byte swizzle span
   const int bkt = K < kBK ? K : kBK;
@@ -859,7 +879,15 @@ cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, i
                              const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
                              cudaStream_t s) {
   return conv1x1_impl(A, B, C, M, N, K, pmean, pinvstd, pg, pb, part, part_rows, nullptr, nullptr, nullptr, nullptr,
-                      nullptr, s);
+                      nullptr, nullptr, s);
+}
+
+cudaError_t conv1x1_bn_res_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                                 const float* pinvstd, const void* pg, const void* pb, const void* res, float* part,
+                                 int* part_rows, cudaStream_t s) {
+  if (res == nullptr) return cudaErrorInvalidValue;
+  return conv1x1_impl(A, B, C, M, N, K, pmean, pinvstd, pg, pb, part, part_rows, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, res, s);
 }
 
 cudaError_t conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
@@ -868,7 +896,7 @@ cudaError_t conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M
   if (x == nullptr || mean == nullptr || invstd == nullptr || g == nullptr || b == nullptr)
     return cudaErrorInvalidValue;
   return conv1x1_impl(dY, Wt, dX, M, N, K, nullptr, nullptr, nullptr, nullptr, part, part_rows, x, mean, invstd, g,
-                      b, s);
+                      b, nullptr, s);
 }
 
 cudaError_t bn_partials_bwd_finalize(const float* part, int part_rows, int N, int64_t M, const float* mean,

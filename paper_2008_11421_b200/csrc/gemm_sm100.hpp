@@ -11,6 +11,10 @@ size_t conv1x1_partials_bytes(int N);
 cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                              const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
                              cudaStream_t s);
+// as conv1x1_bn_fprop, plus a residual: C = f(A) . B^T + res (res [M, N] bf16)
+cudaError_t conv1x1_bn_res_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
+                                 const float* pinvstd, const void* pg, const void* pb, const void* res, float* part,
+                                 int* part_rows, cudaStream_t s);
 // dX[M,N] = dY[M,K] . Wt[N,K]^T (1x1 dgrad, Wt = the weights transposed) with
 // the backward reduce of the BN (+ReLU) whose input is x fused in the epilogue
 cudaError_t conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,

@@ -658,6 +658,35 @@ class PreActBottleneckUnit(_ConvNetUnit):
 
     writes_out = True
 
+    def _tc1x1(self):
+        # both 1x1 convolutions on the tcgen05 GEMM (K and N down to 16)
+        return (self.act == torch.bfloat16 and TC_CONV1X1
+                and all(bnfused.supported(c) for c in (self.cin, self.w))
+                and bnfused.conv1x1_supported(self.cin, self.w, pre=True)
+                and bnfused.conv1x1_supported(self.w, self.cout, pre=True))
+
+    def _forward_tc(self, x, params, st, sv, out):
+        """relu(bn0) applied in conv1's prologue (a0 never written unless the
+        shortcut is strided), BN1 statistics from conv1's epilogue, relu(bn2)
+        in conv3's prologue and the shortcut added in its epilogue."""
+        g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
+        _stats_fw(x, st[0], st[1])
+        bn0 = (st[0], st[1], g0, b0)
+        c1 = bnfused.conv1x1(x, _cl(w1), out=sv(1), pre=bn0, stats=(st[2], st[3]))
+        if not self.down:
+            sc = x
+        elif self.s == 1 and bnfused.conv1x1_supported(self.cin, self.cout, pre=True):
+            sc = bnfused.conv1x1(x, _cl(params[9]), pre=bn0)
+        else:
+            a0 = _bn_relu(x, st[0], st[1], g0, b0)
+            sc = _conv(a0, _cl(params[9]), self.s, 0)
+            del a0
+        a1 = _bn_relu(c1, st[2], st[3], g1, b1)
+        c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
+        del a1
+        _stats_fw(c2, st[4], st[5])
+        return bnfused.conv1x1(c2, _cl(w3), out=out, pre=(st[4], st[5], g2, b2), res=sc)
+
     def forward(self, x, params, saved, out=None):
         g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
         if saved is not None:
@@ -666,6 +695,8 @@ class PreActBottleneckUnit(_ConvNetUnit):
         else:
             st = self._st(torch.empty(self._nstats(), device=x.device))
         sv = (lambda k: None) if saved is None else (lambda k: _cl(saved[k]))
+        if self._tc1x1():
+            return self._forward_tc(x, params, st, sv, out)
         a0 = _stats_bn_relu(x, st[0], st[1], g0, b0)
         c1 = _conv_into(a0, _cl(w1), 1, 0, sv(1))
         sc = _conv(a0, _cl(params[9]), self.s, 0) if self.down else x

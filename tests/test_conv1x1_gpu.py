@@ -96,3 +96,30 @@ def test_conv1x1_dgrad_bn_backward(n, cin, cout, hw):
     # deterministic
     dx3 = bnfused.conv1x1_dgrad_bn_backward(dy, w, x, m, i, g, b)
     assert torch.equal(dx, dx3)
+
+
+@pytest.mark.parametrize("n,cin,cout,hw", [(2, 16, 64, 8), (2, 32, 128, 9), (2, 64, 256, 7), (1, 128, 512, 13),
+                                           (2, 64, 16, 6)])
+def test_conv1x1_residual_epilogue(n, cin, cout, hw):
+    """C = relu(bn(x)) . W^T + res with the statistics of the stored sum (the
+    pre-activation bottleneck's conv3 + shortcut)."""
+    x = cl(rand((n, cin, hw, hw), 5, 2.0))
+    w = cl(rand((cout, cin, 1, 1), 6, cin ** -0.5))
+    res = cl(rand((n, cout, hw, hw), 7))
+    g = (1 + 0.2 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+    b = (0.1 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+    m, i = torch.empty(cin, device="cuda"), torch.empty(cin, device="cuda")
+    bnfused.stats(x, m, i)
+    a = bnfused.apply(x, m, i, g, b, relu=True)
+    sm, si = torch.empty(cout, device="cuda"), torch.empty(cout, device="cuda")
+    y = bnfused.conv1x1(x, w, pre=(m, i, g, b), stats=(sm, si), res=res)
+    y0 = bnfused.conv1x1(x, w, pre=(m, i, g, b), res=res)
+    torch.cuda.synchronize()
+    ref = F.conv2d(a.float(), w.float()) + res.float()
+    err = (y.float() - ref).abs().max() / ref.abs().max()
+    assert err < 1e-2, float(err)
+    assert torch.equal(y, y0)
+    rm, ri = torch.empty_like(sm), torch.empty_like(si)
+    bnfused.stats(y, rm, ri)
+    torch.testing.assert_close(sm, rm, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(si, ri, rtol=1e-4, atol=1e-5)

@@ -132,3 +132,17 @@ def test_resnet_fused_dgrad_path_matches_default(monkeypatch):
     _, _, got, _, _ = run(rec, iters=2)
     for a, b in zip(got, ref):
         assert abs(a - b) <= 2e-2 * abs(b), (got, ref)
+
+
+def test_preact_gemm_path_matches_cudnn_path(monkeypatch):
+    """The pre-activation bottleneck on the tcgen05 GEMM (BN+ReLU prologues,
+    statistics and shortcut-add epilogues) trains the bf16 preact plan to the
+    cuDNN + separate-BN-kernel losses within bf16 resolution."""
+    from paper_2008_11421_b200 import units as U
+    rec = W.load("preact29_small_bf16")
+    units, _, got, _, _ = run(rec, iters=2, lr=0.05)
+    assert all(u._tc1x1() for u in units if isinstance(u, U.PreActBottleneckUnit))
+    monkeypatch.setattr(U, "TC_CONV1X1", False)
+    _, _, ref, _, _ = run(rec, iters=2, lr=0.05)
+    for a, b in zip(got, ref):
+        assert abs(a - b) <= 2e-2 * abs(b), (got, ref)
