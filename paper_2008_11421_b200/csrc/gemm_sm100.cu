@@ -214,12 +214,19 @@ struct Params {
 constexpr int kMaxAstatK = 256;
 constexpr int kMaxNT = 8;  // n-tiles per CTA in A-stationary mode (N <= 2048)
 
+// EPI 3 residual tiles: [BN / kResW boxes][128 rows][kResW columns], each box
+// TMA-loaded with the swizzle of its row width, kResBufs tiles in flight
+template <int BN>
+constexpr int kResW = BN < 64 ? BN : 64;
+template <int BN>
+constexpr int kResBufs = BN <= 64 ? 4 : 2;
+
 template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT>
 struct Smem {
   alignas(1024) uint8_t a[ASTAT ? kMaxAstatK / kBK : STAGES][kBM * BKT * 2];
   alignas(1024) uint8_t b[STAGES][BN * BKT * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
-  uint64_t tfull[2], tempty[2];
+  uint64_t tfull[4], tempty[4];
   uint64_t a_full[kMaxAstatK / kBK], a_ready[kMaxAstatK / kBK], a_free[kMaxAstatK / kBK];  // A-stationary, per k-block
   uint32_t tmem_base;
   alignas(16) float sc[PRO ? kMaxProK : 4];
@@ -229,12 +236,14 @@ struct Smem {
   // column-per-lane reads are both free of bank conflicts
   alignas(1024) uint8_t cstage[kEpiWarps][2][32 * 64];
   // EPI 2: the BN input x of the current tile pair, TMA-loaded by the producer
-  // ahead of the epilogue (row-major [128][BN]); one buffer per accumulator
-  alignas(128) uint8_t xt[EPI == 2 ? 2 : 1][EPI == 2 ? kBM * BN * 2 : 16];
-  uint64_t x_full[2], x_empty[2];
+  // ahead of the epilogue (row-major [128][BN]); one buffer per accumulator.
+  // EPI 3: the residual tiles (swizzled boxes), kResBufs deep
+  alignas(1024) uint8_t xt[EPI == 2 ? 2 : (EPI == 3 ? kResBufs<BN> : 1)][EPI >= 2 ? kBM * BN * 2 : 16];
+  uint64_t x_full[4], x_empty[4];
 };
 
-// EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C
+// EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C,
+// 3 C = acc + residual (p.res through map_x)
 template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
@@ -249,8 +258,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblocks = p.K / BKT;
-  // epilogue column parts: one warp per (part, TMEM lane quarter)
+  // epilogue column parts: one warp per (part, TMEM lane quarter); the 16
+  // epilogue warps form kEpiGroups groups that drain alternate tiles, each
+  // from its own accumulator (kAcc >= 2 accumulators in TMEM)
   constexpr int kEpiParts = BN >= 128 ? 4 : (BN >= 64 ? BN / 32 : 1);
+  constexpr int kEpiGroups = 4 / kEpiParts;
+  constexpr int kAcc = kEpiGroups > 2 ? kEpiGroups : 2;
+  static_assert(EPI != 2 || kAcc == 2, "EPI 2 x tiles are double-buffered with the accumulators");
   // this CTA's tiles: m-tiles strided; either a fixed n-tile (grid is a
   // multiple of n_tiles) or, A-stationary, every n-tile of each m-tile
   const int nts = ASTAT ? p.n_tiles : 1;
@@ -264,9 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       mbar_init(&S.ready[s], kXfThreads);
       mbar_init(&S.empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {  // accumulators; x / residual buffers (<= 4 each)
       mbar_init(&S.tfull[i], 1);
-      mbar_init(&S.tempty[i], 128 * kEpiParts);  // active epilogue threads
+      mbar_init(&S.tempty[i], 128 * kEpiParts);  // one tile group's epilogue threads
       mbar_init(&S.x_full[i], 1);
       mbar_init(&S.x_empty[i], 128 * kEpiParts);
     }
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(&S.tmem_base, 2 * BN);
+  if (warp == 1) tmem_alloc(&S.tmem_base, kAcc * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -299,11 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         }
         for (int nt = 0; nt < nts; ++nt) {
           const int n_tile = ASTAT ? nt : n_fixed;
-          if (EPI == 2) {  // the BN input tile the epilogue of this (m, n) tile reads
+          if (EPI >= 2) {  // the BN input / residual tile the epilogue of this (m, n) tile reads
+            constexpr int kXB = EPI == 2 ? 2 : kResBufs<BN>;
+            constexpr int kW = EPI == 2 ? BN : kResW<BN>;
             mbar_wait(&S.x_empty[xb], xphase ^ 1);
             mbar_expect_tx(&S.x_full[xb], kBM * BN * 2);
-            tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb], n_tile * BN, mt * kBM);
-            if (++xb == 2) {
+#pragma unroll
+            for (int b = 0; b < BN / kW; ++b)
+              tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb] + b * kBM * kW * 2, n_tile * BN + b * kW, mt * kBM);
+            if (++xb == kXB) {
               xb = 0;
               xphase ^= 1;
             }
@@ -358,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             phase ^= 1;
           }
         }
-        if (++acc == 2) {
+        if (++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -428,38 +446,47 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     const int ew = warp - kEpiWarp0;              // 0..15
     constexpr int kCW = BN < 32 ? BN : 32;        // chunk width: 32 columns (16 for BN = 16)
     constexpr int kParts = kEpiParts;
-    const int half = ew >> 2;                     // this warp's column part
+    const int half = (ew >> 2) % kParts;          // this warp's column part
+    const int grp = (ew >> 2) / kParts;           // this warp's tile group
     constexpr int kChunks = BN / kCW / kParts;    // chunks per part
-    if (half < kParts) {                          // BN = 64: two parts only
-    // statistics: one partial row per (m-group, lane quarter); lane = column.
-    // Fixed n-tile: accumulated in registers, written once at the end.
+    {
+    // statistics: one partial row per (m-group, lane quarter, tile group); lane
+    // = column.  Fixed n-tile: accumulated in registers, written once at the end.
     // A-stationary (the n-tile varies per tile): accumulated in the thread's
-    // own slots of the partial rows, written on the first m-tile and
-    // read-modify-written (L2) after it (no dynamically indexed local arrays)
-    float* part_row = EPI != 0 ? p.part + ((size_t)m_first * 4 + q) * 2 * p.N : nullptr;
+    // own slots of the partial rows, zeroed first and read-modify-written (L2)
+    // per tile (no dynamically indexed local arrays)
+    constexpr bool kStats = EPI == 1 || EPI == 2;
+    float* part_row = kStats ? p.part + (((size_t)m_first * 4 + q) * kEpiGroups + grp) * 2 * p.N : nullptr;
+    if (ASTAT && kStats) {
+      for (int nt = 0; nt < nts; ++nt)
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+          float* slot = part_row + (size_t)nt * BN + half * (BN / kParts) + c * kCW + lane;
+          slot[0] = 0.f;
+          slot[p.N] = 0.f;
+        }
+    }
     float acc_s[kChunks], acc_q[kChunks];
 #pragma unroll
     for (int c = 0; c < kChunks; ++c) acc_s[c] = acc_q[c] = 0.f;
-    int acc = 0;
-    uint32_t acc_phase = 0;
     int sbuf = 0;
+    int t = -1;  // tile sequence number, as the MMA warp counts it
     for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
      for (int nt = 0; nt < nts; ++nt) {
+      if (++t % kEpiGroups != grp) continue;      // another group's tile
+      const int acc = t % kAcc;
+      const uint32_t acc_phase = (uint32_t)(t / kAcc) & 1u;
       const int n_tile = ASTAT ? nt : n_fixed;
-      mbar_wait(&S.tfull[acc], acc_phase);
-      if (EPI == 2) mbar_wait(&S.x_full[acc], acc_phase);  // x tiles alternate with the accumulators
-      tc_fence_after();
       const int64_t row0 = (int64_t)mt * kBM + q * 32;
       const bool valid = row0 + lane < p.M;
+      const int rb = EPI == 3 ? t % kResBufs<BN> : 0;  // residual buffer of this tile
+      mbar_wait(&S.tfull[acc], acc_phase);
+      if (EPI == 3) mbar_wait(&S.x_full[rb], (uint32_t)(t / kResBufs<BN>) & 1u);
+      if (EPI == 2) mbar_wait(&S.x_full[acc], acc_phase);  // x tiles alternate with the accumulators
+      tc_fence_after();
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
         const int col = half * (BN / kParts) + c * kCW;  // within the tile
-        uint4 rv[kCW / 8];
-        if (EPI != 2 && p.res != nullptr) {  // in flight while the accumulator is read
-          const uint4* rp = reinterpret_cast<const uint4*>(p.res + (row0 + lane) * p.N + n_tile * BN + col);
-#pragma unroll
-          for (int j = 0; j < kCW / 8; ++j) rv[j] = valid ? __ldg(rp + j) : make_uint4(0, 0, 0, 0);
-        }
         float v[kCW];
         if constexpr (kCW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
         else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
@@ -469,8 +496,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * kCW * 2);
 #pragma unroll
         for (int j = 0; j < kCW / 8; ++j) {
-          if (EPI != 2 && p.res != nullptr) {
-            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rv[j]);
+          if (EPI == 3) {
+            // chunk j of this row in its residual box (row-per-lane reads of
+            // the swizzled box: 8 lanes of a phase hit 8 distinct bank groups)
+            constexpr int RW = kResW<BN>;
+            const int row = q * 32 + lane, cb = col / RW, cj = (col % RW) / 8 + j;
+            const uint4 rw = *reinterpret_cast<const uint4*>(S.xt[rb] + cb * kBM * RW * 2 + row * RW * 2 +
+                                                             swz_chunk<RW>(cj, row) * 16);
+            const __nv_bfloat162* rh = reinterpret_cast<const __nv_bfloat162*>(&rw);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(rh[e]);
@@ -525,13 +558,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           const float t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
           if (ASTAT) {
             float* slot = part_row + (size_t)n_tile * BN + col + lane;
-            if (mt == m_first) {
-              slot[0] = t1;
-              slot[p.N] = t2;
-            } else {
-              slot[0] += t1;
-              slot[p.N] += t2;
-            }
+            slot[0] += t1;
+            slot[p.N] += t2;
           } else {
             acc_s[c] += t1;
             acc_q[c] += t2;
@@ -560,13 +588,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           }
           if (ASTAT) {
             float* slot = part_row + (size_t)n_tile * BN + col + lane;
-            if (mt == m_first) {
-              slot[0] = t1;
-              slot[p.N] = t2;
-            } else {
-              slot[0] += t1;
-              slot[p.N] += t2;
-            }
+            slot[0] += t1;
+            slot[p.N] += t2;
           } else {
             acc_s[c] += t1;
             acc_q[c] += t2;
@@ -577,14 +600,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       tc_fence_before();
       mbar_arrive(&S.tempty[acc]);
       if (EPI == 2) mbar_arrive(&S.x_empty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
+      if (EPI == 3) mbar_arrive(&S.x_empty[rb]);
      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-    if (EPI != 0 && !ASTAT) {
+    if (kStats && !ASTAT) {
       float* out = part_row + (size_t)n_fixed * BN + half * (BN / kParts);
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
@@ -598,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+  if (warp == 1) tmem_dealloc(tmem, kAcc * BN);
 }
 
 // per-channel mean / invstd from the partial rows: CTA = 32 channels, 32 warps
@@ -746,7 +766,8 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
                             const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
   constexpr int fixed = (PRO ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
-                        (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0);
+                        (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
+                        (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
@@ -755,9 +776,26 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
   return launch<BN, stages, PRO, EPI, ASTAT, BKT>(ma, mb, mc, mx, p, grid, s);
 }
 
+// EPI 3 (residual) instantiations: n-tiles up to 128 columns, never
+// A-stationary (its A region and the residual ring do not both fit)
+template <int BKT>
+cudaError_t dispatch_res(int BN, bool pro, const CUtensorMap& ma, const CUtensorMap& mb,
+                         const CUtensorMap& mc, const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
+#define KRT_GEMM_RES(BNV)                                                                   \
+  if (BN == BNV) return pro ? dispatch_stages<BNV, true, 3, false, BKT>(ma, mb, mc, mx, p, grid, s) \
+                            : dispatch_stages<BNV, false, 3, false, BKT>(ma, mb, mc, mx, p, grid, s);
+  KRT_GEMM_RES(16)
+  KRT_GEMM_RES(32)
+  KRT_GEMM_RES(64)
+  KRT_GEMM_RES(128)
+#undef KRT_GEMM_RES
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace
 
-size_t conv1x1_partials_bytes(int N) { return (size_t)num_sms() * 4 * 2 * N * sizeof(float); }
+// partial rows: (m-group <= SMs) x (lane quarter) x (epilogue tile group <= 4)
+size_t conv1x1_partials_bytes(int N) { return (size_t)num_sms() * 16 * 2 * N * sizeof(float); }
 
 bool conv1x1_supported(int64_t M, int N, int K) {
   return M > 0 && (K == 16 || K == 32 || K % kBK == 0) && K <= 65536 &&
@@ -773,8 +811,10 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
     return cudaErrorMisalignedAddress;
   const bool bwd_mode = bx != nullptr;
-  // the BN-backward epilogue keeps two x tiles in shared memory: 128-column tiles
-  const int BN = bwd_mode ? (N < 128 ? N : 128) : (N <= 256 ? N : 256);
+  // the BN-backward epilogue keeps two x tiles in shared memory, the residual
+  // epilogue a ring of residual tiles: 128-column tiles
+  const bool res_mode = res != nullptr;
+  const int BN = (bwd_mode || res_mode) ? (N < 128 ? N : 128) : (N <= 256 ? N : 256);
   Params p{};
   p.M = M;
   p.N = N;
@@ -797,6 +837,7 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   if (res != nullptr && (reinterpret_cast<uintptr_t>(res) & 15)) return cudaErrorMisalignedAddress;
   const bool bwd = bx != nullptr;
   if (bwd && (pmean != nullptr || part == nullptr || N < 64 || res != nullptr)) return cudaErrorInvalidValue;
+  if (res_mode && part != nullptr) return cudaErrorInvalidValue;  // no statistics with the residual epilogue
   // narrow reductions (K = 16, 32: the first stages of ResNet-1001) use one
   // K-wide k-block whose row is the 32/64-byte swizzle span
   const int bkt = K < kBK ? K : kBK;
@@ -808,18 +849,30 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
     return cudaErrorInvalidValue;
   if (bwd_mode) {
     if (!make_map(&mx, bx, M, N, kBM, BN, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  } else if (res_mode) {
+    const int rw = BN < 64 ? BN : 64;
+    if (!make_map(&mx, res, M, N, kBM, rw,
+                  rw == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : (rw == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B)))
+      return cudaErrorInvalidValue;
   } else {
     mx = mc;  // unused
   }
   const bool pro = pmean != nullptr, st = part != nullptr;
   // A-stationary when the prologue would otherwise transform the same A tile once per n-tile
-  const bool astat = pro && bkt == kBK && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
+  const bool astat = pro && !res_mode && bkt == kBK && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
   // whole n-tile groups (or, A-stationary, whole m-tiles), at most one CTA per SM
   int per = astat ? num_sms() : num_sms() / p.n_tiles;
   if (per < 1) per = 1;
   if (per > p.m_tiles) per = p.m_tiles;
   const int grid = astat ? per : per * p.n_tiles;
-  if (part_rows) *part_rows = per * 4;  // every row and column written exactly once
+  const int epi_groups = 4 / (BN >= 128 ? 4 : (BN >= 64 ? BN / 32 : 1));
+  if (part_rows) *part_rows = per * 4 * epi_groups;  // every row and column written exactly once
+  if (res_mode) {
+    if (bkt == 16) return dispatch_res<16>(BN, pro, ma, mb, mc, mx, p, grid, s);
+    if (bkt == 32) return dispatch_res<32>(BN, pro, ma, mb, mc, mx, p, grid, s);
+    return dispatch_res<kBK>(BN, pro, ma, mb, mc, mx, p, grid, s);
+  }
   if (bkt != kBK) {  // no A-stationary / BN-backward instantiations for narrow k-blocks
     if (bwd) return cudaErrorInvalidValue;
 #define KRT_GEMM_NARROW(BNV, BKV)                                                                  \
