@@ -45,7 +45,8 @@ constexpr int kEpiWarps = 16;  // four per TMEM lane quarter, each a quarter of 
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kXfWarp0 = 2 + kEpiWarps;        // prologue transform warps
 constexpr int kXfThreads = 256;                 // two threads per tile row, four 16-byte chunks each
-constexpr int kThreads = 64 + kEpiThreads + kXfThreads;  // producer, MMA, epilogue, transform
+constexpr int kXWarp = kXfWarp0 + kXfThreads / 32;  // epilogue-operand (x / residual tile) producer
+constexpr int kThreads = 64 + kEpiThreads + kXfThreads + 32;  // producer, MMA, epilogue, transform, x producer
 constexpr int kEpiWarp0 = 2;
 constexpr int kMaxProK = 1024;  // prologue channels held in shared memory
 
@@ -300,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int stage = 0, xb = 0;
-      uint32_t phase = 0, aphase = 0, xphase = 0;
+      int stage = 0;
+      uint32_t phase = 0, aphase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         if (ASTAT) {  // this m-tile's A k-blocks, each once the previous m-tile's last MMA on it is done
           for (int kb = 0; kb < kblocks; ++kb) {
@@ -313,19 +314,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         }
         for (int nt = 0; nt < nts; ++nt) {
           const int n_tile = ASTAT ? nt : n_fixed;
-          if (EPI >= 2) {  // the BN input / residual tile the epilogue of this (m, n) tile reads
-            constexpr int kXB = EPI == 2 ? 2 : kResBufs<BN>;
-            constexpr int kW = EPI == 2 ? BN : kResW<BN>;
-            mbar_wait(&S.x_empty[xb], xphase ^ 1);
-            mbar_expect_tx(&S.x_full[xb], kBM * BN * 2);
-#pragma unroll
-            for (int b = 0; b < BN / kW; ++b)
-              tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb] + b * kBM * kW * 2, n_tile * BN + b * kW, mt * kBM);
-            if (++xb == kXB) {
-              xb = 0;
-              xphase ^= 1;
-            }
-          }
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&S.empty[stage], phase ^ 1);
             if (ASTAT) {
@@ -382,6 +370,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         }
       }
       aphase ^= 1;
+    }
+  } else if (warp == kXWarp) {
+    // ------------------------------------------------ x / residual tile producer
+    // its own thread, so waiting for a free buffer never holds back the A/B ring
+    if (EPI >= 2 && lane == 0) {
+      constexpr int kXB = EPI == 2 ? 2 : kResBufs<BN>;
+      constexpr int kW = EPI == 2 ? BN : kResW<BN>;
+      int xb = 0;
+      uint32_t xphase = 0;
+      for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+        for (int nt = 0; nt < nts; ++nt) {
+          const int n_tile = ASTAT ? nt : n_fixed;
+          mbar_wait(&S.x_empty[xb], xphase ^ 1);
+          mbar_expect_tx(&S.x_full[xb], kBM * BN * 2);
+#pragma unroll
+          for (int b = 0; b < BN / kW; ++b)
+            tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb] + b * kBM * kW * 2, n_tile * BN + b * kW, mt * kBM);
+          if (++xb == kXB) {
+            xb = 0;
+            xphase ^= 1;
+          }
+        }
+      }
     }
   } else if (warp >= kXfWarp0) {
     // ------------------------------------------------------------ prologue transform
