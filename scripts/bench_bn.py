@@ -13,7 +13,7 @@ sys.path.insert(0, ".")
 from paper_2008_11421_b200 import bnfused  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--batch", type=int, default=512)
+ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--json", default=None)
 ap.add_argument("--preact", action="store_true", help="ResNet-1001 @ 2048^2 widths (batch 2 unless --batch)")
 args = ap.parse_args()
@@ -22,6 +22,8 @@ args = ap.parse_args()
 SHAPES = [(64, 56), (256, 56), (128, 28), (512, 28), (256, 14), (1024, 14), (512, 7), (2048, 7)]
 if args.preact:   # pre-activation ResNet-1001 at 2048^2: unit input 4w and width w per stage
     SHAPES = [(64, 2048), (16, 2048), (128, 1024), (32, 1024), (256, 512), (64, 512)]
+if args.batch is None:
+    args.batch = 2 if args.preact else 512
 
 
 def t(fn, reps=10):
