@@ -224,12 +224,13 @@ def conv1x1(x, w, out=None, pre=None, stats=None, res=None):
     return y
 
 
-def conv1x1_dgrad_bn_backward(dy, w, x, mean, invstd, g, b, dgamma=None, dbeta=None, relu=True):
+def conv1x1_dgrad_bn_backward(dy, w, x, mean, invstd, g, b, dgamma=None, dbeta=None, relu=True, addend=None):
     """d(input of relu(bn(x)))-chain through a stride-1 1x1 convolution:
     da = dy . W (tcgen05 GEMM, W transposed to K-major) with the BN backward
     reduce of (da, x) in its epilogue, then the BN backward elementwise pass.
     dy: (N, Cout, H, W) grad of the conv output; w: (Cout, Cin, 1, 1); x: the
-    BN input (N, Cin, H, W).  Returns dx = d/dx of conv(relu(bn(x)))."""
+    BN input (N, Cin, H, W).  Returns dx = d/dx of conv(relu(bn(x))), plus
+    addend (a gradient of x from another path, e.g. the identity shortcut)."""
     import ctypes as C
     dy, x = _nhwc(dy), _nhwc(x)
     n, cout, h, ww = dy.shape
@@ -248,8 +249,15 @@ def conv1x1_dgrad_bn_backward(dy, w, x, mean, invstd, g, b, dgamma=None, dbeta=N
                                                            invstd.data_ptr(), g.data_ptr(), _ptr(dgamma),
                                                            _ptr(dbeta), coef.data_ptr(), _stream()))
     dx = torch.empty_like(x, memory_format=torch.channels_last)
-    with _timed("bn_backward_elemt", M * cin * 2 * 3):
+    with _timed("bn_backward_elemt", M * cin * 2 * (3 if addend is None else 4)):
         _lib.check(_lib.lib().krt_bn_backward_elemt(da.data_ptr(), x.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
-                                                    g.data_ptr(), b.data_ptr(), coef.data_ptr(), None, int(relu),
-                                                    dx.data_ptr(), M, cin, _stream()))
+                                                    g.data_ptr(), b.data_ptr(), coef.data_ptr(),
+                                                    None if addend is None else _nhwc(addend).data_ptr(),
+                                                    int(relu), dx.data_ptr(), M, cin, _stream()))
     return dx
+
+
+def conv1x1_dgrad_supported(cout, cin):
+    """conv1x1_dgrad_bn_backward for a (Cout, Cin) 1x1 weight: the GEMM
+    reduces over K = Cout into N = Cin columns (BN-backward epilogue: N >= 64)."""
+    return conv1x1_supported(cout, cin) and cin >= 64 and supported(cin)

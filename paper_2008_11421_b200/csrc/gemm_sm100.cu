@@ -884,8 +884,14 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
     if (bkt == 32) return dispatch_res<32>(BN, pro, ma, mb, mc, mx, p, grid, s);
     return dispatch_res<kBK>(BN, pro, ma, mb, mc, mx, p, grid, s);
   }
-  if (bkt != kBK) {  // no A-stationary / BN-backward instantiations for narrow k-blocks
-    if (bwd) return cudaErrorInvalidValue;
+  if (bkt != kBK) {  // no A-stationary instantiations for narrow k-blocks
+    if (bwd) {
+      if (BN == 64) return bkt == 16 ? dispatch_stages<64, false, 2, false, 16>(ma, mb, mc, mx, p, grid, s)
+                                     : dispatch_stages<64, false, 2, false, 32>(ma, mb, mc, mx, p, grid, s);
+      if (BN == 128) return bkt == 16 ? dispatch_stages<128, false, 2, false, 16>(ma, mb, mc, mx, p, grid, s)
+                                      : dispatch_stages<128, false, 2, false, 32>(ma, mb, mc, mx, p, grid, s);
+      return cudaErrorInvalidValue;
+    }
 #define KRT_GEMM_NARROW(BNV, BKV)                                                                  \
   if (BN == BNV && bkt == BKV) {                                                                  \
     if (pro && st) return dispatch_stages<BNV, true, 1, false, BKV>(ma, mb, mc, mx, p, grid, s); \

@@ -94,6 +94,9 @@ BN_EPS = 1e-5
 # bottleneck 1x1 convolutions on the own tcgen05 GEMM (csrc/gemm_sm100.cu) with
 # the BN work fused in; KRT_TC_CONV1X1=0 selects cuDNN + separate BN kernels
 TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
+# the pre-activation unit's 1x1 dgrads on the same GEMM with the BN-backward
+# reduce fused (narrow, HBM-bound shapes)
+TC_DGRAD_PREACT = os.environ.get("KRT_TC_DGRAD_PREACT", "1") != "0"
 # conv3's backward data gradient on the same GEMM with BN2's reduce fused.  Off
 # by default: measured 1% slower per step than cuDNN dgrad + the bwd_reduce
 # kernel (3643-3655 vs 3685-3689 samples/s, same box, with the x tile
@@ -715,12 +718,21 @@ class PreActBottleneckUnit(_ConvNetUnit):
         g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
         x, c1, c2 = (_cl(t) for t in saved[:3])
         st = self._st(saved[3])
+        tc = self._tc1x1() and TC_DGRAD_PREACT
         a2 = _bn_relu(c2, st[4], st[5], g2, b2)
-        da2, dw3, _ = _conv_bw(dy, a2, _cl(w3), 1, 0)
-        del a2
-        _cl(grads[8]).copy_(dw3)
-        dc2 = _bn_relu_bw(da2, c2, st[4], st[5], g2, b2, grads[6], grads[7])
-        del da2
+        if tc and bnfused.conv1x1_dgrad_supported(self.cout, self.w):
+            # conv3 dgrad on the tcgen05 GEMM with BN2's backward reduce in its epilogue
+            _, dw3, _ = _conv_bw(dy, a2, _cl(w3), 1, 0, need_dx=False)
+            del a2
+            _cl(grads[8]).copy_(dw3)
+            dc2 = bnfused.conv1x1_dgrad_bn_backward(dy, _cl(w3), c2, st[4], st[5], g2, b2, dgamma=grads[6],
+                                                    dbeta=grads[7])
+        else:
+            da2, dw3, _ = _conv_bw(dy, a2, _cl(w3), 1, 0)
+            del a2
+            _cl(grads[8]).copy_(dw3)
+            dc2 = _bn_relu_bw(da2, c2, st[4], st[5], g2, b2, grads[6], grads[7])
+            del da2
         a1 = _bn_relu(c1, st[2], st[3], g1, b1)
         da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
         del dc2, a1
@@ -728,6 +740,14 @@ class PreActBottleneckUnit(_ConvNetUnit):
         dc1 = _bn_relu_bw(da1, c1, st[2], st[3], g1, b1, grads[3], grads[4])
         del da1
         a0 = _bn_relu(x, st[0], st[1], g0, b0)
+        if tc and not self.down and bnfused.conv1x1_dgrad_supported(self.w, self.cin):
+            # conv1 dgrad + BN0's backward reduce on the GEMM; the identity
+            # shortcut's gradient dy added in the elementwise pass
+            _, dw1, _ = _conv_bw(dc1, a0, _cl(w1), 1, 0, need_dx=False)
+            del a0
+            _cl(grads[2]).copy_(dw1)
+            return bnfused.conv1x1_dgrad_bn_backward(dc1, _cl(w1), x, st[0], st[1], g0, b0, dgamma=grads[0],
+                                                     dbeta=grads[1], addend=dy)
         da0, dw1, _ = _conv_bw(dc1, a0, _cl(w1), 1, 0)
         del dc1
         _cl(grads[2]).copy_(dw1)

@@ -134,3 +134,30 @@ def test_conv1x1_residual_epilogue(n, cin, cout, hw, pre):
     with pytest.raises(_lib.KrtError):   # statistics are not reduced with the residual epilogue
         bnfused.conv1x1(x, w, pre=pre_t, res=res, stats=(torch.empty(cout, device="cuda"),
                                                          torch.empty(cout, device="cuda")))
+
+
+@pytest.mark.parametrize("n,cout,cin,hw", [(4, 16, 64, 40), (2, 32, 128, 50), (8, 64, 256, 30), (2, 256, 64, 150)])
+def test_conv1x1_dgrad_bn_backward_narrow(n, cout, cin, hw):
+    """Narrow reductions (K = Cout = 16/32) in the dgrad + BN-backward-reduce
+    GEMM, with the shortcut gradient as addend: vs autograd in fp32 through
+    conv(relu(bn(x))) + the addend (tolerance: bf16 rounding of the stored
+    intermediate gradient)."""
+    x = cl(rand((n, cin, hw, hw), 11, 1.5))
+    w = cl(rand((cout, cin, 1, 1), 12, cin ** -0.5))
+    dy = cl(rand((n, cout, hw, hw), 13))
+    add = cl(rand((n, cin, hw, hw), 14))
+    g = (1 + 0.2 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+    b = (0.1 * torch.randn(cin, device="cuda")).to(torch.bfloat16)
+    m, i = torch.empty(cin, device="cuda"), torch.empty(cin, device="cuda")
+    bnfused.stats(x, m, i)
+    dg, db = torch.empty(cin, device="cuda"), torch.empty(cin, device="cuda")
+    dx = bnfused.conv1x1_dgrad_bn_backward(dy, w, x, m, i, g, b, dgamma=dg, dbeta=db, addend=add)
+    # reference: the unfused kernels on the GEMM's stored da (same rounding point)
+    da = F.conv2d(dy.float(), w.float().transpose(0, 1)).to(torch.bfloat16)
+    dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+    ref = bnfused.backward(cl(da), x, m, i, g, b, relu=True, dgamma=dg2, dbeta=db2, addend=add)
+    torch.cuda.synchronize()
+    err = (dx.float() - ref.float()).abs().max() / ref.float().abs().max()
+    assert err < 2e-2, float(err)
+    torch.testing.assert_close(db, db2, rtol=2e-2, atol=2e-2 * db2.abs().max().item())
+    torch.testing.assert_close(dg, dg2, rtol=2e-2, atol=2e-2 * dg2.abs().max().item())

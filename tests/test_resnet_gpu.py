@@ -142,7 +142,10 @@ def test_preact_gemm_path_matches_cudnn_path(monkeypatch):
     rec = W.load("preact29_small_bf16")
     units, _, got, _, _ = run(rec, iters=2, lr=0.05)
     assert all(u._tc1x1() for u in units if isinstance(u, U.PreActBottleneckUnit))
+    monkeypatch.setattr(U, "TC_DGRAD_PREACT", False)
+    _, _, fwd_only, _, _ = run(rec, iters=2, lr=0.05)
     monkeypatch.setattr(U, "TC_CONV1X1", False)
     _, _, ref, _, _ = run(rec, iters=2, lr=0.05)
-    for a, b in zip(got, ref):
-        assert abs(a - b) <= 2e-2 * abs(b), (got, ref)
+    for a, b, c in zip(got, fwd_only, ref):
+        assert abs(a - c) <= 2e-2 * abs(c), (got, ref)
+        assert abs(b - c) <= 2e-2 * abs(c), (fwd_only, ref)
