@@ -323,6 +323,18 @@ int krt_bn_partials_finalize(const float* part, int part_rows, int N, int64_t M,
 int krt_conv1x1_bn_res(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                        const float* pinvstd, const void* pgamma, const void* pbeta, const void* res, float* part,
                        int* part_rows, void* stream);
+/* RGB NHWC bf16 [pixels, 3] -> [pixels, 4] with a zero 4th channel (the
+ * stem's input for krt_conv_gather_bn: one 8-byte load per pixel); x 4-byte
+ * and y 16-byte aligned. */
+int krt_pad_rgb4(const void* x, void* y, int64_t pixels, void* stream);
+/* Implicit-GEMM convolution for the ResNet stem (7x7/2, 3 -> 64 channels):
+ * C[n*ho*wo, N] = im2col(x) . wk^T, x NHWC bf16 [n, h, w, cin], wk bf16 [N, K]
+ * with column k = (kh*k + kw)*cin + c (zero beyond k*k*cin; K % 32 == 0,
+ * K <= 1024), square kernel k, stride, zero padding pad.  The im2col rows are
+ * gathered into the tcgen05 operand tiles in shared memory, never written to
+ * HBM.  part/part_rows: BN statistics of C as krt_conv1x1_bn.  N = 64. */
+int krt_conv_gather_bn(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo, int k,
+                       int stride, int pad, int N, int K, float* part, int* part_rows, void* stream);
 /* Backward of a 1x1 convolution fused with the reduce of the BN (+ ReLU) in
  * front of it: dX[M,N] = dY[M,K] . Wt[N,K]^T (Wt = weights transposed, K-major)
  * is stored, and with x = that BN's input the epilogue reduces sum(gm) and

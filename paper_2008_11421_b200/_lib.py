@@ -110,6 +110,8 @@ EXPORTS = {
     "krt_conv1x1_bn": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 6
                        + [C.c_void_p]),
     "krt_conv1x1_bn_res": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 8),
+    "krt_pad_rgb4": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "krt_conv_gather_bn": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 11 + [C.c_void_p] * 3),
     "krt_conv1x1_bn_dgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 8),
     "krt_bn_partials_bwd_finalize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64] + [C.c_void_p] * 7),
     "krt_bn_backward_elemt": (C.c_int, [C.c_void_p] * 8 + [C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),

@@ -224,6 +224,44 @@ def conv1x1(x, w, out=None, pre=None, stats=None, res=None):
     return y
 
 
+def conv_gather(x, w, stride, pad, out=None, stats=None):
+    """Implicit-GEMM convolution on tcgen05 (the ResNet stem, 64 output
+    channels): im2col rows gathered into shared memory, never written.
+    x: (N, Cin, H, W) channels_last bf16; w: (64, Cin, k, k) bf16.
+    stats=(mean, invstd): the BN statistics of the result from the epilogue."""
+    import ctypes as C
+    x = _nhwc(x)
+    n, cin, h, ww = x.shape
+    cout, _, k, _ = w.shape
+    if cin == 3:
+        # RGB -> 4 channels (zero), so the gather moves one 8-byte pixel per load
+        x4 = torch.empty((n, 4, h, ww), dtype=x.dtype, device=x.device, memory_format=torch.channels_last)
+        with _timed("pad_rgb4", n * h * ww * (6 + 8)):
+            _lib.check(_lib.lib().krt_pad_rgb4(x.data_ptr(), x4.data_ptr(), n * h * ww, _stream()))
+        w4 = torch.zeros((cout, 4, k, k), dtype=w.dtype, device=w.device)
+        w4[:, :3] = w
+        x, w, cin = x4, w4, 4
+    ho, wo = (h + 2 * pad - k) // stride + 1, (ww + 2 * pad - k) // stride + 1
+    kk = k * k * cin
+    K = (kk + 31) // 32 * 32
+    wk = torch.zeros((cout, K), dtype=w.dtype, device=w.device)
+    wk[:, :kk] = w.permute(0, 2, 3, 1).reshape(cout, kk)      # k = (kh*k + kw)*cin + c
+    y = out if out is not None else torch.empty((n, cout, ho, wo), dtype=x.dtype, device=x.device,
+                                                memory_format=torch.channels_last)
+    M = n * ho * wo
+    part = None
+    rows = C.c_int(0)
+    if stats is not None:
+        part = torch.empty(_lib.lib().krt_conv1x1_partials_bytes(cout) // 4, dtype=torch.float32, device=x.device)
+    with _timed("conv_gather_bn", n * h * ww * cin * 2 + M * cout * 2, 2.0 * M * kk * cout):
+        _lib.check(_lib.lib().krt_conv_gather_bn(x.data_ptr(), wk.data_ptr(), y.data_ptr(), n, h, ww, cin, ho, wo,
+                                                 k, stride, pad, cout, K, _ptr(part), C.byref(rows), _stream()))
+        if stats is not None:
+            _lib.check(_lib.lib().krt_bn_partials_finalize(part.data_ptr(), rows.value, cout, M, EPS,
+                                                           stats[0].data_ptr(), stats[1].data_ptr(), _stream()))
+    return y
+
+
 def conv1x1_dgrad_bn_backward(dy, w, x, mean, invstd, g, b, dgamma=None, dbeta=None, relu=True, addend=None):
     """d(input of relu(bn(x)))-chain through a stride-1 1x1 convolution:
     da = dy . W (tcgen05 GEMM, W transposed to K-major) with the BN backward

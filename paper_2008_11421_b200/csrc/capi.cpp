@@ -480,6 +480,17 @@ int krt_conv1x1_bn_res(const void* A, const void* B, void* C, int64_t M, int N, 
       "conv1x1_bn_res");
 }
 
+int krt_pad_rgb4(const void* x, void* y, int64_t pixels, void* stream) {
+  KRT_CUDA_GUARD(pad_rgb4(x, y, pixels, (cudaStream_t)stream), "pad_rgb4");
+}
+
+int krt_conv_gather_bn(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo, int k,
+                       int stride, int pad, int N, int K, float* part, int* part_rows, void* stream) {
+  KRT_CUDA_GUARD(
+      conv_gather_fprop(x, wk, C, n, h, w, cin, ho, wo, k, stride, pad, N, K, part, part_rows, (cudaStream_t)stream),
+      "conv_gather_bn");
+}
+
 int krt_conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
                          const float* mean, const float* invstd, const void* g, const void* b, float* part,
                          int* part_rows, void* stream) {

@@ -206,6 +206,12 @@ struct Params {
   // residual (nullptr: none): C = acc + res, res [M, N] bf16 row-major,
   // added in fp32 before the single bf16 rounding (EPI 0/1)
   const __nv_bfloat16* res;
+  // GATHER (implicit-GEMM convolution): A rows are gathered from the NHWC
+  // input gx [gn, gh, gw, gc] by the transform warps: row = output pixel
+  // (n, oh, ow), column k = (kh * gk + kw) * gc + c for k < gk*gk*gc, zero
+  // beyond (K padded to a k-block multiple) and outside the image
+  const __nv_bfloat16* gx;
+  int gh, gw, gc, gho, gwo, gk, gs, gp;
 };
 
 // ASTAT (A-stationary, prologue only, K <= kMaxAstatK): the transformed A tile
@@ -245,7 +251,7 @@ struct Smem {
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C,
 // 3 C = acc + residual (p.res through map_x)
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c,
@@ -254,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // memory in this kernel); using it directly keeps every access in the shared
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO, ASTAT, EPI, BKT>*>(smem_raw);
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT>*>(smem_raw);
+  static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           const int n_tile = ASTAT ? nt : n_fixed;
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&S.empty[stage], phase ^ 1);
-            if (ASTAT) {
+            if (ASTAT || GATHER) {  // A is resident / gathered by the transform warps
               mbar_expect_tx(&S.full[stage], BN * BKT * 2);
             } else {
               mbar_expect_tx(&S.full[stage], (kBM + BN) * BKT * 2);
@@ -345,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         const uint32_t d_tmem = tmem + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
           if (ASTAT && nt == 0) mbar_wait(&S.a_ready[kb], aphase);  // this A k-block landed and transformed
-          if (PRO && !ASTAT) mbar_wait(&S.ready[stage], phase);     // transformed by the transform warps
+          if ((PRO || GATHER) && !ASTAT) mbar_wait(&S.ready[stage], phase);  // transformed / gathered
           else mbar_wait(&S.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
@@ -396,7 +403,177 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     }
   } else if (warp >= kXfWarp0) {
     // ------------------------------------------------------------ prologue transform
-    if (PRO) {
+    if (GATHER) {
+      // implicit GEMM: each thread builds kPer 16-byte chunks of one A row per
+      // k-block from the input (L1/L2-resident patch rows), into the swizzled slot
+      const int xt = threadIdx.x - kXfWarp0 * 32;
+      constexpr int kPer = BKT / 16;
+      const int r = xt & 127, jh = kPer * (xt >> 7);
+      const int kvalid = p.gk * p.gk * p.gc;
+      int* ktab = reinterpret_cast<int*>(S.sc);  // k -> (kh * gw + kw) * gc + c and (kh, kw)
+      int* khw = reinterpret_cast<int*>(S.sh);
+      for (int k = xt; k < p.K; k += kXfThreads) {
+        const int c = k % p.gc, t = k / p.gc, kw = t % p.gk, kh = t / p.gk;
+        ktab[k] = k < kvalid ? (kh * p.gw + kw) * p.gc + c : 0;
+        khw[k] = k < kvalid ? (kh << 16) | kw : -1;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kXfThreads) : "memory");
+      const int64_t plane = (int64_t)p.gho * p.gwo;
+      const unsigned short* gx = reinterpret_cast<const unsigned short*>(p.gx);
+      struct Row {
+        bool valid;
+        int ih0, iw0;
+        const unsigned short* base;
+      };
+      auto row_of = [&](int mt) {
+        Row t;
+        const int64_t row = (int64_t)mt * kBM + r;
+        t.valid = row < p.M;
+        const int n = t.valid ? (int)(row / plane) : 0;
+        const int rem = t.valid ? (int)(row - (int64_t)n * plane) : 0;
+        t.ih0 = (rem / p.gwo) * p.gs - p.gp;
+        t.iw0 = (rem % p.gwo) * p.gs - p.gp;
+        t.base = gx + (((int64_t)n * p.gh + t.ih0) * p.gw + t.iw0) * p.gc;
+        return t;
+      };
+      // this thread's kPer chunks of k-block kb of a row (loads only)
+      auto gather = [&](const Row& t, int kb, uint4 (&u)[kPer]) {
+        if (p.gc == 4) {
+          // a 16-byte chunk = two (kh, kw) pixels of 4 channels: one 8-byte load each
+          const uint2* base4 = reinterpret_cast<const uint2*>(t.base);
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            uint2 v[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int q = (kb * BKT + 8 * (jh + i)) / 4 + h;
+              const int hw = khw[4 * q];
+              const int kh = hw >> 16, kw = hw & 0xffff;
+              const int ih = t.ih0 + kh, iw = t.iw0 + kw;
+              const bool in = t.valid && hw >= 0 && ih >= 0 && ih < p.gh && iw >= 0 && iw < p.gw;
+              v[h] = in ? __ldg(base4 + kh * p.gw + kw) : make_uint2(0u, 0u);
+            }
+            u[i] = make_uint4(v[0].x, v[0].y, v[1].x, v[1].y);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            uint32_t w2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint32_t lohi[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int k = kb * BKT + 8 * (jh + i) + 2 * e + h;
+                const int hw = khw[k];
+                const int ih = t.ih0 + (hw >> 16), iw = t.iw0 + (hw & 0xffff);
+                const bool in = t.valid && hw >= 0 && ih >= 0 && ih < p.gh && iw >= 0 && iw < p.gw;
+                lohi[h] = in ? (uint32_t)__ldg(t.base + ktab[k]) : 0u;
+              }
+              w2[e] = lohi[0] | (lohi[1] << 16);
+            }
+            u[i] = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+          }
+        }
+      };
+      int stage = 0;
+      uint32_t phase = 0;
+      auto put = [&](const uint4 (&u)[kPer]) {  // one gathered k-block into the ring
+        mbar_wait(&S.full[stage], phase);  // slot free (its B landed after the MMA released it)
+        uint4* rowp = reinterpret_cast<uint4*>(S.a[stage] + r * BKT * 2);
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) rowp[swz_chunk<BKT>(jh + i, r)] = u[i];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&S.ready[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      bool stem_done = false;
+      if constexpr (BKT == 32) {
+        if (p.gk == 7 && p.gc == 4 && p.K == 224) {
+          // the ResNet stem (7x7, 4-channel pixels, K = 56 pixels): k-blocks
+          // unrolled so every (kh, kw) is a constant; per tile one row / column
+          // validity mask replaces the per-pixel bounds arithmetic
+          struct Stem {
+            uint32_t rmask, cmask;
+            const uint2* base;
+          };
+          auto stem_row = [&](int mt) {
+            const Row t = row_of(mt);
+            Stem st;
+            st.rmask = st.cmask = 0;
+#pragma unroll
+            for (int d = 0; d < 7; ++d) {
+              st.rmask |= (t.valid && t.ih0 + d >= 0 && t.ih0 + d < p.gh) ? 1u << d : 0u;
+              st.cmask |= (t.valid && t.iw0 + d >= 0 && t.iw0 + d < p.gw) ? 1u << d : 0u;
+            }
+            st.base = reinterpret_cast<const uint2*>(t.base);
+            return st;
+          };
+          auto load = [&](const Stem& st, int kb, uint4 (&u)[kPer], int half) {
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+              uint2 v[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int q = kb * 8 + half * 4 + 2 * i + h;  // pixel (kh, kw) = (q / 7, q % 7)
+                const int kh = q / 7, kw = q % 7;
+                const bool in = q < 49 && ((st.rmask >> kh) & (st.cmask >> kw) & 1u);
+                v[h] = in ? __ldg(st.base + kh * p.gw + kw) : make_uint2(0u, 0u);
+              }
+              u[i] = make_uint4(v[0].x, v[0].y, v[1].x, v[1].y);
+            }
+          };
+          auto run = [&](int half) {
+            int mt = m_first;
+            Stem cur = stem_row(mt);
+            uint4 u[kPer], un[kPer];
+            if (mt < p.m_tiles) load(cur, 0, un, half);
+            while (mt < p.m_tiles) {
+              const int nmt = mt + m_step;
+              Stem nxt = stem_row(nmt);
+#pragma unroll
+              for (int kb = 0; kb < 7; ++kb) {
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) u[i] = un[i];
+                if (kb < 6) load(cur, kb + 1, un, half);
+                else if (nmt < p.m_tiles) load(nxt, 0, un, half);
+                put(u);
+              }
+              cur = nxt;
+              mt = nmt;
+            }
+          };
+          if (jh == 0) run(0);  // literal halves: (kh, kw) fold to constants after inlining
+          else run(1);
+          stem_done = true;
+        }
+      }
+      if (!stem_done) {
+      // software pipeline over the flattened (tile, k-block) sequence: the
+      // loads of the next k-block are in flight while this one is stored
+      int mt = m_first, kb = 0;
+      Row cur = row_of(mt);
+      uint4 u[kPer], un[kPer];
+      if (mt < p.m_tiles) gather(cur, 0, un);
+      while (mt < p.m_tiles) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) u[i] = un[i];
+        int nmt = mt, nkb = kb + 1;
+        if (nkb == kblocks) {
+          nkb = 0;
+          nmt += m_step;
+          cur = row_of(nmt);
+        }
+        if (nmt < p.m_tiles) gather(cur, nkb, un);
+        put(u);
+        mt = nmt;
+        kb = nkb;
+      }
+      }
+    } else if (PRO) {
       const int xt = threadIdx.x - kXfWarp0 * 32;  // 0..255
       constexpr int kPer = BKT / 16;                // 16-byte chunks per thread (two threads per row)
       const int r = xt & 127, jh = kPer * (xt >> 7);  // tile row, first logical chunk
@@ -757,11 +934,11 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO, ASTAT, EPI, BKT>);
+  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER>;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT>);
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -772,11 +949,11 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK>
+template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = false>
 cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                             const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
-  constexpr int fixed = (PRO ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
+  constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
                         (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
                         (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * BKT * 2;
@@ -784,7 +961,7 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
   constexpr int stages = avail / stage_bytes > max_stages ? max_stages : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, EPI, ASTAT, BKT>(ma, mb, mc, mx, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER>(ma, mb, mc, mx, p, grid, s);
 }
 
 // EPI 3 (residual) instantiations: n-tiles up to 128 columns, never
@@ -950,6 +1127,70 @@ cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, i
                              cudaStream_t s) {
   return conv1x1_impl(A, B, C, M, N, K, pmean, pinvstd, pg, pb, part, part_rows, nullptr, nullptr, nullptr, nullptr,
                       nullptr, nullptr, s);
+}
+
+namespace {
+// RGB NHWC bf16 -> 4-channel pixels (4th = 0): two pixels per thread, 12-byte
+// (3 x 4-byte) loads, one 16-byte store
+__global__ void pad_rgb4_kernel(const uint32_t* __restrict__ x, uint4* __restrict__ y, int64_t pixels) {
+  const int64_t pairs = pixels / 2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < pairs; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = __ldg(x + 3 * t), b = __ldg(x + 3 * t + 1), c = __ldg(x + 3 * t + 2);
+    // pixel 0 = (a.lo, a.hi, b.lo), pixel 1 = (b.hi, c.lo, c.hi)
+    y[t] = make_uint4(a, b & 0xffffu, (b >> 16) | (c << 16), c >> 16);
+  }
+  if ((pixels & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd count: the last pixel alone
+    const unsigned short* xs = reinterpret_cast<const unsigned short*>(x) + 3 * (pixels - 1);
+    reinterpret_cast<uint2*>(y)[pixels - 1] = make_uint2(xs[0] | ((uint32_t)xs[1] << 16), xs[2]);
+  }
+}
+}  // namespace
+
+cudaError_t pad_rgb4(const void* x, void* y, int64_t pixels, cudaStream_t s) {
+  if (pixels < 1 || (reinterpret_cast<uintptr_t>(x) & 3) || (reinterpret_cast<uintptr_t>(y) & 15))
+    return cudaErrorInvalidValue;
+  const int64_t pairs = pixels / 2;
+  int64_t blocks = (pairs + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  pad_rgb4_kernel<<<(int)blocks, 256, 0, s>>>(static_cast<const uint32_t*>(x), static_cast<uint4*>(y), pixels);
+  return cudaGetLastError();
+}
+
+cudaError_t conv_gather_fprop(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo,
+                              int k, int stride, int pad, int N, int K, float* part, int* part_rows, cudaStream_t s) {
+  const int64_t M = (int64_t)n * ho * wo;
+  if (M <= 0 || N != 64 || K % 32 != 0 || K < k * k * cin || K > kMaxProK || cin < 1 || k < 1 || stride < 1)
+    return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(wk) | reinterpret_cast<uintptr_t>(C)) & 15) return cudaErrorMisalignedAddress;
+  Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.BN = N;
+  p.n_tiles = 1;
+  p.m_tiles = (int)((M + kBM - 1) / kBM);
+  p.C = static_cast<__nv_bfloat16*>(C);
+  p.part = part;
+  p.gx = static_cast<const __nv_bfloat16*>(x);
+  p.gh = h;
+  p.gw = w;
+  p.gc = cin;
+  p.gho = ho;
+  p.gwo = wo;
+  p.gk = k;
+  p.gs = stride;
+  p.gp = pad;
+  CUtensorMap mb, mc;
+  if (!make_map(&mb, wk, N, K, N, 32, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorInvalidValue;
+  int per = num_sms();
+  if (per > p.m_tiles) per = p.m_tiles;
+  if (part_rows) *part_rows = per * 4 * 2;  // BN 64: two epilogue tile groups
+  if (part != nullptr) return dispatch_stages<64, false, 1, false, 32, true>(mb, mb, mc, mc, p, per, s);
+  return dispatch_stages<64, false, 0, false, 32, true>(mb, mb, mc, mc, p, per, s);
 }
 
 cudaError_t conv1x1_bn_res_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,

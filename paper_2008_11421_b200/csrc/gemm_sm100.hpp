@@ -11,6 +11,14 @@ size_t conv1x1_partials_bytes(int N);
 cudaError_t conv1x1_bn_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                              const float* pinvstd, const void* pg, const void* pb, float* part, int* part_rows,
                              cudaStream_t s);
+// RGB NHWC bf16 [pixels, 3] -> [pixels, 4] (4th channel 0)
+cudaError_t pad_rgb4(const void* x, void* y, int64_t pixels, cudaStream_t s);
+// implicit-GEMM convolution (the ResNet stem): C[n*ho*wo, N] = im2col(x) .
+// wk^T with x NHWC [n, h, w, cin], wk [N, K] (K = (kh*k + kw)*cin + c, zero
+// padded to K), the im2col rows gathered in shared memory, never written;
+// part/part_rows: BN statistics partials as conv1x1_bn_fprop.  N = 64.
+cudaError_t conv_gather_fprop(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo,
+                              int k, int stride, int pad, int N, int K, float* part, int* part_rows, cudaStream_t s);
 // as conv1x1_bn_fprop, plus a residual: C = f(A) . B^T + res (res [M, N] bf16)
 cudaError_t conv1x1_bn_res_fprop(const void* A, const void* B, void* C, int64_t M, int N, int K, const float* pmean,
                                  const float* pinvstd, const void* pg, const void* pb, const void* res, float* part,

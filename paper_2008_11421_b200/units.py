@@ -206,10 +206,15 @@ class StemUnit(_ConvNetUnit):
         if saved is not None:
             _cl(saved[0]).copy_(x)
         if self._fused():
-            c = _conv_into(x, wv, 2, 3, None if saved is None else _cl(saved[1]))
             st = saved[2] if saved is not None else torch.empty(2 * self.cout, device=x.device)
             m, i = st[:self.cout], st[self.cout:]
-            bnfused.stats(c, m, i)
+            if TC_CONV1X1 and self.cout == 64:
+                # implicit GEMM on tcgen05 with the BN statistics in its epilogue
+                # (cuDNN runs a 3-channel NHWC conv on a legacy sm80 kernel)
+                c = bnfused.conv_gather(x, wv, 2, 3, out=None if saved is None else _cl(saved[1]), stats=(m, i))
+            else:
+                c = _conv_into(x, wv, 2, 3, None if saved is None else _cl(saved[1]))
+                bnfused.stats(c, m, i)
             return bnfused.relu_maxpool(c, m, i, g, b, 3, 2, 1)   # relu(bn(c)) never materialised
         c = _conv(x, wv, 2, 3)
         o, m, i = _bn_fw(c, g, b)

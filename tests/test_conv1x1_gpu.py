@@ -161,3 +161,34 @@ def test_conv1x1_dgrad_bn_backward_narrow(n, cout, cin, hw):
     assert err < 2e-2, float(err)
     torch.testing.assert_close(db, db2, rtol=2e-2, atol=2e-2 * db2.abs().max().item())
     torch.testing.assert_close(dg, dg2, rtol=2e-2, atol=2e-2 * dg2.abs().max().item())
+
+
+@pytest.mark.parametrize("n,cin,hw,k,s,pad", [(2, 3, 224, 7, 2, 3), (3, 3, 37, 7, 2, 3), (1, 4, 30, 3, 1, 1),
+                                              (12, 3, 64, 7, 2, 3)])
+def test_conv_gather_matches_torch(n, cin, hw, k, s, pad):
+    """Implicit-GEMM stem convolution (im2col gathered in shared memory) vs the
+    fp32 convolution; fused statistics vs the stats kernel on the stored output."""
+    x = cl(rand((n, cin, hw, hw), 21, 1.0))
+    w = cl(rand((64, cin, k, k), 22, (cin * k * k) ** -0.5))
+    sm, si = torch.empty(64, device="cuda"), torch.empty(64, device="cuda")
+    y = bnfused.conv_gather(x, w, s, pad, stats=(sm, si))
+    torch.cuda.synchronize()
+    ref = F.conv2d(x.float(), w.float(), stride=s, padding=pad)
+    assert y.shape == ref.shape
+    err = (y.float() - ref).abs().max() / ref.abs().max()
+    assert err < 1e-2, float(err)
+    rm, ri = torch.empty_like(sm), torch.empty_like(si)
+    bnfused.stats(y, rm, ri)
+    torch.testing.assert_close(sm, rm, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(si, ri, rtol=1e-4, atol=1e-5)
+    assert torch.equal(y, bnfused.conv_gather(x, w, s, pad))
+
+
+@pytest.mark.parametrize("pixels", [1, 2, 7, 4107, 100000])
+def test_pad_rgb4(pixels):
+    from paper_2008_11421_b200 import _lib
+    x = rand((pixels, 3), 31)
+    y = torch.full((pixels, 4), 7.0, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.lib().krt_pad_rgb4(x.data_ptr(), y.data_ptr(), pixels, None))
+    torch.cuda.synchronize()
+    assert torch.equal(y[:, :3], x) and bool((y[:, 3] == 0).all())
