@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -219,6 +220,10 @@ struct Params {
 // relu(bn(.)) transform and the A loads happen once per m-tile instead of once
 // per (m, n) tile; the ring then carries B k-blocks only.
 constexpr int kMaxAstatK = 256;
+// A-stationary k-block slots: a ring one larger than an m-tile's k-blocks, so
+// the next m-tile's first k-block loads and transforms while this m-tile's
+// last n-tile still runs (m-tile i, k-block kb -> slot (i * kblocks + kb) % 5)
+constexpr int kAstatSlots = kMaxAstatK / kBK + 1;
 constexpr int kMaxNT = 8;  // n-tiles per CTA in A-stationary mode (N <= 2048)
 
 // EPI 3 residual tiles: [BN / kResW boxes][128 rows][kResW columns], each box
@@ -230,11 +235,11 @@ constexpr int kResBufs = BN <= 64 ? 4 : 2;
 
 template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT>
 struct Smem {
-  alignas(1024) uint8_t a[ASTAT ? kMaxAstatK / kBK : STAGES][kBM * BKT * 2];
+  alignas(1024) uint8_t a[ASTAT ? kAstatSlots : STAGES][kBM * BKT * 2];
   alignas(1024) uint8_t b[STAGES][BN * BKT * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
   uint64_t tfull[4], tempty[4];
-  uint64_t a_full[kMaxAstatK / kBK], a_ready[kMaxAstatK / kBK], a_free[kMaxAstatK / kBK];  // A-stationary, per k-block
+  uint64_t a_full[kAstatSlots], a_ready[kAstatSlots], a_free[kAstatSlots];  // A-stationary, per slot
   uint32_t tmem_base;
   alignas(16) float sc[PRO ? kMaxProK : 4];
   alignas(16) float sh[PRO ? kMaxProK : 4];
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       mbar_init(&S.x_full[i], 1);
       mbar_init(&S.x_empty[i], 128 * kEpiParts);
     }
-    for (int kb = 0; kb < kMaxAstatK / kBK; ++kb) {
+    for (int kb = 0; kb < kAstatSlots; ++kb) {
       mbar_init(&S.a_full[kb], 1);
       mbar_init(&S.a_ready[kb], kXfThreads);
       mbar_init(&S.a_free[kb], 1);
@@ -308,16 +313,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0, aphase = 0;
+      int stage = 0, ag = 0;  // ag: A-stationary k-block sequence number
+      uint32_t phase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
-        if (ASTAT) {  // this m-tile's A k-blocks, each once the previous m-tile's last MMA on it is done
-          for (int kb = 0; kb < kblocks; ++kb) {
-            mbar_wait(&S.a_free[kb], aphase ^ 1);
-            mbar_expect_tx(&S.a_full[kb], kBM * BKT * 2);
-            tma_load_2d(&map_a, &S.a_full[kb], S.a[kb], kb * BKT, mt * kBM);
+        if (ASTAT) {  // this m-tile's A k-blocks, each into a slot the MMAs released
+          for (int kb = 0; kb < kblocks; ++kb, ++ag) {
+            const int sl = ag % kAstatSlots;
+            mbar_wait(&S.a_free[sl], ((uint32_t)(ag / kAstatSlots) & 1u) ^ 1u);
+            mbar_expect_tx(&S.a_full[sl], kBM * BKT * 2);
+            tma_load_2d(&map_a, &S.a_full[sl], S.a[sl], kb * BKT, mt * kBM);
           }
-          aphase ^= 1;
         }
         for (int nt = 0; nt < nts; ++nt) {
           const int n_tile = ASTAT ? nt : n_fixed;
@@ -341,29 +346,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = instr_desc(BN);
-    int stage = 0;
-    uint32_t phase = 0, aphase = 0;
+    int stage = 0, ag0 = 0;  // ag0: sequence number of this m-tile's first A k-block
+    uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+    for (int mt = m_first; mt < p.m_tiles; mt += m_step, ag0 += kblocks) {
       for (int nt = 0; nt < nts; ++nt) {
         mbar_wait(&S.tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
-          if (ASTAT && nt == 0) mbar_wait(&S.a_ready[kb], aphase);  // this A k-block landed and transformed
+          const int ag = ag0 + kb, sl = ag % kAstatSlots;
+          if (ASTAT && nt == 0) mbar_wait(&S.a_ready[sl], (uint32_t)(ag / kAstatSlots) & 1u);  // landed + transformed
           if ((PRO || GATHER) && !ASTAT) mbar_wait(&S.ready[stage], phase);  // transformed / gathered
           else mbar_wait(&S.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(ASTAT ? S.a[kb] : S.a[stage]), b0 = smem_u32(S.b[stage]);
+            const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[stage]);
 #pragma unroll
             for (int k = 0; k < BKT / kUmmaK; ++k)
               umma_bf16(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
                         idesc, (kb | k) != 0);
             umma_commit(&S.empty[stage]);                       // smem stage free when these MMAs finish
             if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
-            if (ASTAT && nt == nts - 1) umma_commit(&S.a_free[kb]);  // A k-block no longer read
+            if (ASTAT && nt == nts - 1) umma_commit(&S.a_free[sl]);  // A slot no longer read
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -376,7 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           acc_phase ^= 1;
         }
       }
-      aphase ^= 1;
     }
   } else if (warp == kXWarp) {
     // ------------------------------------------------ x / residual tile producer
@@ -584,15 +589,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         S.sh[c] = __bfloat162float(p.pb[c]) - p.pmean[c] * sc;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kXfThreads) : "memory");  // transform warps only
-      int stage = 0;
-      uint32_t phase = 0, aphase = 0;
+      int stage = 0, ag = 0;
+      uint32_t phase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         // a = bf16(relu(a*sc + sh)) in place.  Logical 16-byte chunk jj of row r
         // (channels kb*BKT + 8*jj .. +8) is physical chunk swz_chunk(jj, r)
         for (int kb = 0; kb < kblocks; ++kb) {
-          if (ASTAT) mbar_wait(&S.a_full[kb], aphase);
+          const int sl = ag % kAstatSlots;
+          if (ASTAT) mbar_wait(&S.a_full[sl], (uint32_t)(ag / kAstatSlots) & 1u);
           else mbar_wait(&S.full[stage], phase);
-          uint4* rowp = reinterpret_cast<uint4*>((ASTAT ? S.a[kb] : S.a[stage]) + r * BKT * 2);
+          uint4* rowp = reinterpret_cast<uint4*>((ASTAT ? S.a[sl] : S.a[stage]) + r * BKT * 2);
           uint4 u[kPer];
 #pragma unroll
           for (int i = 0; i < kPer; ++i) u[i] = rowp[swz_chunk<BKT>(jh + i, r)];  // consecutive rows: distinct columns
@@ -616,7 +622,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
           if (ASTAT) {
-            mbar_arrive(&S.a_ready[kb]);
+            mbar_arrive(&S.a_ready[sl]);
+            ++ag;
           } else {
             mbar_arrive(&S.ready[stage]);
             if (++stage == STAGES) {
@@ -625,7 +632,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             }
           }
         }
-        if (ASTAT) aphase ^= 1;
       }
     }
   } else {
@@ -954,7 +960,7 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
                             const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
   constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
-                        (ASTAT ? kMaxAstatK / kBK * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
+                        (ASTAT ? kAstatSlots * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
                         (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
