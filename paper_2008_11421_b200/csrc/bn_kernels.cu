@@ -397,19 +397,23 @@ struct BwdCoef {
 template <bool RELU>
 __device__ __forceinline__ float relu_mask(float v, float sc, float sh, float gm) {
   if (!RELU) return gm;
-  float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(v, sc, sh)));
-  return yk > 0.0f ? gm : 0.0f;
+  // bf16(fma) > 0  <=>  fma > 2^-134 (round-to-nearest-even sends (0, 2^-134]
+  // to +0 and everything above to a positive bf16): the forward's exact mask
+  // without the convert round trip
+  return __fmaf_rn(v, sc, sh) > 0x1p-134f ? gm : 0.0f;
 }
 
-// pass-1 accumulation: s1 += gm, s2 += gm * xhat
+// pass-1 accumulation: s1 += gm, s2 += gm * (x - mu); the finalize applies
+// invstd (sum gm * xhat = invstd * s2), one multiply per channel instead of
+// one per element
 template <bool RELU>
 __device__ __forceinline__ void bwd_acc(const Vec8& v, const Vec8& d, const float* sc, const float* sh,
-                                        const float* mu, const float* is, float* s1, float* s2) {
+                                        const float* mu, float* s1, float* s2) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     float gm = relu_mask<RELU>(v.v[k], sc[k], sh[k], d.v[k]);
     s1[k] += gm;
-    s2[k] += gm * ((v.v[k] - mu[k]) * is[k]);
+    s2[k] = __fmaf_rn(gm, v.v[k] - mu[k], s2[k]);
   }
 }
 
@@ -432,9 +436,10 @@ __device__ __forceinline__ void bwd_finalize(const float* part, int64_t rows, in
     double s1, s2;
     if (sum_octet(part, gridDim.x, C, oct, shd, s1, s2)) {
       const int c = oct * 8 + threadIdx.x;
+      const double is = invstd[c], mu = mean[c];
+      s2 *= is;  // sum gm * (x - mu) -> sum gm * xhat
       if (dbeta) dbeta[c] = (float)s1;
       if (dgamma) dgamma[c] = (float)s2;
-      const double is = invstd[c], mu = mean[c];
       const double gs = (double)bf(g, c) * is;
       const double k1 = s1 / (double)rows, k2 = s2 / (double)rows;
       // dx = gs*(gm - k1 - (x - mu)*is*k2)
@@ -456,13 +461,10 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
   Map m(C);
   Rows rw(m, rows);
   const int c0 = m.tx * 8;
-  float sc[8], sh[8], mu[8], is[8];
+  float sc[8], sh[8], mu[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    mu[j] = mean[c0 + j];
-    is[j] = invstd[c0 + j];
-  }
+  for (int j = 0; j < 8; ++j) mu[j] = mean[c0 + j];
   float s1[8] = {0}, s2[8] = {0};
   for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {
     uint4 v[U], d[U];
@@ -473,7 +475,7 @@ __global__ void __launch_bounds__(kThreads) bwd_reduce_kernel(
       d[u] = r < rows ? ld16s(dy + r * C + c0) : make_uint4(0, 0, 0, 0);  // gm = 0 on padding
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) bwd_acc<RELU>(unpack(v[u]), unpack(d[u]), sc, sh, mu, is, s1, s2);
+    for (int u = 0; u < U; ++u) bwd_acc<RELU>(unpack(v[u]), unpack(d[u]), sc, sh, mu, s1, s2);
   }
   cta_partial(s1, s2, smem, m, part, C, c0);
   cg::this_grid().sync();
@@ -494,13 +496,10 @@ __global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
   Map m(C);
   Rows rw(m, rows);
   const int c0 = m.tx * 8;
-  float sc[8], sh[8], mu[8], is[8];
+  float sc[8], sh[8], mu[8];
   bn_coeffs(mean, invstd, g, b, c0, sc, sh);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    mu[j] = mean[c0 + j];
-    is[j] = invstd[c0 + j];
-  }
+  for (int j = 0; j < 8; ++j) mu[j] = mean[c0 + j];
   float s1[8] = {0}, s2[8] = {0};
   for (int64_t r0 = rw.first; r0 < rows; r0 += rw.step * U) {  // U rows x 3-4 tensors in flight
     uint4 v[U], q[U], d[U], e[U];
@@ -524,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) add_relu_reduce_kernel(
         Vec8 xv = unpack(v[u]);
         Vec8 z = add_relu_row<1>(xv, unpack(q[u]), dd, sc, sh, nullptr, nullptr);
         st16(dz + r * C + c0, z);
-        bwd_acc<false>(xv, z, sc, sh, mu, is, s1, s2);
+        bwd_acc<false>(xv, z, sc, sh, mu, s1, s2);
       }
     }
   }
