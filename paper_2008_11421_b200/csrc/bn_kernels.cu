@@ -332,8 +332,7 @@ __device__ __forceinline__ Vec8 add_relu_row(const Vec8& v, const Vec8& rv, cons
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     float pre = __fadd_rn(__fmaf_rn(v.v[k], sc[k], sh[k]), MODE == 2 ? __fmaf_rn(rv.v[k], rsc[k], rsh[k]) : rv.v[k]);
-    float yk = __bfloat162float(__float2bfloat16_rn(pre));
-    o.v[k] = yk > 0.0f ? d.v[k] : 0.0f;
+    o.v[k] = pre > 0x1p-134f ? d.v[k] : 0.0f;  // == (bf16(pre) > 0), see relu_mask
   }
   return o;
 }
