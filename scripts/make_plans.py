@@ -129,11 +129,14 @@ def _resnet1001():
     # compute_rate measured: these narrow (16-64 channel) units are HBM-bound,
     # 0.320 s predicted at 1.25e14 MAC/s vs 1.625 s of compute-stream busy time
     # -> 2.46e13 MAC/s effective; with it the planner swaps more, recomputes
-    # less, and the exposed stall drops from 9.3% to 0.2%
+    # less, and the exposed stall drops from 9.3% to 0.2%.  Recalibrated after
+    # the GEMM forward/dgrad and BN work (session 3): ~1.45 s busy -> 2.76e13;
+    # that plan (21.0 GB swapped) measures 1.410 samples/s, 1.5% stall, vs
+    # 1.352 and 3.1% for the 2.46e13 plan on the same box
     units = resnet1001_units(res=2048, classes=10, depth=1001)
     make("resnet1001_2048_b2", units, 2, 150e9,
          {"family": "preact", "depth": 1001, "res": 2048, "classes": 10, "act": "bf16"}, max_blocks=64,
-         compute_rate=2.46e13)
+         compute_rate=2.76e13)
 
 
 def _resnet200(only):
