@@ -233,6 +233,22 @@ __global__ void __launch_bounds__(kThreads) stem_pool_tiled_kernel(
     const int lr = op / kTile, lc = op % kTile;
     const int oh = oh0 + lr, ow = ow0 + lc;
     if (oh >= P.oh || ow >= P.ow) continue;
+    if constexpr (!ARGMAX) {
+      // forward: packed bf16x2 max over the window (NaN-propagating like aten's
+      // max_pool; the max of bf16 values is one of them, so no rounding)
+      const __nv_bfloat16* pp = patch + (2 * lr * kPatch + 2 * lc) * kPixStride + o8 * 8;
+      uint4 m = *reinterpret_cast<const uint4*>(pp);
+      __nv_bfloat162* mh = reinterpret_cast<__nv_bfloat162*>(&m);
+#pragma unroll
+      for (int kk = 1; kk < 9; ++kk) {
+        const uint4 u = *reinterpret_cast<const uint4*>(pp + ((kk / 3) * kPatch + kk % 3) * kPixStride);
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mh[e] = __hmax2_nan(mh[e], hv[e]);
+      }
+      *reinterpret_cast<uint4*>(y + (((int64_t)n * P.oh + oh) * P.ow + ow) * kTC + o8 * 8) = m;
+      continue;
+    }
     float mx[8];
     int am[8];
 #pragma unroll
