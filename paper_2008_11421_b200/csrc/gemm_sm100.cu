@@ -744,8 +744,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
             float gm = __bfloat162float(stg[r * 32 + 8 * (cc ^ ((r >> 1) & 3)) + ce]);
-            const float yk = __bfloat162float(__float2bfloat16_rn(__fmaf_rn(xv[r], sc, sh)));
-            gm = yk > 0.0f ? gm : 0.0f;   // rows beyond M: staged gm = 0
+            // bf16(fma) > 0 <=> fma > 2^-134 (bn_kernels.cu relu_mask); rows beyond M: staged gm = 0
+            gm = __fmaf_rn(xv[r], sc, sh) > 0x1p-134f ? gm : 0.0f;
             s1[r & 3] += gm;
             s2[r & 3] += gm * ((xv[r] - mu) * is);
           }
