@@ -233,11 +233,17 @@ constexpr int kResW = BN < 64 ? BN : 64;
 template <int BN>
 constexpr int kResBufs = BN <= 64 ? 4 : 2;
 
-template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT>
+// B-stationary (narrow K = one k-block, not gathered): the CTA's fixed n-tile
+// of B is loaded once and stays; the ring carries A only
+template <int BKT, bool GATHER>
+constexpr bool kBStat = BKT < kBK && !GATHER;
+
+template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT, bool BSTAT = false>
 struct Smem {
   alignas(1024) uint8_t a[ASTAT ? kAstatSlots : STAGES][kBM * BKT * 2];
-  alignas(1024) uint8_t b[STAGES][BN * BKT * 2];
+  alignas(1024) uint8_t b[BSTAT ? 1 : STAGES][BN * BKT * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
+  uint64_t bfull;
   uint64_t tfull[4], tempty[4];
   uint64_t a_full[kAstatSlots], a_ready[kAstatSlots], a_free[kAstatSlots];  // A-stationary, per slot
   uint32_t tmem_base;
@@ -265,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // memory in this kernel); using it directly keeps every access in the shared
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT>*>(smem_raw);
+  constexpr bool BSTAT = kBStat<BKT, GATHER>;
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>*>(smem_raw);
   static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
@@ -286,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   const int m_step = ASTAT ? gridDim.x : gridDim.x / p.n_tiles;
 
   if (threadIdx.x == 0) {
+    mbar_init(&S.bfull, 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.ready[s], kXfThreads);
@@ -315,6 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     if (lane == 0) {
       int stage = 0, ag = 0;  // ag: A-stationary k-block sequence number
       uint32_t phase = 0;
+      if (BSTAT) {  // the CTA's n-tile of B (K = one k-block), once
+        mbar_expect_tx(&S.bfull, BN * BKT * 2);
+        tma_load_2d(&map_b, &S.bfull, S.b[0], 0, n_fixed * BN);
+      }
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         if (ASTAT) {  // this m-tile's A k-blocks, each into a slot the MMAs released
           for (int kb = 0; kb < kblocks; ++kb, ++ag) {
@@ -331,10 +343,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             if (ASTAT || GATHER) {  // A is resident / gathered by the transform warps
               mbar_expect_tx(&S.full[stage], BN * BKT * 2);
             } else {
-              mbar_expect_tx(&S.full[stage], (kBM + BN) * BKT * 2);
+              mbar_expect_tx(&S.full[stage], (kBM + (BSTAT ? 0 : BN)) * BKT * 2);
               tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, mt * kBM);
             }
-            tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN);
+            if (!BSTAT) tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -346,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = instr_desc(BN);
+    if (BSTAT) mbar_wait(&S.bfull, 0);
     int stage = 0, ag0 = 0;  // ag0: sequence number of this m-tile's first A k-block
     uint32_t phase = 0;
     int acc = 0;
@@ -362,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           else mbar_wait(&S.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[stage]);
+            const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[BSTAT ? 0 : stage]);
 #pragma unroll
             for (int k = 0; k < BKT / kUmmaK; ++k)
               umma_bf16(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
@@ -944,7 +957,7 @@ template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHE
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
   auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT>);
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, kBStat<BKT, GATHER>>);
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -959,10 +972,11 @@ template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = fa
 cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                             const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
+  constexpr bool bstat = kBStat<BKT, GATHER>;
   constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
                         (ASTAT ? kAstatSlots * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
-                        (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0);
-  constexpr int stage_bytes = (ASTAT ? BN : kBM + BN) * BKT * 2;
+                        (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? BN * BKT * 2 : 0);
+  constexpr int stage_bytes = (ASTAT ? BN : kBM + (bstat ? 0 : BN)) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
   constexpr int stages = avail / stage_bytes > max_stages ? max_stages : avail / stage_bytes;
