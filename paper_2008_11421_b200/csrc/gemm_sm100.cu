@@ -233,15 +233,17 @@ constexpr int kResW = BN < 64 ? BN : 64;
 template <int BN>
 constexpr int kResBufs = BN <= 64 ? 4 : 2;
 
-// B-stationary (narrow K = one k-block, not gathered): the CTA's fixed n-tile
-// of B is loaded once and stays; the ring carries A only
-template <int BKT, bool GATHER>
-constexpr bool kBStat = BKT < kBK && !GATHER;
+// B-stationary (fixed n-tile per CTA, whole B tile <= 32 KB): the CTA's
+// n-tile of B is loaded once and stays; the ring carries A only.  Re-fetching
+// a small B tile for every 128-row tile starved narrow GEMMs (2x on K=16 N=64)
+constexpr int kBStatBytes = 32 * 1024;
+template <int BN, int BKT>
+constexpr int kBSlots = kBStatBytes / (BN * BKT * 2) > 0 ? kBStatBytes / (BN * BKT * 2) : 1;
 
 template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT, bool BSTAT = false>
 struct Smem {
   alignas(1024) uint8_t a[ASTAT ? kAstatSlots : STAGES][kBM * BKT * 2];
-  alignas(1024) uint8_t b[BSTAT ? 1 : STAGES][BN * BKT * 2];
+  alignas(1024) uint8_t b[BSTAT ? kBSlots<BN, BKT> : STAGES][BN * BKT * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
   uint64_t bfull;
   uint64_t tfull[4], tempty[4];
@@ -262,7 +264,7 @@ struct Smem {
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C,
 // 3 C = acc + residual (p.res through map_x)
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false, bool BSTAT = false>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c,
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // memory in this kernel); using it directly keeps every access in the shared
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  constexpr bool BSTAT = kBStat<BKT, GATHER>;
+  static_assert(!BSTAT || (!ASTAT && !GATHER), "B-stationary needs a fixed n-tile and TMA-loaded A");
   auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>*>(smem_raw);
   static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
@@ -323,9 +325,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     if (lane == 0) {
       int stage = 0, ag = 0;  // ag: A-stationary k-block sequence number
       uint32_t phase = 0;
-      if (BSTAT) {  // the CTA's n-tile of B (K = one k-block), once
-        mbar_expect_tx(&S.bfull, BN * BKT * 2);
-        tma_load_2d(&map_b, &S.bfull, S.b[0], 0, n_fixed * BN);
+      if (BSTAT) {  // the CTA's n-tile of B, every k-block, once
+        mbar_expect_tx(&S.bfull, BN * p.K * 2);
+        for (int kb = 0; kb < kblocks; ++kb) tma_load_2d(&map_b, &S.bfull, S.b[kb], kb * BKT, n_fixed * BN);
       }
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         if (ASTAT) {  // this m-tile's A k-blocks, each into a slot the MMAs released
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           else mbar_wait(&S.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[BSTAT ? 0 : stage]);
+            const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[BSTAT ? kb : stage]);
 #pragma unroll
             for (int k = 0; k < BKT / kUmmaK; ++k)
               umma_bf16(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
@@ -953,11 +955,11 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool BSTAT>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, kBStat<BKT, GATHER>>);
+  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER, BSTAT>;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>);
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -968,20 +970,29 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = false>
-cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                            const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
+template <int BN, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool bstat>
+cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                          const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
-  constexpr bool bstat = kBStat<BKT, GATHER>;
   constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
                         (ASTAT ? kAstatSlots * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
-                        (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? BN * BKT * 2 : 0);
+                        (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? kBSlots<BN, BKT> * BN * BKT * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + (bstat ? 0 : BN)) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
   constexpr int stages = avail / stage_bytes > max_stages ? max_stages : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER>(ma, mb, mc, mx, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER, bstat>(ma, mb, mc, mx, p, grid, s);
+}
+
+template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = false>
+cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                            const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
+  if constexpr (!ASTAT && !GATHER) {
+    if (p.K / BKT <= kBSlots<BN, BKT> && BN * p.K * 2 <= kBStatBytes)
+      return dispatch_ring<BN, PRO, EPI, ASTAT, BKT, GATHER, true>(ma, mb, mc, mx, p, grid, s);
+  }
+  return dispatch_ring<BN, PRO, EPI, ASTAT, BKT, GATHER, false>(ma, mb, mc, mx, p, grid, s);
 }
 
 // EPI 3 (residual) instantiations: n-tiles up to 128 columns, never
