@@ -254,7 +254,8 @@ struct Smem {
   // per-warp C staging for the TMA store: 32 rows x 64 B, SWIZZLE_64B (16-byte
   // chunk c of row r at c ^ ((r >> 1) & 3)), so row-per-lane writes and
   // column-per-lane reads are both free of bank conflicts
-  alignas(1024) uint8_t cstage[kEpiWarps][2][32 * 64];
+  // (A-stationary: one buffer per warp, the 32 KB go to a deeper B ring)
+  alignas(1024) uint8_t cstage[kEpiWarps][ASTAT ? 1 : 2][32 * 64];
   // EPI 2: the BN input x of the current tile pair, TMA-loaded by the producer
   // ahead of the epilogue (row-major [128][BN]); one buffer per accumulator.
   // EPI 3: the residual tiles (swizzled boxes), kResBufs deep
@@ -662,8 +663,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // statistics: one partial row per (m-group, lane quarter, tile group); lane
     // = column.  Fixed n-tile: accumulated in registers, written once at the end.
     // A-stationary (the n-tile varies per tile): accumulated in the thread's
-    // own slots of the partial rows, zeroed first and read-modify-written (L2)
-    // per tile (no dynamically indexed local arrays)
+    // own slots of the partial rows, zeroed first and then added to with
+    // fire-and-forget reductions (no load latency in the epilogue; no
+    // dynamically indexed local arrays)
     constexpr bool kStats = EPI == 1 || EPI == 2;
     float* part_row = kStats ? p.part + (((size_t)m_first * 4 + q) * kEpiGroups + grp) * 2 * p.N : nullptr;
     if (ASTAT && kStats) {
@@ -700,7 +702,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         if constexpr (kCW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
         else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col, v);
         // this warp's staging buffer must be free: the TMA store issued two chunks ago has read it
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0) {
+          if (ASTAT) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         __syncwarp();
         uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * kCW * 2);
 #pragma unroll
@@ -767,8 +772,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           const float t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
           if (ASTAT) {
             float* slot = part_row + (size_t)n_tile * BN + col + lane;
-            slot[0] += t1;
-            slot[p.N] += t2;
+            atomicAdd(slot, t1);  // fire-and-forget RED: only this thread touches the slot,
+            atomicAdd(slot + p.N, t2);  // so the sum order (and result) is fixed
           } else {
             acc_s[c] += t1;
             acc_q[c] += t2;
@@ -797,14 +802,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           }
           if (ASTAT) {
             float* slot = part_row + (size_t)n_tile * BN + col + lane;
-            slot[0] += t1;
-            slot[p.N] += t2;
+            atomicAdd(slot, t1);  // fire-and-forget RED: only this thread touches the slot,
+            atomicAdd(slot + p.N, t2);  // so the sum order (and result) is fixed
           } else {
             acc_s[c] += t1;
             acc_q[c] += t2;
           }
         }
-        sbuf ^= 1;
+        if (!ASTAT) sbuf ^= 1;
       }
       tc_fence_before();
       mbar_arrive(&S.tempty[acc]);
@@ -974,7 +979,7 @@ template <int BN, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool bsta
 cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                           const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
-  constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * 2 * 32 * 64 +
+  constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * (ASTAT ? 1 : 2) * 32 * 64 +
                         (ASTAT ? kAstatSlots * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
                         (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? kBSlots<BN, BKT> * BN * BKT * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + (bstat ? 0 : BN)) * BKT * 2;
