@@ -441,13 +441,13 @@ def run_gpu(args, rec):
             return {"bound": "tensor", "kernel": k, "achieved": v[3] / v[1] / 1e12, "peak": pk["bf16_tflops"],
                     "unit": "TFLOP/s", "frac": v[3] / v[1] / 1e12 / pk["bf16_tflops"], "traffic": None,
                     "peak_kind": f"{pk_kind} dense bf16 (burst)", "hbm_frac": hbm["frac"]}
-        tr = ROOT / "profiles" / "round1_s2_dominant_traffic.json"
+        tr = ROOT / "profiles" / "round1_s3_dominant_traffic.json"
         if tr.exists():
             d = json.loads(tr.read_text())
             if d.get("family") == k:   # ncu DRAM bytes of one launch of this family, with its algorithmic bytes
                 hbm["traffic"] = d["dram_bytes_per_launch"]
                 hbm["traffic_alg_bytes"] = d["alg_bytes_per_launch"]
-                hbm["traffic_source"] = f"{d['kernel']}; {d['shape']}; profiles/round1_s2_dominant_traffic.json"
+                hbm["traffic_source"] = f"{d['kernel']}; {d['shape']}; profiles/round1_s3_dominant_traffic.json"
         return hbm
     line = {
         "metric": metric_name(rec),
