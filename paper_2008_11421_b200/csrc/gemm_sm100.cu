@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // memory in this kernel); using it directly keeps every access in the shared
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  static_assert(!BSTAT || (!ASTAT && !GATHER), "B-stationary needs a fixed n-tile and TMA-loaded A");
+  static_assert(!BSTAT || !ASTAT, "B-stationary needs a fixed n-tile");
   auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>*>(smem_raw);
   static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
@@ -344,7 +344,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&S.empty[stage], phase ^ 1);
             if (ASTAT || GATHER) {  // A is resident / gathered by the transform warps
-              mbar_expect_tx(&S.full[stage], BN * BKT * 2);
+              // (gathered A with B stationary: an empty arrival = "slot free")
+              mbar_expect_tx(&S.full[stage], BSTAT ? 0 : BN * BKT * 2);
             } else {
               mbar_expect_tx(&S.full[stage], (kBM + (BSTAT ? 0 : BN)) * BKT * 2);
               tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, mt * kBM);
@@ -993,7 +994,7 @@ cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CU
 template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = false>
 cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                             const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
-  if constexpr (!ASTAT && !GATHER) {
+  if constexpr (!ASTAT) {
     if (p.K / BKT <= kBSlots<BN, BKT> && BN * p.K * 2 <= kBStatBytes)
       return dispatch_ring<BN, PRO, EPI, ASTAT, BKT, GATHER, true>(ma, mb, mc, mx, p, grid, s);
   }
