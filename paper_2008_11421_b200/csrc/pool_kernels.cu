@@ -251,11 +251,59 @@ __global__ void __launch_bounds__(kThreads) stem_pool_tiled_kernel(
     }
     float mx[8];
     int am[8];
+    // argmax (backward): the packed max first; without a NaN, the index is the
+    // first window position equal to it (aten's strict '>' keeps the first of
+    // ties), found scanning backwards so the last match written is the first
+    const __nv_bfloat16* pp = patch + (2 * lr * kPatch + 2 * lc) * kPixStride + o8 * 8;
+    uint4 m = *reinterpret_cast<const uint4*>(pp);
+    __nv_bfloat162* mh = reinterpret_cast<__nv_bfloat162*>(&m);
+#pragma unroll
+    for (int kk = 1; kk < 9; ++kk) {
+      const uint4 u = *reinterpret_cast<const uint4*>(pp + ((kk / 3) * kPatch + kk % 3) * kPixStride);
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mh[e] = __hmax2_nan(mh[e], hv[e]);
+    }
+    bool nan_seen = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(mh[e]);
+      mx[2 * e] = f.x;
+      mx[2 * e + 1] = f.y;
+      nan_seen |= isnan(f.x) || isnan(f.y);
+    }
+    if (!nan_seen) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) am[j] = 0;
+#pragma unroll
+      for (int kk = 8; kk > 0; --kk) {
+        const uint4 u = *reinterpret_cast<const uint4*>(pp + ((kk / 3) * kPatch + kk % 3) * kPixStride);
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(hv[e]);
+          am[2 * e] = f.x == mx[2 * e] ? kk : am[2 * e];
+          am[2 * e + 1] = f.y == mx[2 * e + 1] ? kk : am[2 * e + 1];
+        }
+      }
+      // position 0 wins whenever it equals the max: am stays 0 unless a later match was the first
+      {
+        const uint4 u = *reinterpret_cast<const uint4*>(pp);
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(hv[e]);
+          am[2 * e] = f.x == mx[2 * e] ? 0 : am[2 * e];
+          am[2 * e + 1] = f.y == mx[2 * e + 1] ? 0 : am[2 * e + 1];
+        }
+      }
+    } else
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       mx[j] = -INFINITY;
       am[j] = -1;
     }
+    if (nan_seen)
 #pragma unroll
     for (int kh = 0; kh < 3; ++kh) {
 #pragma unroll
