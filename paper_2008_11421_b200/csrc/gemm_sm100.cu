@@ -622,18 +622,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < kPer; ++i) {
             const int c0 = kb * BKT + 8 * (jh + i);
-            const float4 sa = *reinterpret_cast<const float4*>(&S.sc[c0]);
-            const float4 sb = *reinterpret_cast<const float4*>(&S.sc[c0 + 4]);
-            const float4 ha = *reinterpret_cast<const float4*>(&S.sh[c0]);
-            const float4 hb = *reinterpret_cast<const float4*>(&S.sh[c0 + 4]);
-            const float sc[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
-            const float sh[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u[i]);
+            // channel pairs: bf16x2 -> two fp32 (shift / mask), one packed
+            // fp32x2 FMA (FFMA2, same rounding as two FFMAs), then ReLU and the
+            // bf16x2 pack in one cvt.rn.relu
+            const ulonglong2 sa = *reinterpret_cast<const ulonglong2*>(&S.sc[c0]);
+            const ulonglong2 sb = *reinterpret_cast<const ulonglong2*>(&S.sc[c0 + 4]);
+            const ulonglong2 ha = *reinterpret_cast<const ulonglong2*>(&S.sh[c0]);
+            const ulonglong2 hb = *reinterpret_cast<const ulonglong2*>(&S.sh[c0 + 4]);
+            const unsigned long long sc2[4] = {sa.x, sa.y, sb.x, sb.y}, sh2[4] = {ha.x, ha.y, hb.x, hb.y};
+            uint32_t* w = reinterpret_cast<uint32_t*>(&u[i]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              float2 f = __bfloat1622float2(h[e]);
-              h[e] = __floats2bfloat162_rn(fmaxf(__fmaf_rn(f.x, sc[2 * e], sh[2 * e]), 0.f),
-                                           fmaxf(__fmaf_rn(f.y, sc[2 * e + 1], sh[2 * e + 1]), 0.f));
+              const uint32_t lo = w[e] << 16, hi = w[e] & 0xffff0000u;  // channels 2e, 2e+1 as fp32
+              const unsigned long long xv = ((unsigned long long)hi << 32) | lo;
+              unsigned long long yv;
+              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(yv) : "l"(xv), "l"(sc2[e]), "l"(sh2[e]));
+              uint32_t packed;
+              asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;"
+                  : "=r"(packed)
+                  : "f"(__uint_as_float((uint32_t)(yv >> 32))), "f"(__uint_as_float((uint32_t)yv)));
+              w[e] = packed;
             }
             rowp[swz_chunk<BKT>(jh + i, r)] = u[i];
           }
