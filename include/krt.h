@@ -201,6 +201,11 @@ int krt_synchronize(krt_ctx* ctx);
 int krt_ipc_export(krt_ctx* ctx, void* out, size_t cap, size_t* len);
 int krt_ipc_import(krt_ctx* ctx, const void* handles, int world);
 
+/* Measurement probe (bench.py's iteration roofline): mean seconds of one
+ * ncclReduceScatter of `bytes` of fp32 gradients on the context's own
+ * communicator and network stream, after 2 warm-ups.  Collective: every rank
+ * calls it with the same arguments.  KRT_USAGE for IPC / in-process exchange. */
+int krt_probe_exchange(krt_ctx* ctx, size_t bytes, int iters, double* seconds);
 /* Wait for the last iteration, then return every host-updated weight to the
  * device copy now (the weight_in the next iteration would do), so the device
  * weights equal the masters — for evaluation and checkpoints. */
@@ -335,6 +340,35 @@ int krt_pad_rgb4(const void* x, void* y, int64_t pixels, void* stream);
  * HBM.  part/part_rows: BN statistics of C as krt_conv1x1_bn.  N = 64. */
 int krt_conv_gather_bn(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo, int k,
                        int stride, int pad, int N, int K, float* part, int* part_rows, void* stream);
+/* Implicit-GEMM convolution on tcgen05 with im2col TMA tiles (the 3x3 and
+ * strided convolutions of a bottleneck, cost_model.py:97-105):
+ * C [n*ho*wo, N] bf16 = f(im2col_k,stride,pad(x)) . wk^T, x [n, h, w, cin]
+ * NHWC bf16 (cin % 64 == 0), wk [N][k][k][cin] bf16 (OHWI), f = relu(bn(.))
+ * per input channel when pmean is non-NULL (cin <= 1024; taps in the zero
+ * padding stay zero).  part/part_rows: the BN statistics of C as
+ * krt_conv1x1_bn (N in {64, 128} or N % 256 == 0).  With bx non-NULL this is
+ * the dgrad form of krt_conv1x1_bn_dgrad instead: the epilogue reduces the
+ * backward of the BN whose input is bx [n*ho*wo, N] into part (N in {64, 128}
+ * or N % 128 == 0, no prologue); wk is then the flipped, transposed weight. */
+int krt_conv_im2col_bn(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo, int k,
+                       int stride, int pad, int N, const float* pmean, const float* pinvstd, const void* pgamma,
+                       const void* pbeta, float* part, int* part_rows, const void* bx, const float* bmean,
+                       const float* binvstd, const void* bgamma, const void* bbeta, void* stream);
+/* Weight gradient of a convolution on tcgen05 (the backward work
+ * cost_model.py:97-105 counts for a Conv layer): dw [cout][k][k][cin] fp32
+ * (OHWI, written, not accumulated) = sum over the output pixels of
+ * dy [n, ho, wo, cout] times the k x k window (stride, zero padding pad) of
+ * f(x), x [n, h, w, cin] NHWC bf16; f = relu(bn(.)) per input channel with
+ * pmean/pinvstd fp32 and pgamma/pbeta bf16 (cin <= 1024) when pmean is
+ * non-NULL: the BN output the forward convolved is never rebuilt in HBM.
+ * The pixel reduction is split across the SMs into fp32 partial tiles summed
+ * in a fixed order (deterministic); ws: krt_conv_wgrad_workspace_bytes.
+ * cout % 128 == 0, cin % 64 == 0, k in {1, 3}, stride in {1, 2},
+ * ho = (h + 2*pad - k)/stride + 1 (same for wo), 16-byte aligned pointers. */
+size_t krt_conv_wgrad_workspace_bytes(int n, int ho, int wo, int cout, int cin, int k);
+int krt_conv_wgrad(const void* dy, const void* x, float* dw, int n, int h, int w, int cin, int ho, int wo, int cout,
+                   int k, int stride, int pad, const float* pmean, const float* pinvstd, const void* pgamma,
+                   const void* pbeta, void* ws, size_t ws_bytes, void* stream);
 /* Backward of a 1x1 convolution fused with the reduce of the BN (+ ReLU) in
  * front of it: dX[M,N] = dY[M,K] . Wt[N,K]^T (Wt = weights transposed, K-major)
  * is stored, and with x = that BN's input the epilogue reduces sum(gm) and

@@ -73,6 +73,7 @@ EXPORTS = {
     "krt_peer_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "krt_peer_group_destroy": (C.c_int, [C.c_void_p]),
     "krt_plan_arena": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.c_int, C.POINTER(C.c_void_p)]),
+    "krt_probe_exchange": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int, C.POINTER(C.c_double)]),
     "krt_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "krt_destroy": (C.c_int, [C.c_void_p]),
     "krt_register_block": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.POINTER(C.c_int64), C.c_int]),
@@ -112,6 +113,9 @@ EXPORTS = {
     "krt_conv1x1_bn_res": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 8),
     "krt_pad_rgb4": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "krt_conv_gather_bn": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 11 + [C.c_void_p] * 3),
+    "krt_conv_im2col_bn": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 10 + [C.c_void_p] * 12),
+    "krt_conv_wgrad_workspace_bytes": (C.c_size_t, [C.c_int] * 6),
+    "krt_conv_wgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 10 + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]),
     "krt_conv1x1_bn_dgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 8),
     "krt_bn_partials_bwd_finalize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64] + [C.c_void_p] * 7),
     "krt_bn_backward_elemt": (C.c_int, [C.c_void_p] * 8 + [C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p]),

@@ -299,3 +299,102 @@ def conv1x1_dgrad_supported(cout, cin):
     """conv1x1_dgrad_bn_backward for a (Cout, Cin) 1x1 weight: the GEMM
     reduces over K = Cout into N = Cin columns (BN-backward epilogue: N >= 64)."""
     return conv1x1_supported(cout, cin) and cin >= 64 and supported(cin)
+
+
+def conv_wgrad_supported(cout, cin, k, stride, pre=False):
+    """krt_conv_wgrad's shape rules (csrc/wgrad_sm100.cu)."""
+    return cout % 128 == 0 and cin % 64 == 0 and k in (1, 3) and stride in (1, 2) and (not pre or cin <= 1024)
+
+
+def conv_wgrad(dy, x, dw, k, stride, pad, pre=None):
+    """Weight gradient of conv(f(x), w) on the tcgen05 wgrad GEMM, written in
+    fp32 into dw (Cout, k, k, Cin) OHWI contiguous (the executor's gradient
+    view).  dy: (N, Cout, Ho, Wo) channels_last bf16 gradient of the conv
+    output; x: (N, Cin, H, W) channels_last bf16; pre=(mean, invstd, gamma,
+    beta): f = relu(bn(.)) applied in shared memory (relu(bn(x)) is never
+    materialised), else f = identity."""
+    import ctypes as C
+    dy, x = _nhwc(dy), _nhwc(x)
+    n, cout, ho, wo = dy.shape
+    _, cin, h, w = x.shape
+    assert dw.dtype == torch.float32 and dw.is_contiguous() and dw.numel() == cout * k * k * cin
+    L = _lib.lib()
+    ws = torch.empty(L.krt_conv_wgrad_workspace_bytes(n, ho, wo, cout, cin, k), dtype=torch.uint8, device=x.device)
+    pm, pi, pg, pb = pre if pre is not None else (None, None, None, None)
+    P = n * ho * wo
+    with _timed("conv_wgrad", P * cout * 2 + n * h * w * cin * 2 + dw.numel() * 4, 2.0 * P * cout * k * k * cin):
+        _lib.check(L.krt_conv_wgrad(dy.data_ptr(), x.data_ptr(), dw.data_ptr(), n, h, w, cin, ho, wo, cout, k, stride,
+                                    pad, _ptr(pm), _ptr(pi), _ptr(pg), _ptr(pb), ws.data_ptr(), ws.numel(),
+                                    _stream()))
+    return dw
+
+
+def conv_im2col_supported(cin, cout, pre=False, dgrad=False):
+    """krt_conv_im2col_bn's shape rules (csrc/gemm_sm100.cu)."""
+    if cin % 64 or (pre and cin > 1024):
+        return False
+    return cout in (64, 128) or cout % (128 if dgrad else 256) == 0
+
+
+def conv_im2col(x, w, stride, pad, out=None, pre=None, stats=None):
+    """k x k convolution on the tcgen05 implicit GEMM (im2col TMA tiles).
+    x: (N, Cin, H, W) channels_last bf16; w: (Cout, k, k, Cin) bf16 OHWI
+    contiguous (the executor's weight view).  pre=(mean, invstd, gamma, beta):
+    convolve relu(bn(x)) (never written; the padding stays zero); stats=(mean,
+    invstd): batch statistics of the bf16 result from the epilogue."""
+    import ctypes as C
+    x = _nhwc(x)
+    n, cin, h, ww = x.shape
+    cout, k = w.shape[0], w.shape[1]
+    assert w.shape == (cout, k, k, cin) and w.is_contiguous()
+    ho, wo = (h + 2 * pad - k) // stride + 1, (ww + 2 * pad - k) // stride + 1
+    y = out if out is not None else torch.empty((n, cout, ho, wo), dtype=x.dtype, device=x.device,
+                                                memory_format=torch.channels_last)
+    M = n * ho * wo
+    part = None
+    rows = C.c_int(0)
+    if stats is not None:
+        part = torch.empty(_lib.lib().krt_conv1x1_partials_bytes(cout) // 4, dtype=torch.float32, device=x.device)
+    pm, pi, pg, pb = pre if pre is not None else (None, None, None, None)
+    with _timed("conv_im2col_bn", n * h * ww * cin * 2 + M * cout * 2, 2.0 * M * k * k * cin * cout):
+        _lib.check(_lib.lib().krt_conv_im2col_bn(x.data_ptr(), w.data_ptr(), y.data_ptr(), n, h, ww, cin, ho, wo, k,
+                                                 stride, pad, cout, _ptr(pm), _ptr(pi), _ptr(pg), _ptr(pb),
+                                                 _ptr(part), C.byref(rows), None, None, None, None, None,
+                                                 _stream()))
+        if stats is not None:
+            _lib.check(_lib.lib().krt_bn_partials_finalize(part.data_ptr(), rows.value, cout, M, EPS,
+                                                           stats[0].data_ptr(), stats[1].data_ptr(), _stream()))
+    return y
+
+
+def conv_im2col_dgrad_bn_backward(dy, w, x, mean, invstd, g, b, dgamma=None, dbeta=None, relu=True, addend=None):
+    """Gradient w.r.t. x of conv_kxk(relu(bn(x))) (stride 1, 'same' padding):
+    da = conv(dy, W flipped and transposed) on the im2col GEMM with the BN
+    backward reduce of (da, x) in its epilogue, then the BN backward
+    elementwise pass.  dy: (N, Cout, H, W); w: (Cout, k, k, Cin) OHWI."""
+    import ctypes as C
+    dy, x = _nhwc(dy), _nhwc(x)
+    n, cout, h, ww = dy.shape
+    k, cin = w.shape[1], w.shape[3]
+    pad = k // 2
+    wt = w.flip(1, 2).permute(3, 1, 2, 0).contiguous()      # [Cin][k][k][Cout]
+    M = n * h * ww
+    da = torch.empty((n, cin, h, ww), dtype=dy.dtype, device=dy.device, memory_format=torch.channels_last)
+    part = torch.empty(_lib.lib().krt_conv1x1_partials_bytes(cin) // 4, dtype=torch.float32, device=dy.device)
+    coef = torch.empty(3 * cin, dtype=torch.float32, device=dy.device)
+    rows = C.c_int(0)
+    with _timed("conv_im2col_dgrad_bn", M * (cout + 2 * cin) * 2, 2.0 * M * k * k * cin * cout):
+        _lib.check(_lib.lib().krt_conv_im2col_bn(dy.data_ptr(), wt.data_ptr(), da.data_ptr(), n, h, ww, cout, h, ww,
+                                                 k, 1, pad, cin, None, None, None, None, part.data_ptr(),
+                                                 C.byref(rows), x.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                                                 g.data_ptr(), b.data_ptr(), _stream()))
+        _lib.check(_lib.lib().krt_bn_partials_bwd_finalize(part.data_ptr(), rows.value, cin, M, mean.data_ptr(),
+                                                           invstd.data_ptr(), g.data_ptr(), _ptr(dgamma),
+                                                           _ptr(dbeta), coef.data_ptr(), _stream()))
+    dx = torch.empty_like(x, memory_format=torch.channels_last)
+    with _timed("bn_backward_elemt", M * cin * 2 * (3 if addend is None else 4)):
+        _lib.check(_lib.lib().krt_bn_backward_elemt(da.data_ptr(), x.data_ptr(), mean.data_ptr(), invstd.data_ptr(),
+                                                    g.data_ptr(), b.data_ptr(), coef.data_ptr(),
+                                                    None if addend is None else _nhwc(addend).data_ptr(),
+                                                    int(relu), dx.data_ptr(), M, cin, _stream()))
+    return dx

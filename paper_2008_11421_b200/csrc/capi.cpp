@@ -16,6 +16,7 @@
 #include "bn_kernels.hpp"
 #include "pool_kernels.hpp"
 #include "gemm_sm100.hpp"
+#include "wgrad_sm100.hpp"
 #include "ln_kernels.hpp"
 #include "kernels.hpp"
 #include "runtime.hpp"
@@ -366,6 +367,10 @@ int krt_ipc_import(krt_ctx* ctx, const void* handles, int world) {
   return guard([&] { ctx->rt->ipc_import(static_cast<const uint8_t*>(handles), world); });
 }
 
+int krt_probe_exchange(krt_ctx* ctx, size_t bytes, int iters, double* seconds) {
+  return guard([&] { *seconds = ctx->rt->probe_exchange(bytes, iters); });
+}
+
 int krt_flush_weights(krt_ctx* ctx) {
   return guard([&] { ctx->rt->flush_weights(); });
 }
@@ -489,6 +494,27 @@ int krt_conv_gather_bn(const void* x, const void* wk, void* C, int n, int h, int
   KRT_CUDA_GUARD(
       conv_gather_fprop(x, wk, C, n, h, w, cin, ho, wo, k, stride, pad, N, K, part, part_rows, (cudaStream_t)stream),
       "conv_gather_bn");
+}
+
+int krt_conv_im2col_bn(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo, int k,
+                       int stride, int pad, int N, const float* pmean, const float* pinvstd, const void* pgamma,
+                       const void* pbeta, float* part, int* part_rows, const void* bx, const float* bmean,
+                       const float* binvstd, const void* bgamma, const void* bbeta, void* stream) {
+  KRT_CUDA_GUARD(conv_im2col_fprop(x, wk, C, n, h, w, cin, ho, wo, k, stride, pad, N, pmean, pinvstd, pgamma, pbeta,
+                                   part, part_rows, bx, bmean, binvstd, bgamma, bbeta, (cudaStream_t)stream),
+                 "conv_im2col_bn");
+}
+
+size_t krt_conv_wgrad_workspace_bytes(int n, int ho, int wo, int cout, int cin, int k) {
+  return conv_wgrad_workspace_bytes(n, ho, wo, cout, cin, k);
+}
+
+int krt_conv_wgrad(const void* dy, const void* x, float* dw, int n, int h, int w, int cin, int ho, int wo, int cout,
+                   int k, int stride, int pad, const float* pmean, const float* pinvstd, const void* pgamma,
+                   const void* pbeta, void* ws, size_t ws_bytes, void* stream) {
+  KRT_CUDA_GUARD(conv_wgrad(dy, x, dw, n, h, w, cin, ho, wo, cout, k, stride, pad, pmean, pinvstd, pgamma, pbeta, ws,
+                            ws_bytes, (cudaStream_t)stream),
+                 "conv_wgrad");
 }
 
 int krt_conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,

@@ -787,7 +787,9 @@ DpLayout dp_layout(const std::vector<int64_t>& block_params, int groups, int wor
     for (int b : gs[gi]) {
       L.block_off[b - 1] = off + n;
       L.group_of[b - 1] = (int)gi + 1;
-      n += block_params[b - 1];
+      // every block 64-element (256-byte fp32) aligned: the vectorised
+      // update and reduce kernels take any block's slice
+      n += (block_params[b - 1] + 63) / 64 * 64;
     }
     int64_t pn = (n + pad - 1) / pad * pad;
     L.group_lo.push_back(off);

@@ -35,13 +35,13 @@
 #include <mutex>
 
 #include "gemm_sm100.hpp"
+#include "sm100_common.cuh"
 
 namespace krt {
 namespace {
+using namespace sm100;
 
-constexpr int kBM = 128;       // tile rows (UMMA M, TMEM lanes)
 constexpr int kBK = 64;        // k-block: 64 bf16 = one 128-byte swizzle row
-constexpr int kUmmaK = 16;     // K per tcgen05.mma (bf16)
 constexpr int kEpiWarps = 16;  // four per TMEM lane quarter, each a quarter of the columns
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kXfWarp0 = 2 + kEpiWarps;        // prologue transform warps
@@ -50,140 +50,6 @@ constexpr int kXWarp = kXfWarp0 + kXfThreads / 32;  // epilogue-operand (x / res
 constexpr int kThreads = 64 + kEpiThreads + kXfThreads + 32;  // producer, MMA, epilogue, transform, x producer
 constexpr int kEpiWarp0 = 2;
 constexpr int kMaxProK = 1024;  // prologue channels held in shared memory
-
-// ---------------------------------------------------------------------------
-// PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t"
-      "}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t cols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
-               "r"(cols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// 32 lanes x 32 consecutive fp32 columns: thread = lane = row, v[j] = column j
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-}
-
-// 32 lanes x 16 consecutive fp32 columns (narrow n-tiles)
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-}
-
-// UMMA shared-memory descriptor, K-major, for a k-block of BKT bf16 per row
-// (row = 2*BKT bytes = the swizzle span: 128 B -> SWIZZLE_128B, 64 B ->
-// SWIZZLE_64B, 32 B -> SWIZZLE_32B), 8-row atoms 8 rows apart
-// (cute/arch/mma_sm100_desc.hpp SmemDescriptor: start>>4 [0,14), LBO>>4 [16,30),
-// SBO>>4 [32,46), version 1 [46,48), base offset [49,52), layout [61,64))
-template <int BKT>
-__device__ __forceinline__ uint64_t kmajor_desc(uint32_t smem_addr) {
-  constexpr uint64_t layout = BKT == 64 ? 2 : (BKT == 32 ? 4 : 6);  // SW128 / SW64 / SW32
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                         // LBO (unused for swizzled K-major)
-  d |= (uint64_t)((8 * BKT * 2) >> 4) << 32;      // SBO: next 8-row group
-  d |= (uint64_t)1 << 46;                         // version
-  d |= layout << 61;
-  return d;
-}
-
-// physical 16-byte chunk of logical chunk jj in row r under the TMA swizzle
-// matching a BKT-wide row (address bits [4,..) ^= bits [7,..))
-template <int BKT>
-__device__ __forceinline__ int swz_chunk(int jj, int r) {
-  if constexpr (BKT == 64) return jj ^ (r & 7);
-  else if constexpr (BKT == 32) return jj ^ ((r >> 1) & 3);
-  else return jj ^ ((r >> 2) & 1);
-}
-
-// instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M=128, N
-__host__ __device__ constexpr uint32_t instr_desc(int n) {
-  return (1u << 4)                      // c_format F32
-         | (1u << 7)                    // a_format BF16
-         | (1u << 10)                   // b_format BF16
-         | ((uint32_t)(n >> 3) << 17)   // n_dim
-         | ((uint32_t)(kBM >> 4) << 24);  // m_dim
-}
 
 // ---------------------------------------------------------------------------
 struct Params {
@@ -265,7 +131,8 @@ struct Smem {
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C,
 // 3 C = acc + residual (p.res through map_x)
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false, bool BSTAT = false>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false, bool BSTAT = false,
+          bool IM2A = false>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c,
@@ -277,10 +144,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   static_assert(!BSTAT || !ASTAT, "B-stationary needs a fixed n-tile");
   auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>*>(smem_raw);
   static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
+  static_assert(!IM2A || (!GATHER && !ASTAT && BKT == kBK), "im2col A: 64-channel k-blocks, streamed");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
   if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B operands need 1024-byte alignment
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblocks = p.K / BKT;
+  const int cblocks = IM2A ? p.gc / BKT : 1;  // im2col: channel blocks per filter tap
   // epilogue column parts: one warp per (part, TMEM lane quarter); the 16
   // epilogue warps form kEpiGroups groups that drain alternate tiles, each
   // from its own accumulator (kAcc >= 2 accumulators in TMEM)
@@ -331,6 +200,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         for (int kb = 0; kb < kblocks; ++kb) tma_load_2d(&map_b, &S.bfull, S.b[kb], kb * BKT, n_fixed * BN);
       }
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+        int a_n = 0, a_ih0 = 0, a_iw0 = 0;  // im2col: window origin of the m-tile's first pixel
+        if (IM2A) {
+          const int64_t pix = (int64_t)mt * kBM, plane = (int64_t)p.gho * p.gwo;
+          a_n = (int)(pix / plane);
+          const int rem = (int)(pix - (int64_t)a_n * plane), oh = rem / p.gwo;
+          a_ih0 = oh * p.gs - p.gp;
+          a_iw0 = (rem - oh * p.gwo) * p.gs - p.gp;
+        }
         if (ASTAT) {  // this m-tile's A k-blocks, each into a slot the MMAs released
           for (int kb = 0; kb < kblocks; ++kb, ++ag) {
             const int sl = ag % kAstatSlots;
@@ -348,7 +225,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
               mbar_expect_tx(&S.full[stage], BSTAT ? 0 : BN * BKT * 2);
             } else {
               mbar_expect_tx(&S.full[stage], (kBM + (BSTAT ? 0 : BN)) * BKT * 2);
-              tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, mt * kBM);
+              if (IM2A) {
+                // k-block kb = (tap, 64-channel block): one im2col box of the
+                // m-tile's 128 output pixels at filter offset (kh, kw)
+                const int tap = kb / cblocks, c0 = (kb - tap * cblocks) * BKT;
+                tma_load_im2col_4d(&map_a, &S.full[stage], S.a[stage], c0, a_iw0, a_ih0, a_n, (uint16_t)(tap % p.gk),
+                                   (uint16_t)(tap / p.gk));
+              } else {
+                tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, mt * kBM);
+              }
             }
             if (!BSTAT) tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN);
             if (++stage == STAGES) {
@@ -599,8 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       const int xt = threadIdx.x - kXfWarp0 * 32;  // 0..255
       constexpr int kPer = BKT / 16;                // 16-byte chunks per thread (two threads per row)
       const int r = xt & 127, jh = kPer * (xt >> 7);  // tile row, first logical chunk
-      // the previous BN's affine, exactly as bn_apply computes it
-      for (int c = xt; c < p.K; c += kXfThreads) {
+      // the previous BN's affine, exactly as bn_apply computes it (per input
+      // channel: K columns, or the im2col input's channels)
+      for (int c = xt; c < (IM2A ? p.gc : p.K); c += kXfThreads) {
         float sc = p.pinvstd[c] * __bfloat162float(p.pg[c]);
         S.sc[c] = sc;
         S.sh[c] = __bfloat162float(p.pb[c]) - p.pmean[c] * sc;
@@ -609,6 +495,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       int stage = 0, ag = 0;
       uint32_t phase = 0;
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
+        // im2col: this row's output pixel and its window origin; rows whose
+        // tap falls in the zero padding (or beyond M) stay zero
+        bool rvalid = true;
+        int ih0 = 0, iw0 = 0;
+        if (IM2A) {
+          const int64_t pix = (int64_t)mt * kBM + r, plane = (int64_t)p.gho * p.gwo;
+          rvalid = pix < p.M;
+          const int n = (int)(pix / plane), rem = (int)(pix - (int64_t)n * plane), oh = rem / p.gwo;
+          ih0 = oh * p.gs - p.gp;
+          iw0 = (rem - oh * p.gwo) * p.gs - p.gp;
+        }
         // a = bf16(relu(a*sc + sh)) in place.  Logical 16-byte chunk jj of row r
         // (channels kb*BKT + 8*jj .. +8) is physical chunk swz_chunk(jj, r)
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -616,12 +513,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           if (ASTAT) mbar_wait(&S.a_full[sl], (uint32_t)(ag / kAstatSlots) & 1u);
           else mbar_wait(&S.full[stage], phase);
           uint4* rowp = reinterpret_cast<uint4*>((ASTAT ? S.a[sl] : S.a[stage]) + r * BKT * 2);
+          int cbase = kb * BKT;  // prologue channel of this k-block's first column
+          bool valid = true;
+          if (IM2A) {
+            const int tap = kb / cblocks, ih = ih0 + tap / p.gk, iw = iw0 + tap % p.gk;
+            cbase = (kb - tap * cblocks) * BKT;
+            valid = rvalid && ih >= 0 && ih < p.gh && iw >= 0 && iw < p.gw;
+          }
           uint4 u[kPer];
 #pragma unroll
           for (int i = 0; i < kPer; ++i) u[i] = rowp[swz_chunk<BKT>(jh + i, r)];  // consecutive rows: distinct columns
 #pragma unroll
           for (int i = 0; i < kPer; ++i) {
-            const int c0 = kb * BKT + 8 * (jh + i);
+            if (IM2A && !valid) {
+              u[i] = make_uint4(0u, 0u, 0u, 0u);
+              rowp[swz_chunk<BKT>(jh + i, r)] = u[i];
+              continue;
+            }
+            const int c0 = cbase + 8 * (jh + i);
             // channel pairs: bf16x2 -> two fp32 (shift / mask), one packed
             // fp32x2 FMA (FFMA2, same rounding as two FFMAs), then ReLU and the
             // bf16x2 pack in one cvt.rn.relu
@@ -928,51 +837,11 @@ __global__ void __launch_bounds__(1024) partials_bwd_finalize_kernel(
 
 // ---------------------------------------------------------------------------
 // host side
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-EncodeFn encode_fn() {
-  static EncodeFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(p);
-  });
-  return fn;
-}
-
-// [rows, cols] bf16 row-major, box [box_rows, box_cols]
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows, int box_cols,
-              CUtensorMapSwizzle sw) {
-  EncodeFn enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int num_sms() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
-
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool BSTAT>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool BSTAT, bool IM2A>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER, BSTAT>;
+  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER, BSTAT, IM2A>;
   const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>);
   static bool configured = false;  // per instantiation
   if (!configured) {
@@ -984,7 +853,7 @@ cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool bstat>
+template <int BN, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool bstat, bool IM2A = false>
 cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                           const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
@@ -996,7 +865,15 @@ cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
   constexpr int stages = avail / stage_bytes > max_stages ? max_stages : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER, bstat>(ma, mb, mc, mx, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER, bstat, IM2A>(ma, mb, mc, mx, p, grid, s);
+}
+
+// im2col A (3x3 / strided convolutions): streamed 64-channel k-blocks, B too
+// wide to stay resident
+template <int BN, bool PRO, int EPI>
+cudaError_t dispatch_im2col(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
+                            const Params& p, int grid, cudaStream_t s) {
+  return dispatch_ring<BN, PRO, EPI, false, kBK, false, false, true>(ma, mb, mc, mx, p, grid, s);
 }
 
 template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = false>
@@ -1268,6 +1145,85 @@ cudaError_t bn_partials_finalize(const float* part, int part_rows, int N, int64_
                                  float* invstd, cudaStream_t s) {
   partials_finalize_kernel<<<(N + 31) / 32, 1024, 0, s>>>(part, part_rows, N, M, eps, mean, invstd);
   return cudaGetLastError();
+}
+
+cudaError_t conv_im2col_fprop(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo,
+                              int k, int stride, int pad, int N, const float* pmean, const float* pinvstd,
+                              const void* pg, const void* pb, float* part, int* part_rows, const void* bx,
+                              const float* bmean, const float* binvstd, const void* bg, const void* bb,
+                              cudaStream_t s) {
+  const int64_t M = (int64_t)n * ho * wo;
+  const int K = k * k * cin;
+  const bool bwd = bx != nullptr, pro = pmean != nullptr, st = part != nullptr;
+  if (M <= 0 || cin % kBK != 0 || k < 1 || k > 7 || stride < 1 || stride > 2 || (pro && cin > kMaxProK))
+    return cudaErrorInvalidValue;
+  // the im2col traversal visits exactly these output rows / columns
+  if (ho != (h + 2 * pad - k) / stride + 1 || wo != (w + 2 * pad - k) / stride + 1) return cudaErrorInvalidValue;
+  if (bwd ? (N != 64 && N != 128 && N % 128 != 0) || pro || part == nullptr
+          : (N != 64 && N != 128 && N % 256 != 0))
+    return cudaErrorInvalidValue;
+  if (M > 0x7fffffffLL) return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wk) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return cudaErrorMisalignedAddress;
+  const int BN = bwd ? (N < 128 ? N : 128) : (N <= 256 ? N : 256);
+  Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.BN = BN;
+  p.n_tiles = N / BN;
+  p.m_tiles = (int)((M + kBM - 1) / kBM);
+  p.C = static_cast<__nv_bfloat16*>(C);
+  p.part = part;
+  p.pmean = pmean;
+  p.pinvstd = pinvstd;
+  p.pg = static_cast<const __nv_bfloat16*>(pg);
+  p.pb = static_cast<const __nv_bfloat16*>(pb);
+  p.bx = static_cast<const __nv_bfloat16*>(bx);
+  p.bmean = bmean;
+  p.binvstd = binvstd;
+  p.bg = static_cast<const __nv_bfloat16*>(bg);
+  p.bb = static_cast<const __nv_bfloat16*>(bb);
+  p.gh = h;
+  p.gw = w;
+  p.gc = cin;
+  p.gho = ho;
+  p.gwo = wo;
+  p.gk = k;
+  p.gs = stride;
+  p.gp = pad;
+  CUtensorMap ma, mb, mc, mx;
+  if (!make_im2col_map(&ma, x, n, h, w, cin, k, stride, pad, kBM) ||
+      !make_map(&mb, wk, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorInvalidValue;
+  if (bwd) {
+    if (!make_map(&mx, bx, M, N, kBM, BN, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  } else {
+    mx = mc;
+  }
+  int per = num_sms() / p.n_tiles;
+  if (per < 1) per = 1;
+  if (per > p.m_tiles) per = p.m_tiles;
+  const int grid = per * p.n_tiles;
+  const int epi_groups = 4 / (BN >= 128 ? 4 : BN / 32);
+  if (part_rows) *part_rows = per * 4 * epi_groups;
+  if (bwd) {
+    if (BN == 64) return dispatch_im2col<64, false, 2>(ma, mb, mc, mx, p, grid, s);
+    return dispatch_im2col<128, false, 2>(ma, mb, mc, mx, p, grid, s);
+  }
+#define KRT_IM2COL_BN(BNV)                                                      \
+  if (BN == BNV) {                                                              \
+    if (pro && st) return dispatch_im2col<BNV, true, 1>(ma, mb, mc, mx, p, grid, s); \
+    if (pro) return dispatch_im2col<BNV, true, 0>(ma, mb, mc, mx, p, grid, s);       \
+    if (st) return dispatch_im2col<BNV, false, 1>(ma, mb, mc, mx, p, grid, s);       \
+    return dispatch_im2col<BNV, false, 0>(ma, mb, mc, mx, p, grid, s);              \
+  }
+  KRT_IM2COL_BN(64)
+  KRT_IM2COL_BN(128)
+  KRT_IM2COL_BN(256)
+#undef KRT_IM2COL_BN
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace krt

@@ -28,6 +28,16 @@ cudaError_t conv1x1_bn_res_fprop(const void* A, const void* B, void* C, int64_t 
 cudaError_t conv1x1_bn_dgrad(const void* dY, const void* Wt, void* dX, int64_t M, int N, int K, const void* x,
                              const float* mean, const float* invstd, const void* g, const void* b, float* part,
                              int* part_rows, cudaStream_t s);
+// implicit-GEMM convolution with im2col TMA A tiles (k x k, stride, pad; cin %
+// 64 == 0): C[n*ho*wo, N] = f(im2col(x)) . wk^T, wk [N, k*k*cin] (OHWI
+// flattened), f = relu(bn(.)) per input channel when pmean (padding stays
+// zero); part: BN statistics of C (EPI 1) or, with bx, the BN-backward reduce
+// of (C, bx) (EPI 2, the dgrad form)
+cudaError_t conv_im2col_fprop(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int ho, int wo,
+                              int k, int stride, int pad, int N, const float* pmean, const float* pinvstd,
+                              const void* pg, const void* pb, float* part, int* part_rows, const void* bx,
+                              const float* bmean, const float* binvstd, const void* bg, const void* bb,
+                              cudaStream_t s);
 cudaError_t bn_partials_bwd_finalize(const float* part, int part_rows, int N, int64_t M, const float* mean,
                                      const float* invstd, const void* g, float* dgamma, float* dbeta, float* coef,
                                      cudaStream_t s);

@@ -11,7 +11,16 @@
 
 namespace krt {
 
-void host_update_range(float* __restrict p, float* __restrict m, float* __restrict v,
+// x86-64: AVX-512 / AVX2 clones picked at load time (ifunc), baseline
+// otherwise; every clone evaluates the same IEEE sequence (no contraction), so
+// the result does not depend on the host ISA.
+#if defined(__x86_64__) && defined(__GNUC__) && !defined(__clang__)
+#define KRT_SIMD_CLONES __attribute__((target_clones("avx512f", "avx2", "default")))
+#else
+#define KRT_SIMD_CLONES
+#endif
+
+KRT_SIMD_CLONES void host_update_range(float* __restrict p, float* __restrict m, float* __restrict v,
                        const float* __restrict grad, void* weights, int weight_dtype, size_t lo,
                        size_t hi, const OptimScalars& s) {
   const float wd = s.weight_decay, gs = s.grad_scale;

@@ -56,15 +56,26 @@ void PeerGroup::mark(int rank, int kind, int group, int step) {
   cv.notify_all();
 }
 
-void PeerGroup::wait_all(int kind, int group, int step) {
+void PeerGroup::wait_all(int kind, int group, int step, double timeout_s) {
   std::unique_lock<std::mutex> lk(mu);
-  cv.wait(lk, [&] {
+  auto ready = [&] {
     for (int r = 0; r < world; ++r) {
       auto it = marks.find({r, kind, group});
       if (it == marks.end() || it->second < step) return false;
     }
     return true;
-  });
+  };
+  if (!cv.wait_for(lk, std::chrono::duration<double>(timeout_s), ready)) {
+    static const char* kinds[] = {"backward", "weight shard", "flush"};
+    std::string missing;
+    for (int r = 0; r < world; ++r) {
+      auto it = marks.find({r, kind, group});
+      if (it == marks.end() || it->second < step) missing += (missing.empty() ? "" : ", ") + std::to_string(r);
+    }
+    throw std::runtime_error("peer wait timed out after " + std::to_string(timeout_s) + " s: rank(s) " + missing +
+                             " never issued the " + kinds[kind] + " of group " + std::to_string(group) +
+                             " for iteration " + std::to_string(step));
+  }
 }
 
 cudaEvent_t PeerGroup::event(int rank, int kind, int group) {
@@ -96,6 +107,11 @@ Runtime::Runtime(const krt_config& cfg) : cfg_(cfg) {
   CK(cudaStreamCreateWithPriority(&streams_[0], cudaStreamNonBlocking, lo));
   for (int i = 1; i < 4; ++i) CK(cudaStreamCreateWithPriority(&streams_[i], cudaStreamNonBlocking, hi));
   CK(cudaEventCreate(&ev_base_));
+  CK(cudaStreamCreateWithPriority(&clock_stream_, cudaStreamNonBlocking, hi));
+  if (const char* w = std::getenv("KRT_WATCHDOG_S")) {
+    double v = std::atof(w);
+    if (v > 0) watchdog_s_ = v;
+  }
   dp_ = world_ > 1 || cfg.force_dp_path;
   ipc_ = dp_ && cfg.ipc_exchange;
   if (ipc_ && cfg.peer_group) throw std::invalid_argument("choose one of peer_group and ipc_exchange");
@@ -159,6 +175,10 @@ Runtime::~Runtime() {
   cudaFreeHost(h_wstage_);
   for (auto s : streams_)
     if (s) cudaStreamDestroy(s);
+  if (clock_stream_) {
+    cudaStreamSynchronize(clock_stream_);
+    cudaStreamDestroy(clock_stream_);
+  }
 }
 
 void Runtime::register_block(int block, size_t act_bytes, const int64_t* numel, int n) {
@@ -556,7 +576,9 @@ void Runtime::host_loop() {
     double t0 = host_now();
     std::string err;
     try {
-      for (auto e : t.waits) CK(cudaEventSynchronize(e));
+      for (auto e : t.waits)
+        wait_event_bounded(e, "host_update of group " + std::to_string(t.group) + " (iteration " +
+                                  std::to_string(t.step) + ") waiting for its grad_out");
       t0 = host_now();
       run_host_task(t);
     } catch (const std::exception& ex) {
@@ -596,11 +618,60 @@ void Runtime::run_host_task(const HostTask& t) {
 
 void Runtime::wait_host_done(int group, int step) {
   std::unique_lock<std::mutex> lk(hmu_);
-  hcv_.wait(lk, [&] {
+  auto done = [&] {
     auto it = host_done_step_.find(group);
     return !host_error_.empty() || (it != host_done_step_.end() && it->second >= step);
-  });
+  };
+  if (!hcv_.wait_for(lk, std::chrono::duration<double>(watchdog_s_), done))
+    throw std::runtime_error("watchdog: host_update of group " + std::to_string(group) + " for iteration " +
+                             std::to_string(step) + " not complete after " + std::to_string(watchdog_s_) + " s (" +
+                             std::to_string(hq_.size()) + " host tasks queued)");
   if (!host_error_.empty()) throw std::runtime_error("host update failed: " + host_error_);
+}
+
+void Runtime::wait_event_bounded(cudaEvent_t e, const std::string& what) const {
+  const double t_end = host_now() + watchdog_s_;
+  int spins = 0;
+  for (;;) {
+    cudaError_t r = cudaEventQuery(e);
+    if (r == cudaSuccess) return;
+    if (r != cudaErrorNotReady) throw CudaError(what + ": " + cudaGetErrorString(r));
+    if (host_now() > t_end)
+      throw std::runtime_error("watchdog: " + what + " not complete after " + std::to_string(watchdog_s_) + " s");
+    if (++spins < 64) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(spins < 1024 ? 20 : 500));
+  }
+}
+
+std::string Runtime::first_pending_op() {
+  auto& ops = last_first_ ? ops_first_ : ops_steady_;
+  auto& order = last_first_ ? order_first_ : order_steady_;
+  for (int idx : order) {
+    const EngineOp& e = ops[idx].e;
+    if (e.action == Action::HOST_UPDATE) continue;
+    if (cudaEventQuery(ev_done_[idx]) == cudaErrorNotReady) {
+      std::string s = std::string(action_name(e.action));
+      if (e.block > 0) s += " block " + std::to_string(e.block);
+      if (e.group > 0) s += " group " + std::to_string(e.group);
+      return s + " on " + res_name(e.res);
+    }
+  }
+  return "no device op (host side)";
+}
+
+void Runtime::fail_iteration(int step, const std::string& why) {
+  // drain what was issued (errors ignored: the device may be the cause)
+  for (auto s : streams_) cudaStreamSynchronize(s);
+  {
+    std::unique_lock<std::mutex> lk(hmu_);
+    hcv_.wait_for(lk, std::chrono::duration<double>(watchdog_s_), [&] { return hq_.empty(); });
+  }
+  if (!iter_mutated_) {
+    step_ = step - 1;  // nothing of this iteration was applied: it can be re-run
+    last_first_ = step_ <= 0 || last_first_;
+  } else {
+    failed_ = "iteration " + std::to_string(step) + " failed after updates were applied: " + why;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -633,6 +704,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
       if (e.action == Action::BW) {
         auto& bp = blocks_.at(e.block);
         if (!bp.host_path && bp.n_params > 0) {
+          iter_mutated_ = true;
           OptimScalars sc = make_scalars(cfg_.optimizer, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps,
                                          cfg_.weight_decay, cfg_.momentum, step, 1.0f);
           float* master = d_master_ ? d_master_ + bp.p_off : reinterpret_cast<float*>(d_weight(bp.p_off));
@@ -713,7 +785,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
           for (int p = 0; p < world_; ++p)
             in[p] = reinterpret_cast<const float*>(ipc_g_[p]) + g.p_lo + (int64_t)rank_ * g.shard_n;
         } else {
-          peers_->wait_all(PK_BW, e.group, step);
+          peers_->wait_all(PK_BW, e.group, step, watchdog_s_);
           for (int p = 0; p < world_; ++p) {
             Runtime* peer = peers_->ranks[p];
             if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
@@ -740,6 +812,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
       t.group = e.group;
       t.step = step;
       for (int d : e.deps) t.waits.push_back(ev_done_[d]);
+      iter_mutated_ = true;
       {
         std::lock_guard<std::mutex> lk(hmu_);
         hq_.push_back(t);
@@ -770,7 +843,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         } else if (peers_) {
           CK(cudaEventRecord(peers_->event(rank_, PK_WSHARD, e.group), s));
           peers_->mark(rank_, PK_WSHARD, e.group, step);
-          peers_->wait_all(PK_WSHARD, e.group, step);
+          peers_->wait_all(PK_WSHARD, e.group, step, watchdog_s_);
           gather_peer_shards(g, e.group, ns, PK_WSHARD);
         } else {
           NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
@@ -792,8 +865,16 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
   }
 }
 
+void CUDART_CB Runtime::anchor_cb(void* arg) {
+  auto* a = static_cast<AnchorArg*>(arg);
+  double t = host_now();
+  std::lock_guard<std::mutex> lk(a->rt->hmu_);
+  a->rt->clock_anchor_[a->step] = t;
+}
+
 void Runtime::run_iteration(krt_compute_cb cb, void* user) {
   if (!prepared_) throw std::logic_error("run_iteration before prepare");
+  if (!failed_.empty()) throw std::runtime_error("context unusable: " + failed_);
   CK(cudaSetDevice(cfg_.device));
   {
     std::lock_guard<std::mutex> lk(hmu_);
@@ -804,18 +885,48 @@ void Runtime::run_iteration(krt_compute_cb cb, void* user) {
   auto& ops = first ? ops_first_ : ops_steady_;
   auto& order = first ? order_first_ : order_steady_;
   iter_bytes_h2d_ = iter_bytes_d2h_ = iter_launches_ = 0;
+  iter_mutated_ = false;
   cur_slot_.clear();
   iter_host_t0_ = host_now();
-  CK(cudaEventRecord(ev_base_, streams_[0]));
-  for (int idx : order) issue(idx, ops, cb, user, step);
+  try {
+    CK(cudaEventRecord(ev_base_, streams_[0]));
+    // host clock when the compute stream reaches ev_base_ (off the compute stream)
+    {
+      std::lock_guard<std::mutex> lk(hmu_);
+      while (anchor_args_.size() > 8) anchor_args_.pop_front();
+      anchor_args_.push_back({this, step});
+      for (auto it = clock_anchor_.begin(); it != clock_anchor_.end();)
+        it = it->first < step - 8 ? clock_anchor_.erase(it) : std::next(it);
+    }
+    CK(cudaStreamWaitEvent(clock_stream_, ev_base_, 0));
+    CK(cudaLaunchHostFunc(clock_stream_, anchor_cb, &anchor_args_.back()));
+    last_first_ = first;
+    for (int idx : order) issue(idx, ops, cb, user, step);
+  } catch (const std::exception& ex) {
+    fail_iteration(step, ex.what());
+    throw;
+  }
   bytes_h2d_ += iter_bytes_h2d_;
   bytes_d2h_ += iter_bytes_d2h_;
-  last_first_ = first;
 }
 
 void Runtime::synchronize() {
+  if (!failed_.empty()) throw std::runtime_error("context unusable: " + failed_);
   CK(cudaSetDevice(cfg_.device));
-  for (auto s : streams_) CK(cudaStreamSynchronize(s));
+  const double t_end = host_now() + watchdog_s_;
+  for (auto s : streams_) {
+    int spins = 0;
+    for (;;) {
+      cudaError_t r = cudaStreamQuery(s);
+      if (r == cudaSuccess) break;
+      if (r != cudaErrorNotReady) throw CudaError(std::string("synchronize: ") + cudaGetErrorString(r));
+      if (host_now() > t_end)
+        throw std::runtime_error("watchdog: iteration " + std::to_string(step_) + " stalled for " +
+                                 std::to_string(watchdog_s_) + " s; first incomplete op: " + first_pending_op());
+      if (++spins < 64) std::this_thread::yield();
+      else std::this_thread::sleep_for(std::chrono::microseconds(spins < 1024 ? 20 : 500));
+    }
+  }
   int step = step_;
   for (size_t gi = 0; gi < groups_.size(); ++gi) {
     bool has_host = false;
@@ -837,11 +948,15 @@ std::string Runtime::trace_csv() {
     const EngineOp& e = ops[i].e;
     double t0 = 0, t1 = 0;
     if (e.action == Action::HOST_UPDATE) {
+      // host clock minus the host time at which the compute stream passed
+      // ev_base_: the same origin as the device rows (within the host
+      // callback latency, microseconds)
       std::lock_guard<std::mutex> lk(hmu_);
       auto it = host_times_.find({e.group, step_});
-      if (it == host_times_.end()) continue;
-      t0 = it->second.first - iter_host_t0_;
-      t1 = it->second.second - iter_host_t0_;
+      auto an = clock_anchor_.find(step_);
+      if (it == host_times_.end() || an == clock_anchor_.end()) continue;
+      t0 = it->second.first - an->second;
+      t1 = it->second.second - an->second;
     } else {
       float ms0 = 0, ms1 = 0;
       if (cudaEventElapsedTime(&ms0, ev_base_, ev_start_[i]) != cudaSuccess) continue;
@@ -903,7 +1018,7 @@ void Runtime::flush_weights() {
         int gi = (int)(&g - groups_.data()) + 1;
         CK(cudaEventRecord(peers_->event(rank_, PK_FLUSH, gi), s));
         peers_->mark(rank_, PK_FLUSH, gi, flush_count_ + 1);
-        peers_->wait_all(PK_FLUSH, gi, flush_count_ + 1);
+        peers_->wait_all(PK_FLUSH, gi, flush_count_ + 1, watchdog_s_);
         gather_peer_shards(g, gi, s, PK_FLUSH);
       } else {
         NK(ncclAllGather(dst, d_weight(g.p_lo), (size_t)g.shard_n,
@@ -921,6 +1036,46 @@ void Runtime::flush_weights() {
   }
   CK(cudaStreamSynchronize(s));
   ++flush_count_;
+}
+
+double Runtime::probe_exchange(size_t bytes, int iters) {
+  if (!nccl_comm_) throw std::invalid_argument("probe_exchange needs the NCCL exchange (not IPC / in-process peers)");
+  if (iters < 1) throw std::invalid_argument("iters must be >= 1");
+  CK(cudaSetDevice(cfg_.device));
+  size_t n = bytes / 4 / (size_t)world_ * (size_t)world_;
+  if (n < (size_t)world_) n = (size_t)world_;
+  float *send = nullptr, *recv = nullptr;
+  CK(cudaMalloc(&send, n * 4));
+  CK(cudaMalloc(&recv, n / world_ * 4));
+  cudaStream_t s = streams_[3];
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double sec = 0;
+  try {
+    CK(cudaMemsetAsync(send, 0, n * 4, s));
+    for (int i = 0; i < 2; ++i)
+      NK(ncclReduceScatter(send, recv, n / world_, ncclFloat, ncclSum, (ncclComm_t)nccl_comm_, s));
+    CK(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i)
+      NK(ncclReduceScatter(send, recv, n / world_, ncclFloat, ncclSum, (ncclComm_t)nccl_comm_, s));
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    sec = ms * 1e-3 / iters;
+  } catch (...) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(send);
+    cudaFree(recv);
+    throw;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(send);
+  cudaFree(recv);
+  return sec;
 }
 
 void Runtime::gather_peer_shards(const GroupPhys& g, int group, cudaStream_t s, int kind) {

@@ -87,7 +87,8 @@ struct PeerGroup {
   std::map<std::tuple<int, int, int>, int> marks;         // (rank, kind, group) -> step
   std::map<std::tuple<int, int, int>, cudaEvent_t> events;
   void mark(int rank, int kind, int group, int step);
-  void wait_all(int kind, int group, int step);
+  // bounded: throws naming the ranks that never marked (a dead or stalled peer)
+  void wait_all(int kind, int group, int step, double timeout_s);
   cudaEvent_t event(int rank, int kind, int group);
   ~PeerGroup();
 };
@@ -110,6 +111,9 @@ class Runtime {
   void read_master(int block, float* out, size_t numel);
   void* block_slot(int block) const;
   void flush_weights();
+  // mean seconds of one ncclReduceScatter of `bytes` fp32 gradient bytes on
+  // this context's communicator and network stream (collective: every rank)
+  double probe_exchange(size_t bytes, int iters);
   void checkpoint_save(const std::string& path);
   void checkpoint_load(const std::string& path);
   std::vector<uint8_t> ipc_export();
@@ -125,6 +129,11 @@ class Runtime {
   void host_loop();
   void run_host_task(const HostTask& t);
   void wait_host_done(int group, int step);
+  // polls an event until it completes or the watchdog expires (then throws `what`)
+  void wait_event_bounded(cudaEvent_t e, const std::string& what) const;
+  // the op of the last issued iteration still incomplete, first in issue order
+  std::string first_pending_op();
+  void fail_iteration(int step, const std::string& why);
   void gather_peer_shards(const GroupPhys& g, int group, cudaStream_t s, int kind);
   float* d_grad(int64_t p_off) const { return d_grads_ + p_off; }
   void* d_weight(int64_t p_off) const;
@@ -189,6 +198,23 @@ class Runtime {
   std::map<int, uint8_t*> cur_slot_;   // block -> resident slot during issue
   int step_ = 0;
   bool prepared_ = false;
+  // watchdog (KRT_WATCHDOG_S, default 900 s): no wait in the runtime blocks
+  // longer; the error names the op that never completed
+  double watchdog_s_ = 900.0;
+  // set when an iteration failed after it had already applied updates: the
+  // context refuses further work instead of hanging on the lost updates
+  std::string failed_;
+  bool iter_mutated_ = false;
+  // host clock of the moment the compute stream passed ev_base_ (per step):
+  // host-update trace rows are put on the GPU timeline with it
+  cudaStream_t clock_stream_ = nullptr;
+  std::map<int, double> clock_anchor_;
+  struct AnchorArg {
+    Runtime* rt;
+    int step;
+  };
+  std::deque<AnchorArg> anchor_args_;
+  static void CUDART_CB anchor_cb(void* arg);
   bool last_first_ = true;
   // stats
   uint64_t bytes_h2d_ = 0, bytes_d2h_ = 0, bytes_net_ = 0, kernel_launches_ = 0;

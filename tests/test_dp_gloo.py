@@ -99,4 +99,5 @@ def test_layout_shards_are_aligned_and_cover():
     lay = _lib.dp_layout([4096, 100, 7, 0, 5000], 2, 8)
     for lo, n, sh in zip(lay["group_lo"], lay["group_n"], lay["shard_n"]):
         assert n % (8 * 64) == 0 and sh * 8 == n and lo % 64 == 0
-    assert lay["block_off"][:3] == [0, 4096, 4196]
+    assert lay["block_off"][:3] == [0, 4096, 4224]   # blocks 64-element aligned
+    assert all(o % 64 == 0 for o in lay["block_off"])
