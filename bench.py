@@ -10,10 +10,18 @@ scripts/make_plans.py).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--plan NAME] [--impl reference]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL); weak scaling: every
-rank trains its own per-GPU batch and the exchange reduce-scatters gradients.
+N > 1: one rank per GPU under torchrun (bench.py re-launches itself through
+torch.distributed.run when WORLD_SIZE is unset, and fails when the world size
+differs from --gpus); the gradient exchange is the runtime's own NCCL
+communicator (reduce-scatter per group, all-gather of the updated shards);
+weak scaling: every rank trains its own per-GPU batch.  Before the timed
+region every rank probes, concurrently, its PCIe link (pinned H2D / D2H /
+duplex) and, at N > 1, the NCCL reduce-scatter bus bandwidth at the plan's
+group sizes; the iteration roofline uses those measured rates.
 `--impl reference` times the CPU reference arm (the in-core fp32 torch CPU
-oracle of the same model, oracle/resnet_oracle.py) on all host cores.
+oracle of the same model, oracle/resnet_oracle.py) on all host cores, plus
+the reference's own executable CPU path (oocsched plan_model +
+simulate_distributed from baseline/_ref).
 """
 from __future__ import annotations
 
@@ -94,6 +102,55 @@ class Clocks:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def self_launch(args):
+    """bench.py --gpus N without torchrun: re-run under torch.distributed.run
+    with N ranks on this node (127.0.0.1 rendezvous) and exit with its code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd))
+
+
+def reference_planner_time(rec, workers):
+    """The reference's only executable CPU path for this workload:
+    oocsched.plan_model on the committed model/hardware texts, then
+    simulate_distributed of the resulting plan at `workers` ranks, timed on
+    this host.  The reference is the unmodified package installed in
+    baseline/_ref (never /root/reference at run time)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "oocsched").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    sys.path.insert(0, str(ref))
+    try:
+        from oocsched.cost_model import parse_hardware_text
+        from oocsched.distsim import DistConfig, simulate_distributed
+        from oocsched.model_ir import parse_model_text
+        from oocsched.planner import plan_model
+        g, hw = parse_model_text(rec["model"]), parse_hardware_text(rec["hardware"])
+        t0 = time.perf_counter()
+        plan = plan_model(g, hw, max_blocks=rec.get("max_blocks"))
+        t1 = time.perf_counter()
+        out = {"plan_model_s": round(t1 - t0, 4), "workers": workers, "cores": 1,
+               "max_blocks": rec.get("max_blocks"),
+               "same_plan_as_committed": [(b.first_layer, b.last_layer) for b in plan.blocks] ==
+                                         [tuple(b["layers"]) for b in rec["plan"]["blocks"]]}
+        try:
+            dr = simulate_distributed(plan, g, hw, DistConfig(workers=max(1, workers)), iterations=3)
+            out["predicted_iteration_s"] = dr.iteration_time
+        except Exception as exc:   # the reference's own verdict (e.g. its DP ledger deadlocks)
+            out["simulate_distributed_error"] = f"{type(exc).__name__}: {str(exc)[:160]}"
+        out["simulate_distributed_s"] = round(time.perf_counter() - t1, 4)
+        return out
+    except Exception as exc:   # report, do not fail the bench
+        return {"error": f"{type(exc).__name__}: {exc}"}
+    finally:
+        sys.path.remove(str(ref))
 
 
 def dist_env():
@@ -217,7 +274,7 @@ def run_reference(args, rec):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    steps, warmup = max(1, min(args.steps, 3)), 1
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
     value, cores, dt = cpu_reference(rec, steps, warmup)
     m = rec["meta"]
     line = {
@@ -231,6 +288,7 @@ def run_reference(args, rec):
                          "sample": f"in-core fp32 torch-CPU {model_name(rec)} step (oracle/) "
                                    f"on {cpu_sample_batch(rec)} samples per step{cpu_sample_note(rec)}"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_planner": reference_planner_time(rec, args.gpus),
     }
     print(json.dumps(line), flush=True)
 
@@ -238,6 +296,60 @@ def run_reference(args, rec):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def probe_pcie(dev, world, nbytes=512 << 20, reps=3):
+    """Pinned H2D, D2H and duplex copy rates with every rank copying at the
+    same time (barrier before each pattern); slowest rank's time."""
+    import torch
+    import torch.distributed as dist
+    h1 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d1 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def run(pattern):
+        ts = []
+        for _ in range(reps + 1):
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            if pattern in ("h2d", "duplex"):
+                with torch.cuda.stream(s1):
+                    d1.copy_(h1, non_blocking=True)
+            if pattern in ("d2h", "duplex"):
+                with torch.cuda.stream(s2):
+                    h2.copy_(d2, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            ts.append(time.perf_counter() - t0)
+        t = torch.tensor([min(ts[1:])])
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return nbytes / float(t.item())
+    out = {"h2d": run("h2d"), "d2h": run("d2h"), "duplex": run("duplex"),
+           "bytes": nbytes, "ranks_concurrent": world,
+           "note": "pinned cudaMemcpyAsync, all ranks at once, slowest rank (best of 3)"}
+    del h1, h2, d1, d2
+    return out
+
+
+def probe_nccl(ex, group_bytes, world):
+    """Reduce-scatter seconds on the runtime's own communicator at the plan's
+    group sizes (<= 8 distinct sizes probed; others scaled linearly from the
+    nearest probed size).  Returns (seconds per iteration for all groups,
+    bus GB/s at each probed size)."""
+    sizes = sorted(set(group_bytes))
+    if len(sizes) > 8:
+        sizes = [sizes[round(i * (len(sizes) - 1) / 7)] for i in range(8)]
+    t = {b: ex.probe_exchange(b, iters=5) for b in sizes}
+    total = 0.0
+    for b in group_bytes:
+        near = min(sizes, key=lambda x: abs(x - b))
+        total += t[near] * b / near
+    bus = {str(b): (world - 1) / world * b / t[b] / 1e9 for b in sizes}
+    return total, bus
+
+
 def run_gpu(args, rec):
     import numpy as np
     import torch
@@ -246,8 +358,13 @@ def run_gpu(args, rec):
     from paper_2008_11421_b200 import workloads as W
     from paper_2008_11421_b200.executor import ExecConfig, Executor
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: world size {world} != --gpus {args.gpus} (launch under torchrun with "
+                         f"--nproc-per-node {args.gpus}, or without WORLD_SIZE to self-launch)")
     if os.environ.get("KRT_BENCH_SHARE_GPU") == "1":
         local = 0      # test mode: every rank on cuda:0 (IPC still crosses processes)
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but only {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
     torch.backends.cudnn.benchmark = True
     nccl_id = None
@@ -260,6 +377,8 @@ def run_gpu(args, rec):
             box = [_lib.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(box, src=0)
             nccl_id = box[0]
+            if rank == 0:
+                print(f"bench.py: NCCL exchange communicator, nranks={world}", file=sys.stderr, flush=True)
     m = rec["meta"]
     batch = m["batch"]
     units = W.units_for(rec)
@@ -282,6 +401,7 @@ def run_gpu(args, rec):
     ex.init_weights(seed=0)
     setup_s = time.perf_counter() - t_setup
     dev = torch.device("cuda", local)
+    import math
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     x, y = workload_inputs(rec, dev, gen)
     cs = ex.compute_stream
@@ -295,6 +415,16 @@ def run_gpu(args, rec):
     for _ in range(args.warmup):
         ex.step(x, y)
     ex.synchronize()
+    barrier()
+    # ---- link probes (all ranks concurrently, before the timed region) ----------
+    from paper_2008_11421_b200 import _lib as _L
+    block_params = [sum(sum(math.prod(p) for p in units[i - 1].param_specs())
+                        for i in range(b["layers"][0], b["layers"][1] + 1)) for b in rec["plan"]["blocks"]]
+    lay = _L.dp_layout(block_params, 0, world)
+    group_bytes = [4 * n for n in lay["group_n"]]
+    pcie = probe_pcie(dev, world) if not args.no_probe else None
+    nccl_rs_s, nccl_bus = (probe_nccl(ex, group_bytes, world)
+                           if world > 1 and args.exchange == "nccl" and not args.no_probe else (None, None))
     barrier()
     # ---- timed region: inputs resident in HBM ----------------------------------
     clk = Clocks(local)
@@ -379,14 +509,32 @@ def run_gpu(args, rec):
     alg_flops = 3.0 * fwd                     # fwd + bwd (2x) per training step
     exec_flops = alg_flops + rec_fwd          # + recomputed forwards
     sustained = pk["bf16_tflops_sustained"] * 1e12
+    # PCIe at the rate measured in this run with every rank copying at once
+    # (duplex when both directions move in the iteration); the probe constants
+    # only when the probe was skipped
+    h2d_rate = (pcie["duplex"] if d2h_iter > 0 else pcie["h2d"]) if pcie else PCIE_H2D
+    d2h_rate = (pcie["duplex"] if h2d_iter > 0 else pcie["d2h"]) if pcie else PCIE_D2H
+    # HBM: algorithmic bytes of every kernel of the last timed step (own
+    # kernels, cuDNN convolutions, cuBLAS GEMMs; each operand read once and
+    # each output written once per launch) over the measured copy bandwidth
     terms = {"compute_s": exec_flops / sustained,
-             "pcie_h2d_s": h2d_iter / PCIE_H2D,
-             "pcie_d2h_s": d2h_iter / PCIE_D2H,
+             "hbm_s": 0.0,
+             "pcie_h2d_s": h2d_iter / h2d_rate,
+             "pcie_d2h_s": d2h_iter / d2h_rate,
              "nvlink_s": 0.0}
+    nvl = None
     if world > 1:
-        # reduce-scatter reads (P-1)/P of the fp32 grads, the gather (P-1)/P of the bf16 weights
-        terms["nvlink_s"] = st["params"] * (world - 1) / world * (4 + 2) / 770e9
-    bind = max(terms, key=terms.get)
+        # reduce-scatter of the fp32 gradients: measured on the communicator at the
+        # plan's group sizes; all-gather of the bf16 weights at the same bus rate
+        w_bytes = st["params"] * 2
+        if nccl_rs_s is not None:
+            best_bus = max(nccl_bus.values()) * 1e9
+            terms["nvlink_s"] = nccl_rs_s + (world - 1) / world * w_bytes / best_bus
+            nvl = {"reduce_scatter_s": nccl_rs_s, "all_gather_s_est": (world - 1) / world * w_bytes / best_bus,
+                   "bus_GBps_by_bytes": nccl_bus, "source": "krt_probe_exchange (ncclReduceScatter, own comm)"}
+        else:
+            terms["nvlink_s"] = st["params"] * (world - 1) / world * (4 + 2) / 770e9
+            nvl = {"source": "B200_PROFILING.md peer copy 770 GB/s (probe skipped / IPC exchange)"}
     rows = [r.split(",") for r in trace.strip().splitlines()[1:]]
     comp = [(float(r[0]), float(r[1])) for r in rows if r[2] == "compute"]
     busy = sum(b - a for a, b in comp)
@@ -430,7 +578,16 @@ def run_gpu(args, rec):
         if v[3] > 0:   # tensor-core family: also against the dense bf16 peak
             kernels[k]["achieved_TFLOPs"] = v[3] / v[1] / 1e12
             kernels[k]["frac_of_tensor"] = v[3] / v[1] / 1e12 / pk["bf16_tflops"]
-    dom = max(fam, key=lambda k: fam[k][1]) if fam else None
+    # library calls (cuDNN, cuBLAS, aten flash attention) are timed for the step
+    # accounting only; the roofline and the launch count are our kernels'
+    lib_fam = ("cudnn_", "cublas_", "flash_attn")
+    own = {k: v for k, v in fam.items() if not k.startswith(lib_fam)}
+    for k in kernels:
+        kernels[k]["library"] = k.startswith(lib_fam)
+    dom = max(own, key=lambda k: own[k][1]) if own else None
+    step_alg_bytes = sum(v[0] for v in fam.values())
+    terms["hbm_s"] = step_alg_bytes / (pk["hbm_gbs"] * 1e9)
+    bind = max(terms, key=terms.get)
 
     def dom_roofline(k):
         v = fam[k]
@@ -479,10 +636,16 @@ def run_gpu(args, rec):
                                    # while a transfer is in flight, against the probed link rate
                                    pcie_h2d_active_GBps=(swap_in_bytes / busy_in / 1e9) if busy_in else None,
                                    pcie_d2h_active_GBps=(swap_out_bytes / busy_out / 1e9) if busy_out else None,
-                                   pcie_h2d_active_frac_of_link=(swap_in_bytes / busy_in / PCIE_H2D) if busy_in else None,
-                                   pcie_d2h_active_frac_of_link=(swap_out_bytes / busy_out / PCIE_D2H) if busy_out else None,
-                                   pcie_link_GBps={"h2d": PCIE_H2D / 1e9, "d2h": PCIE_D2H / 1e9,
-                                                   "source": "scripts/probe_box.py (pinned cudaMemcpyAsync)"}),
+                                   pcie_h2d_active_frac_of_link=(swap_in_bytes / busy_in / (pcie["h2d"] if pcie else PCIE_H2D))
+                                   if busy_in else None,
+                                   pcie_d2h_active_frac_of_link=(swap_out_bytes / busy_out / (pcie["d2h"] if pcie else PCIE_D2H))
+                                   if busy_out else None,
+                                   pcie_link_GBps=({k: (v / 1e9 if k in ("h2d", "d2h", "duplex") else v)
+                                                    for k, v in pcie.items()} if pcie else
+                                                   {"h2d": PCIE_H2D / 1e9, "d2h": PCIE_D2H / 1e9,
+                                                    "source": "scripts/probe_box.py constants (probe skipped)"}),
+                                   hbm_step_alg_bytes=step_alg_bytes,
+                                   nvlink=nvl),
         "overlap": {"compute_busy_frac": busy / span if span else None,
                     "exposed_stall_frac": 1 - busy / span if span else None,
                     "swap_in_busy_s": sum(b - a for a, b in xin),
@@ -495,7 +658,7 @@ def run_gpu(args, rec):
                 "note": "every step: pinned H2D of its inputs, issue, then D2H read of the previous step's loss "
                         "(the last loss read after the loop)",
                 "alloc_retries": e2e_retries},
-        "gpu_launches": launches + sum(v[2] for v in fam.values()) * args.steps,
+        "gpu_launches": launches + sum(v[2] for v in own.values()) * args.steps,
         "runtime": {k: st[k] for k in ("arena_bytes", "ledger_peak_bytes", "host_swap_bytes",
                                        "swapped_blocks", "ops_per_iteration", "params")},
         "setup_s": setup_s,
@@ -507,6 +670,8 @@ def run_gpu(args, rec):
         Path(args.trace_out).write_text(trace)
     ex.close()
     del ex
+    if rank == 0 and not args.no_cpu_baseline:
+        line["reference_planner"] = reference_planner_time(rec, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, dt = cpu_reference(rec, steps=2, warmup=1)
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": "port",
@@ -528,11 +693,15 @@ def main():
     ap.add_argument("--impl", default="krt", choices=["krt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-out", default=None)
-    ap.add_argument("--exchange", default="ipc", choices=["ipc", "nccl"],
-                    help="N>1 gradient exchange: own reduce-scatter over CUDA IPC peer memory, or NCCL")
+    ap.add_argument("--exchange", default="nccl", choices=["ipc", "nccl"],
+                    help="N>1 gradient exchange: NCCL reduce-scatter/all-gather on the runtime's own "
+                         "communicator (default), or the runtime's reduce over CUDA IPC peer memory")
+    ap.add_argument("--no-probe", action="store_true", help="skip the PCIe / NCCL link probes")
     ap.add_argument("--incore", action="store_true",
                     help="same blocks, everything resident (no swap/recompute): the in-core baseline")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     from paper_2008_11421_b200 import workloads as W
     rec = W.load(args.plan)
     if args.impl == "reference":

@@ -353,6 +353,13 @@ class Executor:
         _lib.check(rc)
         return self.loss
 
+    def probe_exchange(self, nbytes: int, iters: int = 5) -> float:
+        """Mean seconds of one reduce-scatter of `nbytes` fp32 on this rank's
+        NCCL communicator (krt_probe_exchange; collective: call on every rank)."""
+        sec = C.c_double()
+        _lib.check(_lib.lib().krt_probe_exchange(self._ctx, int(nbytes), iters, C.byref(sec)))
+        return sec.value
+
     def synchronize(self):
         _lib.check(_lib.lib().krt_synchronize(self._ctx))
 

@@ -109,8 +109,16 @@ def _cl(t):
     return t.permute(0, 3, 1, 2)
 
 
+def _conv_cost(x, w, y):
+    """(algorithmic bytes, flops) of y = conv(x, w): operands read once, output written once."""
+    return (x.numel() + w.numel() + y.numel()) * x.element_size(), 2.0 * y.numel() * (w.numel() // w.shape[0])
+
+
 def _conv(x, w, stride, pad):
-    return _aten.convolution(x, w, None, [stride, stride], [pad, pad], [1, 1], False, [0, 0], 1)
+    with bnfused._timed("cudnn_conv_fwd", 0) as t:
+        y = _aten.convolution(x, w, None, [stride, stride], [pad, pad], [1, 1], False, [0, 0], 1)
+        t.nbytes, t.flops = _conv_cost(x, w, y)
+    return y
 
 
 class GradPair(tuple):
@@ -136,14 +144,21 @@ def _conv_into(x, w, stride, pad, out=None):
     if out is None:
         return _conv(x, w, stride, pad)
     cb = torch.backends.cudnn
-    _aten.cudnn_convolution.out(x, w, [pad, pad], [stride, stride], [1, 1], 1, cb.benchmark,
-                                cb.deterministic, cb.allow_tf32, out=out)
+    with bnfused._timed("cudnn_conv_fwd", 0) as t:
+        _aten.cudnn_convolution.out(x, w, [pad, pad], [stride, stride], [1, 1], 1, cb.benchmark,
+                                    cb.deterministic, cb.allow_tf32, out=out)
+        t.nbytes, t.flops = _conv_cost(x, w, out)
     return out
 
 
 def _conv_bw(dy, x, w, stride, pad, need_dx=True):
-    return _aten.convolution_backward(dy, x, w, None, [stride, stride], [pad, pad], [1, 1], False,
-                                      [0, 0], 1, [need_dx, True, False])
+    # bytes: dy and x read, dw written (+ w read and dx written for the dgrad)
+    es = dy.element_size()
+    nb = (dy.numel() + x.numel() + w.numel()) * es + (w.numel() + x.numel()) * es * need_dx
+    fl = 2.0 * dy.numel() * (w.numel() // w.shape[0]) * (2 if need_dx else 1)
+    with bnfused._timed("cudnn_conv_bwd", nb, fl):
+        return _aten.convolution_backward(dy, x, w, None, [stride, stride], [pad, pad], [1, 1], False,
+                                          [0, 0], 1, [need_dx, True, False])
 
 
 def _bn_fw(c, g, b):
@@ -932,12 +947,22 @@ def _ln_bw(dy, x, g, b, mean, rstd, dg, db):
     return dx
 
 
+def _gemm_cost(m, n, k, es=2):
+    return (m * k + n * k + m * n) * es, 2.0 * m * n * k
+
+
 def _linear(x, w, b, out=None):
-    return torch.addmm(b, x, w.t(), out=out) if out is not None else torch.addmm(b, x, w.t())
+    with bnfused._timed("cublas_gemm", *_gemm_cost(x.shape[0], w.shape[0], x.shape[1], x.element_size())):
+        return torch.addmm(b, x, w.t(), out=out) if out is not None else torch.addmm(b, x, w.t())
 
 
 def _mm_f32_into(a, b, out):
     """out (fp32) = a @ b: cuBLAS writes fp32 straight into the gradient region."""
+    with bnfused._timed("cublas_gemm", *_gemm_cost(a.shape[0], b.shape[1], a.shape[1], a.element_size())):
+        _mm_f32_into_raw(a, b, out)
+
+
+def _mm_f32_into_raw(a, b, out):
     if a.dtype == torch.float32:
         torch.mm(a, b, out=out)
     elif a.is_cuda:
@@ -951,7 +976,10 @@ def _linear_bw(dy, x, w, gw, gb, need_dx=True):
     _mm_f32_into(dy.t(), x, gw)
     if gb is not None:
         torch.sum(dy, 0, dtype=torch.float32, out=gb)   # fp32 accumulation, no fp32 copy of dy
-    return torch.mm(dy, w) if need_dx else None
+    if not need_dx:
+        return None
+    with bnfused._timed("cublas_gemm", *_gemm_cost(dy.shape[0], w.shape[1], dy.shape[1], dy.element_size())):
+        return torch.mm(dy, w)
 
 
 class EmbeddingUnit(Unit):
@@ -1036,7 +1064,10 @@ class TransformerLayerUnit(Unit):
     def _attn_fw(self, qkv, lse_out):
         q, k, v = self._heads(qkv)
         if self._flash():
-            r = _aten._scaled_dot_product_flash_attention(q, k, v, 0.0, True, False)
+            n = qkv.shape[0] // self.s
+            with bnfused._timed("flash_attn_fwd", 4 * qkv.shape[0] * self.h * qkv.element_size(),
+                                2.0 * n * self.nh * self.s * self.s * self.hd):   # causal: half of 4*s^2*hd
+                r = _aten._scaled_dot_product_flash_attention(q, k, v, 0.0, True, False)
             if lse_out is not None:
                 lse_out.copy_(r[1])
             return self._merge(r[0])
@@ -1055,8 +1086,10 @@ class TransformerLayerUnit(Unit):
         if self._flash():
             O = o.view(n, self.s, self.nh, self.hd).transpose(1, 2)
             z = torch.zeros((), dtype=torch.int64, device=q.device)
-            dq, dk, dv = _aten._scaled_dot_product_flash_attention_backward(
-                dO, q, k, v, O, lse, None, None, self.s, self.s, 0.0, True, z, z)
+            with bnfused._timed("flash_attn_bwd", 8 * do.shape[0] * self.h * do.element_size(),
+                                5.0 * n * self.nh * self.s * self.s * self.hd):   # causal, 2.5x the forward
+                dq, dk, dv = _aten._scaled_dot_product_flash_attention_backward(
+                    dO, q, k, v, O, lse, None, None, self.s, self.s, 0.0, True, z, z)
         else:
             p = self._probs(q, k)
             dv = p.transpose(-1, -2) @ dO
@@ -1163,7 +1196,8 @@ class LMHeadUnit(Unit):
         else:
             m = r = None
         h, _ = _ln_fw(x, g, b, m, r)
-        return torch.mm(h, w.t())
+        with bnfused._timed("cublas_gemm", *_gemm_cost(h.shape[0], w.shape[0], h.shape[1], h.element_size())):
+            return torch.mm(h, w.t())
 
     def backward(self, dlogits, params, saved, grads):
         g, b, w = params
@@ -1172,7 +1206,9 @@ class LMHeadUnit(Unit):
         m, r = st[:t], st[t:]
         h = _ln_apply(x, g, b, m, r)
         _mm_f32_into(dlogits.t(), h, grads[2])
-        dh = torch.mm(dlogits, w)
+        with bnfused._timed("cublas_gemm", *_gemm_cost(dlogits.shape[0], w.shape[1], w.shape[0],
+                                                       dlogits.element_size())):
+            dh = torch.mm(dlogits, w)
         return _ln_bw(dh, x, g, b, m, r, grads[0], grads[1])
 
     def fwd_flops(self, n):
