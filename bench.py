@@ -551,11 +551,18 @@ def run_gpu(args, rec):
     theta_meas = next((j for j, o in enumerate(bsteps) if o[3] > 1e-3), None)
     b_busy = sum(o[1] - o[0] for o in bsteps)
     b_idle = sum(o[3] for o in bsteps)
-    occupancy = {"theta_predicted": rec["plan"].get("theta"), "theta_measured": theta_meas,
-                 "backward_steps": len(bsteps),
+    an = bundle.occupancy()   # analytic_report + find_theta (occupancy.py:178-225) in libkrt
+    occupancy = {"theta_predicted": an["theta"], "theta_measured": theta_meas,
+                 "backward_steps": len(bsteps), "backward_steps_predicted": len(an["per_step"]),
+                 "backward_mean_occupancy_predicted": an["mean_occupancy"],
                  "backward_mean_occupancy_measured": b_busy / (b_busy + b_idle) if bsteps else None,
-                 "note": "reference find_theta / report_from_steps semantics on the measured trace; "
-                         "idle = stall_before > 1 ms counts as waiting"}
+                 "per_step_predicted_vs_measured": [
+                     [row[0], round(row[1], 6),
+                      round((o[1] - o[0]) / ((o[1] - o[0]) + o[3]), 6) if (o[1] - o[0]) + o[3] > 0 else 1.0]
+                     for row, o in zip(an["per_step"], bsteps)],
+                 "note": "theta null = the device never waits on a delivery (occupancy.py:186-190); predicted = "
+                         "the plan's own cost model (hardware text of the plan), measured = report_from_steps "
+                         "semantics on the executor trace, a step waits when its stall_before > 1 ms"}
     busy_in = sum(b - a for a, b in xin)
     busy_out = sum(b - a for a, b in xout)
     swap_in_bytes = st["iter_bytes_h2d"]

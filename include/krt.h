@@ -83,12 +83,26 @@ typedef struct krt_dist_config {
   double net_bw;      /* bytes/s                       (distsim.py:50) */
   double net_latency; /* seconds                       (distsim.py:51) */
   int groups;         /* 0 = one group per block       (distsim.py:52) */
+  int variant;        /* bit 0: KRT_DIST_DEVICE_EXCHANGE, bit 1: KRT_DIST_EXACT_DEPS
+                         (0 = the reference's model, bit-exact) */
 } krt_dist_config;
+/* The executor's P >= 2 pipeline: per group a device reduce-scatter
+ * after the members' backward, a 1/P-shard grad_out, a 1/P host update, and a
+ * shard weight_in followed by an "all_gather" network op before the forward. */
+#define KRT_DIST_DEVICE_EXCHANGE 1
+/* Shift each iteration's base-op deps by the real op offset (distsim.py:165
+ * takes it before appending weight_in ops, so from iteration 2 deps point
+ * too early: the reference's quirk, reproduced when the bit is clear). */
+#define KRT_DIST_EXACT_DEPS 2
 
 /* simulate_distributed (distsim.py:140-266): JSON {iteration_time, iteration_times,
  * exposed_comm, peak_mem, makespan, events} or {error}. */
 int krt_plan_simulate_dist(const krt_plan* plan, const krt_dist_config* cfg, int iterations,
                            char** out_json);
+/* analytic_report (occupancy.py:202-225) with find_theta (:178-199): JSON
+ * {theta (null = None), mean_occupancy, per_step[[step, occupancy, busy_s,
+ * idle_s]], csv (OccupancyReport.to_csv), summary (OccupancyReport.summary)}. */
+int krt_plan_occupancy(const krt_plan* plan, char** out_json);
 
 /* Static arena assignment for physical block sizes (block_bytes[i] = slot
  * bytes of block i+1): JSON {arena_bytes, ledger_peak, instances[{block, off,

@@ -36,7 +36,7 @@ class InfeasiblePlanError(KrtError):
 
 class DistConfig(C.Structure):
     _fields_ = [("workers", C.c_int), ("ring", C.c_int), ("net_bw", C.c_double),
-                ("net_latency", C.c_double), ("groups", C.c_int)]
+                ("net_latency", C.c_double), ("groups", C.c_int), ("variant", C.c_int)]
 
 
 class Config(C.Structure):
@@ -64,6 +64,7 @@ EXPORTS = {
     "krt_plan_json": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_plan_validate": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "krt_plan_simulate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "krt_plan_occupancy": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_plan_simulate_dist": (C.c_int, [C.c_void_p, C.POINTER(DistConfig), C.c_int,
                                          C.POINTER(C.c_void_p)]),
     "krt_nccl_unique_id": (C.c_int, [C.c_void_p]),

@@ -187,8 +187,34 @@ int krt_plan_simulate(const krt_plan* p, int enforce, char** out) {
         os << (i ? ", " : "") << "[" << jnum(e.t_start) << ", " << jnum(e.t_end) << ", \"" << res_name(e.res)
            << "\", " << op.block << ", \"" << action_name(op.action) << "\", " << jnum(e.stall_before) << "]";
       }
-      os << "], \"csv\": " << jstr(r.csv()) << "}";
+      // SimTrace occupancy figures (simulator.py:200-236); summary_csv with
+      // find_theta as cli.py:115-116 writes it
+      TraceOccupancy t = trace_occupancy(r, find_theta(p->plan, p->model, p->hw));
+      os << "], \"csv\": " << jstr(r.csv()) << ", \"mean_occupancy\": " << jnum(t.mean_occupancy)
+         << ", \"first_stall_backward_step\": ";
+      if (t.first_stall_step < 0) os << "null";
+      else os << t.first_stall_step;
+      os << ", \"boundary_stall\": " << jnum(t.boundary_stall) << ", \"summary_csv\": " << jstr(t.summary_csv)
+         << "}";
     }
+    *out = dup(os.str());
+  });
+}
+
+int krt_plan_occupancy(const krt_plan* p, char** out) {
+  return guard([&] {
+    OccupancyReport r = analytic_report(p->plan, p->model, p->hw);
+    std::ostringstream os;
+    os << "{\"theta\": ";
+    if (r.theta < 0) os << "null";
+    else os << r.theta;
+    os << ", \"mean_occupancy\": " << jnum(r.mean_occupancy) << ", \"per_step\": [";
+    for (size_t i = 0; i < r.per_step.size(); ++i) {
+      auto& s = r.per_step[i];
+      os << (i ? ", " : "") << "[" << s.step << ", " << jnum(s.occupancy) << ", " << jnum(s.busy_s) << ", "
+         << jnum(s.idle_s) << "]";
+    }
+    os << "], \"csv\": " << jstr(r.csv()) << ", \"summary\": " << jstr(r.summary()) << "}";
     *out = dup(os.str());
   });
 }
@@ -202,6 +228,9 @@ int krt_plan_simulate_dist(const krt_plan* p, const krt_dist_config* c, int iter
     cfg.net_bw = c->net_bw;
     cfg.net_latency = c->net_latency;
     cfg.groups = c->groups;
+    if (c->variant & ~(KRT_DIST_DEVICE_EXCHANGE | KRT_DIST_EXACT_DEPS)) throw std::invalid_argument("unknown dist variant bits");
+    cfg.device_exchange = (c->variant & KRT_DIST_DEVICE_EXCHANGE) != 0;
+    cfg.exact_deps = (c->variant & KRT_DIST_EXACT_DEPS) != 0;
     if (cfg.workers < 1) throw std::invalid_argument("workers must be >= 1");
     if (!(cfg.net_bw > 0)) throw std::invalid_argument("net_bw must be strictly positive");
     if (cfg.net_latency < 0) throw std::invalid_argument("net_latency must be non-negative");

@@ -525,9 +525,118 @@ std::vector<std::vector<int>> assign_groups(int nb, int groups) {
   return out;
 }
 
+namespace {
+// The executor's P >= 2 pipeline (runtime.cu build_ops, dp_ branch) as engine
+// ops: exchange (reduce-scatter) precedes a shard-sized grad_out, the host
+// updates 1/P of the group, and the weight return is a shard H2D plus an
+// all-gather on the network resource.  Gradients live in the executor's
+// gradient region, outside the arena, so a backward frees its block's whole
+// ledger bytes (the reference holds grad_bytes until grad_out, distsim.py:195-202).
+std::vector<EngineOp> build_dist_ops_device(const Plan& p, const Model& g, const Hardware& hw,
+                                            const DistConfig& cfg, int iterations,
+                                            const std::map<int, BlockCost>& costs) {
+  double swap_rate = hw.swap_throughput();
+  const double P = cfg.workers;
+  auto groups = assign_groups((int)p.blocks.size(), cfg.groups);
+  std::map<int, int> group_of;
+  for (size_t gi = 0; gi < groups.size(); ++gi)
+    for (int b : groups[gi]) group_of[b] = (int)gi + 1;
+  std::map<int, double> group_bytes, group_wt, group_wtb;
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    PySum gb, gw, gwb;
+    for (int b : groups[gi]) {
+      gb.add(costs.at(b).grad_bytes);
+      gw.add(costs.at(b).weight_elems);
+      gwb.add(costs.at(b).wt_bytes);
+    }
+    group_bytes[(int)gi + 1] = gb.value();
+    group_wt[(int)gi + 1] = gw.value();
+    group_wtb[(int)gi + 1] = gwb.value();
+  }
+  auto base = build_engine_ops(p, g, hw, costs);
+  int in_res = hw.duplex ? R_XFER_IN : R_XFER, out_res = hw.duplex ? R_XFER_OUT : R_XFER;
+  std::vector<EngineOp> all;
+  std::map<int, int> update_prev;
+  for (int it = 1; it <= iterations; ++it) {
+    int offset = (int)all.size();
+    std::map<int, int> gathered;  // group -> all-gather op
+    if (it >= 2)
+      for (int gi = 1; gi <= (int)groups.size(); ++gi) {
+        EngineOp w;
+        w.action = Action::WEIGHT_IN;
+        w.group = gi;
+        w.iteration = it;
+        w.res = in_res;
+        w.duration = group_wtb[gi] / P / swap_rate;
+        w.deps = {update_prev.at(gi)};
+        int w_idx = (int)all.size();
+        all.push_back(w);
+        EngineOp a;
+        a.action = Action::ALL_GATHER;
+        a.group = gi;
+        a.iteration = it;
+        a.res = R_NETWORK;
+        a.duration = allreduce_time(group_wtb[gi], cfg) * 0.5;
+        a.deps = {w_idx};
+        gathered[gi] = (int)all.size();
+        all.push_back(a);
+      }
+    offset = (int)all.size();  // after the weight ops (distsim.py:165 takes it before them)
+    std::map<int, int> bw_done;
+    for (auto& op : base) {
+      EngineOp e = op;
+      e.iteration = it;
+      for (auto& d : e.deps) d += offset;
+      if (e.gate >= 0) e.gate += offset;
+      int b = op.block;
+      if (op.action == Action::FW && gathered.count(group_of[b])) e.deps.push_back(gathered[group_of[b]]);
+      if (op.action == Action::BW) bw_done[b] = (int)all.size();
+      all.push_back(e);
+    }
+    std::map<int, int> update_done;
+    for (int gi = (int)groups.size(); gi >= 1; --gi) {
+      EngineOp x;
+      x.action = Action::EXCHANGE;
+      x.group = gi;
+      x.iteration = it;
+      x.res = R_NETWORK;
+      x.duration = allreduce_time(group_bytes[gi], cfg) * 0.5;
+      for (int b : groups[gi - 1]) {
+        auto bd = bw_done.find(b);
+        if (bd == bw_done.end()) throw std::runtime_error("no backward for block " + std::to_string(b));
+        x.deps.push_back(bd->second);
+      }
+      int x_idx = (int)all.size();
+      all.push_back(x);
+      EngineOp go;
+      go.action = Action::GRAD_OUT;
+      go.group = gi;
+      go.iteration = it;
+      go.res = out_res;
+      go.duration = group_bytes[gi] / P / swap_rate;
+      go.deps = {x_idx};
+      int go_idx = (int)all.size();
+      all.push_back(go);
+      EngineOp h;
+      h.action = Action::HOST_UPDATE;
+      h.group = gi;
+      h.iteration = it;
+      h.res = R_HOST;
+      h.duration = group_wt[gi] / P / hw.host_update_rate;
+      h.deps = {go_idx};
+      update_done[gi] = (int)all.size();
+      all.push_back(h);
+    }
+    update_prev = update_done;
+  }
+  return all;
+}
+}  // namespace
+
 std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardware& hw,
                                      const DistConfig& cfg, int iterations,
                                      const std::map<int, BlockCost>& costs) {
+  if (cfg.device_exchange && cfg.workers >= 2) return build_dist_ops_device(p, g, hw, cfg, iterations, costs);
   double swap_rate = hw.swap_throughput();
   std::set<int> host_blocks;
   if (cfg.workers >= 2) for (auto& b : p.blocks) host_blocks.insert(b.id);
@@ -567,6 +676,7 @@ std::vector<EngineOp> build_dist_ops(const Plan& p, const Model& g, const Hardwa
         weight_in_idx[b] = (int)all.size();
         all.push_back(e);
       }
+    if (cfg.exact_deps) offset = (int)all.size();
     std::map<int, int> bw_done;
     for (auto& op : base) {
       EngineOp e = op;
@@ -847,7 +957,8 @@ DistResult simulate_distributed(const Plan& p, const Model& g, const Hardware& h
   }
   double exposed = 0.0;
   for (auto& e : dr.events) {
-    if (ops[e.op].action != Action::EXCHANGE || ops[e.op].iteration != iterations) continue;
+    Action a = ops[e.op].action;
+    if ((a != Action::EXCHANGE && a != Action::ALL_GATHER) || ops[e.op].iteration != iterations) continue;
     double hidden = 0.0;
     for (auto& m : merged) hidden += std::max(0.0, std::min(m.second, e.t_end) - std::max(m.first, e.t_start));
     exposed += (e.t_end - e.t_start) - hidden;

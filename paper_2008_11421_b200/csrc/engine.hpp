@@ -93,6 +93,17 @@ struct DistConfig {
   bool ring = true;
   double net_bw = 12.5e9, net_latency = 0.0;
   int groups = 0;  // 0 = one group per block
+  // B200 executor variant (DESIGN 3): per group, in reverse block
+  // order, a device reduce-scatter of the gradients right after the members'
+  // backward, a D2H of this rank's 1/P shard, the host update of that shard,
+  // and next iteration an H2D of the updated shard followed by an all-gather.
+  // The reference (false) swaps whole gradients out and all-reduces on the host.
+  bool device_exchange = false;
+  // distsim.py:165 takes the iteration's index offset BEFORE appending the
+  // weight_in ops, so from iteration 2 on every base op's deps point that many
+  // ops too early (e.g. bw 6 waits on fw 2).  false reproduces it (parity);
+  // true shifts by the real offset, which is what the executor's DAG does.
+  bool exact_deps = false;
 };
 double allreduce_time(double bytes, const DistConfig& cfg);
 std::vector<std::vector<int>> assign_groups(int num_blocks, int groups);

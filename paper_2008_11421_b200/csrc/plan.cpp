@@ -7,7 +7,7 @@
 namespace krt {
 namespace {
 const char* kActionNames[] = {"fw", "bw", "swap_in", "swap_out", "recompute_fw",
-                              "weight_in", "grad_out", "exchange", "host_update"};
+                              "weight_in", "grad_out", "exchange", "host_update", "all_gather"};
 const char* kStrategyNames[] = {"eager", "capacity", "capacity-recompute"};
 
 // rendering priority (plan.py:145-148): compute first, then swap-in, swap-out

@@ -13,7 +13,9 @@ namespace krt {
 
 enum class Action : int { FW = 0, BW, SWAP_IN, SWAP_OUT, RECOMPUTE_FW,
                           // data-parallel pipeline ops (distsim.py:168-236)
-                          WEIGHT_IN, GRAD_OUT, EXCHANGE, HOST_UPDATE };
+                          WEIGHT_IN, GRAD_OUT, EXCHANGE, HOST_UPDATE,
+                          // B200 executor variant: weight shard all-gather
+                          ALL_GATHER };
 const char* action_name(Action a);
 bool action_from_name(const std::string& s, Action* out);
 

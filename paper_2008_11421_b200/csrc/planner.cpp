@@ -706,53 +706,6 @@ Plan finalize_plan(Plan plan, const Model& g, const Hardware& hw) {
 
 }  // namespace
 
-long long find_theta(const Plan& p, const Model& g, const Hardware& hw) {
-  auto costs = plan_costs(p, g, hw);
-  auto skip = skip_requirement_map(p.blocks, g);
-  std::set<int> swapped;
-  for (int b : p.swapped_blocks()) swapped.insert(b);
-  // backward_compute_steps (plan.py:86-102)
-  size_t start = p.stages.size();
-  for (size_t i = 0; i < p.stages.size() && start == p.stages.size(); ++i)
-    for (auto& op : p.stages[i].ops)
-      if (op.action == Action::BW || op.action == Action::RECOMPUTE_FW) {
-        start = i;
-        break;
-      }
-  std::vector<double> durations;
-  std::vector<int> first_need_order;
-  std::map<int, int> first_need;
-  int j = 0;
-  for (size_t i = start; i < p.stages.size(); ++i)
-    for (auto& op : p.stages[i].ops) {
-      if (op.action != Action::BW && op.action != Action::RECOMPUTE_FW) continue;
-      ++j;
-      const BlockCost& c = costs.at(op.block);
-      durations.push_back(op.action == Action::BW ? c.bwd_seconds : c.fwd_seconds);
-      std::vector<int> req;
-      if (op.action == Action::BW) req.push_back(op.block);
-      else if (op.block >= 2) req.push_back(op.block - 1);
-      auto it = skip.find(op.block);
-      if (it != skip.end()) req.insert(req.end(), it->second.begin(), it->second.end());
-      for (int q : req)
-        if (swapped.count(q) && !first_need.count(q)) {
-          first_need[q] = j;
-          first_need_order.push_back(q);
-        }
-    }
-  std::map<int, std::vector<int>> needed_at;
-  for (int q : first_need_order) needed_at[first_need[q]].push_back(q);
-  double cum_proc = 0.0, cum_transfer = 0.0;
-  for (int k = 0; k < (int)durations.size(); ++k) {
-    auto it = needed_at.find(k + 1);
-    if (it != needed_at.end())
-      for (int q : it->second) cum_transfer += costs.at(q).swap_seconds;
-    if (cum_proc + kEps < cum_transfer) return k;
-    cum_proc += durations[k];
-  }
-  return -1;
-}
-
 Plan plan_model(const Model& g, const Hardware& hw, Strategy strategy, const std::string& solver_in, int max_blocks,
                 int layer_bound) {
   std::string solver = solver_in;

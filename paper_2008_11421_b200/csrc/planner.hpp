@@ -13,6 +13,7 @@
 #include <string>
 
 #include "engine.hpp"
+#include "occupancy.hpp"
 
 namespace krt {
 
@@ -26,8 +27,5 @@ struct PlannerMisuse : std::runtime_error {
 // solver: "auto" | "exhaustive" | "dp"; max_blocks <= 0 means None
 Plan plan_model(const Model& g, const Hardware& hw, Strategy strategy, const std::string& solver, int max_blocks,
                 int layer_bound = 20);
-
-// occupancy.py:178-199 (-1 = None)
-long long find_theta(const Plan& p, const Model& g, const Hardware& hw);
 
 }  // namespace krt

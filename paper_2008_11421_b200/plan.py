@@ -11,7 +11,9 @@ this path with the same names and return shapes:
 * ``validate_plan``          — planner.py:342-413 (list of violation strings)
 * ``simulate``               — simulator.py:364-399 (trace dict; raises
                                ``DeadlockError`` like the reference)
-* ``simulate_distributed``   — distsim.py:140-266
+* ``simulate_distributed``   — distsim.py:140-266 (plus the executor's own
+                               device reduce-scatter variant)
+* ``occupancy``              — occupancy.py:202-225 analytic_report
 
 All computation happens in C++ (csrc/engine.cpp); Python only marshals.
 """
@@ -45,6 +47,11 @@ class DistConfig:
     net_bw: float = 12.5e9
     net_latency: float = 0.0
     groups: int = 0
+    # Not in the reference: the B200 executor's P >= 2 pipeline (exchange =
+    # device reduce-scatter before a 1/P grad_out, shard host update, shard
+    # weight_in + all_gather), and the fix of distsim.py:165's dep offset.
+    device_exchange: bool = False
+    exact_deps: bool = False
 
 
 class PlanBundle:
@@ -107,13 +114,21 @@ class PlanBundle:
         _lib.check(_lib.lib().krt_plan_arena(self._h, arr, len(block_bytes), C.byref(out)))
         return json.loads(_lib.take_string(out))
 
+    def occupancy(self) -> dict:
+        """analytic_report + find_theta (occupancy.py:178-225): theta (None =
+        the device never waits), mean_occupancy, per_step rows, csv, summary."""
+        out = C.c_void_p()
+        _lib.check(_lib.lib().krt_plan_occupancy(self._h, C.byref(out)))
+        return json.loads(_lib.take_string(out))
+
     def simulate_distributed(self, cfg: DistConfig, iterations: int = 3) -> dict:
         if iterations < 2:
             raise DistSimError("need at least 2 iterations to observe the steady state")
         if cfg.collective not in ("ring", "flat"):
             raise DistSimError(f"unknown collective {cfg.collective!r}")
         c = _lib.DistConfig(cfg.workers, int(cfg.collective == "ring"), cfg.net_bw,
-                            cfg.net_latency, cfg.groups)
+                            cfg.net_latency, cfg.groups,
+                            int(cfg.device_exchange) | 2 * int(cfg.exact_deps))
         out = C.c_void_p()
         _lib.check(_lib.lib().krt_plan_simulate_dist(self._h, C.byref(c), int(iterations),
                                                      C.byref(out)))

@@ -26,6 +26,8 @@ from oocsched.distsim import Collective, DistConfig, simulate_distributed
 from oocsched.model_ir import serialize_model
 from oocsched.plan import Action, PlanOp, Stage, Strategy, plan_string, plan_to_dict
 from oocsched.planner import InfeasibleModelError, plan_model, validate_plan
+from oocsched.occupancy import analytic_report, find_theta
+from oocsched.planner import build_blocks, generate_schedule
 from oocsched.simulator import DeadlockError, simulate
 from oocsched import zoo
 
@@ -94,6 +96,25 @@ def sim_record(plan, g, hw, enforce=True):
             "peak_mem": tr.peak_mem, "events": trace_rows(tr), "csv": tr.to_csv()}
 
 
+def occupancy_record(plan, g, hw):
+    """analytic_report / find_theta and the trace's own occupancy figures
+    (occupancy.py:178-225, simulator.py:200-236, cli.py:115-121)."""
+    rep = analytic_report(plan, g, hw)
+    theta = find_theta(plan, g, hw)
+    rec = {"theta": theta, "mean_occupancy": rep.mean_occupancy,
+           "per_step": [[s.step, s.occupancy, s.busy_s, s.idle_s] for s in rep.per_step],
+           "csv": rep.to_csv(), "summary": rep.summary()}
+    try:
+        tr = simulate(plan, g, hw)
+    except DeadlockError:
+        return rec
+    rec["trace"] = {"mean_occupancy": tr.mean_occupancy(),
+                    "first_stall_backward_step": tr.first_stall_backward_step(),
+                    "boundary_stall": tr.boundary_stall(),
+                    "summary_csv": tr.summary_csv(theta=theta)}
+    return rec
+
+
 def case(name, g, hw, strategy=Strategy.CAPACITY_RECOMPUTE, solver="auto",
          rng=None, n_perturb=12, dist=True):
     rec = {"name": name, "model": serialize_model(g), "hardware": hw_text(hw),
@@ -107,6 +128,7 @@ def case(name, g, hw, strategy=Strategy.CAPACITY_RECOMPUTE, solver="auto",
     rec["plan_string"] = plan_string(plan)
     rec["validate"] = validate_plan(plan, g, hw)
     rec["sim"] = sim_record(plan, g, hw)
+    rec["occupancy"] = occupancy_record(plan, g, hw)
     rec["sim_open"] = sim_record(plan, g, replace(hw, capacity_bytes=hw.capacity_bytes * 0.5),
                                  enforce=False)
     tight = replace(hw, capacity_bytes=max(b.swap_bytes for b in plan.blocks) * 0.9)
@@ -170,6 +192,29 @@ def main():
                                "reference": "oocsched 0.1.0 (/root/reference/pkg)",
                                "cases": cases}, separators=(",", ":")))
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(cases)} cases)", file=sys.stderr)
+    occ_cases()
+
+
+def occ_cases():
+    """The reference's occupancy fixtures (test_occupancy.py:25-33,
+    :144-161): CAPACITY schedules of uniform chains, with the fast-link and
+    instant-compute variants of test_occupancy.py:87-107."""
+    out = []
+    for n, ratio, cap in [(6, 2.0, 3.0), (8, 1.2, 3.0), (8, 3.0, 4.0), (10, 2.5, 4.0), (6, 4.0, 3.0)]:
+        g = zoo.uniform_chain_model(num_layers=n)
+        hw = zoo.uniform_chain_hardware(g, swap_compute_ratio=ratio, capacity_blocks=cap)
+        blocks, costs = build_blocks([(i, i) for i in range(1, n + 1)], g, hw)
+        plan = generate_schedule(blocks, g, hw, Strategy.CAPACITY, costs=costs)
+        for tag, h in (("", hw), ("_fastlink", replace(hw, interconnect_bw=1e15)),
+                       ("_instant", replace(hw, compute_rate=1e18))):
+            out.append({"name": f"chain{n}_r{ratio}_c{cap}{tag}", "model": serialize_model(g),
+                        "hardware": hw_text(h), "plan": plan_to_dict(plan),
+                        "occupancy": occupancy_record(plan, g, h)})
+    path = OUT.with_name("occupancy_cases.json")
+    path.write_text(json.dumps({"generator": "tests/golden/make_golden.py",
+                                "reference": "oocsched 0.1.0 (/root/reference/pkg)",
+                                "cases": out}, separators=(",", ":")))
+    print(f"wrote {path} ({len(out)} cases)", file=sys.stderr)
 
 
 if __name__ == "__main__":
