@@ -677,6 +677,15 @@ def run_gpu(args, rec):
         Path(args.trace_out).write_text(trace)
     ex.close()
     del ex
+    if rank == 0:
+        # HardwareSpec fields measured on this box (calibrate.py):
+        # the planner's inputs, from the trace of this run and the probes
+        from paper_2008_11421_b200 import calibrate
+        host = calibrate.host_update_rate()
+        pl = pcie or {"h2d": PCIE_H2D, "d2h": PCIE_D2H, "duplex": PCIE_DUPLEX}
+        cal = calibrate.calibrate(bundle, trace, pk, {k: pl[k] / 1e9 for k in ("h2d", "d2h", "duplex")}, host)
+        cal["hw_text"] = calibrate.hw_text(calibrate.capacity_of(rec["hardware"]), cal)
+        line["calibration"] = cal
     if rank == 0 and not args.no_cpu_baseline:
         line["reference_planner"] = reference_planner_time(rec, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -99,6 +99,11 @@ typedef struct krt_dist_config {
  * exposed_comm, peak_mem, makespan, events} or {error}. */
 int krt_plan_simulate_dist(const krt_plan* plan, const krt_dist_config* cfg, int iterations,
                            char** out_json);
+/* block_cost per plan block (cost_model.py:250-273: fwd/bwd/swap seconds,
+ * bytes, wt/grad bytes, weight elements) and layer_ops per layer with its kind
+ * (cost_model.py:97-167): JSON {blocks[...], layers[{id, kind, ops}]}.  The
+ * calibration (calibrate.py) fits measured op times against these. */
+int krt_plan_costs(const krt_plan* plan, char** out_json);
 /* analytic_report (occupancy.py:202-225) with find_theta (:178-199): JSON
  * {theta (null = None), mean_occupancy, per_step[[step, occupancy, busy_s,
  * idle_s]], csv (OccupancyReport.to_csv), summary (OccupancyReport.summary)}. */

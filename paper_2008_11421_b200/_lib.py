@@ -65,6 +65,7 @@ EXPORTS = {
     "krt_plan_validate": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int)]),
     "krt_plan_simulate": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "krt_plan_occupancy": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "krt_plan_costs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "krt_plan_simulate_dist": (C.c_int, [C.c_void_p, C.POINTER(DistConfig), C.c_int,
                                          C.POINTER(C.c_void_p)]),
     "krt_nccl_unique_id": (C.c_int, [C.c_void_p]),

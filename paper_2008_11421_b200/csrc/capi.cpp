@@ -201,6 +201,32 @@ int krt_plan_simulate(const krt_plan* p, int enforce, char** out) {
   });
 }
 
+int krt_plan_costs(const krt_plan* p, char** out) {
+  return guard([&] {
+    auto costs = plan_costs(p->plan, p->model, p->hw);
+    std::ostringstream os;
+    os << "{\"blocks\": [";
+    bool first = true;
+    for (auto& b : p->plan.blocks) {
+      const BlockCost& c = costs.at(b.id);
+      os << (first ? "" : ", ") << "{\"id\": " << b.id << ", \"layers\": [" << b.first_layer << ", "
+         << b.last_layer << "], \"fwd_seconds\": " << jnum(c.fwd_seconds) << ", \"bwd_seconds\": "
+         << jnum(c.bwd_seconds) << ", \"bytes\": " << jnum(c.bytes) << ", \"wt_bytes\": " << jnum(c.wt_bytes)
+         << ", \"grad_bytes\": " << jnum(c.grad_bytes) << ", \"weight_elems\": " << jnum(c.weight_elems)
+         << ", \"swap_seconds\": " << jnum(c.swap_seconds) << "}";
+      first = false;
+    }
+    os << "], \"layers\": [";
+    for (int i = 1; i <= p->model.num_layers(); ++i) {
+      const Layer& l = p->model.layer(i);
+      os << (i > 1 ? ", " : "") << "{\"id\": " << i << ", \"kind\": \"" << kind_name(l.kind)
+         << "\", \"ops\": " << jnum(layer_ops(l, p->model.batch)) << "}";
+    }
+    os << "]}";
+    *out = dup(os.str());
+  });
+}
+
 int krt_plan_occupancy(const krt_plan* p, char** out) {
   return guard([&] {
     OccupancyReport r = analytic_report(p->plan, p->model, p->hw);

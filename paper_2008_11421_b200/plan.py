@@ -114,6 +114,12 @@ class PlanBundle:
         _lib.check(_lib.lib().krt_plan_arena(self._h, arr, len(block_bytes), C.byref(out)))
         return json.loads(_lib.take_string(out))
 
+    def costs(self) -> dict:
+        """block_cost per block and layer_ops per layer (cost_model.py:97-273)."""
+        out = C.c_void_p()
+        _lib.check(_lib.lib().krt_plan_costs(self._h, C.byref(out)))
+        return json.loads(_lib.take_string(out))
+
     def occupancy(self) -> dict:
         """analytic_report + find_theta (occupancy.py:178-225): theta (None =
         the device never waits), mean_occupancy, per_step rows, csv, summary."""
