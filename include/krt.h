@@ -139,6 +139,15 @@ typedef struct krt_config {
                                update / all-gather) even at world_size 1 (NCCL, 1 rank) */
   int ipc_exchange;         /* 1: exchange over CUDA IPC peer memory between processes
                                (own reduce kernel + D2D gather, stream-memop flags) */
+  int grad_slots;           /* 0: one fp32 gradient region for the whole model; R > 0:
+                               a ring of R group-sized gradient slots (group g uses slot
+                               (g-1) mod R), each held from the group's first backward
+                               until its exchange / grad_out / device update consumed it
+                               (distsim.py:195-202 holds grad bytes only until grad_out) */
+  int exchange_bf16;        /* 1: NCCL exchange in bf16: the group's fp32 gradients are cast
+                               into a bf16 pack buffer (krt_reduce_cast), reduce-scattered in
+                               bf16 (half the NVLink bytes) and the shard unpacked to fp32
+                               for the D2H / host update */
 } krt_config;
 
 /* In-process exchange group: world_size ranks living in one process (threads),

@@ -46,7 +46,8 @@ class Config(C.Structure):
                 ("beta2", C.c_float), ("eps", C.c_float), ("weight_decay", C.c_float),
                 ("momentum", C.c_float), ("grad_scale", C.c_float), ("host_threads", C.c_int),
                 ("arena_slack_bytes", C.c_size_t), ("peer_group", C.c_void_p),
-                ("host_path_all", C.c_int), ("force_dp_path", C.c_int), ("ipc_exchange", C.c_int)]
+                ("host_path_all", C.c_int), ("force_dp_path", C.c_int), ("ipc_exchange", C.c_int),
+                ("grad_slots", C.c_int), ("exchange_bf16", C.c_int)]
 
 
 COMPUTE_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p)

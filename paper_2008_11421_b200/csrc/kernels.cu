@@ -130,6 +130,23 @@ __global__ void __launch_bounds__(256) reduce_cast_kernel(InPtrs in, int n_in, v
   }
 }
 
+// bf16 -> fp32 (x scale): the reduce-scattered bf16 shard back to the fp32
+// gradient shard the host update reads
+__global__ void __launch_bounds__(256) unpack_bf16_kernel(const __nv_bfloat16* __restrict__ in,
+                                                          float* __restrict__ out, size_t n, float scale) {
+  size_t n4 = n / 4;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    uint2 u = __ldcs(reinterpret_cast<const uint2*>(in) + i);
+    float2 lo = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+    float2 hi = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+    __stcs(reinterpret_cast<float4*>(out) + i, make_float4(__fmul_rn(lo.x, scale), __fmul_rn(lo.y, scale),
+                                                            __fmul_rn(hi.x, scale), __fmul_rn(hi.y, scale)));
+  }
+  size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __fmul_rn(__bfloat162float(in[i]), scale);
+}
+
 int grid_for(size_t n4) {
   // persistent grid: 148 SMs x 8 resident 256-thread CTAs, fewer for small n
   size_t want = (n4 + 255) / 256;
@@ -145,6 +162,12 @@ cudaError_t launch_update(float* master, float* m, float* v, const float* grad, 
   int grid = grid_for(n / 4 + 1);
   if (weight_dtype == 1) update_kernel<1><<<grid, 256, 0, stream>>>(master, m, v, grad, weights, n, s);
   else update_kernel<0><<<grid, 256, 0, stream>>>(master, m, v, grad, weights, n, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_bf16(const void* in, float* out, size_t n, float scale, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  unpack_bf16_kernel<<<grid_for(n / 4 + 1), 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(in), out, n, scale);
   return cudaGetLastError();
 }
 

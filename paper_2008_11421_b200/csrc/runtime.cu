@@ -159,6 +159,8 @@ Runtime::~Runtime() {
   cudaFree(d_arena_);
   cudaFree(d_weights_);
   cudaFree(d_grads_);
+  cudaFree(d_pack_);
+  cudaFree(d_pack_shard_);
   cudaFree(d_master_);
   cudaFree(d_m_);
   cudaFree(d_v_);
@@ -259,6 +261,23 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
   }
   int64_t off = lay.total;
   total_params_ = off;
+  // gradient ring: R group-sized slots instead of a whole-model region
+  if (cfg_.grad_slots < 0) throw std::invalid_argument("grad_slots must be >= 0");
+  grad_ring_ = (cfg_.grad_slots > 0 && cfg_.grad_slots < (int)groups_.size()) ? cfg_.grad_slots : 0;
+  if (grad_ring_ && (peers_ || cfg_.ipc_exchange))
+    throw std::invalid_argument("grad_slots needs the NCCL exchange: peers read a rank's gradient slot directly "
+                                "over in-process / IPC exchange, with no completion signal to reuse it on");
+  grad_slot_off_.assign(groups_.size(), 0);
+  if (grad_ring_) {
+    int64_t slot = 0;
+    for (auto& g : groups_) slot = std::max(slot, g.p_n);
+    slot = (slot + 63) / 64 * 64;
+    for (size_t gi = 0; gi < groups_.size(); ++gi) grad_slot_off_[gi] = (int64_t)(gi % grad_ring_) * slot;
+    grad_elems_ = slot * grad_ring_;
+  } else {
+    for (size_t gi = 0; gi < groups_.size(); ++gi) grad_slot_off_[gi] = groups_[gi].p_lo;
+    grad_elems_ = total_params_;
+  }
   for (size_t gi = 0; gi < groups_.size(); ++gi)
     group_first_block_[(int)gi + 1] = *std::min_element(groups_[gi].members.begin(), groups_[gi].members.end());
   // host state layout
@@ -380,8 +399,32 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
       }
     }
   };
+  // gradient ring: group g's backward overwrites the slot group g + R used
+  // earlier in the same backward pass, so it waits until that gradient was
+  // consumed (exchange, grad_out or the device update in its bw)
+  auto ring_deps = [&](std::vector<XOp>& out) {
+    if (!grad_ring_) return;
+    std::map<int, std::vector<int>> release_of;
+    for (size_t i = 0; i < out.size(); ++i) {
+      const EngineOp& e = out[i].e;
+      if (dp_ && e.action == Action::EXCHANGE) release_of[e.group].push_back((int)i);
+      if (!dp_ && e.action == Action::GRAD_OUT) release_of[blocks_.at(e.block).group].push_back((int)i);
+      if (!dp_ && e.action == Action::BW && !blocks_.at(e.block).host_path)
+        release_of[blocks_.at(e.block).group].push_back((int)i);
+    }
+    int ng = (int)groups_.size();
+    for (size_t i = 0; i < out.size(); ++i) {
+      EngineOp& e = out[i].e;
+      if (e.action != Action::BW) continue;
+      int g = blocks_.at(e.block).group;
+      if (g + grad_ring_ > ng) continue;
+      for (int r : release_of[g + grad_ring_]) e.deps.push_back(r);
+    }
+  };
   make_list(false, ops_first_);
   make_list(true, ops_steady_);
+  ring_deps(ops_first_);
+  ring_deps(ops_steady_);
   auto order_of = [&](std::vector<XOp>& ops, std::vector<int>& order) {
     std::vector<EngineOp> eo;
     for (auto& x : ops) eo.push_back(x.e);
@@ -420,8 +463,9 @@ void Runtime::allocate() {
   size_t np = (size_t)std::max<int64_t>(total_params_, 64);
   CK(cudaMalloc(&d_weights_, np * wb));
   CK(cudaMemset(d_weights_, 0, np * wb));
-  CK(cudaMalloc((void**)&d_grads_, np * 4));
-  CK(cudaMemset(d_grads_, 0, np * 4));
+  size_t ng = (size_t)std::max<int64_t>(grad_elems_, 64);
+  CK(cudaMalloc((void**)&d_grads_, ng * 4));
+  CK(cudaMemset(d_grads_, 0, ng * 4));
   // device optimizer state for blocks that never take the host path (P = 1)
   bool any_dev = false;
   for (auto& [id, b] : blocks_) any_dev |= !b.host_path;
@@ -439,6 +483,16 @@ void Runtime::allocate() {
     size_t ns = 0;
     for (auto& g : groups_) ns += (size_t)g.shard_n;
     CK(cudaMalloc((void**)&d_shard_, std::max<size_t>(ns, 64) * 4));
+    if (cfg_.exchange_bf16) {
+      if (peers_ || ipc_) throw std::invalid_argument("exchange_bf16 is the NCCL exchange's pack");
+      size_t gp = 64, gs = 64;
+      for (auto& g : groups_) {
+        gp = std::max(gp, (size_t)g.p_n);
+        gs = std::max(gs, (size_t)g.shard_n);
+      }
+      CK(cudaMalloc(&d_pack_, gp * 2));
+      CK(cudaMalloc(&d_pack_shard_, gs * 2));
+    }
   }
   if (ipc_) {
     size_t nf = (size_t)3 * groups_.size() * world_;
@@ -480,7 +534,7 @@ void Runtime::region(int which, int block, void** ptr, size_t* bytes) {
     }
     case KRT_REGION_GRADS: {
       auto& b = blocks_.at(block);
-      *ptr = d_grad(b.p_off);
+      *ptr = d_grad_block(block);
       *bytes = (size_t)b.n_params * 4;
       return;
     }
@@ -708,7 +762,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
           OptimScalars sc = make_scalars(cfg_.optimizer, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps,
                                          cfg_.weight_decay, cfg_.momentum, step, 1.0f);
           float* master = d_master_ ? d_master_ + bp.p_off : reinterpret_cast<float*>(d_weight(bp.p_off));
-          CK(launch_update(master, d_m_ + bp.p_off, d_v_ + bp.p_off, d_grad(bp.p_off), d_weight(bp.p_off),
+          CK(launch_update(master, d_m_ + bp.p_off, d_v_ + bp.p_off, d_grad_block(e.block), d_weight(bp.p_off),
                            cfg_.weight_dtype, (size_t)bp.n_params, sc, s));
           ++kernel_launches_;
           ++iter_launches_;
@@ -766,7 +820,7 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         auto& bp = blocks_.at(e.block);
         auto& g = groups_.at((size_t)bp.group - 1);
         int64_t ho = host_block_off(blocks_, g, e.block);
-        CK(cudaMemcpyAsync(h_grad_ + ho, d_grad(bp.p_off), (size_t)bp.n_params * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_grad_ + ho, d_grad_block(e.block), (size_t)bp.n_params * 4, cudaMemcpyDeviceToHost, s));
         iter_bytes_d2h_ += (size_t)bp.n_params * 4;
       }
       CK(cudaEventRecord(ev_done_[idx], s));
@@ -783,14 +837,15 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         if (ipc_) {
           ipc_wait(s, PK_BW, e.group, (uint32_t)step);
           for (int p = 0; p < world_; ++p)
-            in[p] = reinterpret_cast<const float*>(ipc_g_[p]) + g.p_lo + (int64_t)rank_ * g.shard_n;
+            in[p] = reinterpret_cast<const float*>(ipc_g_[p]) + grad_slot_off_[(size_t)e.group - 1] +
+                    (int64_t)rank_ * g.shard_n;
         } else {
           peers_->wait_all(PK_BW, e.group, step, watchdog_s_);
           for (int p = 0; p < world_; ++p) {
             Runtime* peer = peers_->ranks[p];
             if (!peer) throw std::runtime_error("peer rank " + std::to_string(p) + " missing");
             CK(cudaStreamWaitEvent(s, peers_->event(p, PK_BW, e.group), 0));
-            in[p] = peer->grads_base() + g.p_lo + (int64_t)rank_ * g.shard_n;
+            in[p] = peer->grads_base() + grad_slot_off_[(size_t)e.group - 1] + (int64_t)rank_ * g.shard_n;
           }
         }
         CK(cudaEventRecord(ev_start_[idx], s));
@@ -799,11 +854,22 @@ void Runtime::issue(int idx, std::vector<XOp>& ops, krt_compute_cb cb, void* use
         ++iter_launches_;
       } else {
         CK(cudaEventRecord(ev_start_[idx], s));
-        NK(ncclReduceScatter(d_grad(g.p_lo), d_shard_ + shard_pos, (size_t)g.shard_n, ncclFloat, ncclSum,
-                             (ncclComm_t)nccl_comm_, s));
+        if (d_pack_) {
+          // grad cast pack -> bf16 reduce-scatter -> fp32 shard (the update applies grad_scale)
+          const float* src = d_grad_group(e.group);
+          CK(launch_reduce_cast(&src, 1, d_pack_, KRT_BF16, (size_t)g.p_n, 1.0f, s));
+          NK(ncclReduceScatter(d_pack_, d_pack_shard_, (size_t)g.shard_n, ncclBfloat16, ncclSum,
+                               (ncclComm_t)nccl_comm_, s));
+          CK(launch_unpack_bf16(d_pack_shard_, d_shard_ + shard_pos, (size_t)g.shard_n, 1.0f, s));
+          kernel_launches_ += 2;
+          iter_launches_ += 2;
+        } else {
+          NK(ncclReduceScatter(d_grad_group(e.group), d_shard_ + shard_pos, (size_t)g.shard_n, ncclFloat, ncclSum,
+                               (ncclComm_t)nccl_comm_, s));
+        }
       }
       CK(cudaEventRecord(ev_done_[idx], s));
-      bytes_net_ += (size_t)g.p_n * 4 * (world_ - 1) / world_;
+      bytes_net_ += (size_t)g.p_n * (d_pack_ ? 2 : 4) * (world_ - 1) / world_;
       return;
     }
     case Action::HOST_UPDATE: {
@@ -990,6 +1056,7 @@ std::string Runtime::stats_json() {
   os << "{\"arena_bytes\": " << arena_bytes_ << ", \"ledger_peak_bytes\": " << ledger_peak_
      << ", \"instances\": " << instances_.size() << ", \"host_swap_bytes\": " << h_swap_bytes_
      << ", \"swapped_blocks\": " << nswapped << ", \"params\": " << total_params_
+     << ", \"grad_region_bytes\": " << grad_elems_ * 4 << ", \"grad_slots\": " << grad_ring_
      << ", \"host_elems\": " << host_elems_ << ", \"bytes_h2d_total\": " << bytes_h2d_
      << ", \"bytes_d2h_total\": " << bytes_d2h_ << ", \"bytes_net_total\": " << bytes_net_
      << ", \"iter_bytes_h2d\": " << iter_bytes_h2d_ << ", \"iter_bytes_d2h\": " << iter_bytes_d2h_

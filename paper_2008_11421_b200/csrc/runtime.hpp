@@ -135,7 +135,13 @@ class Runtime {
   std::string first_pending_op();
   void fail_iteration(int step, const std::string& why);
   void gather_peer_shards(const GroupPhys& g, int group, cudaStream_t s, int kind);
-  float* d_grad(int64_t p_off) const { return d_grads_ + p_off; }
+  // gradient addresses: the group's slot (the whole-model region when
+  // grad_slots == 0, where the slot offset is the group's own p_lo)
+  float* d_grad_group(int group) const { return d_grads_ + grad_slot_off_[(size_t)group - 1]; }
+  float* d_grad_block(int block) const {
+    const BlockPhys& b = blocks_.at(block);
+    return d_grad_group(b.group) + (b.p_off - groups_[(size_t)b.group - 1].p_lo);
+  }
   void* d_weight(int64_t p_off) const;
 
   krt_config cfg_;
@@ -155,10 +161,15 @@ class Runtime {
   uint8_t* d_arena_ = nullptr;
   void* d_weights_ = nullptr;
   float* d_grads_ = nullptr;
+  std::vector<int64_t> grad_slot_off_;  // per group (index group-1): element offset in d_grads_
+  int64_t grad_elems_ = 0;              // d_grads_ size in elements
+  int grad_ring_ = 0;                   // slots in use (0: whole-model region)
   float* d_master_ = nullptr;   // device-path masters (bf16 weights only)
   float* d_m_ = nullptr;
   float* d_v_ = nullptr;
   float* d_shard_ = nullptr;    // reduce-scatter landing (P>1)
+  void* d_pack_ = nullptr;      // bf16 exchange: packed group gradients (max group p_n)
+  void* d_pack_shard_ = nullptr;  // bf16 exchange: reduce-scattered bf16 shard (max shard_n)
   uint8_t* h_swap_ = nullptr;
   size_t h_swap_bytes_ = 0;
   float* h_grad_ = nullptr;     // pinned, host_n per group

@@ -124,6 +124,8 @@ class ExecConfig:
     host_path_all: bool = False           # host update for every block even at world_size 1
     force_dp_path: bool = False           # DP op structure through a 1-rank NCCL communicator
     ipc_exchange: bool = False            # exchange over CUDA IPC peer memory (multi-process)
+    grad_slots: int = 0                   # 0: whole-model gradient region; R: ring of R group slots
+    exchange_bf16: bool = False           # NCCL reduce-scatter of bf16-packed gradients
 
 
 class Executor:
@@ -153,7 +155,8 @@ class Executor:
                          cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, cfg.momentum,
                          1.0 / cfg.world_size, cfg.host_threads, cfg.arena_slack_bytes,
                          cfg.peer_group.handle if cfg.peer_group is not None else None,
-                         int(cfg.host_path_all), int(cfg.force_dp_path), int(cfg.ipc_exchange))
+                         int(cfg.host_path_all), int(cfg.force_dp_path), int(cfg.ipc_exchange),
+                         int(cfg.grad_slots), int(cfg.exchange_bf16))
         h = C.c_void_p()
         _lib.check(L.krt_create(C.byref(kc), C.byref(h)))
         self._ctx = h
