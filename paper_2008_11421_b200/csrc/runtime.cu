@@ -268,10 +268,11 @@ void Runtime::build_ops(const Plan& plan, const Model& model, const Hardware& hw
     throw std::invalid_argument("grad_slots needs the NCCL exchange: peers read a rank's gradient slot directly "
                                 "over in-process / IPC exchange, with no completion signal to reuse it on");
   grad_slot_off_.assign(groups_.size(), 0);
+  int64_t slot = 0;
+  for (auto& g : groups_) slot = std::max(slot, g.p_n);
+  slot = (slot + 63) / 64 * 64;
+  if (slot * grad_ring_ >= total_params_) grad_ring_ = 0;   // a ring not smaller than the whole-model region
   if (grad_ring_) {
-    int64_t slot = 0;
-    for (auto& g : groups_) slot = std::max(slot, g.p_n);
-    slot = (slot + 63) / 64 * 64;
     for (size_t gi = 0; gi < groups_.size(); ++gi) grad_slot_off_[gi] = (int64_t)(gi % grad_ring_) * slot;
     grad_elems_ = slot * grad_ring_;
   } else {

