@@ -393,6 +393,7 @@ def run_gpu(args, rec):
     ex = Executor(units, bundle, batch=batch, loss_fn=loss_fn,
                   cfg=ExecConfig(device=local, world_size=world, rank=rank, nccl_id=nccl_id,
                                  ipc_exchange=(world > 1 and args.exchange == "ipc"),
+                                 grad_slots=args.grad_slots, exchange_bf16=args.exchange_bf16,
                                  weight_dtype=torch.bfloat16, **opt_cfg))
     if world > 1 and args.exchange == "ipc":
         handles = [None] * world
@@ -618,7 +619,9 @@ def run_gpu(args, rec):
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": rec["name"], "exchange": args.exchange if world > 1 else "none", "model": model_name(rec), "per_gpu_batch": batch,
+        "config": {"workload": rec["name"], "exchange": args.exchange if world > 1 else "none",
+                   "exchange_dtype": "bf16" if args.exchange_bf16 else "fp32", "grad_slots": args.grad_slots,
+                   "model": model_name(rec), "per_gpu_batch": batch,
                    "global_batch": batch * world, "input": m.get("res", m.get("seq")), "parallelism": f"dp{world}",
                    "plan": rec["plan_string"][:160] + " ...",
                    "activations_bytes": rec["total_bytes"], "hbm_bytes": 183359 * 2 ** 20,
@@ -713,6 +716,10 @@ def main():
                     help="N>1 gradient exchange: NCCL reduce-scatter/all-gather on the runtime's own "
                          "communicator (default), or the runtime's reduce over CUDA IPC peer memory")
     ap.add_argument("--no-probe", action="store_true", help="skip the PCIe / NCCL link probes")
+    ap.add_argument("--grad-slots", type=int, default=0,
+                    help="gradient ring of R group-sized slots instead of a whole-model region (0: off)")
+    ap.add_argument("--exchange-bf16", action="store_true",
+                    help="N>1 NCCL exchange: bf16 cast pack before the reduce-scatter (half the NVLink bytes)")
     ap.add_argument("--incore", action="store_true",
                     help="same blocks, everything resident (no swap/recompute): the in-core baseline")
     args = ap.parse_args()

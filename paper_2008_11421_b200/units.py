@@ -94,6 +94,8 @@ BN_EPS = 1e-5
 # bottleneck 1x1 convolutions on the own tcgen05 GEMM (csrc/gemm_sm100.cu) with
 # the BN work fused in; KRT_TC_CONV1X1=0 selects cuDNN + separate BN kernels
 TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
+# GPT attention on cuDNN's sm100 fused kernels (KRT_ATTN_CUDNN=0: aten flash)
+ATTN_CUDNN = os.environ.get("KRT_ATTN_CUDNN", "1") != "0"
 # the pre-activation unit's 1x1 dgrads on the same GEMM with the BN-backward
 # reduce fused (narrow, HBM-bound shapes)
 TC_DGRAD_PREACT = os.environ.get("KRT_TC_DGRAD_PREACT", "1") != "0"
@@ -1061,15 +1063,28 @@ class TransformerLayerUnit(Unit):
     def _merge(self, o):
         return o.transpose(1, 2).reshape(-1, self.h)
 
+    @staticmethod
+    def _cudnn_attn():
+        # cuDNN's sm100 fused attention (2.2x the forward, 2x the backward of
+        # aten's flash kernel at these shapes, scripts/probe_attention.py);
+        # its backward is not bitwise repeatable (dQ accumulation order), so
+        # deterministic mode (the bitwise out-of-core == in-core tests) runs
+        # the flash kernel's deterministic backward instead
+        return ATTN_CUDNN and not torch.are_deterministic_algorithms_enabled()
+
     def _attn_fw(self, qkv, lse_out):
         q, k, v = self._heads(qkv)
         if self._flash():
             n = qkv.shape[0] // self.s
-            with bnfused._timed("flash_attn_fwd", 4 * qkv.shape[0] * self.h * qkv.element_size(),
+            cud = self._cudnn_attn()
+            with bnfused._timed("cudnn_attn_fwd" if cud else "flash_attn_fwd", 4 * qkv.shape[0] * self.h * qkv.element_size(),
                                 2.0 * n * self.nh * self.s * self.s * self.hd):   # causal: half of 4*s^2*hd
-                r = _aten._scaled_dot_product_flash_attention(q, k, v, 0.0, True, False)
+                if cud:
+                    r = _aten._scaled_dot_product_cudnn_attention(q, k, v, None, True, 0.0, True, False)
+                else:
+                    r = _aten._scaled_dot_product_flash_attention(q, k, v, 0.0, True, False)
             if lse_out is not None:
-                lse_out.copy_(r[1])
+                lse_out.copy_(r[1].reshape(lse_out.shape))
             return self._merge(r[0])
         p = self._probs(q, k)
         return self._merge(p @ v)
@@ -1086,10 +1101,16 @@ class TransformerLayerUnit(Unit):
         if self._flash():
             O = o.view(n, self.s, self.nh, self.hd).transpose(1, 2)
             z = torch.zeros((), dtype=torch.int64, device=q.device)
-            with bnfused._timed("flash_attn_bwd", 8 * do.shape[0] * self.h * do.element_size(),
+            cud = self._cudnn_attn()
+            with bnfused._timed("cudnn_attn_bwd" if cud else "flash_attn_bwd", 8 * do.shape[0] * self.h * do.element_size(),
                                 5.0 * n * self.nh * self.s * self.s * self.hd):   # causal, 2.5x the forward
-                dq, dk, dv = _aten._scaled_dot_product_flash_attention_backward(
-                    dO, q, k, v, O, lse, None, None, self.s, self.s, 0.0, True, z, z)
+                if cud:
+                    dq, dk, dv = _aten._scaled_dot_product_cudnn_attention_backward(
+                        dO, q, k, v, O, lse.view(n, self.nh, self.s, 1), z, z, None, None, None, self.s, self.s,
+                        0.0, True)
+                else:
+                    dq, dk, dv = _aten._scaled_dot_product_flash_attention_backward(
+                        dO, q, k, v, O, lse, None, None, self.s, self.s, 0.0, True, z, z)
         else:
             p = self._probs(q, k)
             dv = p.transpose(-1, -2) @ dO

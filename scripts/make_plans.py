@@ -144,6 +144,9 @@ def main():
     if only == {"sweep"}:
         _sweep()
         return
+    if only == {"megatron"}:
+        _megatron()
+        return
     if only and not any(n.startswith(("resnet200", "resnet1001")) for n in only):
         raise SystemExit("usage: make_plans.py [resnet200_b3072 | resnet1001_2048_b2 ...]  (no args: every workload)")
     if only:
@@ -202,6 +205,21 @@ def _resnet1001():
     make("resnet1001_2048_b2", units, 2, 150e9,
          {"family": "preact", "depth": 1001, "res": 2048, "classes": 10, "act": "bf16"}, max_blocks=64,
          compute_rate=3.0e13)
+
+
+def _megatron():
+    """cfg3 family on one GPU: the Megatron-LM 8.3B layer shape (H 3072, 32
+    heads; seq 1024, vocab 51200) at half its depth (36 of 72
+    layers, 4.4B parameters) so the fp32 master + Adam state of every block
+    fits this single host (53 GB; the full 72 layers need 102 GB plus pinned
+    staging, which is what the 8-way host shard of cfg3 splits).  Batch 128:
+    291 GB of activations = 1.6x HBM.  Planned under the measured GPT spec
+    (plans/calibration/gpt2p5b_b144.json)."""
+    units = gpt_units(3072, 32, 36, 1024, 51200)
+    make("megatron8p3b_l36_b128", units, 128, 120e9,
+         {"family": "gpt", "hidden": 3072, "heads": 32, "layers": 36, "seq": 1024, "vocab": 51200,
+          "act": "bf16"}, max_blocks=16, compute_rate=5.0e14)
+    calibrated("megatron8p3b_l36_b128", cal_from="gpt2p5b_b144")
 
 
 def _sweep(batches=(1280, 2048, 3072, 3584, 4096)):

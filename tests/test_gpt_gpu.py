@@ -72,3 +72,26 @@ def test_gpt_bf16_out_of_core_equals_in_core_and_tracks_oracle():
     xs, ys = batches(rec, 3)
     ref_losses, _ = gpt_oracle.train(units, init, xs, ys, lr=0.05)
     torch.testing.assert_close(torch.tensor(l_ooc), torch.tensor(ref_losses), rtol=2e-2, atol=2e-2)
+
+
+def test_cudnn_attention_matches_flash(monkeypatch):
+    """The decoder layer's attention on cuDNN's sm100 kernels (the bench
+    path) vs aten's flash kernel (the deterministic path): output and every
+    gradient agree to bf16 resolution."""
+    from paper_2008_11421_b200 import units as U
+    torch.use_deterministic_algorithms(False)
+    u = U.TransformerLayerUnit(256, 4, 128)
+    gen = torch.Generator().manual_seed(3)
+    params = [p.to("cuda", torch.bfloat16) for p in u.init_params(gen)]
+    x = (torch.randn(4 * 128, 256, generator=gen)).to("cuda", torch.bfloat16)
+    dy = (torch.randn(4 * 128, 256, generator=gen)).to("cuda", torch.bfloat16)
+    res = {}
+    for flag in (False, True):
+        monkeypatch.setattr(U, "ATTN_CUDNN", flag)
+        saved = [torch.zeros(s.shape, dtype=s.dtype, device="cuda") for s in u.saved_specs(4)]
+        grads = [torch.zeros(p.shape, dtype=torch.float32, device="cuda") for p in params]
+        y = u.forward(x, params, saved)
+        dx = u.backward(dy, params, saved, grads)
+        res[flag] = [y.float(), dx.float()] + grads
+    for a, b in zip(res[False], res[True]):
+        assert ((a - b).norm() / b.norm()).item() <= 2e-2
