@@ -422,6 +422,14 @@ int krt_bn_backward_elemt(const void* dy, const void* x, const float* mean, cons
  * norm).  Deterministic: the backward recompute reproduces h bitwise. */
 int krt_ln_fwd(const void* x, const void* r, void* x2, const void* gamma, const void* beta, void* h,
                float* mean, float* rstd, int64_t T, int H, float eps, void* stream);
+/* LayerNorm backward in one pass: dx = rstd * (g*dy - mean(g*dy) - xhat *
+ * mean(g*dy*xhat)) [+ addend] (bf16; the addend is the residual branch's
+ * gradient), dgamma = sum_t dy*xhat, dbeta = sum_t dy (fp32, written, in a
+ * fixed summation order).  mean/rstd: the forward's (krt_ln_fwd).  H <= 4352.
+ * ws: krt_ln_bwd_workspace bytes. */
+size_t krt_ln_bwd_workspace(int64_t T, int H);
+int krt_ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
+               const void* addend, void* dx, float* dgamma, float* dbeta, void* ws, int64_t T, int H, void* stream);
 /* dx = gelu_tanh'(f) * dy and colsum[n] = sum_t dx[t, n] (fp32, the bias
  * gradient of the layer that produced f) in one pass over the activations;
  * ws: krt_gelu_bwd_colsum_workspace bytes. */

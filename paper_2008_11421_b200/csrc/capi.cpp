@@ -605,6 +605,13 @@ int krt_ln_fwd(const void* x, const void* r, void* x2, const void* g, const void
   KRT_CUDA_GUARD(ln_fwd(x, r, x2, g, b, h, mean, rstd, T, H, eps, (cudaStream_t)stream), "ln_fwd");
 }
 
+size_t krt_ln_bwd_workspace(int64_t T, int H) { return ln_bwd_workspace(T, H); }
+
+int krt_ln_bwd(const void* dy, const void* x, const void* g, const float* mean, const float* rstd, const void* addend,
+               void* dx, float* dgamma, float* dbeta, void* ws, int64_t T, int H, void* stream) {
+  KRT_CUDA_GUARD(ln_bwd(dy, x, g, mean, rstd, addend, dx, dgamma, dbeta, ws, T, H, (cudaStream_t)stream), "ln_bwd");
+}
+
 size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N) { return gelu_bwd_colsum_workspace(T, N); }
 
 int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,

@@ -6,6 +6,11 @@
 //                     the row mean / rstd (fp32) the backward needs.  Used for
 //                     the forward and for the backward's recompute, so the
 //                     recomputed h is bitwise the forward's.
+//   ln_bwd          : LayerNorm backward in one pass over dy and x: dx (+ an
+//                     addend: the residual branch's gradient) and the
+//                     gamma / beta gradients, deterministic (fixed row ->
+//                     CTA mapping, fixed-order shared-memory column sums,
+//                     a double-precision finalize over the CTA partials).
 //   gelu_bwd_colsum : df = gelu'(f) * dg (tanh GELU) and, in the same pass,
 //                     the column sums of df (fc1's bias gradient): no second
 //                     read of the widest activation of the layer.
@@ -270,7 +275,165 @@ __global__ void __launch_bounds__(1024) colsum_finalize_kernel(const float* __re
   out[c] = (float)s;
 }
 
+// LayerNorm backward.  One warp per row, rows strided over a persistent grid;
+// the row (dy, x and the addend) is loaded packed into registers with every
+// load in flight at once (J octets per lane), the two row sums reduced by
+// shuffles, dx stored.  Each warp adds its rows' dy*xhat and dy into its own
+// fp32 column accumulators in shared memory ([2][8][H/8]: lane j owns the
+// columns of octets j, j+32, ..., so no two lanes touch a word and no
+// barrier is needed per row); at the end the CTA sums its warps in warp order
+// into one partial row pair.  Deterministic for a given grid.
+constexpr int kBwdWarps = 4;
+
+template <bool ADD, int J>
+__global__ void __launch_bounds__(32 * kBwdWarps) ln_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+    const float* __restrict__ mean, const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ addend,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ part, int64_t T, int H) {
+  extern __shared__ float stage[];  // [kBwdWarps][2][8][H / 8]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int oct = H / 8;
+  float* ag = stage + (size_t)w * 2 * H;  // this warp's sum of dy*xhat, [8][oct]
+  float* ab = ag + H;                     // and of dy
+  for (int c = lane; c < H; c += 32) ag[c] = ab[c] = 0.f;
+  const float inv_h = 1.f / (float)H;
+  for (int64_t row = (int64_t)blockIdx.x * kBwdWarps + w; row < T; row += (int64_t)gridDim.x * kBwdWarps) {
+    uint4 ud[J], ux[J], ua[ADD ? J : 1];
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const int j = lane + 32 * i;
+      if (j < oct) {
+        ud[i] = __ldcs(reinterpret_cast<const uint4*>(dy + row * H) + j);
+        ux[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * H) + j);
+        if (ADD) ua[i] = __ldcs(reinterpret_cast<const uint4*>(addend + row * H) + j);
+      }
+    }
+    const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
+    float s1 = 0.f, s2 = 0.f;  // sum g*dy, sum g*dy*xhat
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const int j = lane + 32 * i;
+      if (j < oct) {
+        float d[8], xv[8], gg[8];
+        unpack8(ud[i], d);
+        unpack8(ux[i], xv);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float xh = (xv[k] - mu) * rs;
+          const float gd = d[k] * gg[k];
+          s1 += gd;
+          s2 = __fmaf_rn(gd, xh, s2);
+          ag[k * oct + j] += d[k] * xh;
+          ab[k * oct + j] += d[k];
+        }
+      }
+    }
+    const float c1 = warp_sum(s1) * inv_h, c2 = warp_sum(s2) * inv_h;
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const int j = lane + 32 * i;
+      if (j < oct) {
+        float d[8], xv[8], gg[8], o[8];
+        unpack8(ud[i], d);
+        unpack8(ux[i], xv);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
+        if (ADD) unpack8(ua[i], o);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float xh = (xv[k] - mu) * rs;
+          const float v = rs * (d[k] * gg[k] - c1 - xh * c2);
+          o[k] = ADD ? __fadd_rn(v, o[k]) : v;
+        }
+        __stcs(reinterpret_cast<uint4*>(dx + row * H) + j, pack8(o));
+      }
+    }
+  }
+  __syncthreads();
+  // this CTA's partial row pair: its warps' accumulators added in warp order
+  for (int c = threadIdx.x; c < 2 * H; c += 32 * kBwdWarps) {
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < kBwdWarps; ++r) s += stage[(size_t)r * 2 * H + c];
+    // [2][8][oct] -> [2][H] column order
+    const int half = c / H, rem = c - half * H, k = rem / oct, j = rem - k * oct;
+    part[(size_t)blockIdx.x * 2 * H + half * H + 8 * j + k] = s;
+  }
+}
+
+// dgamma / dbeta from the CTA partial rows: part [rows][2][H] -> out_g, out_b
+__global__ void __launch_bounds__(1024) ln_bwd_finalize_kernel(const float* __restrict__ part, int rows, int H,
+                                                               float* __restrict__ out_g, float* __restrict__ out_b) {
+  __shared__ double sh[2][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double sgm = 0, sbt = 0;
+  if (c < H)
+    for (int r = w; r < rows; r += 32) {
+      sgm += (double)part[(size_t)r * 2 * H + c];
+      sbt += (double)part[(size_t)r * 2 * H + H + c];
+    }
+  sh[0][w][lane] = sgm;
+  sh[1][w][lane] = sbt;
+  __syncthreads();
+  if (w != 0 || c >= H) return;
+  sgm = sbt = 0;
+  for (int k = 0; k < 32; ++k) {
+    sgm += sh[0][k][lane];
+    sbt += sh[1][k][lane];
+  }
+  out_g[c] = (float)sgm;
+  out_b[c] = (float)sbt;
+}
+
+int ln_bwd_grid(int64_t T) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (T + kBwdWarps - 1) / kBwdWarps, cap = (int64_t)sms * 4;
+  return (int)(want < cap ? want : cap);
+}
+
+template <bool ADD, int J>
+cudaError_t launch_ln_bwd(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
+                          const void* addend, void* dx, float* part, int grid, int64_t T, int H, cudaStream_t s) {
+  const size_t smem = (size_t)kBwdWarps * 2 * H * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(ln_bwd_kernel<ADD, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  ln_bwd_kernel<ADD, J><<<grid, 32 * kBwdWarps, smem, s>>>(
+      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x),
+      static_cast<const __nv_bfloat16*>(g), mean, rstd, static_cast<const __nv_bfloat16*>(addend),
+      static_cast<__nv_bfloat16*>(dx), part, T, H);
+  return cudaGetLastError();
+}
+
+template <bool ADD>
+cudaError_t ln_bwd_dispatch(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
+                            const void* addend, void* dx, float* part, int grid, int64_t T, int H, cudaStream_t s) {
+  const int oct = H / 8;
+  if (oct <= 32 * 2) return launch_ln_bwd<ADD, 2>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+  if (oct <= 32 * 4) return launch_ln_bwd<ADD, 4>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+  if (oct <= 32 * 8) return launch_ln_bwd<ADD, 8>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+  if (oct <= 32 * 12) return launch_ln_bwd<ADD, 12>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+  return launch_ln_bwd<ADD, 17>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+}
+
 }  // namespace
+
+size_t ln_bwd_workspace(int64_t T, int H) { return (size_t)ln_bwd_grid(T) * 2 * H * sizeof(float); }
+
+cudaError_t ln_bwd(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
+                   const void* addend, void* dx, float* dgamma, float* dbeta, void* ws, int64_t T, int H,
+                   cudaStream_t s) {
+  if (T <= 0 || H <= 0 || H % 8 != 0 || H > 32 * 17 * 8) return cudaErrorInvalidValue;
+  const int grid = ln_bwd_grid(T);
+  float* part = static_cast<float*>(ws);
+  cudaError_t e = addend ? ln_bwd_dispatch<true>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s)
+                         : ln_bwd_dispatch<false>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+  if (e != cudaSuccess) return e;
+  ln_bwd_finalize_kernel<<<(H + 31) / 32, 1024, 0, s>>>(part, grid, H, dgamma, dbeta);
+  return cudaGetLastError();
+}
 
 cudaError_t ln_fwd(const void* x, const void* r, void* x2, const void* g, const void* b, void* h, float* mean,
                    float* rstd, int64_t T, int H, float eps, cudaStream_t s) {

@@ -8,6 +8,10 @@ namespace krt {
 // GPT-layer kernels (ln_kernels.cu)
 cudaError_t ln_fwd(const void* x, const void* r, void* x2, const void* g, const void* b, void* h, float* mean,
                    float* rstd, int64_t T, int H, float eps, cudaStream_t s);
+size_t ln_bwd_workspace(int64_t T, int H);
+cudaError_t ln_bwd(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
+                   const void* addend, void* dx, float* dgamma, float* dbeta, void* ws, int64_t T, int H,
+                   cudaStream_t s);
 size_t gelu_bwd_colsum_workspace(int64_t T, int N);
 cudaError_t gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,
                             cudaStream_t s);

@@ -28,6 +28,22 @@ def ln_fwd(x, g, b, eps, mean, rstd, residual=None, x2_out=None):
     return h
 
 
+def ln_bwd(dy, x, g, mean, rstd, dgamma, dbeta, addend=None):
+    """LayerNorm backward: returns dx (+ addend); dgamma/dbeta (fp32 [H])
+    written.  mean/rstd: the forward's fp32 [T]."""
+    T, H = x.shape
+    dy, x = dy.contiguous(), x.contiguous()
+    if addend is not None:
+        addend = addend.contiguous()
+    dx = torch.empty_like(x)
+    ws = torch.empty(_lib.lib().krt_ln_bwd_workspace(T, H), dtype=torch.uint8, device=x.device)
+    with _timed("ln_bwd", T * H * 2 * (4 if addend is not None else 3)):
+        _lib.check(_lib.lib().krt_ln_bwd(dy.data_ptr(), x.data_ptr(), g.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                                         _ptr(addend), dx.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
+                                         ws.data_ptr(), T, H, _stream()))
+    return dx
+
+
 def gelu_bwd_colsum(dy, f, colsum):
     """dx = gelu_tanh'(f) * dy; colsum (fp32 [N]) = column sums of dx."""
     T, N = f.shape

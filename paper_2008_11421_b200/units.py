@@ -941,12 +941,17 @@ def _ln_apply(x, g, b, mean, rstd):
     return _aten.native_layer_norm(x, [x.shape[-1]], g, b, LN_EPS)[0]
 
 
-def _ln_bw(dy, x, g, b, mean, rstd, dg, db):
+def _ln_bw(dy, x, g, b, mean, rstd, dg, db, addend=None):
+    """LayerNorm backward (+ the residual branch's gradient `addend`): the own
+    one-pass kernel for bf16 (dgamma/dbeta straight into the fp32 gradient
+    region), aten otherwise."""
+    if lnfused.supported(x) and dy.dtype == torch.bfloat16 and dg.is_contiguous() and db.is_contiguous():
+        return lnfused.ln_bwd(dy, x, g, mean.view(-1), rstd.view(-1), dg, db, addend=addend)
     dx, dgg, dbb = _aten.native_layer_norm_backward(dy, x, [x.shape[-1]], mean.view(-1, 1), rstd.view(-1, 1),
                                                     g, b, [True, True, True])
     dg.copy_(dgg)
     db.copy_(dbb)
-    return dx
+    return dx if addend is None else dx + addend
 
 
 def _gemm_cost(m, n, k, es=2):
@@ -1170,7 +1175,7 @@ class TransformerLayerUnit(Unit):
         h2 = _ln_apply(x2, g2, b2, m2, r2)
         dh2 = _linear_bw(df1, h2, w1, grads[8], gb1)
         del df1, h2
-        dx2 = dy + _ln_bw(dh2, x2, g2, b2, m2, r2, grads[6], grads[7])
+        dx2 = _ln_bw(dh2, x2, g2, b2, m2, r2, grads[6], grads[7], addend=dy)
         del dh2
         do = _linear_bw(dx2, o, wo, grads[4], grads[5])
         dqkv = self._attn_bw(do, qkv, o, saved[6] if self._flash() else None)
@@ -1178,7 +1183,7 @@ class TransformerLayerUnit(Unit):
         h1 = _ln_apply(x, g1, b1, m1, r1)
         dh1 = _linear_bw(dqkv, h1, wqkv, grads[2], grads[3])
         del dqkv, h1
-        return dx2 + _ln_bw(dh1, x, g1, b1, m1, r1, grads[0], grads[1])
+        return _ln_bw(dh1, x, g1, b1, m1, r1, grads[0], grads[1], addend=dx2)
 
     def fwd_flops(self, n):
         t = n * self.s

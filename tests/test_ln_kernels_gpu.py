@@ -46,3 +46,29 @@ def test_gelu_bwd_colsum(T, N):
     torch.testing.assert_close(cs, dx.float().sum(0), rtol=1e-4, atol=1e-3)
     cs2 = torch.empty_like(cs)
     assert torch.equal(lnfused.gelu_bwd_colsum(dy, f, cs2), dx) and torch.equal(cs2, cs)
+
+
+@pytest.mark.parametrize("T,H", [(1000, 1920), (257, 3072), (9, 4256), (33, 64), (600, 1024)])
+@pytest.mark.parametrize("add", [False, True])
+def test_ln_bwd(T, H, add):
+    """One-pass LayerNorm backward vs fp32 autograd of layer_norm on the same
+    bf16 input: dx (+ the residual gradient) at bf16 resolution, dgamma and
+    dbeta (fp32, fixed-order sums) at fp32-reduction tolerance; bitwise
+    repeatable."""
+    x, dy, a = rand((T, H), 11, 2.0), rand((T, H), 12), rand((T, H), 13)
+    g, b = rand((H,), 14, 0.2) + 1, rand((H,), 15, 0.1)
+    m, s = torch.empty(T, device="cuda"), torch.empty(T, device="cuda")
+    lnfused.ln_fwd(x, g, b, 1e-5, m, s)
+    dg, db = torch.empty(H, device="cuda"), torch.empty(H, device="cuda")
+    dx = lnfused.ln_bwd(dy, x, g, m, s, dg, db, addend=a if add else None)
+    xf = x.float().requires_grad_(True)
+    gf = g.float().requires_grad_(True)
+    bf = b.float().requires_grad_(True)
+    F.layer_norm(xf, [H], gf, bf, 1e-5).backward(dy.float())
+    ref = xf.grad + (a.float() if add else 0)
+    torch.testing.assert_close(dx.float(), ref, **BF16_TOL)
+    torch.testing.assert_close(dg, gf.grad, rtol=2e-3, atol=2e-3)
+    torch.testing.assert_close(db, bf.grad, rtol=1e-4, atol=1e-3)
+    dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+    dx2 = lnfused.ln_bwd(dy, x, g, m, s, dg2, db2, addend=a if add else None)
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
