@@ -106,10 +106,11 @@ constexpr int kBStatBytes = 32 * 1024;
 template <int BN, int BKT>
 constexpr int kBSlots = kBStatBytes / (BN * BKT * 2) > 0 ? kBStatBytes / (BN * BKT * 2) : 1;
 
-template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT, bool BSTAT = false>
+template <int BN, int STAGES, bool PRO, bool ASTAT, int EPI, int BKT, bool BSTAT = false, bool PAIR = false>
 struct Smem {
   alignas(1024) uint8_t a[ASTAT ? kAstatSlots : STAGES][kBM * BKT * 2];
-  alignas(1024) uint8_t b[BSTAT ? kBSlots<BN, BKT> : STAGES][BN * BKT * 2];
+  // CTA pair: each CTA holds half of the n-tile's B rows
+  alignas(1024) uint8_t b[BSTAT ? kBSlots<BN, BKT> : STAGES][(PAIR ? BN / 2 : BN) * BKT * 2];
   uint64_t full[STAGES], ready[STAGES], empty[STAGES];
   uint64_t bfull;
   uint64_t tfull[4], tempty[4];
@@ -131,8 +132,14 @@ struct Smem {
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C,
 // 3 C = acc + residual (p.res through map_x)
+// PAIR: CTA pair (cluster of 2, tcgen05 cta_group::2).  A pair tile is 256
+// rows x BN columns: each CTA loads its own 128 A rows and half of the B rows,
+// the leader (rank 0) issues M = 256 MMAs that write 128 accumulator rows into
+// each CTA's TMEM, and each CTA drains its own rows.  Per CTA, B bytes per
+// k-block halve, so the ring is deeper and the operand traffic per MMA flop
+// drops by a quarter (BN = 128) to a third (BN = 256).
 template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER = false, bool BSTAT = false,
-          bool IM2A = false>
+          bool IM2A = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_b,
                                                               const __grid_constant__ CUtensorMap map_c,
@@ -142,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   // address space (an integer round-up made them generic LD.E/ST.E)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   static_assert(!BSTAT || !ASTAT, "B-stationary needs a fixed n-tile");
-  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>*>(smem_raw);
+  auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT, PAIR>*>(smem_raw);
+  static_assert(!PAIR || (!ASTAT && !GATHER && !BSTAT && BKT == kBK && EPI != 3), "pair: streamed 64-wide k-blocks");
   static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
   static_assert(!IM2A || (!GATHER && !ASTAT && BKT == kBK), "im2col A: 64-channel k-blocks, streamed");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
@@ -159,21 +167,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   static_assert(EPI != 2 || kAcc == 2, "EPI 2 x tiles are double-buffered with the accumulators");
   // this CTA's tiles: m-tiles strided; either a fixed n-tile (grid is a
   // multiple of n_tiles) or, A-stationary, every n-tile of each m-tile
+  // (pair: m-tiles are 256-row pair tiles, scheduled per cluster)
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int cta = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x, ncta = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nts = ASTAT ? p.n_tiles : 1;
-  const int n_fixed = ASTAT ? 0 : blockIdx.x % p.n_tiles;
-  const int m_first = ASTAT ? blockIdx.x : blockIdx.x / p.n_tiles;
-  const int m_step = ASTAT ? gridDim.x : gridDim.x / p.n_tiles;
+  const int n_fixed = ASTAT ? 0 : cta % p.n_tiles;
+  const int m_first = ASTAT ? cta : cta / p.n_tiles;
+  const int m_step = ASTAT ? ncta : ncta / p.n_tiles;
+  // first A / C row of this CTA in m-tile mt
+  auto rowbase = [&](int mt) -> int64_t { return PAIR ? (int64_t)mt * (2 * kBM) + rank * kBM : (int64_t)mt * kBM; };
+  constexpr int kBRows = PAIR ? BN / 2 : BN;  // B rows per CTA
+  // accumulator-drained barrier: per thread (single CTA) or per warp from both CTAs (pair)
+  constexpr uint32_t kTemptyCount = PAIR ? 2 * 4 * kEpiParts : 128 * kEpiParts;
 
   if (threadIdx.x == 0) {
     mbar_init(&S.bfull, 1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.ready[s], kXfThreads);
+      mbar_init(&S.ready[s], PAIR ? 2 * kXfThreads / 32 : kXfThreads);  // pair: one arrival per warp
       mbar_init(&S.empty[s], 1);
     }
     for (int i = 0; i < 4; ++i) {  // accumulators; x / residual buffers (<= 4 each)
       mbar_init(&S.tfull[i], 1);
-      mbar_init(&S.tempty[i], 128 * kEpiParts);  // one tile group's epilogue threads
+      mbar_init(&S.tempty[i], kTemptyCount);  // one tile group's epilogue threads / warps
       mbar_init(&S.x_full[i], 1);
       mbar_init(&S.x_empty[i], 128 * kEpiParts);
     }
@@ -184,9 +200,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(&S.tmem_base, kAcc * BN);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair(&S.tmem_base, kAcc * BN);
+    else tmem_alloc(&S.tmem_base, kAcc * BN);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       for (int mt = m_first; mt < p.m_tiles; mt += m_step) {
         int a_n = 0, a_ih0 = 0, a_iw0 = 0;  // im2col: window origin of the m-tile's first pixel
         if (IM2A) {
-          const int64_t pix = (int64_t)mt * kBM, plane = (int64_t)p.gho * p.gwo;
+          const int64_t pix = rowbase(mt), plane = (int64_t)p.gho * p.gwo;
           a_n = (int)(pix / plane);
           const int rem = (int)(pix - (int64_t)a_n * plane), oh = rem / p.gwo;
           a_ih0 = oh * p.gs - p.gp;
@@ -223,8 +243,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             if (ASTAT || GATHER) {  // A is resident / gathered by the transform warps
               // (gathered A with B stationary: an empty arrival = "slot free")
               mbar_expect_tx(&S.full[stage], BSTAT ? 0 : BN * BKT * 2);
+            } else if (PAIR && !PRO) {
+              // both CTAs' loads complete on the leader's barrier, which the
+              // leader alone arms with the pair's bytes (its MMA waits there)
+              if (rank == 0) mbar_expect_tx(&S.full[stage], 2 * (kBM + kBRows) * BKT * 2);
+              const uint32_t fb = mapa_rank(&S.full[stage], 0);
+              if (IM2A) {
+                const int tap = kb / cblocks, c0 = (kb - tap * cblocks) * BKT;
+                tma_load_im2col_4d_pair(&map_a, fb, S.a[stage], c0, a_iw0, a_ih0, a_n, (uint16_t)(tap % p.gk),
+                                        (uint16_t)(tap / p.gk));
+              } else {
+                tma_load_2d_pair(&map_a, fb, S.a[stage], kb * BKT, (int)rowbase(mt));
+              }
+              tma_load_2d_pair(&map_b, fb, S.b[stage], kb * BKT, n_tile * BN + (int)rank * kBRows);
             } else {
-              mbar_expect_tx(&S.full[stage], (kBM + (BSTAT ? 0 : BN)) * BKT * 2);
+              mbar_expect_tx(&S.full[stage], (kBM + (BSTAT ? 0 : kBRows)) * BKT * 2);
               if (IM2A) {
                 // k-block kb = (tap, 64-channel block): one im2col box of the
                 // m-tile's 128 output pixels at filter offset (kh, kw)
@@ -232,10 +265,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
                 tma_load_im2col_4d(&map_a, &S.full[stage], S.a[stage], c0, a_iw0, a_ih0, a_n, (uint16_t)(tap % p.gk),
                                    (uint16_t)(tap / p.gk));
               } else {
-                tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, mt * kBM);
+                tma_load_2d(&map_a, &S.full[stage], S.a[stage], kb * BKT, (int)rowbase(mt));
               }
+              // (pair with a prologue: each CTA's transform warps wait on its own barrier)
+              if (!BSTAT) tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN + (int)rank * kBRows);
             }
-            if (!BSTAT) tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN);
+            if (!BSTAT && (ASTAT || GATHER)) tma_load_2d(&map_b, &S.full[stage], S.b[stage], kb * BKT, n_tile * BN);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -243,34 +278,56 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           }
         }
       }
+      if (PAIR) {  // every commit of the leader's MMAs has arrived here before the CTA may exit
+        for (int i = 0; i < STAGES; ++i) {
+          mbar_wait(&S.empty[stage], phase ^ 1);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = instr_desc(BN);
+    // (pair: the leader's; the peer's MMA warp only allocated TMEM)
+    constexpr uint32_t idesc = PAIR ? instr_desc_pair(BN) : instr_desc(BN);
     if (BSTAT) mbar_wait(&S.bfull, 0);
+    if (!PAIR || rank == 0) {
     int stage = 0, ag0 = 0;  // ag0: sequence number of this m-tile's first A k-block
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int mt = m_first; mt < p.m_tiles; mt += m_step, ag0 += kblocks) {
       for (int nt = 0; nt < nts; ++nt) {
-        mbar_wait(&S.tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
+        if (PAIR) mbar_wait_cluster(&S.tempty[acc], acc_phase ^ 1);  // both CTAs' epilogues drained it
+        else mbar_wait(&S.tempty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
           const int ag = ag0 + kb, sl = ag % kAstatSlots;
           if (ASTAT && nt == 0) mbar_wait(&S.a_ready[sl], (uint32_t)(ag / kAstatSlots) & 1u);  // landed + transformed
-          if ((PRO || GATHER) && !ASTAT) mbar_wait(&S.ready[stage], phase);  // transformed / gathered
+          if (PAIR && PRO) mbar_wait_cluster(&S.ready[stage], phase);  // both CTAs' A transformed
+          else if ((PRO || GATHER) && !ASTAT) mbar_wait(&S.ready[stage], phase);  // transformed / gathered
           else mbar_wait(&S.full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[BSTAT ? kb : stage]);
+            if (PAIR) {
+#pragma unroll
+              for (int k = 0; k < BKT / kUmmaK; ++k)
+                umma_bf16_pair(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
+                               idesc, (kb | k) != 0);
+              umma_commit_pair(&S.empty[stage]);                       // both CTAs' stage free
+              if (kb == kblocks - 1) umma_commit_pair(&S.tfull[acc]);  // both CTAs' accumulator rows complete
+            } else {
 #pragma unroll
             for (int k = 0; k < BKT / kUmmaK; ++k)
               umma_bf16(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
                         idesc, (kb | k) != 0);
             umma_commit(&S.empty[stage]);                       // smem stage free when these MMAs finish
             if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
+            }
             if (ASTAT && nt == nts - 1) umma_commit(&S.a_free[sl]);  // A slot no longer read
           }
           __syncwarp();
@@ -284,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           acc_phase ^= 1;
         }
       }
+    }
     }
   } else if (warp == kXWarp) {
     // ------------------------------------------------ x / residual tile producer
@@ -300,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           mbar_expect_tx(&S.x_full[xb], kBM * BN * 2);
 #pragma unroll
           for (int b = 0; b < BN / kW; ++b)
-            tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb] + b * kBM * kW * 2, n_tile * BN + b * kW, mt * kBM);
+            tma_load_2d(&map_x, &S.x_full[xb], S.xt[xb] + b * kBM * kW * 2, n_tile * BN + b * kW, (int)rowbase(mt));
           if (++xb == kXB) {
             xb = 0;
             xphase ^= 1;
@@ -500,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         bool rvalid = true;
         int ih0 = 0, iw0 = 0;
         if (IM2A) {
-          const int64_t pix = (int64_t)mt * kBM + r, plane = (int64_t)p.gho * p.gwo;
+          const int64_t pix = rowbase(mt) + r, plane = (int64_t)p.gho * p.gwo;
           rvalid = pix < p.M;
           const int n = (int)(pix / plane), rem = (int)(pix - (int64_t)n * plane), oh = rem / p.gwo;
           ih0 = oh * p.gs - p.gp;
@@ -559,7 +617,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             mbar_arrive(&S.a_ready[sl]);
             ++ag;
           } else {
-            mbar_arrive(&S.ready[stage]);
+            if (PAIR) {  // one release per warp on the leader's barrier (its MMAs read this tile)
+              __syncwarp();
+              if (lane == 0) mbar_arrive_rank(&S.ready[stage], 0);
+            } else {
+              mbar_arrive(&S.ready[stage]);
+            }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -585,7 +648,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // fire-and-forget reductions (no load latency in the epilogue; no
     // dynamically indexed local arrays)
     constexpr bool kStats = EPI == 1 || EPI == 2;
-    float* part_row = kStats ? p.part + (((size_t)m_first * 4 + q) * kEpiGroups + grp) * 2 * p.N : nullptr;
+    const int mgroup = PAIR ? 2 * m_first + (int)rank : m_first;  // partial-row group of this CTA
+    float* part_row = kStats ? p.part + (((size_t)mgroup * 4 + q) * kEpiGroups + grp) * 2 * p.N : nullptr;
     if (ASTAT && kStats) {
       for (int nt = 0; nt < nts; ++nt)
 #pragma unroll
@@ -606,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       const int acc = t % kAcc;
       const uint32_t acc_phase = (uint32_t)(t / kAcc) & 1u;
       const int n_tile = ASTAT ? nt : n_fixed;
-      const int64_t row0 = (int64_t)mt * kBM + q * 32;
+      const int64_t row0 = rowbase(mt) + q * 32;
       const bool valid = row0 + lane < p.M;
       const int rb = EPI == 3 ? t % kResBufs<BN> : 0;  // residual buffer of this tile
       mbar_wait(&S.tfull[acc], acc_phase);
@@ -730,7 +794,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         if (!ASTAT) sbuf ^= 1;
       }
       tc_fence_before();
-      mbar_arrive(&S.tempty[acc]);
+      if (PAIR) {  // one arrival per warp, on the leader's barrier
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(&S.tempty[acc]);
+          else mbar_arrive_rank(&S.tempty[acc], 0);
+        }
+      } else {
+        mbar_arrive(&S.tempty[acc]);
+      }
       if (EPI == 2) mbar_arrive(&S.x_empty[acc]);
       if (EPI == 3) mbar_arrive(&S.x_empty[rb]);
      }
@@ -749,8 +821,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, kAcc * BN);
+  if (PAIR) {
+    cluster_sync();  // neither CTA leaves while the peer may still touch its barriers or TMEM
+    if (warp == 1) tmem_dealloc_pair(tmem, kAcc * BN);
+  } else {
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, kAcc * BN);
+  }
 }
 
 // per-channel mean / invstd from the partial rows: CTA = 32 channels, 32 warps
@@ -838,42 +915,76 @@ __global__ void __launch_bounds__(1024) partials_bwd_finalize_kernel(
 // ---------------------------------------------------------------------------
 // host side
 
-template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool BSTAT, bool IM2A>
+template <int BN, int STAGES, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool BSTAT, bool IM2A, bool PAIR>
 cudaError_t launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
                    const Params& p, int grid, cudaStream_t s) {
-  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER, BSTAT, IM2A>;
-  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT>);
+  auto k = conv1x1_kernel<BN, STAGES, PRO, EPI, ASTAT, BKT, GATHER, BSTAT, IM2A, PAIR>;
+  const size_t smem = sizeof(Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT, PAIR>);
   static bool configured = false;  // per instantiation
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  if (PAIR) {  // clusters of two CTAs on one TPC
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, ma, mb, mc, mx, p);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   k<<<grid, kThreads, smem, s>>>(ma, mb, mc, mx, p);
   return cudaGetLastError();
 }
 
-template <int BN, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool bstat, bool IM2A = false>
+template <int BN, bool PRO, int EPI, bool ASTAT, int BKT, bool GATHER, bool bstat, bool IM2A = false, bool PAIR = false>
 cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                           const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   // deepest ring that fits next to everything else (227 KB per CTA)
   constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * (ASTAT ? 1 : 2) * 32 * 64 +
                         (ASTAT ? kAstatSlots * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
                         (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? kBSlots<BN, BKT> * BN * BKT * 2 : 0);
-  constexpr int stage_bytes = (ASTAT ? BN : kBM + (bstat ? 0 : BN)) * BKT * 2;
+  constexpr int stage_bytes = (ASTAT ? BN : kBM + (bstat ? 0 : (PAIR ? BN / 2 : BN))) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
   constexpr int stages = avail / stage_bytes > max_stages ? max_stages : avail / stage_bytes;
   static_assert(stages >= 2, "shared memory");
-  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER, bstat, IM2A>(ma, mb, mc, mx, p, grid, s);
+  return launch<BN, stages, PRO, EPI, ASTAT, BKT, GATHER, bstat, IM2A, PAIR>(ma, mb, mc, mx, p, grid, s);
+}
+
+// CTA-pair instantiations: streamed A and B, 64-wide k-blocks
+template <int BN, bool PRO, int EPI, bool IM2A>
+cudaError_t dispatch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
+                          const Params& p, int grid, cudaStream_t s) {
+  return dispatch_ring<BN, PRO, EPI, false, kBK, false, false, IM2A, true>(ma, mb, mc, mx, p, grid, s);
 }
 
 // im2col A (3x3 / strided convolutions): streamed 64-channel k-blocks, B too
 // wide to stay resident
 template <int BN, bool PRO, int EPI>
 cudaError_t dispatch_im2col(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
-                            const Params& p, int grid, cudaStream_t s) {
+                            const Params& p, int grid, bool pair, cudaStream_t s) {
+  if (pair) return dispatch_pair<BN, PRO, EPI, true>(ma, mb, mc, mx, p, grid, s);
   return dispatch_ring<BN, PRO, EPI, false, kBK, false, false, true>(ma, mb, mc, mx, p, grid, s);
+}
+
+// CTA pairs for streamed GEMMs (KRT_GEMM_PAIR=0 turns them off)
+bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("KRT_GEMM_PAIR");
+    return e == nullptr || std::strcmp(e, "0") != 0;
+  }();
+  return on;
 }
 
 template <int BN, bool PRO, int EPI, bool ASTAT, int BKT = kBK, bool GATHER = false>
@@ -971,13 +1082,20 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   const bool pro = pmean != nullptr, st = part != nullptr;
   // A-stationary when the prologue would otherwise transform the same A tile once per n-tile
   const bool astat = pro && !res_mode && bkt == kBK && p.n_tiles > 1 && K <= kMaxAstatK && p.n_tiles <= kMaxNT;
+  // CTA pairs for the streamed 64-wide k-block path at 256-column n-tiles with
+  // K >= 256 (measured, scripts/bench_gemm_pair.py: 2-8% faster there, up to
+  // 16% slower at K = 128 where the epilogue, not the operand ring, bounds it)
+  const bool pair = pair_enabled() && !astat && !res_mode && bkt == kBK && BN == 256 && K >= 256;
+  if (pair) p.m_tiles = (int)((M + 2 * kBM - 1) / (2 * kBM));
   // whole n-tile groups (or, A-stationary, whole m-tiles), at most one CTA per SM
-  int per = astat ? num_sms() : num_sms() / p.n_tiles;
+  const int units = pair ? num_sms() / 2 : num_sms();  // CTAs or CTA pairs
+  int per = astat ? units : units / p.n_tiles;
   if (per < 1) per = 1;
   if (per > p.m_tiles) per = p.m_tiles;
-  const int grid = astat ? per : per * p.n_tiles;
+  const int grid = (astat ? per : per * p.n_tiles) * (pair ? 2 : 1);
   const int epi_groups = 4 / (BN >= 128 ? 4 : (BN >= 64 ? BN / 32 : 1));
-  if (part_rows) *part_rows = per * 4 * epi_groups;  // every row and column written exactly once
+  if (part_rows) *part_rows = per * (pair ? 2 : 1) * 4 * epi_groups;  // every row and column written exactly once
+  if (pair && !make_map(&mb, B, N, K, BN / 2, bkt, ksw)) return cudaErrorInvalidValue;  // half the n-tile per CTA
   if (res_mode) {
     if (bkt == 16) return dispatch_res<16>(BN, pro, ma, mb, mc, mx, p, grid, s);
     if (bkt == 32) return dispatch_res<32>(BN, pro, ma, mb, mc, mx, p, grid, s);
@@ -1012,12 +1130,18 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
     return cudaErrorInvalidValue;
   }
   if (bwd) {
-    if (BN == 64) return dispatch_stages<64, false, 2, false>(ma, mb, mc, mx, p, grid, s);
-    if (BN == 128) return dispatch_stages<128, false, 2, false>(ma, mb, mc, mx, p, grid, s);
+    if (BN == 64) return pair ? dispatch_pair<64, false, 2, false>(ma, mb, mc, mx, p, grid, s)
+                              : dispatch_stages<64, false, 2, false>(ma, mb, mc, mx, p, grid, s);
+    if (BN == 128) return pair ? dispatch_pair<128, false, 2, false>(ma, mb, mc, mx, p, grid, s)
+                               : dispatch_stages<128, false, 2, false>(ma, mb, mc, mx, p, grid, s);
     return cudaErrorInvalidValue;
   }
 #define KRT_GEMM_BN(BNV)                                                                          \
   if (BN == BNV) {                                                                                \
+    if (pair && pro && st) return dispatch_pair<BNV, true, 1, false>(ma, mb, mc, mx, p, grid, s); \
+    if (pair && pro) return dispatch_pair<BNV, true, 0, false>(ma, mb, mc, mx, p, grid, s);       \
+    if (pair && st) return dispatch_pair<BNV, false, 1, false>(ma, mb, mc, mx, p, grid, s);       \
+    if (pair) return dispatch_pair<BNV, false, 0, false>(ma, mb, mc, mx, p, grid, s);             \
     if (astat && st) return dispatch_stages<BNV, true, 1, true>(ma, mb, mc, mx, p, grid, s);     \
     if (astat) return dispatch_stages<BNV, true, 0, true>(ma, mb, mc, mx, p, grid, s);           \
     if (pro && st) return dispatch_stages<BNV, true, 1, false>(ma, mb, mc, mx, p, grid, s);      \
@@ -1192,9 +1316,11 @@ cudaError_t conv_im2col_fprop(const void* x, const void* wk, void* C, int n, int
   p.gk = k;
   p.gs = stride;
   p.gp = pad;
+  const bool pair = pair_enabled();
+  if (pair) p.m_tiles = (int)((M + 2 * kBM - 1) / (2 * kBM));
   CUtensorMap ma, mb, mc, mx;
   if (!make_im2col_map(&ma, x, n, h, w, cin, k, stride, pad, kBM) ||
-      !make_map(&mb, wk, N, K, BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mb, wk, N, K, pair ? BN / 2 : BN, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&mc, C, M, N, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
   if (bwd) {
@@ -1202,22 +1328,22 @@ cudaError_t conv_im2col_fprop(const void* x, const void* wk, void* C, int n, int
   } else {
     mx = mc;
   }
-  int per = num_sms() / p.n_tiles;
+  int per = (pair ? num_sms() / 2 : num_sms()) / p.n_tiles;
   if (per < 1) per = 1;
   if (per > p.m_tiles) per = p.m_tiles;
-  const int grid = per * p.n_tiles;
+  const int grid = per * p.n_tiles * (pair ? 2 : 1);
   const int epi_groups = 4 / (BN >= 128 ? 4 : BN / 32);
-  if (part_rows) *part_rows = per * 4 * epi_groups;
+  if (part_rows) *part_rows = per * (pair ? 2 : 1) * 4 * epi_groups;
   if (bwd) {
-    if (BN == 64) return dispatch_im2col<64, false, 2>(ma, mb, mc, mx, p, grid, s);
-    return dispatch_im2col<128, false, 2>(ma, mb, mc, mx, p, grid, s);
+    if (BN == 64) return dispatch_im2col<64, false, 2>(ma, mb, mc, mx, p, grid, pair, s);
+    return dispatch_im2col<128, false, 2>(ma, mb, mc, mx, p, grid, pair, s);
   }
-#define KRT_IM2COL_BN(BNV)                                                      \
-  if (BN == BNV) {                                                              \
-    if (pro && st) return dispatch_im2col<BNV, true, 1>(ma, mb, mc, mx, p, grid, s); \
-    if (pro) return dispatch_im2col<BNV, true, 0>(ma, mb, mc, mx, p, grid, s);       \
-    if (st) return dispatch_im2col<BNV, false, 1>(ma, mb, mc, mx, p, grid, s);       \
-    return dispatch_im2col<BNV, false, 0>(ma, mb, mc, mx, p, grid, s);              \
+#define KRT_IM2COL_BN(BNV)                                                            \
+  if (BN == BNV) {                                                                    \
+    if (pro && st) return dispatch_im2col<BNV, true, 1>(ma, mb, mc, mx, p, grid, pair, s); \
+    if (pro) return dispatch_im2col<BNV, true, 0>(ma, mb, mc, mx, p, grid, pair, s);       \
+    if (st) return dispatch_im2col<BNV, false, 1>(ma, mb, mc, mx, p, grid, pair, s);       \
+    return dispatch_im2col<BNV, false, 0>(ma, mb, mc, mx, p, grid, pair, s);              \
   }
   KRT_IM2COL_BN(64)
   KRT_IM2COL_BN(128)

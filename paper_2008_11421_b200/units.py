@@ -104,6 +104,14 @@ TC_DGRAD_PREACT = os.environ.get("KRT_TC_DGRAD_PREACT", "1") != "0"
 # kernel (3643-3655 vs 3685-3689 samples/s, same box, with the x tile
 # TMA-prefetched); KRT_TC_DGRAD=1 selects it
 TC_DGRAD = os.environ.get("KRT_TC_DGRAD", "0") == "1"
+# bottleneck weight gradients on the own tcgen05 wgrad GEMM (csrc/wgrad_sm100.cu)
+# where it measured faster than cuDNN (scripts/bench_conv3_bwd.py, b1024,
+# profiles/round2_conv3_bwd_b1024.log): conv3's wgrad with relu(bn2(c2))
+# applied in shared memory at the 64/128-wide stages (a2 is never
+# materialised; with conv3's dgrad + BN2 reduce also own at width 64: 1.083 ->
+# 0.932 ms; width 128: 0.585 -> 0.532 ms), and conv1's wgrad at width 256
+# (0.121 -> 0.113 ms).  KRT_TC_WGRAD=0: cuDNN for all of them
+TC_WGRAD = os.environ.get("KRT_TC_WGRAD", "1") != "0"
 
 
 def _cl(t):
@@ -153,14 +161,14 @@ def _conv_into(x, w, stride, pad, out=None):
     return out
 
 
-def _conv_bw(dy, x, w, stride, pad, need_dx=True):
-    # bytes: dy and x read, dw written (+ w read and dx written for the dgrad)
+def _conv_bw(dy, x, w, stride, pad, need_dx=True, need_dw=True):
+    # bytes: dy read; wgrad: x read, dw written; dgrad: w read, dx written
     es = dy.element_size()
-    nb = (dy.numel() + x.numel() + w.numel()) * es + (w.numel() + x.numel()) * es * need_dx
-    fl = 2.0 * dy.numel() * (w.numel() // w.shape[0]) * (2 if need_dx else 1)
+    nb = dy.numel() * es + (x.numel() + w.numel()) * es * need_dw + (w.numel() + x.numel()) * es * need_dx
+    fl = 2.0 * dy.numel() * (w.numel() // w.shape[0]) * (int(need_dx) + int(need_dw))
     with bnfused._timed("cudnn_conv_bwd", nb, fl):
         return _aten.convolution_backward(dy, x, w, None, [stride, stride], [pad, pad], [1, 1], False,
-                                          [0, 0], 1, [need_dx, True, False])
+                                          [0, 0], 1, [need_dx, need_dw, False])
 
 
 def _bn_fw(c, g, b):
@@ -387,6 +395,21 @@ class BottleneckUnit(_ConvNetUnit):
             dz, dc3 = bnfused.add_relu_backward(dy, c3, st[4], st[5], g3, b3, x, dgamma=grads[7],
                                                 dbeta=grads[8], dy2=dy2)
         del dy, dy2
+        if self._own_wgrad3():
+            # conv3's weight gradient on the tcgen05 wgrad GEMM, relu(bn2(c2))
+            # applied in shared memory (a2 never materialised)
+            bnfused.conv_wgrad(dc3, c2, grads[6].view(-1), 1, 1, 0, pre=(st[2], st[3], g2, b2))
+            if self.w == 64 and bnfused.conv1x1_dgrad_supported(self.cout, self.w):
+                # its data gradient with BN2's backward reduce in the epilogue
+                dc2 = bnfused.conv1x1_dgrad_bn_backward(dc3, _cl(w3), c2, st[2], st[3], g2, b2,
+                                                        dgamma=grads[4], dbeta=grads[5])
+            else:
+                da2, _, _ = _conv_bw(dc3, c2, _cl(w3), 1, 0, need_dw=False)
+                dc2 = bnfused.backward(da2, c2, st[2], st[3], g2, b2, relu=True, dgamma=grads[4],
+                                       dbeta=grads[5])
+                del da2
+            del dc3
+            return self._backward_tail(dz, params, saved, grads, c1, st, dc2)
         a2 = bnfused.apply(c2, st[2], st[3], g2, b2, relu=True)
         if self._tc1x1() and TC_DGRAD:
             # conv3 dgrad on the tcgen05 GEMM with BN2's backward reduce in its
@@ -403,16 +426,33 @@ class BottleneckUnit(_ConvNetUnit):
             _cl(grads[6]).copy_(dw3)
             dc2 = bnfused.backward(da2, c2, st[2], st[3], g2, b2, relu=True, dgamma=grads[4], dbeta=grads[5])
             del da2
+        return self._backward_tail(dz, params, saved, grads, c1, st, dc2)
+
+    def _own_wgrad3(self):
+        return (self._tc1x1() and TC_WGRAD and self.w in (64, 128)
+                and bnfused.conv_wgrad_supported(self.cout, self.w, 1, 1, pre=True))
+
+    def _backward_tail(self, dz, params, saved, grads, c1, st, dc2):
+        """conv2 / BN1 / conv1 (and the downsample branch) backward from dc2."""
+        w1, g1, b1, w2 = params[:4]
+        x = _cl(saved[0])
         a1 = bnfused.apply(c1, st[0], st[1], g1, b1, relu=True)
         da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
         del dc2, a1
         _cl(grads[3]).copy_(dw2)
         dc1 = bnfused.backward(da1, c1, st[0], st[1], g1, b1, relu=True, dgamma=grads[1], dbeta=grads[2])
         del da1
-        dx, dw1, _ = _conv_bw(dc1, x, _cl(w1), 1, 0)
+        if TC_WGRAD and self._tc1x1() and self.w == 256 and bnfused.conv_wgrad_supported(self.w, self.cin, 1, 1):
+            # conv1's weight gradient on the tcgen05 wgrad GEMM (x is the unit input)
+            bnfused.conv_wgrad(dc1, x, grads[0].view(-1), 1, 1, 0)
+            dx, _, _ = _conv_bw(dc1, x, _cl(w1), 1, 0, need_dw=False)
+        else:
+            dx, dw1, _ = _conv_bw(dc1, x, _cl(w1), 1, 0)
+            _cl(grads[0]).copy_(dw1)
         del dc1
-        _cl(grads[0]).copy_(dw1)
         if self.down:
+            wd, gd, bd = params[9:12]
+            cd = _cl(saved[4])
             dcd = bnfused.backward(dz, cd, st[6], st[7], gd, bd, relu=False, dgamma=grads[10],
                                    dbeta=grads[11])
             dxd, dwd, _ = _conv_bw(dcd, x, _cl(wd), self.s, 0)
