@@ -572,11 +572,14 @@ def run_gpu(args, rec):
     fam = {}
     for kind, nbytes, a, b, flops in prof or []:
         t = a.elapsed_time(b) * 1e-3
-        f = fam.setdefault(kind, [0, 0.0, 0, 0.0])
+        f = fam.setdefault(kind, [0, 0.0, 0, 0.0, 0.0])
         f[0] += nbytes
         f[1] += t
         f[2] += 1
         f[3] += flops
+        # this launch's own roofline time: the slower of its bytes at HBM
+        # bandwidth and its flops at the dense bf16 peak
+        f[4] += max(nbytes / (pk["hbm_gbs"] * 1e9), flops / (pk["bf16_tflops"] * 1e12))
     kernels = {}
     for k, v in fam.items():
         if v[1] <= 0:
@@ -586,6 +589,9 @@ def run_gpu(args, rec):
         if v[3] > 0:   # tensor-core family: also against the dense bf16 peak
             kernels[k]["achieved_TFLOPs"] = v[3] / v[1] / 1e12
             kernels[k]["frac_of_tensor"] = v[3] / v[1] / 1e12 / pk["bf16_tflops"]
+            # mixed HBM- and tensor-bound launches: sum of per-launch roofline
+            # times (max of the two bounds) over the measured time
+            kernels[k]["frac_of_roofline"] = v[4] / v[1]
     # library calls (cuDNN, cuBLAS, aten flash attention) are timed for the step
     # accounting only; the roofline and the launch count are our kernels'
     lib_fam = ("cudnn_", "cublas_", "flash_attn")

@@ -35,6 +35,7 @@
 #include <mutex>
 
 #include "gemm_sm100.hpp"
+#include "halo_sm100.hpp"
 #include "sm100_common.cuh"
 
 namespace krt {
@@ -311,26 +312,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
           else if ((PRO || GATHER) && !ASTAT) mbar_wait(&S.ready[stage], phase);  // transformed / gathered
           else mbar_wait(&S.full[stage], phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t a0 = smem_u32(ASTAT ? S.a[sl] : S.a[stage]), b0 = smem_u32(S.b[BSTAT ? kb : stage]);
-            if (PAIR) {
+          {
+            // converged warp, one lane elected inside each tcgen05 asm;
+            // descriptors advance by (bytes >> 4)
+            const uint64_t adesc = kmajor_desc<BKT>(smem_u32(ASTAT ? S.a[sl] : S.a[stage]));
+            const uint64_t bdesc = kmajor_desc<BKT>(smem_u32(S.b[BSTAT ? kb : stage]));
 #pragma unroll
-              for (int k = 0; k < BKT / kUmmaK; ++k)
-                umma_bf16_pair(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
-                               idesc, (kb | k) != 0);
-              umma_commit_pair(&S.empty[stage]);                       // both CTAs' stage free
-              if (kb == kblocks - 1) umma_commit_pair(&S.tfull[acc]);  // both CTAs' accumulator rows complete
-            } else {
-#pragma unroll
-            for (int k = 0; k < BKT / kUmmaK; ++k)
-              umma_bf16(d_tmem, kmajor_desc<BKT>(a0 + k * kUmmaK * 2), kmajor_desc<BKT>(b0 + k * kUmmaK * 2),
-                        idesc, (kb | k) != 0);
-            umma_commit(&S.empty[stage]);                       // smem stage free when these MMAs finish
-            if (kb == kblocks - 1) umma_commit(&S.tfull[acc]);  // accumulator complete
+            for (int k = 0; k < BKT / kUmmaK; ++k) {
+              if (PAIR)
+                umma_bf16_pair_elect(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+              else
+                umma_bf16_elect(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
             }
-            if (ASTAT && nt == nts - 1) umma_commit(&S.a_free[sl]);  // A slot no longer read
+            if (PAIR) {
+              umma_commit_pair_elect(&S.empty[stage]);                       // both CTAs' stage free
+              if (kb == kblocks - 1) umma_commit_pair_elect(&S.tfull[acc]);  // both CTAs' accumulator rows complete
+            } else {
+              umma_commit_elect(&S.empty[stage]);                       // smem stage free when these MMAs finish
+              if (kb == kblocks - 1) umma_commit_elect(&S.tfull[acc]);  // accumulator complete
+            }
+            if (ASTAT && nt == nts - 1) umma_commit_elect(&S.a_free[sl]);  // A slot no longer read
           }
-          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -1279,6 +1281,10 @@ cudaError_t conv_im2col_fprop(const void* x, const void* wk, void* C, int n, int
   const int64_t M = (int64_t)n * ho * wo;
   const int K = k * k * cin;
   const bool bwd = bx != nullptr, pro = pmean != nullptr, st = part != nullptr;
+  // 3x3 / stride 1 / pad 1 forward at 64/128 output channels: halo windows
+  // (each input pixel loaded and transformed once for all nine taps)
+  if (!bwd && k == 3 && stride == 1 && pad == 1 && ho == h && wo == w && conv3x3_halo_supported(h, w, cin, N, pro))
+    return conv3x3_halo_fprop(x, wk, C, n, h, w, cin, N, pmean, pinvstd, pg, pb, part, part_rows, s);
   if (M <= 0 || cin % kBK != 0 || k < 1 || k > 7 || stride < 1 || stride > 2 || (pro && cin > kMaxProK))
     return cudaErrorInvalidValue;
   // the im2col traversal visits exactly these output rows / columns

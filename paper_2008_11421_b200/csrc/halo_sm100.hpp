@@ -1,0 +1,18 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace krt {
+// 3x3 / stride-1 / pad-1 convolution with halo windows (halo_sm100.cu):
+// C[n*h*w, N] = f(x) (*) wk, x NHWC bf16 [n, h, w, cin] (cin % 64 == 0), wk
+// [N][3][3][cin] bf16 (OHWI), N in {64, 128}; f = relu(bn(.)) per input channel
+// when pmean is non-NULL (the zero padding stays zero); part/part_rows: BN
+// statistics partials of C as conv1x1_bn_fprop (bn_partials_finalize).
+// KRT_CONV_HALO=0 disables it (conv3x3_halo_supported then returns false).
+bool conv3x3_halo_supported(int h, int w, int cin, int N, bool pro);
+cudaError_t conv3x3_halo_fprop(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int N,
+                               const float* pmean, const float* pinvstd, const void* pg, const void* pb, float* part,
+                               int* part_rows, cudaStream_t s);
+}  // namespace krt
