@@ -382,6 +382,13 @@ int krt_conv_im2col_bn(const void* x, const void* wk, void* C, int n, int h, int
                        int stride, int pad, int N, const float* pmean, const float* pinvstd, const void* pgamma,
                        const void* pbeta, float* part, int* part_rows, const void* bx, const float* bmean,
                        const float* binvstd, const void* bgamma, const void* bbeta, void* stream);
+/* 1 when krt_conv_im2col_bn runs a 3x3 / stride-1 / pad-1 forward of this
+ * shape on the halo-window kernel (csrc/halo_sm100.cu: each input pixel of a
+ * 256-output-row window loaded, and with pmean transformed, once for all nine
+ * taps; N in {64, 128}, cin % 64 == 0, the windows fit shared memory), 0 when
+ * on the im2col-TMA GEMM.  KRT_CONV_HALO=0 in the environment disables the
+ * halo kernel. */
+int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue);
 /* Weight gradient of a convolution on tcgen05 (the backward work
  * cost_model.py:97-105 counts for a Conv layer): dw [cout][k][k][cin] fp32
  * (OHWI, written, not accumulated) = sum over the output pixels of

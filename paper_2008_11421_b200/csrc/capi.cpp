@@ -16,6 +16,7 @@
 #include "bn_kernels.hpp"
 #include "pool_kernels.hpp"
 #include "gemm_sm100.hpp"
+#include "halo_sm100.hpp"
 #include "wgrad_sm100.hpp"
 #include "ln_kernels.hpp"
 #include "kernels.hpp"
@@ -558,6 +559,10 @@ int krt_conv_im2col_bn(const void* x, const void* wk, void* C, int n, int h, int
   KRT_CUDA_GUARD(conv_im2col_fprop(x, wk, C, n, h, w, cin, ho, wo, k, stride, pad, N, pmean, pinvstd, pgamma, pbeta,
                                    part, part_rows, bx, bmean, binvstd, bgamma, bbeta, (cudaStream_t)stream),
                  "conv_im2col_bn");
+}
+
+int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue) {
+  return conv3x3_halo_supported(h, w, cin, N, prologue != 0) ? 1 : 0;
 }
 
 size_t krt_conv_wgrad_workspace_bytes(int n, int ho, int wo, int cout, int cin, int k) {

@@ -1268,7 +1268,37 @@ struct CkptHeader {
   uint32_t version, world, rank, weight_dtype;
   uint64_t params, host_elems, step;
   uint32_t has_dev_master, has_dev_moments;
+  uint64_t layout_hash;  // version 2: parameter / host-state layout of the plan
 };
+
+// FNV-1a over the parameter and host-state layout (block offsets, sizes, host
+// path, group ranges and shards): two plans with equal totals but a different
+// swap / host-path split hash differently
+uint64_t layout_hash(const std::map<int, BlockPhys>& blocks, const std::vector<GroupPhys>& groups) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  for (const auto& kv : blocks) {
+    const BlockPhys& b = kv.second;
+    mix((uint64_t)kv.first);
+    mix((uint64_t)b.p_off);
+    mix((uint64_t)b.n_params);
+    mix((uint64_t)b.host_path);
+    mix((uint64_t)b.group);
+  }
+  for (const auto& g : groups) {
+    mix((uint64_t)g.p_lo);
+    mix((uint64_t)g.p_n);
+    mix((uint64_t)g.shard_n);
+    mix((uint64_t)g.host_off);
+    mix((uint64_t)g.host_n);
+  }
+  return h;
+}
 
 void write_all(std::FILE* f, const void* p, size_t n) {
   if (n && std::fwrite(p, 1, n, f) != n) throw std::runtime_error("checkpoint: short write");
@@ -1307,7 +1337,8 @@ void Runtime::checkpoint_save(const std::string& path) {
   const size_t he = std::max<size_t>(host_elems_, 64);
   CkptHeader h{};
   std::memcpy(h.magic, "KRTCKPT1", 8);
-  h.version = 1;
+  h.version = 2;
+  h.layout_hash = layout_hash(blocks_, groups_);
   h.world = (uint32_t)world_;
   h.rank = (uint32_t)rank_;
   h.weight_dtype = (uint32_t)cfg_.weight_dtype;
@@ -1352,12 +1383,18 @@ void Runtime::checkpoint_load(const std::string& path) {
   try {
     CkptHeader h{};
     read_all(f, &h, sizeof(h));
-    if (std::memcmp(h.magic, "KRTCKPT1", 8) != 0 || h.version != 1)
+    if (std::memcmp(h.magic, "KRTCKPT1", 8) != 0 || h.version != 2)
       throw std::invalid_argument("checkpoint: not a krt checkpoint (bad magic/version)");
     if (h.world != (uint32_t)world_ || h.rank != (uint32_t)rank_ || h.weight_dtype != (uint32_t)cfg_.weight_dtype ||
         h.params != np || h.host_elems != he || h.has_dev_master != (d_master_ != nullptr) ||
-        h.has_dev_moments != (d_m_ != nullptr))
+        h.has_dev_moments != (d_m_ != nullptr) || h.layout_hash != layout_hash(blocks_, groups_))
       throw std::invalid_argument("checkpoint: saved for a different model, plan, dtype or rank");
+    // multi-rank exchanges synchronise on monotone per-step flags and marks
+    // (IPC flags, peer-group marks): replaying steps this context already ran
+    // would let the waits pass before the peers' buffers are written
+    if (world_ > 1 && (int64_t)h.step < (int64_t)step_)
+      throw std::invalid_argument("checkpoint: step " + std::to_string(h.step) + " is behind this context's step " +
+                                  std::to_string(step_) + " (multi-rank: load into a fresh context)");
     file_to_dev(f, d_weights_, np * wb);
     if (d_master_) file_to_dev(f, d_master_, np * 4);
     if (d_m_) {
