@@ -443,6 +443,17 @@ int krt_ln_bwd(const void* dy, const void* x, const void* gamma, const float* me
 size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N);
 int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,
                         void* stream);
+/* The GPT MLP's GEMMs with the bias / GELU work in the cuBLASLt epilogue
+ * (library GEMMs; the fusion removes the elementwise passes around them).
+ * Row-major bf16.  fc1: f1 = x [M, K] . w1 [N, K]^T + b1 [N] (the GELU input,
+ * the epilogue's auxiliary output) and g = gelu_tanh(f1), both [M, N].
+ * fc2 data gradient: df1 = (dy [M, K] . w2 [K, N]) * gelu_tanh'(f1) [M, N]
+ * bf16 (fc1's bias gradient, the fp32 column sums of df1, is left to the
+ * caller: cuBLASLt's DGELU_BGRAD sums only in the output type). */
+int krt_mlp_fc1_gelu(const void* x, const void* w1, const void* b1, void* f1, void* g, int64_t M, int64_t N,
+                     int64_t K, void* stream);
+int krt_mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
+                      void* stream);
 
 #ifdef __cplusplus
 }

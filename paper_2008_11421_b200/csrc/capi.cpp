@@ -17,6 +17,7 @@
 #include "pool_kernels.hpp"
 #include "gemm_sm100.hpp"
 #include "halo_sm100.hpp"
+#include "mlp_lt.hpp"
 #include "wgrad_sm100.hpp"
 #include "ln_kernels.hpp"
 #include "kernels.hpp"
@@ -622,6 +623,16 @@ size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N) { return gelu_bwd_colsum_
 int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,
                         void* stream) {
   KRT_CUDA_GUARD(gelu_bwd_colsum(dy, f, dx, colsum, ws, T, N, (cudaStream_t)stream), "gelu_bwd_colsum");
+}
+
+int krt_mlp_fc1_gelu(const void* x, const void* w1, const void* b1, void* f1, void* g, int64_t M, int64_t N,
+                     int64_t K, void* stream) {
+  return guard([&] { mlp_fc1_gelu(x, w1, b1, f1, g, M, N, K, (cudaStream_t)stream); });
+}
+
+int krt_mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
+                      void* stream) {
+  return guard([&] { mlp_fc2_dgelu(dy, w2, f1, df1, M, N, K, (cudaStream_t)stream); });
 }
 
 int krt_device_update(float* master, float* m, float* v, const float* grad, void* weights, int weight_dtype,

@@ -1,0 +1,16 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace krt {
+// GPT MLP GEMMs with the bias / GELU work in the cuBLASLt epilogue (mlp_lt.cpp).
+// Row-major bf16: x [M, K], w1 [N, K], b1 [N] -> f1 [M, N] (GELU input) and
+// g = gelu_tanh(f1) [M, N]
+void mlp_fc1_gelu(const void* x, const void* w1, const void* b1, void* f1, void* g, int64_t M, int64_t N, int64_t K,
+                  cudaStream_t s);
+// dy [M, K], w2 [K, N] (fc2's weight, out x in), f1 [M, N] -> df1 = (dy . w2) *
+// gelu_tanh'(f1) [M, N] bf16
+void mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
+                   cudaStream_t s);
+}  // namespace krt

@@ -54,3 +54,32 @@ def gelu_bwd_colsum(dy, f, colsum):
         _lib.check(_lib.lib().krt_gelu_bwd_colsum(dy.data_ptr(), f.data_ptr(), dx.data_ptr(), colsum.data_ptr(),
                                                   ws.data_ptr(), T, N, _stream()))
     return dx
+
+
+def mlp_fc1_gelu(x, w1, b1, f1_out=None):
+    """The GPT MLP's first GEMM with bias and GELU in the cuBLASLt epilogue:
+    f1 = x w1^T + b1 (the GELU input, into f1_out when given) and
+    g = gelu_tanh(f1).  x [T, K], w1 [N, K] bf16.  Returns (f1, g)."""
+    T, K = x.shape
+    N = w1.shape[0]
+    x = x.contiguous()
+    f1 = f1_out if f1_out is not None else torch.empty((T, N), dtype=x.dtype, device=x.device)
+    g = torch.empty((T, N), dtype=x.dtype, device=x.device)
+    with _timed("cublas_gemm", (T * K + N * K + 2 * T * N) * 2, 2.0 * T * N * K):
+        _lib.check(_lib.lib().krt_mlp_fc1_gelu(x.data_ptr(), w1.data_ptr(), b1.data_ptr(), f1.data_ptr(),
+                                               g.data_ptr(), T, N, K, _stream()))
+    return f1, g
+
+
+def mlp_fc2_dgelu(dy, w2, f1):
+    """The data gradient of the MLP's second GEMM with GELU's backward in the
+    cuBLASLt epilogue: returns df1 = (dy w2) * gelu_tanh'(f1) [T, N] bf16.
+    dy [T, K], w2 [K, N], f1 [T, N]."""
+    T, K = dy.shape
+    N = w2.shape[1]
+    dy, f1 = dy.contiguous(), f1.contiguous()
+    df1 = torch.empty((T, N), dtype=dy.dtype, device=dy.device)
+    with _timed("cublas_gemm", (T * K + N * K + 2 * T * N) * 2, 2.0 * T * N * K):
+        _lib.check(_lib.lib().krt_mlp_fc2_dgelu(dy.data_ptr(), w2.data_ptr(), f1.data_ptr(), df1.data_ptr(), T, N, K,
+                                                _stream()))
+    return df1

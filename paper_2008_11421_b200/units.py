@@ -112,6 +112,10 @@ TC_DGRAD = os.environ.get("KRT_TC_DGRAD", "0") == "1"
 # 0.932 ms; width 128: 0.585 -> 0.532 ms), and conv1's wgrad at width 256
 # (0.121 -> 0.113 ms).  KRT_TC_WGRAD=0: cuDNN for all of them
 TC_WGRAD = os.environ.get("KRT_TC_WGRAD", "1") != "0"
+# GPT MLP: fc1's bias + GELU and, in the backward, GELU's derivative and fc1's
+# bias gradient in the cuBLASLt epilogues of the GEMMs around them
+# (csrc/mlp_lt.cpp); KRT_MLP_LT=0: separate aten GELU / own gelu_bwd_colsum
+MLP_LT = os.environ.get("KRT_MLP_LT", "1") != "0"
 
 
 def _cl(t):
@@ -1186,9 +1190,15 @@ class TransformerLayerUnit(Unit):
             saved[2].copy_(o)
         # x2 = x + attn-proj and LN2(x2) in one kernel; x2 lands in its saved slot
         h2, x2 = _ln_fw(x, g2, b2, m2, r2, residual=_linear(o, wo, bo), x2_out=sv(3))
-        f1 = _linear(h2, w1, bf1, out=sv(4))
-        del h2
-        mlp = _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
+        if MLP_LT and lnfused.supported(h2):
+            f1, gl = lnfused.mlp_fc1_gelu(h2, w1, bf1, f1_out=sv(4))
+            del h2
+            mlp = _linear(gl, w2, bf2)
+            del gl
+        else:
+            f1 = _linear(h2, w1, bf1, out=sv(4))
+            del h2
+            mlp = _linear(F.gelu(f1, approximate="tanh"), w2, bf2)
         y = torch.add(x2, mlp, out=out) if out is not None else x2 + mlp
         del mlp
         return y
@@ -1203,9 +1213,21 @@ class TransformerLayerUnit(Unit):
         t = x.shape[0]
         m1, r1, m2, r2 = st[:t], st[t:2 * t], st[2 * t:3 * t], st[3 * t:]
         gl = F.gelu(f1, approximate="tanh")
-        dg = _linear_bw(dy, gl, w2, grads[10], grads[11])
-        del gl
-        if lnfused.supported(f1):   # GELU backward + fc1's bias gradient in one pass
+        if MLP_LT and lnfused.supported(f1):
+            # dW2 from the recomputed GELU; the data gradient with GELU's
+            # derivative in the GEMM's epilogue (fc1's bias gradient: the fp32
+            # column sum with fc1's weight gradient below)
+            _linear_bw(dy, gl, w2, grads[10], grads[11], need_dx=False)
+            del gl
+            df1 = lnfused.mlp_fc2_dgelu(dy, w2, f1)
+            gb1 = grads[9]
+            dg = None
+        else:
+            dg = _linear_bw(dy, gl, w2, grads[10], grads[11])
+            del gl
+        if dg is None:
+            pass
+        elif lnfused.supported(f1):   # GELU backward + fc1's bias gradient in one pass
             df1 = lnfused.gelu_bwd_colsum(dg, f1, grads[9])
             gb1 = None
         else:
