@@ -454,6 +454,10 @@ int krt_mlp_fc1_gelu(const void* x, const void* w1, const void* b1, void* f1, vo
                      int64_t K, void* stream);
 int krt_mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
                       void* stream);
+/* fc2 with the layer's residual: y = x2 [M, N] + g [M, K] . w2 [N, K]^T +
+ * b2 [N] (bias epilogue, beta = 1 on x2; y may alias x2). */
+int krt_mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void* x2, void* y, int64_t M,
+                         int64_t N, int64_t K, void* stream);
 
 #ifdef __cplusplus
 }

@@ -630,6 +630,11 @@ int krt_mlp_fc1_gelu(const void* x, const void* w1, const void* b1, void* f1, vo
   return guard([&] { mlp_fc1_gelu(x, w1, b1, f1, g, M, N, K, (cudaStream_t)stream); });
 }
 
+int krt_mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void* x2, void* y, int64_t M,
+                         int64_t N, int64_t K, void* stream) {
+  return guard([&] { mlp_fc2_residual(g, w2, b2, x2, y, M, N, K, (cudaStream_t)stream); });
+}
+
 int krt_mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
                       void* stream) {
   return guard([&] { mlp_fc2_dgelu(dy, w2, f1, df1, M, N, K, (cudaStream_t)stream); });

@@ -11,6 +11,9 @@
 //             DGELU_BGRAD form would also sum fc1's bias gradient, but only in
 //             the output type, bf16; the fp32 sum stays with fc1's weight
 //             gradient, which reads df1 anyway.)
+//   fc2       y = x2 + g . W2^T + b2 in one GEMM (bias epilogue, beta = 1 on
+//             the residual): the layer output is written once, no separate
+//             add pass and no intermediate fc2 output
 //
 // Row-major torch tensors map to column-major cuBLASLt as transposes: the
 // row-major [M, N] output is the column-major N x M matrix D with ld = N.
@@ -64,7 +67,7 @@ struct Desc {
 // algorithm cache
 void run(int kind, cublasOperation_t ta, cublasOperation_t tb, int64_t m, int64_t n, int64_t k, const void* A,
          int64_t lda, const void* B, int64_t ldb, void* D, cublasLtEpilogue_t epi, const void* bias, int bias_type,
-         void* aux, cudaStream_t stream) {
+         void* aux, cudaStream_t stream, const void* C = nullptr) {
   LtState& s = lt();
   std::lock_guard<std::mutex> lk(s.mu);
   if (!s.h) {
@@ -79,11 +82,14 @@ void run(int kind, cublasOperation_t ta, cublasOperation_t tb, int64_t m, int64_
   LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias)));
   int32_t bt = bias_type;
   LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof(bt)));
-  LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_POINTER, &aux, sizeof(aux)));
-  int64_t aux_ld = m;
-  LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_LD, &aux_ld, sizeof(aux_ld)));
-  int32_t aux_t = CUDA_R_16BF;
-  LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_DATA_TYPE, &aux_t, sizeof(aux_t)));
+  if (aux) {
+    LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_POINTER, &aux, sizeof(aux)));
+    int64_t aux_ld = m;
+    LT_CHECK(cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_LD, &aux_ld, sizeof(aux_ld)));
+    int32_t aux_t = CUDA_R_16BF;
+    LT_CHECK(
+        cublasLtMatmulDescSetAttribute(g.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_DATA_TYPE, &aux_t, sizeof(aux_t)));
+  }
   const bool tA = ta == CUBLAS_OP_T, tB = tb == CUBLAS_OP_T;
   LT_CHECK(cublasLtMatrixLayoutCreate(&g.a, CUDA_R_16BF, tA ? k : m, tA ? m : k, lda));
   LT_CHECK(cublasLtMatrixLayoutCreate(&g.b, CUDA_R_16BF, tB ? n : k, tB ? k : n, ldb));
@@ -106,8 +112,8 @@ void run(int kind, cublasOperation_t ta, cublasOperation_t tb, int64_t m, int64_
     it = s.algos.emplace(key, res.algo).first;
   }
   const float one = 1.f, zero = 0.f;
-  LT_CHECK(cublasLtMatmul(s.h, g.op, &one, A, g.a, B, g.b, &zero, D, g.d, D, g.d, &it->second, s.ws, s.ws_bytes,
-                          stream));
+  LT_CHECK(cublasLtMatmul(s.h, g.op, &one, A, g.a, B, g.b, C ? &one : &zero, C ? C : D, g.d, D, g.d, &it->second,
+                          s.ws, s.ws_bytes, stream));
 }
 }  // namespace
 
@@ -122,6 +128,12 @@ void mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, in
   // df1^T (N x M) = W2^T (N x K: W2 [K, N] row-major read column-major) . dy^T (K x M), times gelu' of f1^T
   run(1, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, w2, N, dy, K, df1, CUBLASLT_EPILOGUE_DGELU, nullptr, CUDA_R_16BF,
       const_cast<void*>(f1), s);
+}
+
+void mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void* x2, void* y, int64_t M, int64_t N,
+                      int64_t K, cudaStream_t s) {
+  // y^T (N x M) = W2 (K x N col-major, transposed) . g^T (K x M) + b2 + x2^T
+  run(2, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, w2, K, g, K, y, CUBLASLT_EPILOGUE_BIAS, b2, CUDA_R_16BF, nullptr, s, x2);
 }
 
 }  // namespace krt

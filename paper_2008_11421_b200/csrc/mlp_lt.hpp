@@ -13,4 +13,8 @@ void mlp_fc1_gelu(const void* x, const void* w1, const void* b1, void* f1, void*
 // gelu_tanh'(f1) [M, N] bf16
 void mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
                    cudaStream_t s);
+// g [M, K], w2 [N, K], b2 [N], x2 [M, N] -> y = x2 + g . w2^T + b2 [M, N]
+// (y may alias x2)
+void mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void* x2, void* y, int64_t M, int64_t N,
+                      int64_t K, cudaStream_t s);
 }  // namespace krt

@@ -83,3 +83,17 @@ def mlp_fc2_dgelu(dy, w2, f1):
         _lib.check(_lib.lib().krt_mlp_fc2_dgelu(dy.data_ptr(), w2.data_ptr(), f1.data_ptr(), df1.data_ptr(), T, N, K,
                                                 _stream()))
     return df1
+
+
+def mlp_fc2_residual(g, w2, b2, x2, out=None):
+    """The MLP's second GEMM with the layer's residual add in the cuBLASLt
+    epilogue: y = x2 + g w2^T + b2 (into out when given).  g [T, K], w2 [N, K],
+    x2 [T, N] bf16."""
+    T, K = g.shape
+    N = w2.shape[0]
+    g, x2 = g.contiguous(), x2.contiguous()
+    y = out if out is not None else torch.empty((T, N), dtype=g.dtype, device=g.device)
+    with _timed("cublas_gemm", (T * K + N * K + 2 * T * N) * 2, 2.0 * T * N * K):
+        _lib.check(_lib.lib().krt_mlp_fc2_residual(g.data_ptr(), w2.data_ptr(), b2.data_ptr(), x2.data_ptr(),
+                                                   y.data_ptr(), T, N, K, _stream()))
+    return y

@@ -1193,8 +1193,8 @@ class TransformerLayerUnit(Unit):
         if MLP_LT and lnfused.supported(h2):
             f1, gl = lnfused.mlp_fc1_gelu(h2, w1, bf1, f1_out=sv(4))
             del h2
-            mlp = _linear(gl, w2, bf2)
-            del gl
+            # y = x2 + gelu(f1) W2^T + b2: the residual add in fc2's epilogue
+            return lnfused.mlp_fc2_residual(gl, w2, bf2, x2, out=out)
         else:
             f1 = _linear(h2, w1, bf1, out=sv(4))
             del h2

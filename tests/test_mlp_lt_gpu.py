@@ -46,3 +46,14 @@ def test_fc1_gelu_and_fc2_dgelu(T, H):
     f1b, gb = lnfused.mlp_fc1_gelu(x, w1, b1)
     assert torch.equal(f1b, f1) and torch.equal(gb, g)
     assert torch.equal(lnfused.mlp_fc2_dgelu(dy, w2, f1), df1)
+
+
+@pytest.mark.parametrize("T,H", [(256, 128), (2048, 1920)])
+def test_fc2_residual(T, H):
+    K = 4 * H
+    g, w2, b2, x2 = rand((T, K), 6), rand((H, K), 7, K ** -0.5), rand((H,), 8, 0.1), rand((T, H), 9)
+    y = lnfused.mlp_fc2_residual(g, w2, b2, x2)
+    ref = x2.float() + g.float() @ w2.float().t() + b2.float()
+    assert rel(y, ref) < 1e-2
+    out = torch.empty_like(x2)
+    assert torch.equal(lnfused.mlp_fc2_residual(g, w2, b2, x2, out=out), y)
