@@ -330,10 +330,25 @@ def conv_wgrad(dy, x, dw, k, stride, pad, pre=None):
 
 
 def conv_im2col_supported(cin, cout, pre=False, dgrad=False):
-    """krt_conv_im2col_bn's shape rules (csrc/gemm_sm100.cu)."""
+    """krt_conv_im2col_bn's shape rules (csrc/gemm_sm100.cu) for any stride;
+    3x3 / stride 1 also takes 16 -> 16 and 32 -> 32 channels (halo kernel,
+    conv3x3_halo_supported)."""
     if cin % 64 or (pre and cin > 1024):
         return False
     return cout in (64, 128) or cout % (128 if dgrad else 256) == 0
+
+
+def conv3x3_halo_supported(h, w, cin, cout, pre=False):
+    """krt_conv_im2col_bn runs this 3x3 / stride-1 / pad-1 shape on the halo kernel."""
+    return bool(_lib.lib().krt_conv3x3_halo_supported(h, w, cin, cout, int(pre)))
+
+
+def conv3x3_dgrad(dy, w, out=None):
+    """Data gradient of a 3x3 / stride-1 / pad-1 convolution (w: (Cout, 3, 3,
+    Cin) OHWI): the same convolution of dy with the flipped, transposed
+    weights, on the halo kernel when conv3x3_halo_supported."""
+    wt = w.flip(1, 2).permute(3, 1, 2, 0).contiguous()
+    return conv_im2col(dy, wt, 1, 1, out=out)
 
 
 def conv_im2col(x, w, stride, pad, out=None, pre=None, stats=None):

@@ -1281,8 +1281,9 @@ cudaError_t conv_im2col_fprop(const void* x, const void* wk, void* C, int n, int
   const int64_t M = (int64_t)n * ho * wo;
   const int K = k * k * cin;
   const bool bwd = bx != nullptr, pro = pmean != nullptr, st = part != nullptr;
-  // 3x3 / stride 1 / pad 1 forward at 64/128 output channels: halo windows
-  // (each input pixel loaded and transformed once for all nine taps)
+  // 3x3 / stride 1 / pad 1 forward at 64/128 output channels (cin % 64 == 0)
+  // or 16/32 -> 16/32 channels: halo windows (each input pixel loaded and
+  // transformed once for all nine taps; halo_sm100.cu)
   if (!bwd && k == 3 && stride == 1 && pad == 1 && ho == h && wo == w && conv3x3_halo_supported(h, w, cin, N, pro))
     return conv3x3_halo_fprop(x, wk, C, n, h, w, cin, N, pmean, pinvstd, pg, pb, part, part_rows, s);
   if (M <= 0 || cin % kBK != 0 || k < 1 || k > 7 || stride < 1 || stride > 2 || (pro && cin > kMaxProK))

@@ -116,6 +116,14 @@ TC_WGRAD = os.environ.get("KRT_TC_WGRAD", "1") != "0"
 # bias gradient in the cuBLASLt epilogues of the GEMMs around them
 # (csrc/mlp_lt.cpp); KRT_MLP_LT=0: separate aten GELU / own gelu_bwd_colsum
 MLP_LT = os.environ.get("KRT_MLP_LT", "1") != "0"
+# the pre-activation unit's 3x3 convolution on the own halo-window kernel
+# (csrc/halo_sm100.cu) where it measured faster than cuDNN
+# (scripts/bench_narrow3x3.py, ResNet-1001 2048^2 b2, profiles/round2_s3):
+# forward with relu(bn1) in its prologue and BN2's statistics in its epilogue
+# at 16 / 32 channels (0.35 vs 0.46 ms, 0.18 vs 0.20 ms for cuDNN + apply +
+# stats), data gradient at 16 channels (0.30 vs 0.34 ms).  KRT_HALO_UNITS=0:
+# cuDNN for all of them
+HALO_UNITS = os.environ.get("KRT_HALO_UNITS", "1") != "0"
 
 
 def _cl(t):
@@ -750,11 +758,24 @@ class PreActBottleneckUnit(_ConvNetUnit):
             a0 = _bn_relu(x, st[0], st[1], g0, b0)
             sc = _conv(a0, _cl(params[9]), self.s, 0)
             del a0
-        a1 = _bn_relu(c1, st[2], st[3], g1, b1)
-        c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
-        del a1
-        _stats_fw(c2, st[4], st[5])
+        if self._halo_fwd():
+            # the 3x3 convolution of relu(bn1(c1)) (never written) with BN2's
+            # statistics in the epilogue
+            c2 = bnfused.conv_im2col(c1, w2, 1, 1, out=sv(2), pre=(st[2], st[3], g1, b1), stats=(st[4], st[5]))
+        else:
+            a1 = _bn_relu(c1, st[2], st[3], g1, b1)
+            c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
+            del a1
+            _stats_fw(c2, st[4], st[5])
         return bnfused.conv1x1(c2, _cl(w3), out=out, pre=(st[4], st[5], g2, b2), res=sc)
+
+    def _halo_fwd(self):
+        return (HALO_UNITS and self.act == torch.bfloat16 and self.s == 1 and self.w in (16, 32)
+                and bnfused.conv3x3_halo_supported(self.ho, self.ho, self.w, self.w, pre=True))
+
+    def _halo_dgrad(self):
+        return (HALO_UNITS and self.act == torch.bfloat16 and self.s == 1 and self.w == 16
+                and bnfused.conv3x3_halo_supported(self.ho, self.ho, self.w, self.w))
 
     def forward(self, x, params, saved, out=None):
         g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
@@ -800,7 +821,13 @@ class PreActBottleneckUnit(_ConvNetUnit):
             dc2 = _bn_relu_bw(da2, c2, st[4], st[5], g2, b2, grads[6], grads[7])
             del da2
         a1 = _bn_relu(c1, st[2], st[3], g1, b1)
-        da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
+        if self._halo_dgrad():
+            # data gradient on the halo kernel (flipped, transposed weights);
+            # cuDNN keeps the weight gradient
+            _, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1, need_dx=False)
+            da1 = bnfused.conv3x3_dgrad(dc2, w2)
+        else:
+            da1, dw2, _ = _conv_bw(dc2, a1, _cl(w2), self.s, 1)
         del dc2, a1
         _cl(grads[5]).copy_(dw2)
         dc1 = _bn_relu_bw(da1, c1, st[2], st[3], g1, b1, grads[3], grads[4])

@@ -1,8 +1,12 @@
 """3x3 / stride-1 / pad-1 convolution on the halo-window kernel
 (csrc/halo_sm100.cu, reached through krt_conv_im2col_bn) vs torch fp32:
 image sizes with and without partial 128-row sub-tiles and junk columns
-(every tap crosses the window's 128-byte row phase), single images and
-batches, 64 and 128 output channels, more input than output channels, with
+(every tap crosses the window's swizzle-row phase), single images and
+batches, 64 and 128 output channels on 64-channel blocks, the narrow 16 / 32
+channel convolutions of ResNet-1001 (32 / 64-byte window rows), images wider
+than one 256-pixel TMA box or than shared memory holds (column segments whose
+windows take their halo columns from the neighbouring segment), more input
+than output channels, with
 the relu(bn(.)) prologue (the zero padding must stay zero: the reference
 convolves the bn_apply output) and the statistics epilogue (junk rows
 excluded).  Tolerances as tests/test_conv_im2col_gpu.py: bf16 output rounding
@@ -33,7 +37,9 @@ def bn_params(c, seed):
 
 
 SHAPES = [(1, 64, 64, 1, 1), (2, 64, 64, 5, 9), (3, 64, 64, 56, 56), (2, 128, 128, 28, 28), (5, 64, 128, 14, 14),
-          (4, 128, 64, 7, 7), (2, 256, 128, 13, 17), (1, 256, 64, 30, 6), (2, 64, 128, 33, 50)]
+          (4, 128, 64, 7, 7), (2, 256, 128, 13, 17), (1, 256, 64, 30, 6), (2, 64, 128, 33, 50),
+          (2, 16, 16, 17, 30), (1, 32, 32, 9, 13), (2, 16, 16, 64, 64), (2, 16, 16, 12, 300),
+          (1, 32, 32, 21, 520), (1, 64, 64, 11, 600), (1, 16, 16, 130, 2048)]
 
 
 @pytest.mark.parametrize("n,cin,cout,h,w", SHAPES)
@@ -65,12 +71,13 @@ def test_conv_halo_matches_torch(n, cin, cout, h, w, pre, stats):
     assert torch.equal(y, bnfused.conv_im2col(x, wt, 1, 1, pre=pre_t, stats=st))   # deterministic
 
 
-def test_halo_rejects_windows_beyond_shared_memory():
-    # 200 columns: two 5-row windows of 202 padded pixels exceed shared memory,
-    # so krt_conv_im2col_bn keeps the im2col path (still correct)
-    assert _lib.lib().krt_conv3x3_halo_supported(4, 200, 64, 64, 0) == 0
-    x = cl(rand((1, 64, 4, 200), 4))
-    wt = rand((64, 3, 3, 64), 5, (64 * 9) ** -0.5).contiguous()
+def test_halo_declines_other_channel_counts():
+    # 256 output channels (and 48 input channels) stay on the im2col GEMM path,
+    # which krt_conv_im2col_bn then takes (still correct)
+    assert _lib.lib().krt_conv3x3_halo_supported(8, 8, 64, 256, 0) == 0
+    assert _lib.lib().krt_conv3x3_halo_supported(8, 8, 48, 48, 0) == 0
+    x = cl(rand((1, 64, 8, 8), 4))
+    wt = rand((256, 3, 3, 64), 5, (64 * 9) ** -0.5).contiguous()
     y = bnfused.conv_im2col(x, wt, 1, 1)
     ref = F.conv2d(x.float(), wt.permute(0, 3, 1, 2).float(), padding=1)
     assert (y.float() - ref).abs().max() / ref.abs().max() < 1e-2
