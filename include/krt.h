@@ -389,6 +389,20 @@ int krt_conv_im2col_bn(const void* x, const void* wk, void* C, int n, int h, int
  * on the im2col-TMA GEMM.  KRT_CONV_HALO=0 in the environment disables the
  * halo kernel. */
 int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue);
+/* Weight gradient of a 3x3 / stride-1 / pad-1 convolution with few channels
+ * (C = cin = cout in {16, 32, 64}: the ResNet-1001 bottleneck widths;
+ * cost_model.py:97-105 counts this backward work for a Conv layer) from halo
+ * windows on tcgen05: dw [C][3][3][C] fp32 (OHWI, written) = sum over the
+ * pixels of dy [n, h, w, C] times the 3x3 window of f(x), x [n, h, w, C] NHWC
+ * bf16, f = relu(bn(.)) per channel when pmean is non-NULL.  The pixel sum is
+ * split over the SMs into fp32 partials summed in a fixed order
+ * (deterministic); ws: krt_wgrad3x3_narrow_workspace(C) bytes.  _supported: 1
+ * when the shape's windows fit (KRT_WGRAD_HALO=0 disables the kernel). */
+int krt_wgrad3x3_narrow_supported(int h, int w, int C);
+size_t krt_wgrad3x3_narrow_workspace(int C);
+int krt_wgrad3x3_narrow(const void* x, const void* dy, float* dw, int n, int h, int w, int C, const float* pmean,
+                        const float* pinvstd, const void* pgamma, const void* pbeta, void* ws, size_t ws_bytes,
+                        void* stream);
 /* Weight gradient of a convolution on tcgen05 (the backward work
  * cost_model.py:97-105 counts for a Conv layer): dw [cout][k][k][cin] fp32
  * (OHWI, written, not accumulated) = sum over the output pixels of

@@ -343,6 +343,27 @@ def conv3x3_halo_supported(h, w, cin, cout, pre=False):
     return bool(_lib.lib().krt_conv3x3_halo_supported(h, w, cin, cout, int(pre)))
 
 
+def wgrad3x3_narrow_supported(h, w, c):
+    return bool(_lib.lib().krt_wgrad3x3_narrow_supported(h, w, c))
+
+
+def wgrad3x3_narrow(dy, x, dw, pre=None):
+    """Weight gradient of a 3x3 / stride-1 / pad-1 convolution with C = cin =
+    cout in {16, 32, 64} (halo windows on tcgen05), written in fp32 into dw
+    (C, 3, 3, C) OHWI contiguous.  pre=(mean, invstd, gamma, beta): the
+    forward convolved relu(bn(x)) (never materialised here)."""
+    dy, x = _nhwc(dy), _nhwc(x)
+    n, c, h, w = x.shape
+    assert dw.dtype == torch.float32 and dw.is_contiguous() and dw.numel() == c * 9 * c
+    L = _lib.lib()
+    ws = torch.empty(L.krt_wgrad3x3_narrow_workspace(c), dtype=torch.uint8, device=x.device)
+    pm, pi, pg, pb = pre if pre is not None else (None, None, None, None)
+    with _timed("conv_wgrad", 2 * x.numel() * 2 + dw.numel() * 4, 2.0 * n * h * w * 9 * c * c):
+        _lib.check(L.krt_wgrad3x3_narrow(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), n, h, w, c, _ptr(pm), _ptr(pi),
+                                          _ptr(pg), _ptr(pb), ws.data_ptr(), ws.numel(), _stream()))
+    return dw
+
+
 def conv3x3_dgrad(dy, w, out=None):
     """Data gradient of a 3x3 / stride-1 / pad-1 convolution (w: (Cout, 3, 3,
     Cin) OHWI): the same convolution of dy with the flipped, transposed

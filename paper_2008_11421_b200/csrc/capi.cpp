@@ -562,6 +562,18 @@ int krt_conv_im2col_bn(const void* x, const void* wk, void* C, int n, int h, int
                  "conv_im2col_bn");
 }
 
+int krt_wgrad3x3_narrow_supported(int h, int w, int C) { return wgrad3x3_halo_supported(h, w, C) ? 1 : 0; }
+
+size_t krt_wgrad3x3_narrow_workspace(int C) { return wgrad3x3_halo_workspace(C); }
+
+int krt_wgrad3x3_narrow(const void* x, const void* dy, float* dw, int n, int h, int w, int C, const float* pmean,
+                        const float* pinvstd, const void* pgamma, const void* pbeta, void* ws, size_t ws_bytes,
+                        void* stream) {
+  KRT_CUDA_GUARD(wgrad3x3_halo(x, dy, dw, n, h, w, C, pmean, pinvstd, pgamma, pbeta, ws, ws_bytes,
+                               (cudaStream_t)stream),
+                 "wgrad3x3_narrow");
+}
+
 int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue) {
   return conv3x3_halo_supported(h, w, cin, N, prologue != 0) ? 1 : 0;
 }

@@ -15,4 +15,13 @@ bool conv3x3_halo_supported(int h, int w, int cin, int N, bool pro);
 cudaError_t conv3x3_halo_fprop(const void* x, const void* wk, void* C, int n, int h, int w, int cin, int N,
                                const float* pmean, const float* pinvstd, const void* pg, const void* pb, float* part,
                                int* part_rows, cudaStream_t s);
+// Weight gradient of a 3x3 / stride-1 / pad-1 convolution with C = cin = cout
+// in {16, 32, 64} from halo windows (wgrad_halo_sm100.cu): dw [C][3][3][C] fp32
+// (OHWI, written) = sum over pixels of dy (x) f(x), f = relu(bn(.)) when pmean;
+// ws: wgrad3x3_halo_workspace(C) bytes (per-CTA partial accumulators).
+bool wgrad3x3_halo_supported(int h, int w, int C);
+size_t wgrad3x3_halo_workspace(int C);
+cudaError_t wgrad3x3_halo(const void* x, const void* dy, float* dw, int n, int h, int w, int C, const float* pmean,
+                          const float* pinvstd, const void* pg, const void* pb, void* ws, size_t ws_bytes,
+                          cudaStream_t s);
 }  // namespace krt

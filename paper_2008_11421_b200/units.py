@@ -124,6 +124,12 @@ MLP_LT = os.environ.get("KRT_MLP_LT", "1") != "0"
 # stats), data gradient at 16 channels (0.30 vs 0.34 ms).  KRT_HALO_UNITS=0:
 # cuDNN for all of them
 HALO_UNITS = os.environ.get("KRT_HALO_UNITS", "1") != "0"
+# its weight gradient on the own narrow-channel wgrad kernel
+# (csrc/wgrad_halo_sm100.cu), relu(bn1(c1)) applied in shared memory so the
+# backward never rebuilds a1: 0.32 vs 0.90 + 0.10 ms (16 channels), 0.16 vs
+# 0.31 + 0.06 ms (32), 0.11 vs 0.09 + 0.03 ms (64) against cuDNN wgrad + the
+# bn_apply it needs (scripts/bench_narrow3x3.py).  KRT_WGRAD_UNITS=0: cuDNN
+WGRAD_UNITS = os.environ.get("KRT_WGRAD_UNITS", "1") != "0"
 
 
 def _cl(t):
@@ -820,6 +826,18 @@ class PreActBottleneckUnit(_ConvNetUnit):
             _cl(grads[8]).copy_(dw3)
             dc2 = _bn_relu_bw(da2, c2, st[4], st[5], g2, b2, grads[6], grads[7])
             del da2
+        if self._narrow_wgrad():
+            # weight gradient from c1 with relu(bn1) in shared memory (a1 is
+            # never rebuilt); the data gradient on the halo kernel or cuDNN
+            bnfused.wgrad3x3_narrow(dc2, c1, grads[5], pre=(st[2], st[3], g1, b1))
+            if self._halo_dgrad():
+                da1 = bnfused.conv3x3_dgrad(dc2, w2)
+            else:
+                da1, _, _ = _conv_bw(dc2, c1, _cl(w2), self.s, 1, need_dw=False)
+            del dc2
+            dc1 = _bn_relu_bw(da1, c1, st[2], st[3], g1, b1, grads[3], grads[4])
+            del da1
+            return self._backward_conv1(dy, params, x, st, grads, dc1, tc)
         a1 = _bn_relu(c1, st[2], st[3], g1, b1)
         if self._halo_dgrad():
             # data gradient on the halo kernel (flipped, transposed weights);
@@ -832,6 +850,15 @@ class PreActBottleneckUnit(_ConvNetUnit):
         _cl(grads[5]).copy_(dw2)
         dc1 = _bn_relu_bw(da1, c1, st[2], st[3], g1, b1, grads[3], grads[4])
         del da1
+        return self._backward_conv1(dy, params, x, st, grads, dc1, tc)
+
+    def _narrow_wgrad(self):
+        return (WGRAD_UNITS and self.act == torch.bfloat16 and self.s == 1 and self.w in (16, 32, 64)
+                and bnfused.wgrad3x3_narrow_supported(self.ho, self.ho, self.w))
+
+    def _backward_conv1(self, dy, params, x, st, grads, dc1, tc):
+        """BN0 / conv1 (and the projection shortcut) backward from dc1."""
+        g0, b0, w1 = params[:3]
         a0 = _bn_relu(x, st[0], st[1], g0, b0)
         if tc and not self.down and bnfused.conv1x1_dgrad_supported(self.w, self.cin):
             # conv1 dgrad + BN0's backward reduce on the GEMM; the identity

@@ -51,6 +51,9 @@ for w, side in ((16, 2048), (32, 1024), (64, 512)):
     r["own_fprop_ms"] = timeit(lambda: bnfused.conv_im2col(x, wo, 1, 1))
     r["own_fprop_pre_stats_ms"] = timeit(lambda: bnfused.conv_im2col(x, wo, 1, 1, pre=(m, i, g, b), stats=(sm, si)))
     r["own_dgrad_ms"] = timeit(lambda: bnfused.conv3x3_dgrad(dy, wo))
+    dwo = torch.empty(w, 3, 3, w, device="cuda")
+    r["own_wgrad_ms"] = timeit(lambda: bnfused.wgrad3x3_narrow(dy, x, dwo))
+    r["own_wgrad_pre_ms"] = timeit(lambda: bnfused.wgrad3x3_narrow(dy, x, dwo, pre=(m, i, g, b)))
     r["bn_apply_ms"] = timeit(lambda: bnfused.apply(x, m, i, g, b, relu=True))
     r["bn_stats_ms"] = timeit(lambda: bnfused.stats(x, sm, si))
     r["frac_of_floor"] = {k: round(r["floor_ms"] / r[k], 3) for k in r if k.endswith("_ms") and k != "floor_ms"
