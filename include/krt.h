@@ -398,6 +398,15 @@ int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue);
  * split over the SMs into fp32 partials summed in a fixed order
  * (deterministic); ws: krt_wgrad3x3_narrow_workspace(C) bytes.  _supported: 1
  * when the shape's windows fit (KRT_WGRAD_HALO=0 disables the kernel). */
+/* Weight gradient of a 1x1 convolution with few channels (one side 64, 128
+ * or 256 channels, the other 16, 32 or 64): dw [co][ci] fp32 (written) = sum
+ * over the M pixels of dy [M, co] (x) f(x [M, ci]), NHWC bf16, f = relu(bn(.))
+ * when pmean is non-NULL; deterministic; ws: krt_wgrad1x1_narrow_workspace. */
+int krt_wgrad1x1_narrow_supported(int ci, int co);
+size_t krt_wgrad1x1_narrow_workspace(int ci, int co);
+int krt_wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M, int ci, int co, const float* pmean,
+                        const float* pinvstd, const void* pgamma, const void* pbeta, void* ws, size_t ws_bytes,
+                        void* stream);
 int krt_wgrad3x3_narrow_supported(int h, int w, int C);
 size_t krt_wgrad3x3_narrow_workspace(int C);
 int krt_wgrad3x3_narrow(const void* x, const void* dy, float* dw, int n, int h, int w, int C, const float* pmean,

@@ -343,6 +343,28 @@ def conv3x3_halo_supported(h, w, cin, cout, pre=False):
     return bool(_lib.lib().krt_conv3x3_halo_supported(h, w, cin, cout, int(pre)))
 
 
+def wgrad1x1_narrow_supported(cin, cout):
+    return bool(_lib.lib().krt_wgrad1x1_narrow_supported(cin, cout))
+
+
+def wgrad1x1_narrow(dy, x, dw, pre=None):
+    """Weight gradient of a 1x1 / stride-1 convolution with few channels on
+    tcgen05 (krt_wgrad1x1_narrow), fp32 into dw (Cout, 1, 1, Cin) contiguous.
+    pre=(mean, invstd, gamma, beta): the forward convolved relu(bn(x))."""
+    dy, x = _nhwc(dy), _nhwc(x)
+    n, ci, h, w = x.shape
+    co = dy.shape[1]
+    assert dw.dtype == torch.float32 and dw.is_contiguous() and dw.numel() == ci * co
+    L = _lib.lib()
+    ws = torch.empty(L.krt_wgrad1x1_narrow_workspace(ci, co), dtype=torch.uint8, device=x.device)
+    pm, pi, pg, pb = pre if pre is not None else (None, None, None, None)
+    M = n * h * w
+    with _timed("conv_wgrad", (x.numel() + dy.numel()) * 2 + dw.numel() * 4, 2.0 * M * ci * co):
+        _lib.check(L.krt_wgrad1x1_narrow(x.data_ptr(), dy.data_ptr(), dw.data_ptr(), M, ci, co, _ptr(pm), _ptr(pi),
+                                          _ptr(pg), _ptr(pb), ws.data_ptr(), ws.numel(), _stream()))
+    return dw
+
+
 def wgrad3x3_narrow_supported(h, w, c):
     return bool(_lib.lib().krt_wgrad3x3_narrow_supported(h, w, c))
 

@@ -574,6 +574,18 @@ int krt_wgrad3x3_narrow(const void* x, const void* dy, float* dw, int n, int h, 
                  "wgrad3x3_narrow");
 }
 
+int krt_wgrad1x1_narrow_supported(int ci, int co) { return wgrad1x1_narrow_supported(ci, co) ? 1 : 0; }
+
+size_t krt_wgrad1x1_narrow_workspace(int ci, int co) { return wgrad1x1_narrow_workspace(ci, co); }
+
+int krt_wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M, int ci, int co, const float* pmean,
+                        const float* pinvstd, const void* pgamma, const void* pbeta, void* ws, size_t ws_bytes,
+                        void* stream) {
+  KRT_CUDA_GUARD(wgrad1x1_narrow(x, dy, dw, M, ci, co, pmean, pinvstd, pgamma, pbeta, ws, ws_bytes,
+                                 (cudaStream_t)stream),
+                 "wgrad1x1_narrow");
+}
+
 int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue) {
   return conv3x3_halo_supported(h, w, cin, N, prologue != 0) ? 1 : 0;
 }

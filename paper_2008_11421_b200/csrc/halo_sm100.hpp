@@ -24,4 +24,12 @@ size_t wgrad3x3_halo_workspace(int C);
 cudaError_t wgrad3x3_halo(const void* x, const void* dy, float* dw, int n, int h, int w, int C, const float* pmean,
                           const float* pinvstd, const void* pg, const void* pb, void* ws, size_t ws_bytes,
                           cudaStream_t s);
+// Weight gradient of a 1x1 convolution with few channels (one side 64 / 128 /
+// 256, the other 16 / 32 / 64): dw [co][ci] fp32 (written) = sum over the M
+// pixels of dy [M, co] (x) f(x [M, ci]), f = relu(bn(.)) when pmean
+bool wgrad1x1_narrow_supported(int ci, int co);
+size_t wgrad1x1_narrow_workspace(int ci, int co);
+cudaError_t wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M, int ci, int co, const float* pmean,
+                            const float* pinvstd, const void* pg, const void* pb, void* ws, size_t ws_bytes,
+                            cudaStream_t s);
 }  // namespace krt

@@ -342,6 +342,218 @@ cudaError_t launch_wg(const CUtensorMap& mx, const CUtensorMap& mdy, const WgPar
   k<<<grid, wThreads, smem, s>>>(mx, mdy, p);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// 1x1 weight gradient with few channels: dW[co][ci] = sum over pixels of
+// dy[pix][co] * f(x)[pix][ci].  The wider side (>= 64 channels) is the MMA's
+// M (two 64-channel atoms per M = 128; a 64-channel side adds a junk atom),
+// the narrower side (16 .. 64) its N, the pixels its K; both operands
+// MN-major straight from their TMA tiles ([channel block][V rows][64 or fewer
+// channels]).  The BN prologue transforms the x tile in shared memory (rows
+// beyond the tensor stay zero).
+struct Wg1Params {
+  int64_t M;       // pixels
+  int ci, co, V;   // channels, pixels per tile
+  int tiles;
+  int xm;          // 1: x is the M side (ci >= co)
+  uint32_t x_bytes, dy_bytes, slot_bytes;
+  float* part;     // [gridDim.x][n_mb][128][nch]
+  const float* pmean;
+  const float* pinvstd;
+  const __nv_bfloat16* pg;
+  const __nv_bfloat16* pb;
+};
+
+// MCH: M-side channels (64, 128, 256); NCH: N-side channels (16, 32, 64)
+template <int MCH, int NCH, bool PRO>
+__global__ void __launch_bounds__(wThreads, 1) wgrad1x1_narrow_kernel(const __grid_constant__ CUtensorMap map_x,
+                                                                      const __grid_constant__ CUtensorMap map_dy,
+                                                                      Wg1Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  constexpr int kMb = MCH / 128 > 0 ? MCH / 128 : 1;   // M = 128 MMAs per K chunk
+  constexpr uint32_t kCols = kMb * NCH <= 32 ? 32 : (kMb * NCH <= 64 ? 64 : 128);
+  constexpr int kNRB = NCH * 2;                          // N-side row bytes
+  const int cix = p.ci < 64 ? p.ci : 64;                 // x tile channels per block
+  const int cbx = (p.ci + 63) / 64, cbd = (p.co + 63) / 64;
+  const int xrb = cix * 2;                               // x row bytes
+  uint8_t* slots = smem;
+  float* sc = reinterpret_cast<float*>(smem + 2 * (size_t)p.slot_bytes);
+  float* sh = sc + p.ci;
+  WgBars& B = *reinterpret_cast<WgBars*>(sh + p.ci);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.full[i], 1);
+      mbar_init(&B.ready[i], wXfThreads);
+      mbar_init(&B.empty[i], 1);
+    }
+    mbar_init(&B.done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(&B.tmem_base, kCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_base;
+  const int dyc = p.co < 64 ? p.co : 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int sl = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+        const int row0 = t * p.V;
+        mbar_wait(&B.empty[sl], ph ^ 1);
+        mbar_expect_tx(&B.full[sl], (uint32_t)p.V * (p.ci + p.co) * 2);
+        uint8_t* dst = slots + (size_t)sl * p.slot_bytes;
+        for (int cb = 0; cb < cbx; ++cb)
+          tma_load_2d(&map_x, &B.full[sl], dst + (size_t)cb * p.V * xrb, cb * 64, row0);
+        for (int cb = 0; cb < cbd; ++cb)
+          tma_load_2d(&map_dy, &B.full[sl], dst + p.x_bytes + (size_t)cb * p.V * dyc * 2, cb * 64, row0);
+        if (++sl == 2) {
+          sl = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_mn(NCH);
+    int sl = 0;
+    uint32_t ph = 0;
+    bool first = true;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      mbar_wait(&B.ready[sl], ph);
+      tc_fence_after();
+      const uint32_t base = smem_u32(slots + (size_t)sl * p.slot_bytes);
+      const uint32_t mbase = p.xm ? base : base + p.x_bytes, nbase = p.xm ? base + p.x_bytes : base;
+      for (int kc = 0; kc < p.V / 16; ++kc) {
+        const uint64_t bdesc = mn_desc<NCH>(nbase + (uint32_t)(kc * 16 * kNRB), kNRB);
+#pragma unroll
+        for (int mb = 0; mb < kMb; ++mb) {
+          // two 64-channel atoms per M = 128, p.V rows apart (a 64-channel M
+          // side repeats its one atom: LBO 0, D rows 64..127 junk)
+          const uint32_t a = mbase + (uint32_t)(mb * 2 * p.V * 128 + kc * 16 * 128);
+          umma_bf16_elect(tmem + mb * NCH, mn_desc<64>(a, MCH == 64 ? 0u : (uint32_t)p.V * 128), bdesc, idesc,
+                          first ? 0u : 1u);
+        }
+        first = false;
+      }
+      umma_commit_elect(&B.empty[sl]);
+      if (++sl == 2) {
+        sl = 0;
+        ph ^= 1;
+      }
+    }
+    umma_commit_elect(&B.done);
+  } else if (warp >= wXf0) {
+    const int xt = threadIdx.x - wXf0 * 32;
+    if (PRO) {
+      for (int c = xt; c < p.ci; c += wXfThreads) {
+        const float s = p.pinvstd[c] * __bfloat162float(p.pg[c]);
+        sc[c] = s;
+        sh[c] = __bfloat162float(p.pb[c]) - p.pmean[c] * s;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(wXfThreads) : "memory");
+    }
+    const int cpr = cix / 8;  // 16-byte chunks per x row
+    int sl = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      mbar_wait(&B.full[sl], ph);
+      if (PRO) {
+        // each thread keeps one 16-byte chunk (8 channels) per channel block
+        // and walks the tile's rows with its coefficients in registers
+        uint8_t* xb = slots + (size_t)sl * p.slot_bytes;
+        const int64_t row0 = (int64_t)t * p.V;
+        const int ch = xt % cpr, rs = wXfThreads / cpr;
+        const int vmax = (int)(p.M - row0 < p.V ? p.M - row0 : p.V);  // rows beyond the tensor: the TMA's zeros stay
+        for (int cb = 0; cb < cbx; ++cb) {
+          unsigned long long sc2[4], sh2[4];
+          const int c0 = cb * 64 + ch * 8;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            sc2[e] = ((unsigned long long)__float_as_uint(sc[c0 + 2 * e + 1]) << 32) | __float_as_uint(sc[c0 + 2 * e]);
+            sh2[e] = ((unsigned long long)__float_as_uint(sh[c0 + 2 * e + 1]) << 32) | __float_as_uint(sh[c0 + 2 * e]);
+          }
+          uint8_t* cbase = xb + (size_t)cb * p.V * xrb;
+          for (int j = xt / cpr; j < vmax; j += rs) {
+            const int sw = cix == 64 ? (ch ^ (j & 7)) : (cix == 32 ? (ch ^ ((j >> 1) & 3)) : (ch ^ ((j >> 2) & 1)));
+            uint4* cp = reinterpret_cast<uint4*>(cbase + (size_t)j * xrb + (sw << 4));
+            uint4 u = *cp;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t lo = w[e] << 16, hi = w[e] & 0xffff0000u;
+              const unsigned long long xv = ((unsigned long long)hi << 32) | lo;
+              unsigned long long yv;
+              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(yv) : "l"(xv), "l"(sc2[e]), "l"(sh2[e]));
+              uint32_t packed;
+              asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;"
+                  : "=r"(packed)
+                  : "f"(__uint_as_float((uint32_t)(yv >> 32))), "f"(__uint_as_float((uint32_t)yv)));
+              w[e] = packed;
+            }
+            *cp = u;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      mbar_arrive(&B.ready[sl]);
+      if (++sl == 2) {
+        sl = 0;
+        ph ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    mbar_wait(&B.done, 0);
+    tc_fence_after();
+    float* out = p.part + (size_t)blockIdx.x * kMb * 128 * NCH;
+    for (int mb = 0; mb < kMb; ++mb)
+      for (int c = 0; c < NCH; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + mb * NCH + c, v);
+        float* dst = out + ((size_t)mb * 128 + q * 32 + lane) * NCH + c;
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kCols);
+}
+
+// dW[co][ci] from the CTAs' partials (fixed order): D[m][n] with m the wide side
+__global__ void wgrad1x1_narrow_finalize(const float* __restrict__ part, int ctas, int ci, int co, int xm, int nmb,
+                                         int nch, float* __restrict__ dw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over co, ci
+  if (i >= ci * co) return;
+  const int c_in = i % ci, c_out = i / ci;
+  const int m = xm ? c_in : c_out, n = xm ? c_out : c_in;
+  double acc = 0.0;
+  for (int k = 0; k < ctas; ++k) acc += (double)part[((size_t)k * nmb * 128 + m) * nch + n];
+  dw[i] = (float)acc;
+}
+
+bool wg1_shape(int ci, int co) {
+  const int mch = ci > co ? ci : co, nch = ci > co ? co : ci;
+  return (mch == 64 || mch == 128 || mch == 256) && (nch == 16 || nch == 32 || nch == 64);
+}
+
+template <int MCH, int NCH, bool PRO>
+cudaError_t launch_wg1(const CUtensorMap& mx, const CUtensorMap& mdy, const Wg1Params& p, int grid, size_t smem,
+                       cudaStream_t s) {
+  auto k = wgrad1x1_narrow_kernel<MCH, NCH, PRO>;
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<grid, wThreads, smem, s>>>(mx, mdy, p);
+  return cudaGetLastError();
+}
 }  // namespace
 
 bool wgrad3x3_halo_supported(int h, int w, int C) {
@@ -413,6 +625,73 @@ cudaError_t wgrad3x3_halo(const void* x, const void* dy, float* dw, int n, int h
   if (C == 16) wgrad3x3_halo_finalize<16><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw);
   else if (C == 32) wgrad3x3_halo_finalize<32><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw);
   else wgrad3x3_halo_finalize<64><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw);
+  return cudaGetLastError();
+}
+
+bool wgrad1x1_narrow_supported(int ci, int co) { return wg_enabled() && wg1_shape(ci, co); }
+
+size_t wgrad1x1_narrow_workspace(int ci, int co) {
+  const int mch = ci > co ? ci : co, nch = ci > co ? co : ci;
+  const int nmb = mch / 128 > 0 ? mch / 128 : 1;
+  return (size_t)num_sms() * nmb * 128 * nch * sizeof(float);
+}
+
+cudaError_t wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M, int ci, int co, const float* pmean,
+                            const float* pinvstd, const void* pg, const void* pb, void* ws, size_t ws_bytes,
+                            cudaStream_t s) {
+  if (M < 1 || !wgrad1x1_narrow_supported(ci, co) || ws_bytes < wgrad1x1_narrow_workspace(ci, co))
+    return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(ws)) & 15)
+    return cudaErrorMisalignedAddress;
+  const int mch = ci > co ? ci : co, nch = ci > co ? co : ci;
+  const int nmb = mch / 128 > 0 ? mch / 128 : 1;
+  Wg1Params p{};
+  p.M = M;
+  p.ci = ci;
+  p.co = co;
+  p.xm = ci >= co ? 1 : 0;
+  // pixels per tile: two slots of (ci + co) channels in shared memory, TMA boxes <= 256 rows
+  int V = (int)((96 * 1024) / ((size_t)(ci + co) * 2)) / 16 * 16;
+  if (V > 256) V = 256;
+  if (V < 16) return cudaErrorInvalidValue;
+  p.V = V;
+  p.tiles = (int)((M + V - 1) / V);
+  const int cix = ci < 64 ? ci : 64, dyc = co < 64 ? co : 64;
+  p.x_bytes = (uint32_t)r1k((size_t)((ci + 63) / 64) * V * cix * 2);
+  p.dy_bytes = (uint32_t)r1k((size_t)((co + 63) / 64) * V * dyc * 2);
+  p.slot_bytes = p.x_bytes + p.dy_bytes;
+  p.part = static_cast<float*>(ws);
+  p.pmean = pmean;
+  p.pinvstd = pinvstd;
+  p.pg = static_cast<const __nv_bfloat16*>(pg);
+  p.pb = static_cast<const __nv_bfloat16*>(pb);
+  auto swz = [](int c) {
+    return c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : (c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  };
+  CUtensorMap mx, mdy;
+  if (!make_map(&mx, x, M, ci, V, cix, swz(cix)) || !make_map(&mdy, dy, M, co, V, dyc, swz(dyc)))
+    return cudaErrorInvalidValue;
+  int grid = num_sms();
+  if (grid > p.tiles) grid = p.tiles;
+  const size_t smem = 2 * (size_t)p.slot_bytes + 2 * (size_t)ci * 4 + sizeof(WgBars) + 1024;
+  const bool pro = pmean != nullptr;
+  cudaError_t e = cudaErrorInvalidValue;
+#define KRT_WG1(MC, NC)                                                                                  \
+  if (mch == MC && nch == NC)                                                                            \
+    e = pro ? launch_wg1<MC, NC, true>(mx, mdy, p, grid, smem, s) : launch_wg1<MC, NC, false>(mx, mdy, p, grid, smem, s);
+  KRT_WG1(64, 16)
+  KRT_WG1(128, 32)
+  KRT_WG1(256, 64)
+  KRT_WG1(64, 64)
+  KRT_WG1(128, 16)
+  KRT_WG1(128, 64)
+  KRT_WG1(256, 16)
+  KRT_WG1(256, 32)
+  KRT_WG1(64, 32)
+#undef KRT_WG1
+  if (e != cudaSuccess) return e;
+  const int total = ci * co, thr = 256;
+  wgrad1x1_narrow_finalize<<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, ci, co, p.xm, nmb, nch, dw);
   return cudaGetLastError();
 }
 

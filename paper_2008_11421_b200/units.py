@@ -812,8 +812,14 @@ class PreActBottleneckUnit(_ConvNetUnit):
         x, c1, c2 = (_cl(t) for t in saved[:3])
         st = self._st(saved[3])
         tc = self._tc1x1() and TC_DGRAD_PREACT
-        a2 = _bn_relu(c2, st[4], st[5], g2, b2)
-        if tc and bnfused.conv1x1_dgrad_supported(self.cout, self.w):
+        if tc and self._narrow_wgrad1(self.w, self.cout) and bnfused.conv1x1_dgrad_supported(self.cout, self.w):
+            # conv3's weight gradient from c2 with relu(bn2) in shared memory
+            # (a2 never rebuilt); its dgrad with BN2's backward reduce on the GEMM
+            bnfused.wgrad1x1_narrow(dy, c2, grads[8], pre=(st[4], st[5], g2, b2))
+            dc2 = bnfused.conv1x1_dgrad_bn_backward(dy, _cl(w3), c2, st[4], st[5], g2, b2, dgamma=grads[6],
+                                                    dbeta=grads[7])
+        elif tc and bnfused.conv1x1_dgrad_supported(self.cout, self.w):
+            a2 = _bn_relu(c2, st[4], st[5], g2, b2)
             # conv3 dgrad on the tcgen05 GEMM with BN2's backward reduce in its epilogue
             _, dw3, _ = _conv_bw(dy, a2, _cl(w3), 1, 0, need_dx=False)
             del a2
@@ -821,6 +827,7 @@ class PreActBottleneckUnit(_ConvNetUnit):
             dc2 = bnfused.conv1x1_dgrad_bn_backward(dy, _cl(w3), c2, st[4], st[5], g2, b2, dgamma=grads[6],
                                                     dbeta=grads[7])
         else:
+            a2 = _bn_relu(c2, st[4], st[5], g2, b2)
             da2, dw3, _ = _conv_bw(dy, a2, _cl(w3), 1, 0)
             del a2
             _cl(grads[8]).copy_(dw3)
@@ -856,9 +863,20 @@ class PreActBottleneckUnit(_ConvNetUnit):
         return (WGRAD_UNITS and self.act == torch.bfloat16 and self.s == 1 and self.w in (16, 32, 64)
                 and bnfused.wgrad3x3_narrow_supported(self.ho, self.ho, self.w))
 
+    def _narrow_wgrad1(self, cin, cout):
+        return WGRAD_UNITS and self.act == torch.bfloat16 and bnfused.wgrad1x1_narrow_supported(cin, cout)
+
     def _backward_conv1(self, dy, params, x, st, grads, dc1, tc):
         """BN0 / conv1 (and the projection shortcut) backward from dc1."""
         g0, b0, w1 = params[:3]
+        if (tc and not self.down and self._narrow_wgrad1(self.cin, self.w)
+                and bnfused.conv1x1_dgrad_supported(self.w, self.cin)):
+            # conv1's weight gradient from x with relu(bn0) in shared memory (a0
+            # never rebuilt); dgrad + BN0's backward reduce on the GEMM, the
+            # identity shortcut's gradient dy added in the elementwise pass
+            bnfused.wgrad1x1_narrow(dc1, x, grads[2], pre=(st[0], st[1], g0, b0))
+            return bnfused.conv1x1_dgrad_bn_backward(dc1, _cl(w1), x, st[0], st[1], g0, b0, dgamma=grads[0],
+                                                     dbeta=grads[1], addend=dy)
         a0 = _bn_relu(x, st[0], st[1], g0, b0)
         if tc and not self.down and bnfused.conv1x1_dgrad_supported(self.w, self.cin):
             # conv1 dgrad + BN0's backward reduce on the GEMM; the identity

@@ -49,3 +49,29 @@ def test_wgrad_narrow_matches_torch(n, c, h, w, pre):
     dw2 = torch.empty_like(dw)
     bnfused.wgrad3x3_narrow(dy, x, dw2, pre=pre_t)
     assert torch.equal(dw, dw2)
+
+
+@pytest.mark.parametrize("n,ci,co,h,w", [(2, 64, 16, 9, 13), (1, 16, 64, 33, 20), (2, 128, 32, 17, 9),
+                                         (1, 32, 128, 8, 70), (1, 256, 64, 12, 11), (2, 64, 256, 7, 9),
+                                         (2, 64, 64, 16, 16)])
+@pytest.mark.parametrize("pre", [False, True])
+def test_wgrad1x1_narrow_matches_torch(n, ci, co, h, w, pre):
+    assert bnfused.wgrad1x1_narrow_supported(ci, co)
+    x = cl(rand((n, ci, h, w), 3, 2.0))
+    dy = cl(rand((n, co, h, w), 4))
+    if pre:
+        g = (1 + 0.2 * torch.randn(ci, device="cuda")).to(torch.bfloat16)
+        b = (0.1 * torch.randn(ci, device="cuda")).to(torch.bfloat16)
+        m, i = torch.empty(ci, device="cuda"), torch.empty(ci, device="cuda")
+        bnfused.stats(x, m, i)
+        a, pre_t = bnfused.apply(x, m, i, g, b, relu=True), (m, i, g, b)
+    else:
+        a, pre_t = x, None
+    dw = torch.empty(co, 1, 1, ci, device="cuda")
+    bnfused.wgrad1x1_narrow(dy, x, dw, pre=pre_t)
+    ref = torch.einsum("nchw,nkhw->kc", a.float(), dy.float()).view(co, 1, 1, ci)
+    err = float((dw - ref).abs().max() / ref.abs().max())
+    assert err < 2e-3, err
+    dw2 = torch.empty_like(dw)
+    bnfused.wgrad1x1_narrow(dy, x, dw2, pre=pre_t)
+    assert torch.equal(dw, dw2)
