@@ -93,7 +93,7 @@ constexpr int kMaxAstatK = 256;
 constexpr int kAstatSlots = kMaxAstatK / kBK + 1;
 constexpr int kMaxNT = 8;  // n-tiles per CTA in A-stationary mode (N <= 2048)
 
-// EPI 3 residual tiles: [BN / kResW boxes][128 rows][kResW columns], each box
+// EPI 3 / 4 residual tiles: [BN / kResW boxes][128 rows][kResW columns], each box
 // TMA-loaded with the swizzle of its row width, kResBufs tiles in flight
 template <int BN>
 constexpr int kResW = BN < 64 ? BN : 64;
@@ -127,12 +127,13 @@ struct Smem {
   // EPI 2: the BN input x of the current tile pair, TMA-loaded by the producer
   // ahead of the epilogue (row-major [128][BN]); one buffer per accumulator.
   // EPI 3: the residual tiles (swizzled boxes), kResBufs deep
-  alignas(1024) uint8_t xt[EPI == 2 ? 2 : (EPI == 3 ? kResBufs<BN> : 1)][EPI >= 2 ? kBM * BN * 2 : 16];
+  alignas(1024) uint8_t xt[EPI == 2 ? 2 : (EPI >= 3 ? kResBufs<BN> : 1)][EPI >= 2 ? kBM * BN * 2 : 16];
   uint64_t x_full[4], x_empty[4];
 };
 
 // EPI: 0 store only, 1 + batch statistics of C, 2 + BN-backward reduce of C,
-// 3 C = acc + residual (p.res through map_x)
+// 3 C = acc + residual (p.res through map_x), 4 = 3 + the batch statistics of
+// that C (the next pre-activation unit's BN0 statistics)
 // PAIR: CTA pair (cluster of 2, tcgen05 cta_group::2).  A pair tile is 256
 // rows x BN columns: each CTA loads its own 128 A rows and half of the B rows,
 // the leader (rank 0) issues M = 256 MMAs that write 128 accumulator rows into
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   static_assert(!BSTAT || !ASTAT, "B-stationary needs a fixed n-tile");
   auto& S = *reinterpret_cast<Smem<BN, STAGES, PRO || GATHER, ASTAT, EPI, BKT, BSTAT, PAIR>*>(smem_raw);
-  static_assert(!PAIR || (!ASTAT && !GATHER && !BSTAT && BKT == kBK && EPI != 3), "pair: streamed 64-wide k-blocks");
+  static_assert(!PAIR || (!ASTAT && !GATHER && !BSTAT && BKT == kBK && EPI < 3), "pair: streamed 64-wide k-blocks");
   static_assert(!GATHER || (!PRO && !ASTAT), "gathered A has no prologue");
   static_assert(!IM2A || (!GATHER && !ASTAT && BKT == kBK), "im2col A: 64-channel k-blocks, streamed");
   static_assert(!ASTAT || (BKT == kBK && BN >= 64), "A-stationary uses 64-wide k-blocks and n-tiles");
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
     // own slots of the partial rows, zeroed first and then added to with
     // fire-and-forget reductions (no load latency in the epilogue; no
     // dynamically indexed local arrays)
-    constexpr bool kStats = EPI == 1 || EPI == 2;
+    constexpr bool kStats = EPI == 1 || EPI == 2 || EPI == 4;
     const int mgroup = PAIR ? 2 * m_first + (int)rank : m_first;  // partial-row group of this CTA
     float* part_row = kStats ? p.part + (((size_t)mgroup * 4 + q) * kEpiGroups + grp) * 2 * p.N : nullptr;
     if (ASTAT && kStats) {
@@ -674,9 +675,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
       const int n_tile = ASTAT ? nt : n_fixed;
       const int64_t row0 = rowbase(mt) + q * 32;
       const bool valid = row0 + lane < p.M;
-      const int rb = EPI == 3 ? t % kResBufs<BN> : 0;  // residual buffer of this tile
+      const int rb = EPI >= 3 ? t % kResBufs<BN> : 0;  // residual buffer of this tile
       mbar_wait(&S.tfull[acc], acc_phase);
-      if (EPI == 3) mbar_wait(&S.x_full[rb], (uint32_t)(t / kResBufs<BN>) & 1u);
+      if (EPI >= 3) mbar_wait(&S.x_full[rb], (uint32_t)(t / kResBufs<BN>) & 1u);
       if (EPI == 2) mbar_wait(&S.x_full[acc], acc_phase);  // x tiles alternate with the accumulators
       tc_fence_after();
 #pragma unroll
@@ -694,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         uint4* st = reinterpret_cast<uint4*>(S.cstage[ew][sbuf] + lane * kCW * 2);
 #pragma unroll
         for (int j = 0; j < kCW / 8; ++j) {
-          if (EPI == 3) {
+          if (EPI >= 3) {
             // chunk j of this row in its residual box (row-per-lane reads of
             // the swizzled box: 8 lanes of a phase hit 8 distinct bank groups)
             constexpr int RW = kResW<BN>;
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
             acc_q[c] += t2;
           }
         }
-        if (EPI == 1) {
+        if (EPI == 1 || EPI == 4) {
           // column `lane` of the staged (stored) bf16 chunk, rows in order;
           // rows beyond M were staged as zeros.  16-wide chunks: lanes 16..31
           // take rows 16..31 of the same columns, folded in with one shuffle
@@ -806,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv1x1_kernel(const __grid_const
         mbar_arrive(&S.tempty[acc]);
       }
       if (EPI == 2) mbar_arrive(&S.x_empty[acc]);
-      if (EPI == 3) mbar_arrive(&S.x_empty[rb]);
+      if (EPI >= 3) mbar_arrive(&S.x_empty[rb]);
      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
@@ -955,7 +956,7 @@ cudaError_t dispatch_ring(const CUtensorMap& ma, const CUtensorMap& mb, const CU
   // deepest ring that fits next to everything else (227 KB per CTA)
   constexpr int fixed = (PRO || GATHER ? 2 * kMaxProK * 4 : 0) + kEpiWarps * (ASTAT ? 1 : 2) * 32 * 64 +
                         (ASTAT ? kAstatSlots * kBM * kBK * 2 : 0) + (EPI == 2 ? 2 * kBM * BN * 2 : 0) +
-                        (EPI == 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? kBSlots<BN, BKT> * BN * BKT * 2 : 0);
+                        (EPI >= 3 ? kResBufs<BN> * kBM * BN * 2 : 0) + (bstat ? kBSlots<BN, BKT> * BN * BKT * 2 : 0);
   constexpr int stage_bytes = (ASTAT ? BN : kBM + (bstat ? 0 : (PAIR ? BN / 2 : BN))) * BKT * 2;
   constexpr int avail = 220 * 1024 - fixed;
   constexpr int max_stages = 8 * kBK / BKT;  // same bytes in flight for narrow k-blocks
@@ -1002,11 +1003,15 @@ cudaError_t dispatch_stages(const CUtensorMap& ma, const CUtensorMap& mb, const 
 // EPI 3 (residual) instantiations: n-tiles up to 128 columns, never
 // A-stationary (its A region and the residual ring do not both fit)
 template <int BKT>
-cudaError_t dispatch_res(int BN, bool pro, const CUtensorMap& ma, const CUtensorMap& mb,
+cudaError_t dispatch_res(int BN, bool pro, bool st, const CUtensorMap& ma, const CUtensorMap& mb,
                          const CUtensorMap& mc, const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
-#define KRT_GEMM_RES(BNV)                                                                   \
-  if (BN == BNV) return pro ? dispatch_stages<BNV, true, 3, false, BKT>(ma, mb, mc, mx, p, grid, s) \
-                            : dispatch_stages<BNV, false, 3, false, BKT>(ma, mb, mc, mx, p, grid, s);
+#define KRT_GEMM_RES(BNV)                                                                                   \
+  if (BN == BNV) {                                                                                          \
+    if (st) return pro ? dispatch_stages<BNV, true, 4, false, BKT>(ma, mb, mc, mx, p, grid, s)               \
+                       : dispatch_stages<BNV, false, 4, false, BKT>(ma, mb, mc, mx, p, grid, s);             \
+    return pro ? dispatch_stages<BNV, true, 3, false, BKT>(ma, mb, mc, mx, p, grid, s)                       \
+               : dispatch_stages<BNV, false, 3, false, BKT>(ma, mb, mc, mx, p, grid, s);                     \
+  }
   KRT_GEMM_RES(16)
   KRT_GEMM_RES(32)
   KRT_GEMM_RES(64)
@@ -1060,7 +1065,6 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   if (res != nullptr && (reinterpret_cast<uintptr_t>(res) & 15)) return cudaErrorMisalignedAddress;
   const bool bwd = bx != nullptr;
   if (bwd && (pmean != nullptr || part == nullptr || N < 64 || res != nullptr)) return cudaErrorInvalidValue;
-  if (res_mode && part != nullptr) return cudaErrorInvalidValue;  // no statistics with the residual epilogue
   // narrow reductions (K = 16, 32: the first stages of ResNet-1001) use one
   // K-wide k-block whose row is the 32/64-byte swizzle span
   const int bkt = K < kBK ? K : kBK;
@@ -1099,9 +1103,9 @@ cudaError_t conv1x1_impl(const void* A, const void* B, void* C, int64_t M, int N
   if (part_rows) *part_rows = per * (pair ? 2 : 1) * 4 * epi_groups;  // every row and column written exactly once
   if (pair && !make_map(&mb, B, N, K, BN / 2, bkt, ksw)) return cudaErrorInvalidValue;  // half the n-tile per CTA
   if (res_mode) {
-    if (bkt == 16) return dispatch_res<16>(BN, pro, ma, mb, mc, mx, p, grid, s);
-    if (bkt == 32) return dispatch_res<32>(BN, pro, ma, mb, mc, mx, p, grid, s);
-    return dispatch_res<kBK>(BN, pro, ma, mb, mc, mx, p, grid, s);
+    if (bkt == 16) return dispatch_res<16>(BN, pro, st, ma, mb, mc, mx, p, grid, s);
+    if (bkt == 32) return dispatch_res<32>(BN, pro, st, ma, mb, mc, mx, p, grid, s);
+    return dispatch_res<kBK>(BN, pro, st, ma, mb, mc, mx, p, grid, s);
   }
   if (bkt != kBK) {  // no A-stationary instantiations for narrow k-blocks
     if (bwd) {

@@ -134,6 +134,9 @@ class Executor:
     def __init__(self, units: Sequence[Unit], bundle: PlanBundle, batch: int,
                  loss_fn: Callable, cfg: ExecConfig = ExecConfig()):
         self.units = list(units)
+        for prev, u in zip(self.units, self.units[1:]):
+            if hasattr(u, "prev_unit"):   # the unit whose forward output u takes (units.py STATS_HANDOFF)
+                u.prev_unit = prev
         self.bundle = bundle
         self.batch = batch
         self.loss_fn = loss_fn

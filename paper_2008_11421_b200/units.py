@@ -130,6 +130,13 @@ HALO_UNITS = os.environ.get("KRT_HALO_UNITS", "1") != "0"
 # 0.31 + 0.06 ms (32), 0.11 vs 0.09 + 0.03 ms (64) against cuDNN wgrad + the
 # bn_apply it needs (scripts/bench_narrow3x3.py).  KRT_WGRAD_UNITS=0: cuDNN
 WGRAD_UNITS = os.environ.get("KRT_WGRAD_UNITS", "1") != "0"
+# BN0 statistics of a pre-activation unit's input taken from the previous
+# unit's conv3 + shortcut GEMM epilogue instead of a bn_stats pass over it.
+# The executor hands a unit its producer's latest forward output in every
+# path (handoff or regeneration, executor.py _block_input), so in-core and
+# out-of-core runs take the statistics from the same place (bitwise equal).
+# KRT_STATS_HANDOFF=0: bn_stats
+STATS_HANDOFF = os.environ.get("KRT_STATS_HANDOFF", "1") != "0"
 
 
 def _cl(t):
@@ -704,6 +711,9 @@ class PreActBottleneckUnit(_ConvNetUnit):
         self.cout = 4 * width
         self.hi, self.ho = side_in, side_in // stride
         self.down = stride != 1 or cin != self.cout
+        self.prev_unit = None     # set by the executor: the unit whose output this one takes
+        self._ostats = None       # fp32 [2, cout]: batch statistics of the latest forward output
+        self._ostats_ptr = None   # ... and that output's address
 
     def param_specs(self):
         p = [(self.cin,), (self.cin,), (self.w, 1, 1, self.cin),
@@ -753,7 +763,12 @@ class PreActBottleneckUnit(_ConvNetUnit):
         shortcut is strided), BN1 statistics from conv1's epilogue, relu(bn2)
         in conv3's prologue and the shortcut added in its epilogue."""
         g0, b0, w1, g1, b1, w2, g2, b2, w3 = params[:9]
-        _stats_fw(x, st[0], st[1])
+        src = self._input_stats(x)
+        if src is not None:
+            st[0].copy_(src[0])
+            st[1].copy_(src[1])
+        else:
+            _stats_fw(x, st[0], st[1])
         bn0 = (st[0], st[1], g0, b0)
         c1 = bnfused.conv1x1(x, _cl(w1), out=sv(1), pre=bn0, stats=(st[2], st[3]))
         if not self.down:
@@ -773,7 +788,22 @@ class PreActBottleneckUnit(_ConvNetUnit):
             c2 = _conv_into(a1, _cl(w2), self.s, 1, sv(2))
             del a1
             _stats_fw(c2, st[4], st[5])
-        return bnfused.conv1x1(c2, _cl(w3), out=out, pre=(st[4], st[5], g2, b2), res=sc)
+        ostats = None
+        if STATS_HANDOFF:
+            if self._ostats is None or self._ostats.device != c2.device:
+                self._ostats = torch.empty(2, self.cout, dtype=torch.float32, device=c2.device)
+            ostats = (self._ostats[0], self._ostats[1])
+        y = bnfused.conv1x1(c2, _cl(w3), out=out, pre=(st[4], st[5], g2, b2), res=sc, stats=ostats)
+        self._ostats_ptr = y.data_ptr() if ostats is not None else None
+        return y
+
+    def _input_stats(self, x):
+        """The producer's epilogue statistics of x, when x is its latest output."""
+        p = self.prev_unit
+        if (STATS_HANDOFF and isinstance(p, PreActBottleneckUnit) and p._ostats_ptr is not None
+                and p._ostats_ptr == x.data_ptr() and p.cout == self.cin):
+            return p._ostats[0], p._ostats[1]
+        return None
 
     def _halo_fwd(self):
         return (HALO_UNITS and self.act == torch.bfloat16 and self.s == 1 and self.w in (16, 32)

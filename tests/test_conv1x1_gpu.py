@@ -108,8 +108,8 @@ def test_conv1x1_dgrad_bn_backward(n, cin, cout, hw):
 @pytest.mark.parametrize("pre", [True, False])
 def test_conv1x1_residual_epilogue(n, cin, cout, hw, pre):
     """C = relu(bn(x)) . W^T + res, the residual tile TMA-loaded into the
-    epilogue (the pre-activation bottleneck's conv3 + shortcut)."""
-    from paper_2008_11421_b200 import _lib
+    epilogue (the pre-activation bottleneck's conv3 + shortcut), with and
+    without the batch statistics of C."""
     x = cl(rand((n, cin, hw, hw), 5, 2.0))
     w = cl(rand((cout, cin, 1, 1), 6, cin ** -0.5))
     res = cl(rand((n, cout, hw, hw), 7))
@@ -131,9 +131,15 @@ def test_conv1x1_residual_epilogue(n, cin, cout, hw, pre):
     bound = 2 ** -7 * (plain.float().abs() + res.float().abs()) + 1e-3   # one bf16 ulp of each term
     assert ((y.float() - (plain.float() + res.float())).abs() <= bound).all()
     assert torch.equal(y, bnfused.conv1x1(x, w, pre=pre_t, res=res))   # deterministic
-    with pytest.raises(_lib.KrtError):   # statistics are not reduced with the residual epilogue
-        bnfused.conv1x1(x, w, pre=pre_t, res=res, stats=(torch.empty(cout, device="cuda"),
-                                                         torch.empty(cout, device="cuda")))
+    # EPI 4: the statistics of the stored sum reduced in the same epilogue
+    # (the next pre-activation unit's BN0 statistics), vs the stats kernel
+    sm, si = torch.empty(cout, device="cuda"), torch.empty(cout, device="cuda")
+    y2 = bnfused.conv1x1(x, w, pre=pre_t, res=res, stats=(sm, si))
+    assert torch.equal(y2, y)
+    rm, ri = torch.empty_like(sm), torch.empty_like(si)
+    bnfused.stats(y, rm, ri)
+    torch.testing.assert_close(sm, rm, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(si, ri, rtol=1e-4, atol=1e-5)
 
 
 @pytest.mark.parametrize("n,cout,cin,hw", [(4, 16, 64, 40), (2, 32, 128, 50), (8, 64, 256, 30), (2, 256, 64, 150)])
