@@ -200,11 +200,16 @@ def _resnet1001():
     # that plan (21.0 GB swapped) measures 1.410 samples/s, 1.5% stall, vs
     # 1.352 and 3.1% for the 2.46e13 plan on the same box.  After B-stationary
     # narrow GEMMs: 3.0e13 (19.3 GB swapped) measures 1.49 samples/s, 0.3%
-    # stall, vs 1.456 and 2.4% for the 2.76e13 plan (same box, twice each)
+    # stall, vs 1.456 and 2.4% for the 2.76e13 plan (same box, twice each).
+    # Round 2 session 3 (halo 3x3 forward, narrow weight gradients, BN0
+    # statistics hand-over: the compute stream ~20% faster): the 3.0e13 plan
+    # measures 1.758 samples/s with 4.2% exposed stall; plans at 3.4e13 /
+    # 3.7e13 / 4.0e13 measure 1.772 / 1.768 / 1.769 with 3.1-3.2% (same box,
+    # profiles/round2_s3/replan_resnet1001.md) -> 3.4e13
     units = resnet1001_units(res=2048, classes=10, depth=1001)
     make("resnet1001_2048_b2", units, 2, 150e9,
          {"family": "preact", "depth": 1001, "res": 2048, "classes": 10, "act": "bf16"}, max_blocks=64,
-         compute_rate=3.0e13)
+         compute_rate=3.4e13)
 
 
 def _megatron():
