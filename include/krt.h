@@ -402,6 +402,15 @@ int krt_conv3x3_halo_supported(int h, int w, int cin, int N, int prologue);
  * or 256 channels, the other 16, 32 or 64): dw [co][ci] fp32 (written) = sum
  * over the M pixels of dy [M, co] (x) f(x [M, ci]), NHWC bf16, f = relu(bn(.))
  * when pmean is non-NULL; deterministic; ws: krt_wgrad1x1_narrow_workspace. */
+/* Weight gradient of the ResNet stem convolution (7x7 / stride 2 / pad 3, 3
+ * input and 64 output channels; the counterpart of krt_conv_gather_bn) on
+ * tcgen05: x4 [n, h, w, 4] NHWC bf16 (RGB padded to 4 channels, krt_pad_rgb4),
+ * dc [n, ho, wo, 64] bf16 the output gradient -> dw [64][7][7][3] fp32 (OHWI,
+ * written).  The 7x7 windows are gathered into shared memory, never written;
+ * fixed-order CTA sums (deterministic); ws: krt_stem_wgrad_workspace() bytes. */
+size_t krt_stem_wgrad_workspace(void);
+int krt_stem_wgrad(const void* x4, const void* dc, float* dw, int n, int h, int w, void* ws, size_t ws_bytes,
+                   void* stream);
 int krt_wgrad1x1_narrow_supported(int ci, int co);
 size_t krt_wgrad1x1_narrow_workspace(int ci, int co);
 int krt_wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M, int ci, int co, const float* pmean,

@@ -119,6 +119,8 @@ EXPORTS = {
     "krt_conv_im2col_bn": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 10 + [C.c_void_p] * 12),
     "krt_conv_wgrad_workspace_bytes": (C.c_size_t, [C.c_int] * 6),
     "krt_conv3x3_halo_supported": (C.c_int, [C.c_int] * 5),
+    "krt_stem_wgrad_workspace": (C.c_size_t, []),
+    "krt_stem_wgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 3 + [C.c_void_p, C.c_size_t, C.c_void_p]),
     "krt_wgrad1x1_narrow_supported": (C.c_int, [C.c_int] * 2),
     "krt_wgrad1x1_narrow_workspace": (C.c_size_t, [C.c_int] * 2),
     "krt_wgrad1x1_narrow": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 5

@@ -224,6 +224,27 @@ def conv1x1(x, w, out=None, pre=None, stats=None, res=None):
     return y
 
 
+def stem_wgrad(dc, x, dw):
+    """Weight gradient of the ResNet stem convolution (7x7 / stride 2 / pad 3,
+    3 -> 64 channels) on tcgen05 (krt_stem_wgrad): fp32 into dw (64, 7, 7, 3)
+    OHWI contiguous.  dc: (N, 64, Ho, Wo) channels_last bf16 output gradient;
+    x: (N, 3, H, W) channels_last bf16 input."""
+    x, dc = _nhwc(x), _nhwc(dc)
+    n, cin, h, ww = x.shape
+    assert cin == 3 and dc.shape[1] == 64 and dw.dtype == torch.float32 and dw.is_contiguous()
+    assert dw.numel() == 64 * 49 * 3
+    x4 = torch.empty((n, 4, h, ww), dtype=x.dtype, device=x.device, memory_format=torch.channels_last)
+    with _timed("pad_rgb4", n * h * ww * (6 + 8)):
+        _lib.check(_lib.lib().krt_pad_rgb4(x.data_ptr(), x4.data_ptr(), n * h * ww, _stream()))
+    L = _lib.lib()
+    ws = torch.empty(L.krt_stem_wgrad_workspace(), dtype=torch.uint8, device=x.device)
+    P = dc.numel() // 64
+    with _timed("conv_wgrad", x4.numel() * 2 + dc.numel() * 2 + dw.numel() * 4, 2.0 * P * 64 * 49 * 3):
+        _lib.check(L.krt_stem_wgrad(x4.data_ptr(), dc.data_ptr(), dw.data_ptr(), n, h, ww, ws.data_ptr(), ws.numel(),
+                                    _stream()))
+    return dw
+
+
 def conv_gather(x, w, stride, pad, out=None, stats=None):
     """Implicit-GEMM convolution on tcgen05 (the ResNet stem, 64 output
     channels): im2col rows gathered into shared memory, never written.

@@ -574,6 +574,13 @@ int krt_wgrad3x3_narrow(const void* x, const void* dy, float* dw, int n, int h, 
                  "wgrad3x3_narrow");
 }
 
+size_t krt_stem_wgrad_workspace(void) { return stem_wgrad_workspace(); }
+
+int krt_stem_wgrad(const void* x4, const void* dc, float* dw, int n, int h, int w, void* ws, size_t ws_bytes,
+                   void* stream) {
+  KRT_CUDA_GUARD(stem_wgrad(x4, dc, dw, n, h, w, ws, ws_bytes, (cudaStream_t)stream), "stem_wgrad");
+}
+
 int krt_wgrad1x1_narrow_supported(int ci, int co) { return wgrad1x1_narrow_supported(ci, co) ? 1 : 0; }
 
 size_t krt_wgrad1x1_narrow_workspace(int ci, int co) { return wgrad1x1_narrow_workspace(ci, co); }

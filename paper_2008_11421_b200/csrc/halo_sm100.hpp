@@ -32,4 +32,10 @@ size_t wgrad1x1_narrow_workspace(int ci, int co);
 cudaError_t wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M, int ci, int co, const float* pmean,
                             const float* pinvstd, const void* pg, const void* pb, void* ws, size_t ws_bytes,
                             cudaStream_t s);
+// The ResNet stem's weight gradient (7x7 / stride 2 / pad 3, 64 output
+// channels): x4 [n, h, w, 4] bf16 (RGB padded to 4 channels, krt_pad_rgb4),
+// dc [n, ho, wo, 64] bf16 -> dw [64][7][7][3] fp32 (OHWI, written)
+size_t stem_wgrad_workspace();
+cudaError_t stem_wgrad(const void* x4, const void* dc, float* dw, int n, int h, int w, void* ws, size_t ws_bytes,
+                       cudaStream_t s);
 }  // namespace krt

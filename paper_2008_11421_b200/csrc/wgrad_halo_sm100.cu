@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(wThreads, 1) wgrad3x3_halo_kernel(const __grid
     // after the CTA's last MMA: every accumulator's 128 lanes x C columns
     // into this CTA's partial block
     const int q = warp & 3;
-    mbar_wait(&B.done, 0);
+    mbar_wait_sleep(&B.done, 0, 4000);
     tc_fence_after();
     float* out = p.part + (size_t)blockIdx.x * kAcc * 128 * C;
     for (int a = 0; a < kAcc; ++a)
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(wThreads, 1) wgrad1x1_narrow_kernel(const __gr
     }
   } else {
     const int q = warp & 3;
-    mbar_wait(&B.done, 0);
+    mbar_wait_sleep(&B.done, 0, 4000);
     tc_fence_after();
     float* out = p.part + (size_t)blockIdx.x * kMb * 128 * NCH;
     for (int mb = 0; mb < kMb; ++mb)
@@ -553,6 +553,184 @@ cudaError_t launch_wg1(const CUtensorMap& mx, const CUtensorMap& mdy, const Wg1P
   }
   k<<<grid, wThreads, smem, s>>>(mx, mdy, p);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// The ResNet stem's weight gradient (7x7 / stride 2 / pad 3, 4-channel padded
+// RGB input, 64 output channels): dW[co][kh][kw][c] = sum over output pixels
+// of dc[pix][co] * x4[2*oh - 3 + kh][2*ow - 3 + kw][c].  Per tile of V output
+// pixels the gather warps build each pixel's 7x7x4 window (49 taps x 8 bytes;
+// taps 49..63 zero) as four 64-element SW128 atoms ([atom][V rows][64]) - the
+// MN-major A operand, M = (tap, c) in two M = 128 blocks; dc arrives by TMA
+// as the MN-major B operand (N = 64); pixels are K.  cuDNN runs this on a
+// legacy sm80 kernel (~9 ms per b3072 step) after an NHWC padding kernel.
+struct StemWgParams {
+  int n, H, W, Ho, Wo;
+  int64_t M;  // output pixels
+  int V, tiles;
+  uint32_t a_bytes, slot_bytes;
+  const uint2* x4;  // [n, H, W] pixels of 4 bf16
+  float* part;      // [gridDim.x][2][128][64]
+};
+
+constexpr int sGather = 384;                      // 12 gather warps
+constexpr int sThreads = 64 + 128 + sGather;
+
+__global__ void __launch_bounds__(sThreads, 1) stem_wgrad_kernel(const __grid_constant__ CUtensorMap map_dc,
+                                                                 StemWgParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint8_t* slots = smem;
+  WgBars& B = *reinterpret_cast<WgBars*>(smem + 2 * (size_t)p.slot_bytes);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&B.full[i], 1);
+      mbar_init(&B.ready[i], sGather);
+      mbar_init(&B.empty[i], 1);
+    }
+    mbar_init(&B.done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // atom 3's chunks 1..7 (taps 50..63) are never gathered: zero them once
+  for (int i = threadIdx.x; i < 2 * p.V * 7; i += blockDim.x) {
+    const int sl = i / (p.V * 7), r = (i / 7) % p.V, cc = 1 + i % 7;
+    *reinterpret_cast<uint4*>(slots + (size_t)sl * p.slot_bytes + (size_t)3 * p.V * 128 + (size_t)r * 128 +
+                              ((cc ^ (r & 7)) << 4)) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (warp == 1) tmem_alloc(&B.tmem_base, 128);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int sl = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+        mbar_wait(&B.empty[sl], ph ^ 1);
+        mbar_expect_tx(&B.full[sl], (uint32_t)p.V * 128);
+        tma_load_2d(&map_dc, &B.full[sl], slots + (size_t)sl * p.slot_bytes + p.a_bytes, 0, t * p.V);
+        if (++sl == 2) {
+          sl = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_mn(64);
+    int sl = 0;
+    uint32_t ph = 0;
+    bool first = true;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      mbar_wait(&B.full[sl], ph);
+      mbar_wait(&B.ready[sl], ph);
+      tc_fence_after();
+      const uint32_t abase = smem_u32(slots + (size_t)sl * p.slot_bytes), dbase = abase + p.a_bytes;
+      for (int kc = 0; kc < p.V / 16; ++kc) {
+        const uint64_t bdesc = mn_desc<64>(dbase + (uint32_t)(kc * 16 * 128), 128);
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+          umma_bf16_elect(tmem + mb * 64,
+                          mn_desc<64>(abase + (uint32_t)(mb * 2 * p.V * 128 + kc * 16 * 128), (uint32_t)p.V * 128),
+                          bdesc, idesc, first ? 0u : 1u);
+        first = false;
+      }
+      umma_commit_elect(&B.empty[sl]);
+      if (++sl == 2) {
+        sl = 0;
+        ph ^= 1;
+      }
+    }
+    umma_commit_elect(&B.done);
+  } else if (warp >= wXf0) {
+    // gather: task = (pixel, 16-byte chunk of two taps), chunks 0..24
+    const int xt = threadIdx.x - wXf0 * 32;
+    int sl = 0;
+    uint32_t ph = 0;
+    const int plane = p.Ho * p.Wo;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      mbar_wait_sleep(&B.empty[sl], ph ^ 1, 64);  // the MMAs no longer read this slot
+      uint8_t* ab = slots + (size_t)sl * p.slot_bytes;
+      const int64_t pix0 = (int64_t)t * p.V;
+      // eight tasks per thread in flight: all sixteen 8-byte loads issued
+      // before any store; pixel coordinates stepped from the tile start
+      // (no 64-bit division per task)
+      const int n0 = (int)(pix0 / plane), rem0 = (int)(pix0 - (int64_t)n0 * plane);
+      constexpr int kB = 8;
+      for (int t0 = xt; t0 < p.V * 25; t0 += kB * sGather) {
+        uint2 v[kB][2];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int task = t0 + b * sGather;
+          v[b][0] = v[b][1] = make_uint2(0u, 0u);
+          const int r = task / 25, c = task - r * 25;
+          if (task < p.V * 25 && pix0 + r < p.M) {
+            int n = n0, rem = rem0 + r;
+            while (rem >= plane) {  // (only when images are smaller than a tile)
+              rem -= plane;
+              ++n;
+            }
+            const int oh = rem / p.Wo, ow = rem - oh * p.Wo;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              // tap -> (kh, kw) by arithmetic: a constant-memory table read
+              // with 32 different indices per warp serialised the memory pipe
+              const int tap = 2 * c + h, kh = tap / 7, kw = tap - 7 * kh;
+              const int ih = 2 * oh - 3 + kh, iw = 2 * ow - 3 + kw;
+              if (tap < 49 && ih >= 0 && ih < p.H && iw >= 0 && iw < p.W)
+                v[b][h] = __ldg(p.x4 + ((int64_t)n * p.H + ih) * p.W + iw);
+            }
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int task = t0 + b * sGather;
+          if (task < p.V * 25) {
+            const int r = task / 25, c = task - r * 25;
+            const int a = c >> 3, cc = c & 7;
+            *reinterpret_cast<uint4*>(ab + ((size_t)a * p.V + r) * 128 + ((cc ^ (r & 7)) << 4)) =
+                make_uint4(v[b][0].x, v[b][0].y, v[b][1].x, v[b][1].y);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&B.ready[sl]);
+      if (++sl == 2) {
+        sl = 0;
+        ph ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    mbar_wait_sleep(&B.done, 0, 4000);
+    tc_fence_after();
+    float* out = p.part + (size_t)blockIdx.x * 2 * 128 * 64;
+    for (int mb = 0; mb < 2; ++mb)
+      for (int c = 0; c < 64; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + mb * 64 + c, v);
+        float* dst = out + ((size_t)mb * 128 + q * 32 + lane) * 64 + c;
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 128);
+}
+
+// dW[co][kh][kw][c] (c < 3) = sum over CTAs of D[(tap, c)][co], tap = kh * 7 + kw
+__global__ void stem_wgrad_finalize(const float* __restrict__ part, int ctas, float* __restrict__ dw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over co, kh, kw, c
+  if (i >= 64 * 49 * 3) return;
+  const int c = i % 3, tap = (i / 3) % 49, co = i / (3 * 49);
+  const int m = tap * 4 + c;
+  double acc = 0.0;
+  for (int k = 0; k < ctas; ++k) acc += (double)part[(((size_t)k * 2 + m / 128) * 128 + m % 128) * 64 + co];
+  dw[i] = (float)acc;
 }
 }  // namespace
 
@@ -692,6 +870,45 @@ cudaError_t wgrad1x1_narrow(const void* x, const void* dy, float* dw, int64_t M,
   if (e != cudaSuccess) return e;
   const int total = ci * co, thr = 256;
   wgrad1x1_narrow_finalize<<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, ci, co, p.xm, nmb, nch, dw);
+  return cudaGetLastError();
+}
+
+size_t stem_wgrad_workspace() { return (size_t)num_sms() * 2 * 128 * 64 * sizeof(float); }
+
+cudaError_t stem_wgrad(const void* x4, const void* dc, float* dw, int n, int h, int w, void* ws, size_t ws_bytes,
+                       cudaStream_t s) {
+  const int ho = (h + 2 * 3 - 7) / 2 + 1, wo = (w + 2 * 3 - 7) / 2 + 1;
+  if (n < 1 || ho < 1 || wo < 1 || ws_bytes < stem_wgrad_workspace()) return cudaErrorInvalidValue;
+  if ((reinterpret_cast<uintptr_t>(x4) | reinterpret_cast<uintptr_t>(dc) | reinterpret_cast<uintptr_t>(ws)) & 15)
+    return cudaErrorMisalignedAddress;
+  StemWgParams p{};
+  p.n = n;
+  p.H = h;
+  p.W = w;
+  p.Ho = ho;
+  p.Wo = wo;
+  p.M = (int64_t)n * ho * wo;
+  p.V = 128;
+  p.tiles = (int)((p.M + p.V - 1) / p.V);
+  p.a_bytes = 4 * p.V * 128;
+  p.slot_bytes = p.a_bytes + p.V * 128;
+  p.x4 = static_cast<const uint2*>(x4);
+  p.part = static_cast<float*>(ws);
+  CUtensorMap mdc;
+  if (!make_map(&mdc, dc, p.M, 64, p.V, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  int grid = num_sms();
+  if (grid > p.tiles) grid = p.tiles;
+  const size_t smem = 2 * (size_t)p.slot_bytes + sizeof(WgBars) + 1024;
+  static size_t configured = 0;
+  if (configured < smem) {
+    cudaError_t e = cudaFuncSetAttribute(stem_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  stem_wgrad_kernel<<<grid, sThreads, smem, s>>>(mdc, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  stem_wgrad_finalize<<<(64 * 49 * 3 + 255) / 256, 256, 0, s>>>(p.part, grid, dw);
   return cudaGetLastError();
 }
 

@@ -284,6 +284,11 @@ class StemUnit(_ConvNetUnit):
         if self._fused():
             da = bnfused.relu_maxpool_backward(dy, c, m, i, g, b, 3, 2, 1)
             dc = bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=grads[1], dbeta=grads[2])
+            if WGRAD_UNITS and self.cout == 64 and self.res % 2 == 0:
+                # own tcgen05 kernel, 7x7 windows gathered in shared memory
+                # (cuDNN: a legacy sm80 kernel after an NHWC padding pass)
+                bnfused.stem_wgrad(dc, x, grads[0])
+                return None
             _, dw, _ = _conv_bw(dc, x, _cl(w), 2, 3, need_dx=False)
             _cl(grads[0]).copy_(dw)
             return None

@@ -75,3 +75,20 @@ def test_wgrad1x1_narrow_matches_torch(n, ci, co, h, w, pre):
     dw2 = torch.empty_like(dw)
     bnfused.wgrad1x1_narrow(dy, x, dw2, pre=pre_t)
     assert torch.equal(dw, dw2)
+
+
+@pytest.mark.parametrize("n,h", [(2, 224), (3, 30), (1, 8), (5, 64)])
+def test_stem_wgrad_matches_torch(n, h):
+    x = cl(rand((n, 3, h, h), 8, 2.0))
+    ho = (h + 6 - 7) // 2 + 1
+    dc = cl(rand((n, 64, ho, ho), 9))
+    dw = torch.empty(64, 7, 7, 3, device="cuda")
+    bnfused.stem_wgrad(dc, x, dw)
+    wr = torch.zeros(64, 3, 7, 7, device="cuda", requires_grad=True)
+    F.conv2d(x.float(), wr, stride=2, padding=3).backward(dc.float())
+    ref = wr.grad.permute(0, 2, 3, 1)
+    err = float((dw - ref).abs().max() / ref.abs().max())
+    assert err < 2e-3, err
+    dw2 = torch.empty_like(dw)
+    bnfused.stem_wgrad(dc, x, dw2)
+    assert torch.equal(dw, dw2)
