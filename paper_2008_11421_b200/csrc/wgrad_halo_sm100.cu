@@ -71,10 +71,15 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t addr, uint32_t lbo) {
 }
 
 // kind::f16 instruction descriptor, D f32, A/B bf16 both MN-major, M = 128, N
-__host__ __device__ constexpr uint32_t idesc_mn(int n) {
+__host__ __device__ constexpr uint32_t idesc_mn(int n, int m = 128) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
+         ((uint32_t)(m >> 4) << 24);
 }
+
+// M of the narrow 3x3 weight gradient's MMAs: 64 at 16 channels (four window
+// atoms, filter columns 0..2 + one junk, instead of eight), else 128
+template <int C>
+__host__ __device__ constexpr int wg_mm() { return C == 16 ? 64 : 128; }
 
 template <int C, bool PRO>
 __global__ void __launch_bounds__(wThreads, 1) wgrad3x3_halo_kernel(const __grid_constant__ CUtensorMap map_x,
@@ -83,7 +88,8 @@ __global__ void __launch_bounds__(wThreads, 1) wgrad3x3_halo_kernel(const __grid
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
   constexpr int kRB = C * 2;           // row bytes
-  constexpr int kApm = 128 / C;        // M atoms (filter columns) per MMA
+  constexpr int kMM = wg_mm<C>();      // MMA M
+  constexpr int kApm = kMM / C;        // M atoms (filter columns) per MMA
   constexpr int kNm = (3 + kApm - 1) / kApm;  // MMAs per filter row
   constexpr int kAcc = 3 * kNm;        // accumulators of C columns
   constexpr uint32_t kCols = kAcc * C <= 32 ? 32 : (kAcc * C <= 64 ? 64 : (kAcc * C <= 128 ? 128 : (kAcc * C <= 256 ? 256 : 512)));
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(wThreads, 1) wgrad3x3_halo_kernel(const __grid
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = idesc_mn(C);
+    constexpr uint32_t idesc = idesc_mn(C, kMM);
     int sl = 0;
     uint32_t ph = 0;
     bool first = true;
@@ -276,13 +282,22 @@ __global__ void __launch_bounds__(wThreads, 1) wgrad3x3_halo_kernel(const __grid
 }
 
 // dW[co][r][s][ci] = sum over CTAs (fixed order) of D_(r, s / apm)[(s % apm) * C + ci][co]
+// M = 64 accumulators: row m sits in TMEM lane (m / 16) * 32 + m % 16 (lanes
+// 0..15 of each 32-lane quarter) - determined by test: lane_mode 0 passes
+// tests/test_wgrad_narrow_gpu.py, 1 (lanes 0..63) fails; KRT_M64_LANES
+// selects it for such checks
+__device__ __forceinline__ int m64_lane(int m, int mode) { return mode ? m : (m >> 4) * 32 + (m & 15); }
+
 template <int C>
-__global__ void wgrad3x3_halo_finalize(const float* __restrict__ part, int ctas, float* __restrict__ dw) {
-  constexpr int kApm = 128 / C, kNm = (3 + kApm - 1) / kApm, kAcc = 3 * kNm;
+__global__ void wgrad3x3_halo_finalize(const float* __restrict__ part, int ctas, float* __restrict__ dw,
+                                       int lane_mode) {
+  constexpr int kMM = wg_mm<C>();
+  constexpr int kApm = kMM / C, kNm = (3 + kApm - 1) / kApm, kAcc = 3 * kNm;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over co, r, s, ci
   if (i >= C * 9 * C) return;
   const int ci = i % C, s = (i / C) % 3, r = (i / (3 * C)) % 3, co = i / (9 * C);
-  const int a = r * kNm + s / kApm, lanei = (s % kApm) * C + ci;
+  const int a = r * kNm + s / kApm, mrow = (s % kApm) * C + ci;
+  const int lanei = kMM == 64 ? m64_lane(mrow, lane_mode) : mrow;
   double acc = 0.0;
   for (int k = 0; k < ctas; ++k) acc += (double)part[(((size_t)k * kAcc + a) * 128 + lanei) * C + co];
   dw[i] = (float)acc;
@@ -740,7 +755,7 @@ bool wgrad3x3_halo_supported(int h, int w, int C) {
 }
 
 size_t wgrad3x3_halo_workspace(int C) {
-  const int apm = 128 / C, nm = (3 + apm - 1) / apm;
+  const int apm = (C == 16 ? 64 : 128) / C, nm = (3 + apm - 1) / apm;
   return (size_t)num_sms() * 3 * nm * 128 * C * sizeof(float);
 }
 
@@ -800,9 +815,10 @@ cudaError_t wgrad3x3_halo(const void* x, const void* dy, float* dw, int n, int h
   else e = pro ? launch_wg<64, true>(mx, mdy, p, grid, smem, s) : launch_wg<64, false>(mx, mdy, p, grid, smem, s);
   if (e != cudaSuccess) return e;
   const int total = C * 9 * C, thr = 256;
-  if (C == 16) wgrad3x3_halo_finalize<16><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw);
-  else if (C == 32) wgrad3x3_halo_finalize<32><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw);
-  else wgrad3x3_halo_finalize<64><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw);
+  static const int lane_mode = std::getenv("KRT_M64_LANES") ? std::atoi(std::getenv("KRT_M64_LANES")) : 0;
+  if (C == 16) wgrad3x3_halo_finalize<16><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw, lane_mode);
+  else if (C == 32) wgrad3x3_halo_finalize<32><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw, lane_mode);
+  else wgrad3x3_halo_finalize<64><<<(total + thr - 1) / thr, thr, 0, s>>>(p.part, grid, dw, lane_mode);
   return cudaGetLastError();
 }
 

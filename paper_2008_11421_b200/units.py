@@ -283,7 +283,9 @@ class StemUnit(_ConvNetUnit):
         m, i = saved[2][:self.cout], saved[2][self.cout:]
         if self._fused():
             da = bnfused.relu_maxpool_backward(dy, c, m, i, g, b, 3, 2, 1)
+            del dy
             dc = bnfused.backward(da, c, m, i, g, b, relu=True, dgamma=grads[1], dbeta=grads[2])
+            del da   # (the weight gradient below allocates the padded input)
             if WGRAD_UNITS and self.cout == 64 and self.res % 2 == 0:
                 # own tcgen05 kernel, 7x7 windows gathered in shared memory
                 # (cuDNN: a legacy sm80 kernel after an NHWC padding pass)
