@@ -150,6 +150,9 @@ def main():
     if only == {"megatron"}:
         _megatron()
         return
+    if only == {"tnlg"}:
+        _tnlg()
+        return
     if only and not any(n.startswith(("resnet200", "resnet1001")) for n in only):
         raise SystemExit("usage: make_plans.py [resnet200_b3072 | resnet1001_2048_b2 ...]  (no args: every workload)")
     if only:
@@ -228,6 +231,20 @@ def _megatron():
          {"family": "gpt", "hidden": 3072, "heads": 32, "layers": 36, "seq": 1024, "vocab": 51200,
           "act": "bf16"}, max_blocks=16, compute_rate=5.0e14)
     calibrated("megatron8p3b_l36_b128", cal_from="gpt2p5b_b144")
+
+
+def _tnlg():
+    """cfg4 family on one GPU: the Turing-NLG 17B layer shape (H 4256, 28
+    heads of 152; seq 1024, vocab 51200) at 18 of its 78 layers
+    (4.35B parameters: the same host budget as the Megatron L36 instance, whose
+    host peak measured 135 of 196 GB; the full 78 layers' 17B parameters need
+    the 8-way host shard of cfg4).  Batch 176: 278 GB of activations = 1.55x
+    HBM.  Planned under the measured GPT spec (plans/calibration/gpt2p5b_b144.json)."""
+    units = gpt_units(4256, 28, 18, 1024, 51200)
+    make("tnlg17b_l18_b176", units, 176, 120e9,
+         {"family": "gpt", "hidden": 4256, "heads": 28, "layers": 18, "seq": 1024, "vocab": 51200,
+          "act": "bf16"}, max_blocks=16, compute_rate=5.0e14)
+    calibrated("tnlg17b_l18_b176", cal_from="gpt2p5b_b144")
 
 
 # arena capacity per sweep batch: 150 GB leaves the b3584 / b4096 steps 1.4 /

@@ -28,7 +28,8 @@ def test_golden_cases_bit_exact(sched_cases):
 @pytest.mark.parametrize("name", ["resnet_small_f32_a", "resnet_small_f32_b", "resnet_small_bf16",
                                   "preact29_small_f32", "preact29_small_bf16", "gpt_small_f32",
                                   "gpt_small_bf16", "resnet200_b3072", "resnet200_b3072_unbounded",
-                                  "resnet200_b512", "resnet200_b2560", "gpt2p5b_b144"])
+                                  "resnet200_b512", "resnet200_b2560", "gpt2p5b_b144",
+                                  "megatron8p3b_l36_b128", "tnlg17b_l18_b176"])
 def test_workload_plans_bit_exact(name):
     rec = W.load(name)
     got = plan_model(rec["model"], rec["hardware"], "capacity-recompute", "auto", rec.get("max_blocks"))
