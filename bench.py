@@ -256,7 +256,7 @@ def workload_inputs(rec, dev, gen, batch=None):
         y = torch.randint(0, m["vocab"], (n, m["seq"]), device=dev, generator=gen)
         return x, y
     x = torch.randn(n, 3, m["res"], m["res"], device=dev, generator=gen, dtype=torch.float32).to(
-        torch.bfloat16).contiguous(memory_format=torch.channels_last)
+        torch.float32 if m.get("act") == "f32" else torch.bfloat16).contiguous(memory_format=torch.channels_last)
     y = torch.randint(0, m["classes"], (n,), device=dev, generator=gen)
     return x, y
 
@@ -624,9 +624,12 @@ def run_gpu(args, rec):
         "metric": metric_name(rec),
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if m.get("act") == "f32" else "bf16",
+        "data": "synthetic",
         "config": {"workload": rec["name"], "exchange": args.exchange if world > 1 else "none",
                    "exchange_dtype": "bf16" if args.exchange_bf16 else "fp32", "grad_slots": args.grad_slots,
+                   **({"conv_math": "fp32" if args.no_tf32 else "tf32 (cuDNN default for fp32 tensors)"}
+                      if m.get("act") == "f32" else {}),
                    "model": model_name(rec), "per_gpu_batch": batch,
                    "global_batch": batch * world, "input": m.get("res", m.get("seq")), "parallelism": f"dp{world}",
                    "plan": rec["plan_string"][:160] + " ...",
@@ -728,7 +731,13 @@ def main():
                     help="N>1 NCCL exchange: bf16 cast pack before the reduce-scatter (half the NVLink bytes)")
     ap.add_argument("--incore", action="store_true",
                     help="same blocks, everything resident (no swap/recompute): the in-core baseline")
+    ap.add_argument("--no-tf32", action="store_true",
+                    help="fp32 workloads: cuDNN / cuBLAS in true fp32 (default: their TF32 tensor-core math)")
     args = ap.parse_args()
+    if args.no_tf32:
+        import torch
+        torch.backends.cudnn.allow_tf32 = False
+        torch.backends.cuda.matmul.allow_tf32 = False
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         self_launch(args)
     from paper_2008_11421_b200 import workloads as W

@@ -153,6 +153,9 @@ def main():
     if only == {"tnlg"}:
         _tnlg()
         return
+    if only == {"resnet200_f32"}:
+        _resnet200_f32()
+        return
     if only and not any(n.startswith(("resnet200", "resnet1001")) for n in only):
         raise SystemExit("usage: make_plans.py [resnet200_b3072 | resnet1001_2048_b2 ...]  (no args: every workload)")
     if only:
@@ -267,6 +270,18 @@ def _sweep(batches=(1280, 2048, 3072, 3584, 4096)):
              {"family": "resnet", "depth": 200, "res": 224, "classes": 1000, "act": "bf16"},
              max_blocks=16, compute_rate=2.0e14)
         calibrated(f"resnet200_sweep_b{batch}", cal_from="resnet200_b3072")
+
+
+def _resnet200_f32():
+    """cfg1 in fp32 (activations, weights and BN statistics fp32; the units'
+    aten / cuDNN branch), the precision of the reference's CPU path, so the
+    reference arm has a same-precision GPU number beside it.  Batch 1536:
+    the same 320 GB of activations as the bf16 b3072 bench plan; a 120 GB
+    arena leaves room for the unfused branch's fp32 temporaries."""
+    units = resnet_units(200, act_dtype=torch.float32)
+    make("resnet200_f32_b1536", units, 1536, 120e9,
+         {"family": "resnet", "depth": 200, "res": 224, "classes": 1000, "act": "f32"},
+         max_blocks=16, compute_rate=6.0e13)
 
 
 def _resnet200(only):
