@@ -394,7 +394,8 @@ def run_gpu(args, rec):
                   cfg=ExecConfig(device=local, world_size=world, rank=rank, nccl_id=nccl_id,
                                  ipc_exchange=(world > 1 and args.exchange == "ipc"),
                                  grad_slots=args.grad_slots, exchange_bf16=args.exchange_bf16,
-                                 weight_dtype=torch.bfloat16, **opt_cfg))
+                                 weight_dtype=torch.float32 if m.get("act") == "f32" else torch.bfloat16,
+                                 **opt_cfg))
     if world > 1 and args.exchange == "ipc":
         handles = [None] * world
         dist.all_gather_object(handles, ex.ipc_handles())

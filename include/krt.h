@@ -464,11 +464,19 @@ int krt_ln_fwd(const void* x, const void* r, void* x2, const void* gamma, const 
 /* LayerNorm backward in one pass: dx = rstd * (g*dy - mean(g*dy) - xhat *
  * mean(g*dy*xhat)) [+ addend] (bf16; the addend is the residual branch's
  * gradient), dgamma = sum_t dy*xhat, dbeta = sum_t dy (fp32, written, in a
- * fixed summation order).  mean/rstd: the forward's (krt_ln_fwd).  H <= 4352.
+ * fixed summation order).  mean/rstd: the forward's (krt_ln_fwd).  H <= 12288.
  * ws: krt_ln_bwd_workspace bytes. */
 size_t krt_ln_bwd_workspace(int64_t T, int H);
 int krt_ln_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                const void* addend, void* dx, float* dgamma, float* dbeta, void* ws, int64_t T, int H, void* stream);
+/* The LM head's next-token cross-entropy, forward and backward in one pass
+ * over the logits (replaces the loss the reference's cost model counts as
+ * the Softmax layer kind, model_ir.py:47-59, cost_model.py:139-148):
+ * logits / dlogits bf16 [T, V] row-major, target int64 [T] (0 <= y < V),
+ * row_loss[t] = logsumexp(z_t) - z_t[y_t] (fp32),
+ * dlogits[t] = (softmax(z_t) - onehot(y_t)) * scale.  V % 8 == 0, V <= 65536. */
+int krt_lm_xent(const void* logits, const int64_t* target, void* dlogits, float* row_loss, int64_t T, int V,
+                float scale, void* stream);
 /* dx = gelu_tanh'(f) * dy and colsum[n] = sum_t dx[t, n] (fp32, the bias
  * gradient of the layer that produced f) in one pass over the activations;
  * ws: krt_gelu_bwd_colsum_workspace bytes. */

@@ -649,6 +649,11 @@ int krt_ln_bwd(const void* dy, const void* x, const void* g, const float* mean, 
   KRT_CUDA_GUARD(ln_bwd(dy, x, g, mean, rstd, addend, dx, dgamma, dbeta, ws, T, H, (cudaStream_t)stream), "ln_bwd");
 }
 
+int krt_lm_xent(const void* logits, const int64_t* target, void* dlogits, float* row_loss, int64_t T, int V,
+                float scale, void* stream) {
+  KRT_CUDA_GUARD(lm_xent(logits, target, dlogits, row_loss, T, V, scale, (cudaStream_t)stream), "lm_xent");
+}
+
 size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N) { return gelu_bwd_colsum_workspace(T, N); }
 
 int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,

@@ -14,6 +14,10 @@
 //   gelu_bwd_colsum : df = gelu'(f) * dg (tanh GELU) and, in the same pass,
 //                     the column sums of df (fc1's bias gradient): no second
 //                     read of the widest activation of the layer.
+//   lm_xent         : the LM head's next-token cross-entropy, forward and
+//                     backward in one pass over the bf16 logits (the row in
+//                     registers): per-row loss lse - z[y] and
+//                     dz = (softmax(z) - onehot(y)) * scale, fp32 math.
 //
 // LayerNorm: one warp per row, 16-byte vectors; mean from the rounded x2,
 // variance by a second pass over x2 (L2-resident re-read), both in fp32.
@@ -275,44 +279,61 @@ __global__ void __launch_bounds__(1024) colsum_finalize_kernel(const float* __re
   out[c] = (float)s;
 }
 
-// LayerNorm backward.  One warp per row, rows strided over a persistent grid;
-// the row (dy, x and the addend) is loaded packed into registers with every
-// load in flight at once (J octets per lane), the two row sums reduced by
-// shuffles, dx stored.  Each warp adds its rows' dy*xhat and dy into its own
-// fp32 column accumulators in shared memory ([2][8][H/8]: lane j owns the
-// columns of octets j, j+32, ..., so no two lanes touch a word and no
-// barrier is needed per row); at the end the CTA sums its warps in warp order
-// into one partial row pair.  Deterministic for a given grid.
-constexpr int kBwdWarps = 4;
+// LayerNorm backward.  One CTA per row at a time, rows strided over a
+// persistent grid; thread t owns the J octets t, t + nt, ... of every row
+// (nt = blockDim.x, sized to the row), so its dgamma / dbeta column partials
+// stay in registers for all the CTA's rows (no shared-memory accumulators:
+// those capped the old warp-per-row kernel at 12 warps per SM, latency-bound
+// at 0.33-0.55 of HBM).  The next row's dy / x / addend are loaded while the
+// current row is reduced and written (one row of prefetch per CTA).  The two
+// row sums: warp shuffles, then the warps' partials summed in warp order
+// through a parity-double-buffered shared slot (one barrier per row).  At the
+// end each thread stores its column partials: one partial row pair per CTA.
+// Deterministic for a given grid.
+constexpr int kBwdMaxWarps = 12;  // 384 threads: J = 2 octets per thread up to H = 6144, J = 4 up to 12288
 
 template <bool ADD, int J>
-__global__ void __launch_bounds__(32 * kBwdWarps) ln_bwd_kernel(
+__device__ __forceinline__ void ln_bwd_load(const __nv_bfloat16* dy, const __nv_bfloat16* x,
+                                            const __nv_bfloat16* addend, int64_t row, int H, int oct, uint4* ud,
+                                            uint4* ux, uint4* ua) {
+#pragma unroll
+  for (int i = 0; i < J; ++i) {
+    const int j = threadIdx.x + blockDim.x * i;
+    if (j < oct) {
+      ud[i] = __ldcs(reinterpret_cast<const uint4*>(dy + row * H) + j);
+      ux[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * H) + j);
+      if (ADD) ua[i] = __ldcs(reinterpret_cast<const uint4*>(addend + row * H) + j);
+    }
+  }
+}
+
+template <bool ADD, int J>
+__global__ void __maxnreg__(112) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
     const float* __restrict__ mean, const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ addend,
     __nv_bfloat16* __restrict__ dx, float* __restrict__ part, int64_t T, int H) {
-  extern __shared__ float stage[];  // [kBwdWarps][2][8][H / 8]
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ float red[2][kBwdMaxWarps][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int oct = H / 8;
-  float* ag = stage + (size_t)w * 2 * H;  // this warp's sum of dy*xhat, [8][oct]
-  float* ab = ag + H;                     // and of dy
-  for (int c = lane; c < H; c += 32) ag[c] = ab[c] = 0.f;
   const float inv_h = 1.f / (float)H;
-  for (int64_t row = (int64_t)blockIdx.x * kBwdWarps + w; row < T; row += (int64_t)gridDim.x * kBwdWarps) {
-    uint4 ud[J], ux[J], ua[ADD ? J : 1];
+  float accg[J][8], accb[J][8];  // gamma is re-read per row (L1-resident): registers go to the prefetch
 #pragma unroll
-    for (int i = 0; i < J; ++i) {
-      const int j = lane + 32 * i;
-      if (j < oct) {
-        ud[i] = __ldcs(reinterpret_cast<const uint4*>(dy + row * H) + j);
-        ux[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * H) + j);
-        if (ADD) ua[i] = __ldcs(reinterpret_cast<const uint4*>(addend + row * H) + j);
-      }
-    }
+  for (int i = 0; i < J; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) accg[i][k] = accb[i][k] = 0.f;
+  uint4 ud[J], ux[J], ua[ADD ? J : 1];
+  int64_t row = blockIdx.x;
+  if (row < T) ln_bwd_load<ADD, J>(dy, x, addend, row, H, oct, ud, ux, ua);
+  for (int par = 0; row < T; row += gridDim.x, par ^= 1) {
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
+    // prefetch the next row
+    uint4 nd[J], nx[J], na[ADD ? J : 1];
+    const int64_t nrow = row + gridDim.x;
+    if (nrow < T) ln_bwd_load<ADD, J>(dy, x, addend, nrow, H, oct, nd, nx, na);
     float s1 = 0.f, s2 = 0.f;  // sum g*dy, sum g*dy*xhat
 #pragma unroll
     for (int i = 0; i < J; ++i) {
-      const int j = lane + 32 * i;
+      const int j = threadIdx.x + blockDim.x * i;
       if (j < oct) {
         float d[8], xv[8], gg[8];
         unpack8(ud[i], d);
@@ -324,17 +345,29 @@ __global__ void __launch_bounds__(32 * kBwdWarps) ln_bwd_kernel(
           const float gd = d[k] * gg[k];
           s1 += gd;
           s2 = __fmaf_rn(gd, xh, s2);
-          ag[k * oct + j] += d[k] * xh;
-          ab[k * oct + j] += d[k];
+          accg[i][k] += d[k] * xh;
+          accb[i][k] += d[k];
         }
       }
     }
-    const float c1 = warp_sum(s1) * inv_h, c2 = warp_sum(s2) * inv_h;
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      red[par][w][0] = s1;
+      red[par][w][1] = s2;
+    }
+    __syncthreads();
+    float t1 = 0.f, t2 = 0.f;
+    for (int k = 0; k < nw; ++k) {
+      t1 += red[par][k][0];
+      t2 += red[par][k][1];
+    }
+    const float c1 = t1 * inv_h, c2 = t2 * inv_h;
 #pragma unroll
     for (int i = 0; i < J; ++i) {
-      const int j = lane + 32 * i;
+      const int j = threadIdx.x + blockDim.x * i;
       if (j < oct) {
-        float d[8], xv[8], gg[8], o[8];
+        float d[8], xv[8], o[8], gg[8];
         unpack8(ud[i], d);
         unpack8(ux[i], xv);
         unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
@@ -348,16 +381,25 @@ __global__ void __launch_bounds__(32 * kBwdWarps) ln_bwd_kernel(
         __stcs(reinterpret_cast<uint4*>(dx + row * H) + j, pack8(o));
       }
     }
-  }
-  __syncthreads();
-  // this CTA's partial row pair: its warps' accumulators added in warp order
-  for (int c = threadIdx.x; c < 2 * H; c += 32 * kBwdWarps) {
-    float s = 0.f;
 #pragma unroll
-    for (int r = 0; r < kBwdWarps; ++r) s += stage[(size_t)r * 2 * H + c];
-    // [2][8][oct] -> [2][H] column order
-    const int half = c / H, rem = c - half * H, k = rem / oct, j = rem - k * oct;
-    part[(size_t)blockIdx.x * 2 * H + half * H + 8 * j + k] = s;
+    for (int i = 0; i < J; ++i) {
+      ud[i] = nd[i];
+      ux[i] = nx[i];
+      if (ADD) ua[i] = na[i];
+    }
+  }
+  // this CTA's partial row pair, straight from the registers
+#pragma unroll
+  for (int i = 0; i < J; ++i) {
+    const int j = threadIdx.x + blockDim.x * i;
+    if (j < oct) {
+      float4* pg = reinterpret_cast<float4*>(part + (size_t)blockIdx.x * 2 * H + 8 * j);
+      float4* pb = reinterpret_cast<float4*>(part + (size_t)blockIdx.x * 2 * H + H + 8 * j);
+      pg[0] = make_float4(accg[i][0], accg[i][1], accg[i][2], accg[i][3]);
+      pg[1] = make_float4(accg[i][4], accg[i][5], accg[i][6], accg[i][7]);
+      pb[0] = make_float4(accb[i][0], accb[i][1], accb[i][2], accb[i][3]);
+      pb[1] = make_float4(accb[i][4], accb[i][5], accb[i][6], accb[i][7]);
+    }
   }
 }
 
@@ -386,50 +428,142 @@ __global__ void __launch_bounds__(1024) ln_bwd_finalize_kernel(const float* __re
   out_b[c] = (float)sbt;
 }
 
-int ln_bwd_grid(int64_t T) {
-  int dev = 0, sms = 148;
+// octets per thread and threads per CTA: the row's octets over J per thread, whole warps
+int ln_bwd_j(int H) { return H / 8 <= 32 * kBwdMaxWarps * 2 ? 2 : 4; }
+
+int ln_bwd_threads(int H) {
+  const int oct = H / 8, J = ln_bwd_j(H);
+  const int t = ((oct + J - 1) / J + 31) / 32 * 32;
+  return t < 32 ? 32 : t;
+}
+
+template <int J>
+int ln_bwd_grid_j(int64_t T, int H, bool add) {
+  int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (T + kBwdWarps - 1) / kBwdWarps, cap = (int64_t)sms * 4;
-  return (int)(want < cap ? want : cap);
+  const int nt = ln_bwd_threads(H);
+  if (add) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ln_bwd_kernel<true, J>, nt, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ln_bwd_kernel<false, J>, nt, 0);
+  const int64_t cap = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);  // one full wave, no tail
+  return (int)(T < cap ? T : cap);
 }
 
-template <bool ADD, int J>
-cudaError_t launch_ln_bwd(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
-                          const void* addend, void* dx, float* part, int grid, int64_t T, int H, cudaStream_t s) {
-  const size_t smem = (size_t)kBwdWarps * 2 * H * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(ln_bwd_kernel<ADD, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  ln_bwd_kernel<ADD, J><<<grid, 32 * kBwdWarps, smem, s>>>(
-      static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x),
-      static_cast<const __nv_bfloat16*>(g), mean, rstd, static_cast<const __nv_bfloat16*>(addend),
-      static_cast<__nv_bfloat16*>(dx), part, T, H);
-  return cudaGetLastError();
+int ln_bwd_grid(int64_t T, int H, bool add) {
+  return ln_bwd_j(H) == 2 ? ln_bwd_grid_j<2>(T, H, add) : ln_bwd_grid_j<4>(T, H, add);
 }
 
-template <bool ADD>
-cudaError_t ln_bwd_dispatch(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
-                            const void* addend, void* dx, float* part, int grid, int64_t T, int H, cudaStream_t s) {
-  const int oct = H / 8;
-  if (oct <= 32 * 2) return launch_ln_bwd<ADD, 2>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
-  if (oct <= 32 * 4) return launch_ln_bwd<ADD, 4>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
-  if (oct <= 32 * 8) return launch_ln_bwd<ADD, 8>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
-  if (oct <= 32 * 12) return launch_ln_bwd<ADD, 12>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
-  return launch_ln_bwd<ADD, 17>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+template <int J>
+void launch_ln_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* g, const float* mean,
+                   const float* rstd, const __nv_bfloat16* addend, __nv_bfloat16* dx, float* part, int grid, int nt,
+                   int64_t T, int H, cudaStream_t s) {
+  if (addend) ln_bwd_kernel<true, J><<<grid, nt, 0, s>>>(dy, x, g, mean, rstd, addend, dx, part, T, H);
+  else ln_bwd_kernel<false, J><<<grid, nt, 0, s>>>(dy, x, g, mean, rstd, addend, dx, part, T, H);
+}
+
+
+// ---------------------------------------------------------------------------
+// lm_xent: one CTA per row (grid-stride), the row's V / 8 octets spread over
+// the CTA's threads (J per thread, all loads in flight at once), block
+// reductions for the max and the sum of exp(z - max) in a fixed order
+// (deterministic), then dz written from the registers: 2 bytes read and 2
+// written per logit instead of the fp32 chunk passes of an unfused softmax.
+constexpr int kXentThreads = 512;
+
+__device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const float t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, t) : v + t;
+  }
+  __syncthreads();  // sh reused across calls
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float r = sh[0];
+  for (int k = 1; k < kXentThreads / 32; ++k) r = is_max ? fmaxf(r, sh[k]) : r + sh[k];
+  return r;
+}
+
+template <int J>
+__global__ void __launch_bounds__(kXentThreads, 1) lm_xent_kernel(const __nv_bfloat16* __restrict__ z,
+                                                                  const int64_t* __restrict__ y,
+                                                                  __nv_bfloat16* __restrict__ dz,
+                                                                  float* __restrict__ row_loss, int64_t T, int V,
+                                                                  float scale) {
+  __shared__ float sh[kXentThreads / 32];
+  const int oct = V / 8;
+  for (int64_t row = blockIdx.x; row < T; row += gridDim.x) {
+    const uint4* zr = reinterpret_cast<const uint4*>(z + row * V);
+    uint4 u[J];
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const int j = threadIdx.x + kXentThreads * i;
+      if (j < oct) u[i] = __ldcs(zr + j);
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      if (threadIdx.x + kXentThreads * i < oct) {
+        float f[8];
+        unpack8(u[i], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m = fmaxf(m, f[k]);
+      }
+    }
+    m = block_reduce(m, sh, true);
+    float se = 0.f;
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      if (threadIdx.x + kXentThreads * i < oct) {
+        float f[8];
+        unpack8(u[i], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) se += __expf(f[k] - m);
+      }
+    }
+    se = block_reduce(se, sh, false);
+    const float lse = m + __logf(se);
+    const int64_t tgt = y[row];
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      const int j = threadIdx.x + kXentThreads * i;
+      if (j < oct) {
+        float f[8];
+        unpack8(u[i], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int col = 8 * j + k;
+          if (col == tgt) row_loss[row] = lse - f[k];
+          f[k] = __fmul_rn(__expf(f[k] - lse), scale) - (col == tgt ? scale : 0.f);
+        }
+        __stcs(reinterpret_cast<uint4*>(dz + row * V) + j, pack8(f));
+      }
+    }
+  }
 }
 
 }  // namespace
 
-size_t ln_bwd_workspace(int64_t T, int H) { return (size_t)ln_bwd_grid(T) * 2 * H * sizeof(float); }
+size_t ln_bwd_workspace(int64_t T, int H) {
+  const int a = ln_bwd_grid(T, H, true), b = ln_bwd_grid(T, H, false);
+  return (size_t)(a > b ? a : b) * 2 * H * sizeof(float);
+}
 
 cudaError_t ln_bwd(const void* dy, const void* x, const void* g, const float* mean, const float* rstd,
                    const void* addend, void* dx, float* dgamma, float* dbeta, void* ws, int64_t T, int H,
                    cudaStream_t s) {
-  if (T <= 0 || H <= 0 || H % 8 != 0 || H > 32 * 17 * 8) return cudaErrorInvalidValue;
-  const int grid = ln_bwd_grid(T);
+  if (T <= 0 || H <= 0 || H % 8 != 0 || ln_bwd_threads(H) > 32 * kBwdMaxWarps) return cudaErrorInvalidValue;
+  const int grid = ln_bwd_grid(T, H, addend != nullptr), nt = ln_bwd_threads(H);
   float* part = static_cast<float*>(ws);
-  cudaError_t e = addend ? ln_bwd_dispatch<true>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s)
-                         : ln_bwd_dispatch<false>(dy, x, g, mean, rstd, addend, dx, part, grid, T, H, s);
+  auto DY = static_cast<const __nv_bfloat16*>(dy);
+  auto X = static_cast<const __nv_bfloat16*>(x);
+  auto G = static_cast<const __nv_bfloat16*>(g);
+  auto A = static_cast<const __nv_bfloat16*>(addend);
+  auto DX = static_cast<__nv_bfloat16*>(dx);
+  if (ln_bwd_j(H) == 2) launch_ln_bwd<2>(DY, X, G, mean, rstd, A, DX, part, grid, nt, T, H, s);
+  else launch_ln_bwd<4>(DY, X, G, mean, rstd, A, DX, part, grid, nt, T, H, s);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   ln_bwd_finalize_kernel<<<(H + 31) / 32, 1024, 0, s>>>(part, grid, H, dgamma, dbeta);
   return cudaGetLastError();
@@ -446,14 +580,20 @@ cudaError_t ln_fwd(const void* x, const void* r, void* x2, const void* g, const 
   auto B = static_cast<const __nv_bfloat16*>(b);
   auto Hh = static_cast<__nv_bfloat16*>(h);
   const int oct = H / 8;
-  if (oct <= 32 * 8) {  // row in registers, persistent grid
+  if (oct <= 32 * 17) {  // row in registers, persistent grid
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t want = (T + kRowsPerCta - 1) / kRowsPerCta, cap = (int64_t)sms * 8;
     const dim3 pgrid((unsigned)(want < cap ? want : cap));
-    if (r) ln_fwd_reg_kernel<true, 8><<<pgrid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
-    else ln_fwd_reg_kernel<false, 8><<<pgrid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
+    auto go = [&](auto k_res, auto k_plain) {
+      if (r) k_res<<<pgrid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
+      else k_plain<<<pgrid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
+    };
+    // J octets per lane: H <= 2048 / 3072 (Megatron) / 4352 (Turing-NLG 4256)
+    if (oct <= 32 * 8) go(ln_fwd_reg_kernel<true, 8>, ln_fwd_reg_kernel<false, 8>);
+    else if (oct <= 32 * 12) go(ln_fwd_reg_kernel<true, 12>, ln_fwd_reg_kernel<false, 12>);
+    else go(ln_fwd_reg_kernel<true, 17>, ln_fwd_reg_kernel<false, 17>);
   } else if (r) {
     ln_fwd_kernel<true><<<grid, 32 * kRowsPerCta, 0, s>>>(X, R, X2, G, B, Hh, mean, rstd, T, H, eps);
   } else {
@@ -476,6 +616,26 @@ cudaError_t gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* cols
                                                       static_cast<const __nv_bfloat16*>(f),
                                                       static_cast<__nv_bfloat16*>(dx), part, T, N);
   colsum_finalize_kernel<<<(N + 31) / 32, 1024, 0, s>>>(part, rb, N, colsum);
+  return cudaGetLastError();
+}
+
+cudaError_t lm_xent(const void* z, const int64_t* y, void* dz, float* row_loss, int64_t T, int V, float scale,
+                    cudaStream_t s) {
+  if (T <= 0 || V <= 0 || V % 8 != 0 || V / 8 > kXentThreads * 16) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cap = (int64_t)sms * 4;
+  const dim3 grid((unsigned)(T < cap ? T : cap));
+  auto Z = static_cast<const __nv_bfloat16*>(z);
+  auto D = static_cast<__nv_bfloat16*>(dz);
+  const int oct = V / 8;
+  if (oct <= kXentThreads) lm_xent_kernel<1><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
+  else if (oct <= kXentThreads * 4) lm_xent_kernel<4><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
+  else if (oct <= kXentThreads * 8) lm_xent_kernel<8><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
+  else if (oct <= kXentThreads * 13)
+    lm_xent_kernel<13><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
+  else lm_xent_kernel<16><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
   return cudaGetLastError();
 }
 

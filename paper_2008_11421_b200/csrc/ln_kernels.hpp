@@ -15,4 +15,6 @@ cudaError_t ln_bwd(const void* dy, const void* x, const void* g, const float* me
 size_t gelu_bwd_colsum_workspace(int64_t T, int N);
 cudaError_t gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,
                             cudaStream_t s);
+cudaError_t lm_xent(const void* z, const int64_t* y, void* dz, float* row_loss, int64_t T, int V, float scale,
+                    cudaStream_t s);
 }  // namespace krt

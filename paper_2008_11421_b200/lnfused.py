@@ -44,6 +44,20 @@ def ln_bwd(dy, x, g, mean, rstd, dgamma, dbeta, addend=None):
     return dx
 
 
+def lm_xent(logits, target, scale):
+    """Fused next-token cross-entropy: returns (row_loss fp32 [T], dlogits
+    bf16 [T, V]) with dlogits = (softmax - onehot) * scale."""
+    T, V = logits.shape
+    logits = logits.contiguous()
+    target = target.reshape(-1).to(torch.int64).contiguous()
+    dl = torch.empty_like(logits)
+    rl = torch.empty(T, dtype=torch.float32, device=logits.device)
+    with _timed("lm_xent", T * V * 2 * 2):
+        _lib.check(_lib.lib().krt_lm_xent(logits.data_ptr(), target.data_ptr(), dl.data_ptr(), rl.data_ptr(), T, V,
+                                          float(scale), _stream()))
+    return rl, dl
+
+
 def gelu_bwd_colsum(dy, f, colsum):
     """dx = gelu_tanh'(f) * dy; colsum (fp32 [N]) = column sums of dx."""
     T, N = f.shape

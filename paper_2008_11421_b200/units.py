@@ -1221,14 +1221,17 @@ class TransformerLayerUnit(Unit):
     def _merge(self, o):
         return o.transpose(1, 2).reshape(-1, self.h)
 
-    @staticmethod
-    def _cudnn_attn():
+    def _cudnn_attn(self, backward=False):
         # cuDNN's sm100 fused attention (2.2x the forward, 2x the backward of
         # aten's flash kernel at these shapes, scripts/probe_attention.py);
         # its backward is not bitwise repeatable (dQ accumulation order), so
         # deterministic mode (the bitwise out-of-core == in-core tests) runs
-        # the flash kernel's deterministic backward instead
-        return ATTN_CUDNN and not torch.are_deterministic_algorithms_enabled()
+        # the flash kernel's deterministic backward instead.  cuDNN's backward
+        # takes head dims <= 128 only: Turing-NLG's 152 runs the cuDNN forward
+        # (its natural-log logsumexp is the flash backward's softmax statistic)
+        # and the flash backward
+        return (ATTN_CUDNN and not torch.are_deterministic_algorithms_enabled()
+                and (not backward or self.hd <= 128))
 
     def _attn_fw(self, qkv, lse_out):
         q, k, v = self._heads(qkv)
@@ -1259,7 +1262,7 @@ class TransformerLayerUnit(Unit):
         if self._flash():
             O = o.view(n, self.s, self.nh, self.hd).transpose(1, 2)
             z = torch.zeros((), dtype=torch.int64, device=q.device)
-            cud = self._cudnn_attn()
+            cud = self._cudnn_attn(backward=True)
             with bnfused._timed("cudnn_attn_bwd" if cud else "flash_attn_bwd", 8 * do.shape[0] * self.h * do.element_size(),
                                 5.0 * n * self.nh * self.s * self.s * self.hd):   # causal, 2.5x the forward
                 if cud:
@@ -1425,9 +1428,14 @@ def gpt_units(hidden, heads, layers, seq, vocab, act_dtype=torch.bfloat16):
 def lm_loss(logits, target, chunk_rows=8192):
     """Next-token cross-entropy over all rows; dlogits in the logits dtype.
     Row chunks keep the fp32 softmax transient small (the full [T, vocab]
-    fp32 matrix would be 30 GB at the 2.5B bench shape)."""
+    fp32 matrix would be 30 GB at the 2.5B bench shape).  bf16 logits: the
+    fused one-pass kernel (csrc/ln_kernels.cu lm_xent), per-row losses
+    summed by torch in a fixed order."""
     t = target.reshape(-1)
     n = logits.shape[0]
+    if lnfused.supported(logits) and logits.shape[1] <= 65536:
+        rl, dl = lnfused.lm_xent(logits, t, 1.0 / n)
+        return rl.sum() * (1.0 / n), dl
     dl = torch.empty_like(logits)
     total = torch.zeros((), dtype=torch.float32, device=logits.device)
     inv = 1.0 / n

@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2008_11421_b200 import lnfused
 
-for T, H in [(147456, 1920), (131072, 3072)]:
+for T, H in [(147456, 1920), (131072, 3072), (180224, 4256)]:
     x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
     dy = torch.randn(T, H, device="cuda").to(torch.bfloat16)
     a = torch.randn(T, H, device="cuda").to(torch.bfloat16)
@@ -27,7 +27,10 @@ for T, H in [(147456, 1920), (131072, 3072)]:
                                                                  [True, True, True])
         return dx + a
 
-    for name, fn in (("own ln_bwd", own), ("aten ln_bwd + add", aten)):
+    def own_fwd():
+        lnfused.ln_fwd(x, g, b, 1e-5, m, s, residual=a, x2_out=dy)
+
+    for name, fn in (("own ln_bwd", own), ("aten ln_bwd + add", aten), ("own ln_fwd + residual", own_fwd)):
         for _ in range(3):
             fn()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -37,5 +40,5 @@ for T, H in [(147456, 1920), (131072, 3072)]:
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        nb = T * H * 2 * 4   # dy, x, addend read, dx written
+        nb = T * H * 2 * 4   # bwd: dy, x, addend read, dx written; fwd: x, r read, x2, h written
         print(f"T{T} H{H} {name}: {ms:.3f} ms, {nb / ms / 1e6:.0f} GB/s (algorithmic 8 B/elem)", flush=True)

@@ -74,17 +74,19 @@ def test_gpt_bf16_out_of_core_equals_in_core_and_tracks_oracle():
     torch.testing.assert_close(torch.tensor(l_ooc), torch.tensor(ref_losses), rtol=2e-2, atol=2e-2)
 
 
-def test_cudnn_attention_matches_flash(monkeypatch):
+@pytest.mark.parametrize("hidden,heads", [(256, 4), (608, 4)])
+def test_cudnn_attention_matches_flash(monkeypatch, hidden, heads):
     """The decoder layer's attention on cuDNN's sm100 kernels (the bench
     path) vs aten's flash kernel (the deterministic path): output and every
-    gradient agree to bf16 resolution."""
+    gradient agree to bf16 resolution.  Head dim 152 (Turing-NLG's 4256 / 28):
+    cuDNN forward, its logsumexp handed to the flash backward."""
     from paper_2008_11421_b200 import units as U
     torch.use_deterministic_algorithms(False)
-    u = U.TransformerLayerUnit(256, 4, 128)
+    u = U.TransformerLayerUnit(hidden, heads, 128)
     gen = torch.Generator().manual_seed(3)
     params = [p.to("cuda", torch.bfloat16) for p in u.init_params(gen)]
-    x = (torch.randn(4 * 128, 256, generator=gen)).to("cuda", torch.bfloat16)
-    dy = (torch.randn(4 * 128, 256, generator=gen)).to("cuda", torch.bfloat16)
+    x = (torch.randn(4 * 128, hidden, generator=gen)).to("cuda", torch.bfloat16)
+    dy = (torch.randn(4 * 128, hidden, generator=gen)).to("cuda", torch.bfloat16)
     res = {}
     for flag in (False, True):
         monkeypatch.setattr(U, "ATTN_CUDNN", flag)

@@ -16,7 +16,7 @@ def rand(shape, seed, scale=1.0):
     return (torch.randn(*shape, device="cuda", generator=g) * scale).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("T,H", [(64, 1920), (7, 4256), (33, 64), (1, 8)])
+@pytest.mark.parametrize("T,H", [(64, 1920), (7, 4256), (33, 64), (1, 8), (64, 3072), (300, 4256), (10000, 3072)])
 @pytest.mark.parametrize("res", [False, True])
 def test_ln_fwd(T, H, res):
     x, r = rand((T, H), 1, 2.0), rand((T, H), 2)
@@ -48,7 +48,7 @@ def test_gelu_bwd_colsum(T, N):
     assert torch.equal(lnfused.gelu_bwd_colsum(dy, f, cs2), dx) and torch.equal(cs2, cs)
 
 
-@pytest.mark.parametrize("T,H", [(1000, 1920), (257, 3072), (9, 4256), (33, 64), (600, 1024)])
+@pytest.mark.parametrize("T,H", [(1000, 1920), (257, 3072), (9, 4256), (33, 64), (600, 1024), (5000, 3072), (3001, 4256)])
 @pytest.mark.parametrize("add", [False, True])
 def test_ln_bwd(T, H, add):
     """One-pass LayerNorm backward vs fp32 autograd of layer_norm on the same
@@ -72,3 +72,27 @@ def test_ln_bwd(T, H, add):
     dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
     dx2 = lnfused.ln_bwd(dy, x, g, m, s, dg2, db2, addend=a if add else None)
     assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
+@pytest.mark.parametrize("T,V", [(37, 128), (300, 51200), (5, 4104), (9, 65536), (2000, 51200)])
+def test_lm_xent(T, V):
+    """Fused next-token cross-entropy vs fp32 torch on the same bf16 logits:
+    per-row losses at fp32 tolerance, dlogits at bf16 resolution; bitwise
+    repeatable; lm_loss's fused branch equals the kernel's."""
+    from paper_2008_11421_b200.units import lm_loss
+    z = rand((T, V), 21, 4.0)
+    g = torch.Generator(device="cuda").manual_seed(22)
+    y = torch.randint(0, V, (T,), device="cuda", generator=g)
+    y[0] = V - 1
+    scale = 1.0 / T
+    rl, dl = lnfused.lm_xent(z, y, scale)
+    zf = z.float().requires_grad_(True)
+    ref = F.cross_entropy(zf, y, reduction="none")
+    ref.sum().mul(scale).backward()
+    torch.testing.assert_close(rl, ref.detach(), rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(dl.float(), zf.grad, rtol=1.6e-2, atol=1e-6 * scale + 1e-8)
+    rl2, dl2 = lnfused.lm_xent(z, y, scale)
+    assert torch.equal(rl, rl2) and torch.equal(dl, dl2)
+    loss, dl3 = lm_loss(z, y)
+    assert torch.equal(dl3, dl)
+    torch.testing.assert_close(loss, ref.detach().mean(), rtol=1e-5, atol=1e-6)
