@@ -477,6 +477,15 @@ int krt_ln_bwd(const void* dy, const void* x, const void* gamma, const float* me
  * dlogits[t] = (softmax(z_t) - onehot(y_t)) * scale.  V % 8 == 0, V <= 65536. */
 int krt_lm_xent(const void* logits, const int64_t* target, void* dlogits, float* row_loss, int64_t T, int V,
                 float scale, void* stream);
+/* The elementwise middle of an unfused causal attention backward (head dims
+ * above 128, where cuDNN's fused backward is unavailable; the SelfAttention
+ * layer kind, model_ir.py:47-59, cost_model.py:126-129): from the fp32
+ * S = Q K^T and dP = dO V^T of `rows` = pairs x s query rows (s keys each),
+ * lse (the forward's natural-log logsumexp of scale * S) and D = rowsum(dO * O),
+ * writes P = exp(scale * S - lse) and dS = P * (dP - D) * scale as bf16,
+ * both 0 above the diagonal.  s % 8 == 0. */
+int krt_attn_softmax_bwd(const float* S, const float* dP, const float* lse, const float* D, void* P, void* dS,
+                         int64_t rows, int s, float scale, void* stream);
 /* dx = gelu_tanh'(f) * dy and colsum[n] = sum_t dx[t, n] (fp32, the bias
  * gradient of the layer that produced f) in one pass over the activations;
  * ws: krt_gelu_bwd_colsum_workspace bytes. */

@@ -140,6 +140,7 @@ EXPORTS = {
     "krt_ln_fwd": (C.c_int, [C.c_void_p] * 8 + [C.c_int64, C.c_int, C.c_float, C.c_void_p]),
     "krt_ln_bwd_workspace": (C.c_size_t, [C.c_int64, C.c_int]),
     "krt_ln_bwd": (C.c_int, [C.c_void_p] * 10 + [C.c_int64, C.c_int, C.c_void_p]),
+    "krt_attn_softmax_bwd": (C.c_int, [C.c_void_p] * 6 + [C.c_int64, C.c_int, C.c_float, C.c_void_p]),
     "krt_lm_xent": (C.c_int, [C.c_void_p] * 4 + [C.c_int64, C.c_int, C.c_float, C.c_void_p]),
     "krt_gelu_bwd_colsum_workspace": (C.c_size_t, [C.c_int64, C.c_int]),
     "krt_gelu_bwd_colsum": (C.c_int, [C.c_void_p] * 5 + [C.c_int64, C.c_int, C.c_void_p]),

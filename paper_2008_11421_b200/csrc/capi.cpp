@@ -654,6 +654,11 @@ int krt_lm_xent(const void* logits, const int64_t* target, void* dlogits, float*
   KRT_CUDA_GUARD(lm_xent(logits, target, dlogits, row_loss, T, V, scale, (cudaStream_t)stream), "lm_xent");
 }
 
+int krt_attn_softmax_bwd(const float* S, const float* dP, const float* lse, const float* D, void* P, void* dS,
+                         int64_t rows, int s, float scale, void* stream) {
+  KRT_CUDA_GUARD(attn_softmax_bwd(S, dP, lse, D, P, dS, rows, s, scale, (cudaStream_t)stream), "attn_softmax_bwd");
+}
+
 size_t krt_gelu_bwd_colsum_workspace(int64_t T, int N) { return gelu_bwd_colsum_workspace(T, N); }
 
 int krt_gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* colsum, void* ws, int64_t T, int N,

@@ -719,6 +719,50 @@ __global__ void __launch_bounds__(kXentThreads, 2) lm_xent_kernel(const __nv_bfl
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// attn_softmax_bwd: the elementwise middle of an unfused causal attention
+// backward (head dims cuDNN's fused backward rejects): from the fp32 score
+// and score-gradient matrices S = Q K^T and dP = dO V^T of a batch of
+// (sequence, head) pairs, one pass writes
+//   P  = exp(scale * S - lse)          (bf16; 0 above the diagonal)
+//   dS = P * (dP - D) * scale          (bf16, from the fp32 P)
+// with lse the forward's natural-log logsumexp and D = rowsum(dO * O).
+// 8 columns per thread; fully masked octets read nothing.
+__global__ void __launch_bounds__(256) attn_softmax_bwd_kernel(const float* __restrict__ S,
+                                                               const float* __restrict__ dP,
+                                                               const float* __restrict__ lse,
+                                                               const float* __restrict__ Dr,
+                                                               __nv_bfloat16* __restrict__ P,
+                                                               __nv_bfloat16* __restrict__ dS, int64_t rows, int s,
+                                                               float scale) {
+  const int oct = s / 8;
+  const int64_t total = rows * oct;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / oct;           // (pair, query row) flattened
+    const int j0 = (int)(t - r * oct) * 8;
+    const int i = (int)(r % s);
+    float p[8], g[8];
+    if (j0 > i) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k] = g[k] = 0.f;
+    } else {
+      const float l = lse[r], d = Dr[r];
+      const float4* s4 = reinterpret_cast<const float4*>(S + r * s + j0);
+      const float4* d4 = reinterpret_cast<const float4*>(dP + r * s + j0);
+      const float4 a0 = __ldcs(s4), a1 = __ldcs(s4 + 1), b0 = __ldcs(d4), b1 = __ldcs(d4 + 1);
+      const float sv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float dv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        p[k] = (j0 + k <= i) ? expf(__fmaf_rn(sv[k], scale, -l)) : 0.f;
+        g[k] = p[k] * (dv[k] - d) * scale;
+      }
+    }
+    __stcs(reinterpret_cast<uint4*>(P + r * s + j0), pack8(p));
+    __stcs(reinterpret_cast<uint4*>(dS + r * s + j0), pack8(g));
+  }
+}
 }  // namespace
 
 size_t ln_bwd_workspace(int64_t T, int H) {
@@ -824,6 +868,18 @@ cudaError_t lm_xent(const void* z, const int64_t* y, void* dz, float* row_loss, 
   else if (oct <= kXentThreads * 25)   // V 51200
     lm_xent_kernel<25><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
   else lm_xent_kernel<32><<<grid, kXentThreads, 0, s>>>(Z, y, D, row_loss, T, V, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_softmax_bwd(const float* S, const float* dP, const float* lse, const float* D, void* P, void* dS,
+                             int64_t rows, int s, float scale, cudaStream_t st) {
+  if (rows <= 0 || s <= 0 || s % 8 != 0) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (rows * (s / 8) + 255) / 256, cap = (int64_t)sms * 8;
+  attn_softmax_bwd_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(
+      S, dP, lse, D, static_cast<__nv_bfloat16*>(P), static_cast<__nv_bfloat16*>(dS), rows, s, scale);
   return cudaGetLastError();
 }
 

@@ -17,4 +17,6 @@ cudaError_t gelu_bwd_colsum(const void* dy, const void* f, void* dx, float* cols
                             cudaStream_t s);
 cudaError_t lm_xent(const void* z, const int64_t* y, void* dz, float* row_loss, int64_t T, int V, float scale,
                     cudaStream_t s);
+cudaError_t attn_softmax_bwd(const float* S, const float* dP, const float* lse, const float* D, void* P, void* dS,
+                             int64_t rows, int s, float scale, cudaStream_t st);
 }  // namespace krt

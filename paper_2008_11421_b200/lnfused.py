@@ -58,6 +58,18 @@ def lm_xent(logits, target, scale):
     return rl, dl
 
 
+def attn_softmax_bwd(S, dP, lse, D, P, dS, scale):
+    """P = exp(scale * S - lse), dS = P * (dP - D) * scale (bf16 outputs, 0
+    above the diagonal) for contiguous fp32 S / dP [..., s, s]; lse / D fp32
+    [..., s] (made contiguous here)."""
+    s = S.shape[-1]
+    rows = S.numel() // s
+    assert S.is_contiguous() and dP.is_contiguous() and P.is_contiguous() and dS.is_contiguous()
+    lse, D = lse.contiguous(), D.contiguous()
+    _lib.check(_lib.lib().krt_attn_softmax_bwd(S.data_ptr(), dP.data_ptr(), lse.data_ptr(), D.data_ptr(),
+                                               P.data_ptr(), dS.data_ptr(), rows, s, float(scale), _stream()))
+
+
 def gelu_bwd_colsum(dy, f, colsum):
     """dx = gelu_tanh'(f) * dy; colsum (fp32 [N]) = column sums of dx."""
     T, N = f.shape

@@ -96,6 +96,12 @@ BN_EPS = 1e-5
 TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
 # GPT attention on cuDNN's sm100 fused kernels (KRT_ATTN_CUDNN=0: aten flash)
 ATTN_CUDNN = os.environ.get("KRT_ATTN_CUDNN", "1") != "0"
+# head dims above cuDNN's backward limit (128): aten's flash backward by
+# default; KRT_ATTN_UNFUSED_BW=1 selects the unfused cuBLAS + own-pass form,
+# measured 2.1x slower at Turing-NLG's shape (1576 vs 766 ms/step: its fp32
+# s x s score / score-gradient matrices cost ~30 MB of HBM traffic per
+# (sequence, head) pair at seq 1024; profiles/round2_s4/README.md)
+ATTN_UNFUSED_BW = os.environ.get("KRT_ATTN_UNFUSED_BW", "0") == "1"
 # the pre-activation unit's 1x1 dgrads on the same GEMM with the BN-backward
 # reduce fused (narrow, HBM-bound shapes)
 TC_DGRAD_PREACT = os.environ.get("KRT_TC_DGRAD_PREACT", "1") != "0"
@@ -1233,6 +1239,50 @@ class TransformerLayerUnit(Unit):
         return (ATTN_CUDNN and not torch.are_deterministic_algorithms_enabled()
                 and (not backward or self.hd <= 128))
 
+    def _unfused_bw(self):
+        # head dims cuDNN's fused backward rejects (Turing-NLG's 152): aten's
+        # flash backward runs them at ~100 TFLOP/s (sm80 mma.sync kernels);
+        # the unfused form puts the five s x s x hd contractions on cuBLAS
+        # tensor-core GEMMs (the two fp32-output ones as TF32 on the exactly
+        # representable bf16 inputs) and the softmax-gradient middle on one
+        # own pass -- opt-in only: the materialised fp32 s x s matrices make
+        # it HBM-bound and 2.1x slower than flash at seq 1024.  Not in
+        # deterministic mode (the flash backward there).
+        return (self.hd > 128 and ATTN_CUDNN and ATTN_UNFUSED_BW and not torch.are_deterministic_algorithms_enabled()
+                and self.s % 8 == 0)
+
+    def _attn_bw_unfused(self, dO, q, k, v, O, lse, n, chunk=8):
+        """Causal attention backward for [n, nh, s, hd] bf16 views: per chunk
+        of sequences S = Q K^T and dP = dO V^T in fp32, P and dS in bf16 from
+        one pass of krt_attn_softmax_bwd (lse: the forward's [n, nh, s]), then
+        dV = P^T dO, dQ = dS K, dK = dS^T Q (bf16 GEMMs, fp32 accumulation)
+        written straight into the [n, s, 3, nh, hd] gradient of qkv."""
+        d = torch.empty((n, self.s, 3, self.nh, self.hd), dtype=dO.dtype, device=dO.device)
+        dq, dk, dv = (d[:, :, i].transpose(1, 2) for i in range(3))
+        scale = 1.0 / math.sqrt(self.hd)
+        tf32 = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        try:
+            for b0 in range(0, n, chunk):
+                sl = slice(b0, min(n, b0 + chunk))
+                qs, ks, vs, dos = q[sl], k[sl], v[sl], dO[sl]
+                dof = dos.float()
+                S = torch.matmul(qs.float(), ks.float().transpose(-1, -2))
+                dP = torch.matmul(dof, vs.float().transpose(-1, -2))
+                D = (dof * O[sl].float()).sum(-1)
+                del dof
+                P = torch.empty(S.shape, dtype=dO.dtype, device=dO.device)
+                dS = torch.empty_like(P)
+                lnfused.attn_softmax_bwd(S, dP, lse[sl], D, P, dS, scale)
+                del S, dP, D
+                dv[sl] = torch.matmul(P.transpose(-1, -2), dos)
+                dq[sl] = torch.matmul(dS, ks)
+                dk[sl] = torch.matmul(dS.transpose(-1, -2), qs)
+                del P, dS
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+        return d.reshape(-1, 3 * self.h)
+
     def _attn_fw(self, qkv, lse_out):
         q, k, v = self._heads(qkv)
         if self._flash():
@@ -1259,6 +1309,11 @@ class TransformerLayerUnit(Unit):
         q, k, v = self._heads(qkv)
         n = do.shape[0] // self.s
         dO = do.view(n, self.s, self.nh, self.hd).transpose(1, 2)
+        if self._flash() and self._unfused_bw():
+            O = o.view(n, self.s, self.nh, self.hd).transpose(1, 2)
+            with bnfused._timed("attn_bwd_unfused", 8 * do.shape[0] * self.h * do.element_size(),
+                                10.0 * n * self.nh * self.s * self.s * self.hd):   # 5 full s x s x hd GEMMs
+                return self._attn_bw_unfused(dO, q, k, v, O, lse, n)
         if self._flash():
             O = o.view(n, self.s, self.nh, self.hd).transpose(1, 2)
             z = torch.zeros((), dtype=torch.int64, device=q.device)

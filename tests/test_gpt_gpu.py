@@ -97,3 +97,32 @@ def test_cudnn_attention_matches_flash(monkeypatch, hidden, heads):
         res[flag] = [y.float(), dx.float()] + grads
     for a, b in zip(res[False], res[True]):
         assert ((a - b).norm() / b.norm()).item() <= 2e-2
+
+
+@pytest.mark.parametrize("n,nh,s,hd,chunk", [(3, 2, 64, 152, 2), (1, 4, 256, 152, 8)])
+def test_unfused_attention_backward_vs_fp32(n, nh, s, hd, chunk):
+    """The unfused causal attention backward (head dims > 128: TF32 / bf16
+    cuBLAS GEMMs + the own softmax-gradient pass) vs fp32 autograd of causal
+    attention on the same bf16 q, k, v, dO: dQ, dK, dV within bf16 resolution."""
+    import math
+    from paper_2008_11421_b200 import units as U
+    torch.use_deterministic_algorithms(False)
+    u = U.TransformerLayerUnit(nh * hd, nh, s)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = torch.randn(n * s, 3 * nh * hd, device="cuda", generator=g).to(torch.bfloat16)
+    do = torch.randn(n * s, nh * hd, device="cuda", generator=g).to(torch.bfloat16)
+    q, k, v = (t.float().requires_grad_(True) for t in u._heads(qkv))
+    sc = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
+    mask = torch.ones(s, s, dtype=torch.bool, device="cuda").triu(1)
+    sc = sc.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(sc, dim=-1)
+    o = torch.softmax(sc, dim=-1) @ v
+    dO = do.view(n, s, nh, hd).transpose(1, 2)
+    o.backward(dO.float())
+    ob = o.detach().to(torch.bfloat16)
+    qb, kb, vb = u._heads(qkv)
+    d = u._attn_bw_unfused(dO, qb, kb, vb, ob, lse.detach().float(), n, chunk=chunk)
+    got = d.view(n, s, 3, nh, hd)
+    for i, ref in enumerate((q.grad, k.grad, v.grad)):
+        x = got[:, :, i].transpose(1, 2).float()
+        assert ((x - ref).norm() / ref.norm()).item() <= 1e-2, i
