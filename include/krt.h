@@ -507,6 +507,11 @@ int krt_mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1,
  * b2 [N] (bias epilogue, beta = 1 on x2; y may alias x2). */
 int krt_mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void* x2, void* y, int64_t M,
                          int64_t N, int64_t K, void* stream);
+/* A linear layer's weight and bias gradients in one cuBLASLt GEMM (BGRADB
+ * epilogue): dy [M, N], x [M, K] row-major bf16 -> dw = dy^T x [N, K] and
+ * db = sum over rows of dy [N], both fp32 (the gradient region's type). */
+int krt_linear_wgrad_bgrad(const void* dy, const void* x, float* dw, float* db, int64_t M, int64_t N, int64_t K,
+                           void* stream);
 
 #ifdef __cplusplus
 }

@@ -131,6 +131,7 @@ EXPORTS = {
     "krt_mlp_fc1_gelu": (C.c_int, [C.c_void_p] * 5 + [C.c_int64] * 3 + [C.c_void_p]),
     "krt_mlp_fc2_dgelu": (C.c_int, [C.c_void_p] * 4 + [C.c_int64] * 3 + [C.c_void_p]),
     "krt_mlp_fc2_residual": (C.c_int, [C.c_void_p] * 5 + [C.c_int64] * 3 + [C.c_void_p]),
+    "krt_linear_wgrad_bgrad": (C.c_int, [C.c_void_p] * 4 + [C.c_int64] * 3 + [C.c_void_p]),
     "krt_conv_wgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int] * 10 + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]),
     "krt_conv1x1_bn_dgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 8),
     "krt_bn_partials_bwd_finalize": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64] + [C.c_void_p] * 7),

@@ -676,6 +676,11 @@ int krt_mlp_fc2_residual(const void* g, const void* w2, const void* b2, const vo
   return guard([&] { mlp_fc2_residual(g, w2, b2, x2, y, M, N, K, (cudaStream_t)stream); });
 }
 
+int krt_linear_wgrad_bgrad(const void* dy, const void* x, float* dw, float* db, int64_t M, int64_t N, int64_t K,
+                           void* stream) {
+  return guard([&] { linear_wgrad_bgrad(dy, x, dw, db, M, N, K, (cudaStream_t)stream); });
+}
+
 int krt_mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, int64_t M, int64_t N, int64_t K,
                       void* stream) {
   return guard([&] { mlp_fc2_dgelu(dy, w2, f1, df1, M, N, K, (cudaStream_t)stream); });

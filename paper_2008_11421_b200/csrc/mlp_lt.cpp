@@ -67,7 +67,7 @@ struct Desc {
 // algorithm cache
 void run(int kind, cublasOperation_t ta, cublasOperation_t tb, int64_t m, int64_t n, int64_t k, const void* A,
          int64_t lda, const void* B, int64_t ldb, void* D, cublasLtEpilogue_t epi, const void* bias, int bias_type,
-         void* aux, cudaStream_t stream, const void* C = nullptr) {
+         void* aux, cudaStream_t stream, const void* C = nullptr, cudaDataType_t d_type = CUDA_R_16BF) {
   LtState& s = lt();
   std::lock_guard<std::mutex> lk(s.mu);
   if (!s.h) {
@@ -93,7 +93,7 @@ void run(int kind, cublasOperation_t ta, cublasOperation_t tb, int64_t m, int64_
   const bool tA = ta == CUBLAS_OP_T, tB = tb == CUBLAS_OP_T;
   LT_CHECK(cublasLtMatrixLayoutCreate(&g.a, CUDA_R_16BF, tA ? k : m, tA ? m : k, lda));
   LT_CHECK(cublasLtMatrixLayoutCreate(&g.b, CUDA_R_16BF, tB ? n : k, tB ? k : n, ldb));
-  LT_CHECK(cublasLtMatrixLayoutCreate(&g.d, CUDA_R_16BF, m, n, m));
+  LT_CHECK(cublasLtMatrixLayoutCreate(&g.d, d_type, m, n, m));
   auto key = std::make_tuple(kind, m, n, k, bias_type);
   auto it = s.algos.find(key);
   if (it == s.algos.end()) {
@@ -106,7 +106,7 @@ void run(int kind, cublasOperation_t ta, cublasOperation_t tb, int64_t m, int64_
     cublasStatus_t st = cublasLtMatmulAlgoGetHeuristic(s.h, g.op, g.a, g.b, g.d, g.d, pref, 1, &res, &found);
     cublasLtMatmulPreferenceDestroy(pref);
     if (st != CUBLAS_STATUS_SUCCESS || found == 0)
-      throw std::runtime_error("cublasLt: no algorithm for the fused MLP epilogue (kind " + std::to_string(kind) +
+      throw std::runtime_error("cublasLt: no algorithm for the fused epilogue (kind " + std::to_string(kind) +
                                ", m " + std::to_string(m) + ", n " + std::to_string(n) + ", k " +
                                std::to_string(k) + ", bias type " + std::to_string(bias_type) + ")");
     it = s.algos.emplace(key, res.algo).first;
@@ -134,6 +134,16 @@ void mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void*
                       int64_t K, cudaStream_t s) {
   // y^T (N x M) = W2 (K x N col-major, transposed) . g^T (K x M) + b2 + x2^T
   run(2, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, w2, K, g, K, y, CUBLASLT_EPILOGUE_BIAS, b2, CUDA_R_16BF, nullptr, s, x2);
+}
+
+void linear_wgrad_bgrad(const void* dy, const void* x, float* dw, float* db, int64_t M, int64_t N, int64_t K,
+                        cudaStream_t s) {
+  // dW (row-major [N, K], fp32) = dy^T . x, and db [N] (fp32) = the column sums
+  // of dy in the same GEMM: column-major dW^T (K x N) = x^T (K x M, x read
+  // column-major) . dy (M x N read as dy^T, transposed); BGRADB sums the B
+  // operand (dy) over the reduction dimension M
+  run(3, CUBLAS_OP_N, CUBLAS_OP_T, K, N, M, x, K, dy, N, dw, CUBLASLT_EPILOGUE_BGRADB, db, CUDA_R_32F, nullptr, s,
+      nullptr, CUDA_R_32F);
 }
 
 }  // namespace krt

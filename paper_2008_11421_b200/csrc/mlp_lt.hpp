@@ -17,4 +17,9 @@ void mlp_fc2_dgelu(const void* dy, const void* w2, const void* f1, void* df1, in
 // (y may alias x2)
 void mlp_fc2_residual(const void* g, const void* w2, const void* b2, const void* x2, void* y, int64_t M, int64_t N,
                       int64_t K, cudaStream_t s);
+// a linear layer's weight and bias gradients in one GEMM (cuBLASLt BGRADB
+// epilogue): dy [M, N], x [M, K] bf16 -> dw = dy^T . x [N, K] and db = the
+// column sums of dy [N], both fp32
+void linear_wgrad_bgrad(const void* dy, const void* x, float* dw, float* db, int64_t M, int64_t N, int64_t K,
+                        cudaStream_t s);
 }  // namespace krt

@@ -123,3 +123,25 @@ def mlp_fc2_residual(g, w2, b2, x2, out=None):
         _lib.check(_lib.lib().krt_mlp_fc2_residual(g.data_ptr(), w2.data_ptr(), b2.data_ptr(), x2.data_ptr(),
                                                    y.data_ptr(), T, N, K, _stream()))
     return y
+
+
+_WGRAD_BGRAD_OK = [True]
+
+
+def linear_wgrad_bgrad(dy, x, gw, gb):
+    """gw (fp32 [N, K]) = dy^T x and gb (fp32 [N]) = dy.sum(0) in one cuBLASLt
+    GEMM (BGRADB epilogue).  Returns False (nothing written) when the shapes
+    or cuBLASLt do not support it; the caller then runs GEMM + sum."""
+    if not (_WGRAD_BGRAD_OK[0] and supported(dy) and x.dtype == dy.dtype and gw.dtype == torch.float32
+            and gb.dtype == torch.float32 and gw.is_contiguous() and gb.is_contiguous()):
+        return False
+    M, N = dy.shape
+    K = x.shape[1]
+    dy, x = dy.contiguous(), x.contiguous()
+    with _timed("cublas_gemm", (M * N + M * K) * 2 + N * K * 4, 2.0 * M * N * K):
+        rc = _lib.lib().krt_linear_wgrad_bgrad(dy.data_ptr(), x.data_ptr(), gw.data_ptr(), gb.data_ptr(), M, N, K,
+                                               _stream())
+    if rc != 0:
+        _WGRAD_BGRAD_OK[0] = False   # no cuBLASLt algorithm for the epilogue here: GEMM + sum from now on
+        return False
+    return True

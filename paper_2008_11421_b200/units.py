@@ -96,6 +96,11 @@ BN_EPS = 1e-5
 TC_CONV1X1 = os.environ.get("KRT_TC_CONV1X1", "1") != "0"
 # GPT attention on cuDNN's sm100 fused kernels (KRT_ATTN_CUDNN=0: aten flash)
 ATTN_CUDNN = os.environ.get("KRT_ATTN_CUDNN", "1") != "0"
+# linear layers' bias gradient in the weight-gradient GEMM's epilogue
+# (cuBLASLt BGRADB), opt-in with KRT_LINEAR_BGRAD=1: measured slower than
+# GEMM + a separate column sum on B200 (Megatron L36: GEMMs 2841 -> 2959
+# ms/step, 33.8 -> 33.0 samples/s; profiles/round2_s4/README.md)
+LINEAR_BGRAD = os.environ.get("KRT_LINEAR_BGRAD", "0") == "1"
 # head dims above cuDNN's backward limit (128): aten's flash backward by
 # default; KRT_ATTN_UNFUSED_BW=1 selects the unfused cuBLAS + own-pass form,
 # measured 2.1x slower at Turing-NLG's shape (1576 vs 766 ms/step: its fp32
@@ -1138,10 +1143,12 @@ def _mm_f32_into_raw(a, b, out):
 
 
 def _linear_bw(dy, x, w, gw, gb, need_dx=True):
-    """y = x W^T + b: writes fp32 dW, db (gb None: already written); returns dx."""
-    _mm_f32_into(dy.t(), x, gw)
-    if gb is not None:
-        torch.sum(dy, 0, dtype=torch.float32, out=gb)   # fp32 accumulation, no fp32 copy of dy
+    """y = x W^T + b: writes fp32 dW, db (gb None: already written); returns dx.
+    KRT_LINEAR_BGRAD=1: dW and db from one cuBLASLt GEMM (BGRADB epilogue)."""
+    if gb is None or not (dy.is_cuda and LINEAR_BGRAD and lnfused.linear_wgrad_bgrad(dy, x, gw, gb)):
+        _mm_f32_into(dy.t(), x, gw)
+        if gb is not None:
+            torch.sum(dy, 0, dtype=torch.float32, out=gb)   # fp32 accumulation, no fp32 copy of dy
     if not need_dx:
         return None
     with bnfused._timed("cublas_gemm", *_gemm_cost(dy.shape[0], w.shape[1], dy.shape[1], dy.element_size())):

@@ -57,3 +57,18 @@ def test_fc2_residual(T, H):
     assert rel(y, ref) < 1e-2
     out = torch.empty_like(x2)
     assert torch.equal(lnfused.mlp_fc2_residual(g, w2, b2, x2, out=out), y)
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 768, 256), (1024, 1920, 7680), (4096, 4256, 1064)])
+def test_linear_wgrad_bgrad(M, N, K):
+    """dW = dy^T x and db = dy.sum(0) from one cuBLASLt GEMM (BGRADB epilogue)
+    vs fp32 torch on the same bf16 operands."""
+    from paper_2008_11421_b200 import lnfused
+    g = torch.Generator(device="cuda").manual_seed(9)
+    dy = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+    x = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    gw = torch.full((N, K), float("nan"), device="cuda")
+    gb = torch.full((N,), float("nan"), device="cuda")
+    assert lnfused.linear_wgrad_bgrad(dy, x, gw, gb)
+    torch.testing.assert_close(gw, dy.float().t() @ x.float(), rtol=1e-3, atol=1e-2)
+    torch.testing.assert_close(gb, dy.float().sum(0), rtol=1e-4, atol=1e-3)
