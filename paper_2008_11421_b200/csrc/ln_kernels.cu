@@ -641,9 +641,9 @@ void launch_ln_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_b
 // (deterministic), then dz written from the registers: 2 bytes read and 2
 // written per logit instead of the fp32 chunk passes of an unfused softmax.
 // 256 threads, two CTAs per SM (launch bounds cap the registers at 128).
-// Measured at V 51200: 0.32 of HBM in the GPT step, the same as one
-// 512-thread CTA per SM -- the row's serial max / sum-of-exp chains and the
-// two exp passes (MUFU) per logit bound it, not the loads (open item)
+// Measured at V 51200 with single max / sum chains: 0.32 of HBM in the GPT
+// step, the same as one 512-thread CTA per SM (latency of the chains and the
+// two exp passes per logit, not the loads)
 constexpr int kXentThreads = 256;
 
 __device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
@@ -677,28 +677,30 @@ __global__ void __launch_bounds__(kXentThreads, 2) lm_xent_kernel(const __nv_bfl
       const int j = threadIdx.x + kXentThreads * i;
       if (j < oct) u[i] = __ldcs(zr + j);
     }
-    float m = -INFINITY;
+    // four independent max / sum chains per thread (the single 8J-long
+    // chains were latency-bound), combined in a fixed order
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int i = 0; i < J; ++i) {
       if (threadIdx.x + kXentThreads * i < oct) {
         float f[8];
         unpack8(u[i], f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) m = fmaxf(m, f[k]);
+        for (int k = 0; k < 8; ++k) m4[k & 3] = fmaxf(m4[k & 3], f[k]);
       }
     }
-    m = block_reduce(m, sh, true);
-    float se = 0.f;
+    const float m = block_reduce(fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])), sh, true);
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int i = 0; i < J; ++i) {
       if (threadIdx.x + kXentThreads * i < oct) {
         float f[8];
         unpack8(u[i], f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) se += __expf(f[k] - m);
+        for (int k = 0; k < 8; ++k) s4[k & 3] += __expf(f[k] - m);
       }
     }
-    se = block_reduce(se, sh, false);
+    const float se = block_reduce((s4[0] + s4[1]) + (s4[2] + s4[3]), sh, false);
     const float lse = m + __logf(se);
     const int64_t tgt = y[row];
 #pragma unroll
