@@ -451,11 +451,14 @@ __global__ void __launch_bounds__(32 * kBwdMaxWarps) ln_bwd_bulk_kernel(
   __syncthreads();
   if (threadIdx.x == 0)
     for (int it = 0; it < S; ++it) issue(it);
-  float accg[J][8], accb[J][8];
+  float accg[J][8], accb[J][8], gam[J][8];  // gamma held in registers for all rows
 #pragma unroll
-  for (int i = 0; i < J; ++i)
+  for (int i = 0; i < J; ++i) {
+    const int j = threadIdx.x + blockDim.x * i;
+    if (j < oct) unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gam[i]);
 #pragma unroll
     for (int k = 0; k < 8; ++k) accg[i][k] = accb[i][k] = 0.f;
+  }
   int it = 0;
   for (int64_t row = blockIdx.x; row < T; row += gridDim.x, ++it) {
     const int st = it % S, par = it & 1;
@@ -476,14 +479,13 @@ __global__ void __launch_bounds__(32 * kBwdMaxWarps) ln_bwd_bulk_kernel(
     for (int i = 0; i < J; ++i) {
       const int j = threadIdx.x + blockDim.x * i;
       if (j < oct) {
-        float d[8], xv[8], gg[8];
+        float d[8], xv[8];
         unpack8(ud[i], d);
         unpack8(ux[i], xv);
-        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float xh = (xv[k] - mu) * rs;
-          const float gd = d[k] * gg[k];
+          const float gd = d[k] * gam[i][k];
           s1 += gd;
           s2 = __fmaf_rn(gd, xh, s2);
           accg[i][k] += d[k] * xh;
@@ -512,15 +514,14 @@ __global__ void __launch_bounds__(32 * kBwdMaxWarps) ln_bwd_bulk_kernel(
     for (int i = 0; i < J; ++i) {
       const int j = threadIdx.x + blockDim.x * i;
       if (j < oct) {
-        float d[8], xv[8], o[8], gg[8];
+        float d[8], xv[8], o[8];
         unpack8(ud[i], d);
         unpack8(ux[i], xv);
-        unpack8(__ldg(reinterpret_cast<const uint4*>(g) + j), gg);
         if (ADD) unpack8(ua[i], o);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float xh = (xv[k] - mu) * rs;
-          const float v = rs * (d[k] * gg[k] - c1 - xh * c2);
+          const float v = rs * (d[k] * gam[i][k] - c1 - xh * c2);
           o[k] = ADD ? __fadd_rn(v, o[k]) : v;
         }
         __stcs(reinterpret_cast<uint4*>(dx + row * H) + j, pack8(o));
